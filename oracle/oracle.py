@@ -1,0 +1,163 @@
+"""ctypes front-end of the CPU checker (oracle/render_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / ``--impl reference`` leg, never by the product
+package.  Every function mirrors a reference function (cited) on NumPy fp64
+arrays:
+
+* ``render_arrays``  -> splatmap renderloss.py:170-218 (+ _composite 106-152)
+* ``render_backward`` -> (absent in the reference) reverse-order backward of
+  the same forward; pinned by finite differences of the reference forward
+  (tests/golden/render_fd.npz).
+* ``total_loss``     -> renderloss.py:226-274, optional dL/d(rgb, depth)
+* ``adam``           -> torch.optim.Adam formula (the reference has no Adam)
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+_LIB_PATH = _HERE / "liboracle.so"
+_lib = None
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+def build() -> Path:
+    """Compile the checker in place (gcc, -ffp-contract=off)."""
+    subprocess.run(["make", "-s", "-C", str(_HERE)], check=True)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            build()
+        _lib = ctypes.CDLL(str(_LIB_PATH))
+        _lib.or_render_fwd.restype = ctypes.c_int
+        _lib.or_render_fwd.argtypes = (
+            [ctypes.c_int64] + [_dp] * 7 + [ctypes.c_double] * 5 + [ctypes.c_int] * 2
+            + [_dp] * 3 + [_i64p, ctypes.c_int])
+        _lib.or_render_bwd.restype = ctypes.c_int
+        _lib.or_render_bwd.argtypes = (
+            [ctypes.c_int64] + [_dp] * 7 + [ctypes.c_double] * 5 + [ctypes.c_int] * 2
+            + [_dp] * 3 + [_dp] * 5 + [ctypes.c_int])
+        _lib.or_total_loss.restype = ctypes.c_double
+        _lib.or_total_loss.argtypes = [_dp] * 4 + [ctypes.c_int] * 2 + [ctypes.c_double] * 2 + [_dp] * 2
+        _lib.or_adam.restype = None
+        _lib.or_adam.argtypes = ([ctypes.c_int64] + [_dp] * 4 + [ctypes.c_double] * 4
+                                 + [ctypes.c_int64])
+    return _lib
+
+
+def _c(a, shape=None) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if shape is not None:
+        a = a.reshape(shape)
+    return a
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(_dp)
+
+
+def default_threads() -> int:
+    return int(os.environ.get("ORACLE_THREADS", os.cpu_count() or 1))
+
+
+def quat_to_matrix(q) -> np.ndarray:
+    """core.py:88-97 rotation matrix of a (w, x, y, z) quaternion."""
+    w, x, y, z = (float(v) for v in q)
+    return np.array(
+        [
+            [1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+            [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+            [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)],
+        ]
+    )
+
+
+def _scene_args(positions, rotations, scales, opacities, sh0):
+    pos = _c(positions, (-1, 3))
+    n = pos.shape[0]
+    return n, pos, _c(rotations, (n, 4)), _c(scales, (n, 3)), _c(opacities, (n,)), _c(sh0, (n, 3))
+
+
+def render_arrays(positions, rotations, scales, opacities, sh0, pose_rotation, pose_translation,
+                  fx, fy, cx, cy, near, width, height, threads=None, return_pairs=False):
+    """fp64 restatement of renderloss.render_arrays; returns (rgb, depth, alpha)."""
+    n, pos, rot, sc, op, sh = _scene_args(positions, rotations, scales, opacities, sh0)
+    r_wc = _c(quat_to_matrix(pose_rotation))
+    t = _c(pose_translation, (3,))
+    rgb = np.zeros((height, width, 3))
+    depth = np.zeros((height, width))
+    alpha = np.zeros((height, width))
+    pairs = ctypes.c_int64(0)
+    rc = lib().or_render_fwd(n, _p(pos), _p(rot), _p(sc), _p(op), _p(sh), _p(r_wc), _p(t),
+                             fx, fy, cx, cy, near, width, height, _p(rgb), _p(depth), _p(alpha),
+                             ctypes.byref(pairs), threads or default_threads())
+    if rc:
+        raise MemoryError("oracle render failed")
+    if return_pairs:
+        return rgb, depth, alpha, int(pairs.value)
+    return rgb, depth, alpha
+
+
+def render_backward(positions, rotations, scales, opacities, sh0, pose_rotation, pose_translation,
+                    fx, fy, cx, cy, near, width, height, d_rgb=None, d_depth=None, d_alpha=None,
+                    threads=None):
+    """Analytic gradient of <d_rgb,rgb> + <d_depth,depth> + <d_alpha,alpha>.
+
+    Returns dict of fp64 arrays: positions (n,3), rotations (n,4), scales (n,3),
+    opacities (n,), sh0 (n,3).
+    """
+    n, pos, rot, sc, op, sh = _scene_args(positions, rotations, scales, opacities, sh0)
+    r_wc = _c(quat_to_matrix(pose_rotation))
+    t = _c(pose_translation, (3,))
+    dr = None if d_rgb is None else _c(d_rgb, (height, width, 3))
+    dd = None if d_depth is None else _c(d_depth, (height, width))
+    da = None if d_alpha is None else _c(d_alpha, (height, width))
+    out = {
+        "positions": np.zeros((n, 3)), "rotations": np.zeros((n, 4)), "scales": np.zeros((n, 3)),
+        "opacities": np.zeros(n), "sh0": np.zeros((n, 3)),
+    }
+    rc = lib().or_render_bwd(n, _p(pos), _p(rot), _p(sc), _p(op), _p(sh), _p(r_wc), _p(t),
+                             fx, fy, cx, cy, near, width, height, _p(dr), _p(dd), _p(da),
+                             _p(out["positions"]), _p(out["rotations"]), _p(out["scales"]),
+                             _p(out["opacities"]), _p(out["sh0"]), threads or default_threads())
+    if rc:
+        raise MemoryError("oracle backward failed")
+    return out
+
+
+def total_loss(rgb, depth, gt_rgb, gt_depth, lambda_s=0.2, lambda_depth=0.5, grad=False):
+    """renderloss.total_loss on arrays; with grad=True also (d_rgb, d_depth)."""
+    rgb = _c(rgb)
+    h, w = rgb.shape[:2]
+    depth = _c(depth, (h, w))
+    gt_rgb = _c(gt_rgb, (h, w, 3))
+    gt_depth = _c(gt_depth, (h, w))
+    if grad:
+        d_rgb = np.zeros((h, w, 3))
+        d_depth = np.zeros((h, w))
+        val = lib().or_total_loss(_p(rgb), _p(depth), _p(gt_rgb), _p(gt_depth), h, w,
+                                  lambda_s, lambda_depth, _p(d_rgb), _p(d_depth))
+        return float(val), d_rgb, d_depth
+    return float(lib().or_total_loss(_p(rgb), _p(depth), _p(gt_rgb), _p(gt_depth), h, w,
+                                     lambda_s, lambda_depth, None, None))
+
+
+def adam(param, m, v, grad, lr, beta1, beta2, eps, step):
+    """In-place torch.optim.Adam step on fp64 flat arrays (step = post-increment count)."""
+    for a in (param, m, v):
+        assert a.dtype == np.float64 and a.flags.c_contiguous
+    g = _c(grad)
+    lib().or_adam(param.size, _p(param), _p(m), _p(v), _p(g), lr, beta1, beta2, eps, int(step))

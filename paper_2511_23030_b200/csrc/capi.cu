@@ -1,0 +1,156 @@
+// extern "C" entry points of libsplatmap_cuda.so (declared in include/splatmap_cuda.h).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "render.cuh"
+
+namespace sm {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char *what) {
+    set_error("%s: CUDA error %d (%s)", what, (int)e, cudaGetErrorString(e));
+    return SM_ERR_CUDA;
+}
+
+int64_t loss_workspace_size(int W, int H);
+int loss_forward_backward(const float *, const float *, const uint8_t *, const float *, const float *,
+                          int, int, int, float, float, void *, int64_t, float *, float *, float *,
+                          cudaStream_t);
+int adam_step(float *, float *, float *, float *, const int32_t *, int64_t, const sm_adam_config &,
+              const uint32_t *, cudaStream_t);
+int cull_chunks(const int32_t *, int64_t, const double *, const double *, double, double, uint8_t *,
+                cudaStream_t);
+int encode_positions(const float *, int64_t, double, uint64_t *, int64_t *, cudaStream_t);
+int expand_segments(const int64_t *, const int64_t *, const int64_t *, int64_t, int64_t, int32_t *,
+                    cudaStream_t);
+int chunk_unpack(const uint8_t *, int64_t, int64_t, float *, float *, float *, float *, int64_t *,
+                 cudaStream_t);
+int chunk_pack(const float *, const float *, const float *, const float *, int64_t, int64_t,
+               uint8_t *, cudaStream_t);
+
+}  // namespace sm
+
+using namespace sm;
+
+#define SM_STREAM(s) reinterpret_cast<cudaStream_t>(s)
+
+extern "C" {
+
+int sm_abi_version(void) { return SM_ABI_VERSION; }
+
+const char *sm_last_error(void) { return g_err; }
+
+int sm_device_sm_count(void) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+    return n;
+}
+
+int64_t sm_render_workspace_size(const sm_render_dims *dims) {
+    if (!dims) return -1;
+    return render_layout(*dims).total;
+}
+
+int sm_render_forward(const float *params, const int32_t *slots, int64_t n, const sm_camera *cam,
+                      const sm_render_dims *dims, void *workspace, int64_t workspace_bytes,
+                      float *out_rgb, float *out_depth, float *out_alpha, void *stream) {
+    if (!cam || !dims || !workspace || !out_rgb || !out_depth || !out_alpha || (n > 0 && !params)) {
+        set_error("sm_render_forward: null argument");
+        return SM_ERR_INVALID;
+    }
+    return render_forward(params, slots, n, *cam, *dims, workspace, workspace_bytes, out_rgb,
+                          out_depth, out_alpha, SM_STREAM(stream));
+}
+
+int sm_render_backward(const float *params, const int32_t *slots, int64_t n, const sm_camera *cam,
+                       const sm_render_dims *dims, void *workspace, int64_t workspace_bytes,
+                       const float *d_rgb, const float *d_depth, const float *d_alpha, float *grads,
+                       void *stream) {
+    if (!cam || !dims || !workspace || (n > 0 && (!params || !grads))) {
+        set_error("sm_render_backward: null argument");
+        return SM_ERR_INVALID;
+    }
+    return render_backward(params, slots, n, *cam, *dims, workspace, workspace_bytes, d_rgb, d_depth,
+                           d_alpha, grads, SM_STREAM(stream));
+}
+
+int64_t sm_loss_workspace_size(int32_t width, int32_t height) { return loss_workspace_size(width, height); }
+
+int sm_loss_forward_backward(const float *rgb, const float *depth, const uint8_t *gt_rgb_u8,
+                             const float *gt_rgb_f32, const float *gt_depth, int32_t width,
+                             int32_t height, int32_t channels, float lambda_s, float lambda_depth,
+                             void *workspace, int64_t workspace_bytes, float *loss_out, float *d_rgb,
+                             float *d_depth, void *stream) {
+    if (!rgb || !workspace || !loss_out) {
+        set_error("sm_loss_forward_backward: null argument");
+        return SM_ERR_INVALID;
+    }
+    return loss_forward_backward(rgb, depth, gt_rgb_u8, gt_rgb_f32, gt_depth, width, height, channels,
+                                 lambda_s, lambda_depth, workspace, workspace_bytes, loss_out, d_rgb,
+                                 d_depth, SM_STREAM(stream));
+}
+
+int sm_adam_step(float *params, float *m, float *v, float *grads, const int32_t *slots, int64_t n,
+                 const sm_adam_config *cfg, const uint32_t *skip_flag, void *stream) {
+    if (!cfg || (n > 0 && (!params || !m || !v || !grads))) {
+        set_error("sm_adam_step: null argument");
+        return SM_ERR_INVALID;
+    }
+    return adam_step(params, m, v, grads, slots, n, *cfg, skip_flag, SM_STREAM(stream));
+}
+
+int sm_cull_chunks(const int32_t *coords, int64_t n, const double *planes, const double *cam_center,
+                   double max_distance, double chunk_size, uint8_t *visible_out, void *stream) {
+    if (!planes || !cam_center || (n > 0 && (!coords || !visible_out))) {
+        set_error("sm_cull_chunks: null argument");
+        return SM_ERR_INVALID;
+    }
+    return cull_chunks(coords, n, planes, cam_center, max_distance, chunk_size, visible_out,
+                       SM_STREAM(stream));
+}
+
+int sm_encode_positions(const float *params, int64_t n, double chunk_size, uint64_t *ids_out,
+                        int64_t *err_out, void *stream) {
+    if (!err_out || (n > 0 && (!params || !ids_out))) {
+        set_error("sm_encode_positions: null argument");
+        return SM_ERR_INVALID;
+    }
+    return encode_positions(params, n, chunk_size, ids_out, err_out, SM_STREAM(stream));
+}
+
+int sm_expand_segments(const int64_t *seg_offset, const int64_t *seg_count, const int64_t *seg_prefix,
+                       int64_t n_segments, int64_t total, int32_t *slots_out, void *stream) {
+    return expand_segments(seg_offset, seg_count, seg_prefix, n_segments, total, slots_out,
+                           SM_STREAM(stream));
+}
+
+int sm_chunk_unpack(const uint8_t *records, int64_t n, int64_t stride, float *params, float *sh_rest,
+                    float *adam_m, float *adam_v, int64_t *err_out, void *stream) {
+    if (!err_out || (n > 0 && (!records || !params || !sh_rest || !adam_m || !adam_v))) {
+        set_error("sm_chunk_unpack: null argument");
+        return SM_ERR_INVALID;
+    }
+    return chunk_unpack(records, n, stride, params, sh_rest, adam_m, adam_v, err_out,
+                        SM_STREAM(stream));
+}
+
+int sm_chunk_pack(const float *params, const float *sh_rest, const float *adam_m, const float *adam_v,
+                  int64_t n, int64_t stride, uint8_t *records, void *stream) {
+    if (n > 0 && (!params || !sh_rest || !adam_m || !adam_v || !records)) {
+        set_error("sm_chunk_pack: null argument");
+        return SM_ERR_INVALID;
+    }
+    return chunk_pack(params, sh_rest, adam_m, adam_v, n, stride, records, SM_STREAM(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,148 @@
+// Render pipeline shared declarations: workspace layout + fp64 projection.
+#pragma once
+#include "common.cuh"
+
+namespace sm {
+
+constexpr int kG2dStride = 12;   // per-rank 2D grads: u v ia ib ic op r g b z - -
+
+struct RenderLayout {
+    int tiles_x, tiles_y;
+    int64_t n_tiles;
+    int rank_bits, tile_bits;
+    int depth_passes, tile_passes;
+    int64_t sort_blocks;
+    int64_t o_counters, o_rec, o_rec_sorted, o_p64, o_dkey0, o_dkey1, o_order0, o_order1;
+    int64_t o_tcount, o_tcount_r, o_toff, o_ikey0, o_ikey1, o_ranges;
+    int64_t o_pix_cd, o_pix_t, o_pix_tlast, o_pix_last, o_g2d, o_sort_hist, o_scan;
+    int64_t total;
+};
+
+RenderLayout render_layout(const sm_render_dims &d);
+
+struct RenderBufs {
+    sm_render_counters *ctr;
+    ProjRec *rec, *rec_sorted;
+    Proj64 *p64;
+    unsigned long long *dkey0, *dkey1;
+    uint32_t *order0, *order1, *tcount, *tcount_r, *toff, *ikey0, *ikey1, *ranges;
+    float4 *pix_cd;
+    float *pix_t, *pix_tlast;
+    int32_t *pix_last;
+    float *g2d;
+    uint32_t *sort_hist, *scan;
+};
+
+inline RenderBufs render_bufs(void *ws, const RenderLayout &L) {
+    char *b = static_cast<char *>(ws);
+    RenderBufs r;
+    r.ctr = reinterpret_cast<sm_render_counters *>(b + L.o_counters);
+    r.rec = reinterpret_cast<ProjRec *>(b + L.o_rec);
+    r.rec_sorted = reinterpret_cast<ProjRec *>(b + L.o_rec_sorted);
+    r.p64 = reinterpret_cast<Proj64 *>(b + L.o_p64);
+    r.dkey0 = reinterpret_cast<unsigned long long *>(b + L.o_dkey0);
+    r.dkey1 = reinterpret_cast<unsigned long long *>(b + L.o_dkey1);
+    r.order0 = reinterpret_cast<uint32_t *>(b + L.o_order0);
+    r.order1 = reinterpret_cast<uint32_t *>(b + L.o_order1);
+    r.tcount = reinterpret_cast<uint32_t *>(b + L.o_tcount);
+    r.tcount_r = reinterpret_cast<uint32_t *>(b + L.o_tcount_r);
+    r.toff = reinterpret_cast<uint32_t *>(b + L.o_toff);
+    r.ikey0 = reinterpret_cast<uint32_t *>(b + L.o_ikey0);
+    r.ikey1 = reinterpret_cast<uint32_t *>(b + L.o_ikey1);
+    r.ranges = reinterpret_cast<uint32_t *>(b + L.o_ranges);
+    r.pix_cd = reinterpret_cast<float4 *>(b + L.o_pix_cd);
+    r.pix_t = reinterpret_cast<float *>(b + L.o_pix_t);
+    r.pix_tlast = reinterpret_cast<float *>(b + L.o_pix_tlast);
+    r.pix_last = reinterpret_cast<int32_t *>(b + L.o_pix_last);
+    r.g2d = reinterpret_cast<float *>(b + L.o_g2d);
+    r.sort_hist = reinterpret_cast<uint32_t *>(b + L.o_sort_hist);
+    r.scan = reinterpret_cast<uint32_t *>(b + L.o_scan);
+    return r;
+}
+
+// fp64 projection of one Gaussian (renderloss.py:176-199).  Keeps the
+// intermediates the backward needs.
+struct ProjGeom {
+    double x, y, z;        // camera-frame centre
+    double u, v;           // pixel mean
+    double a, b, c;        // cov2 (+0.3 on the diagonal)
+    double R[9];           // Gaussian rotation (unnormalised-quaternion formula)
+    double s2[3];
+    double Sc[6];          // camera covariance, symmetric: xx xy xz yy yz zz
+};
+
+__device__ __forceinline__ void project_geometry(double px, double py, double pz, double qw,
+                                                 double qx, double qy, double qz, double sx,
+                                                 double sy, double sz, const double *rwc,
+                                                 const double *t, double fx, double fy,
+                                                 double cx, double cy, ProjGeom &g) {
+    const double d0 = px - t[0], d1 = py - t[1], d2 = pz - t[2];
+    // cam = (p - t) @ r_wc
+    g.x = d0 * rwc[0] + d1 * rwc[3] + d2 * rwc[6];
+    g.y = d0 * rwc[1] + d1 * rwc[4] + d2 * rwc[7];
+    g.z = d0 * rwc[2] + d1 * rwc[5] + d2 * rwc[8];
+    const double x = g.x, y = g.y, z = g.z;
+    g.u = fx * x / z + cx;
+    g.v = fy * y / z + cy;
+    // renderloss.py:155-167
+    double *R = g.R;
+    R[0] = 1 - 2 * (qy * qy + qz * qz);
+    R[1] = 2 * (qx * qy - qw * qz);
+    R[2] = 2 * (qx * qz + qw * qy);
+    R[3] = 2 * (qx * qy + qw * qz);
+    R[4] = 1 - 2 * (qx * qx + qz * qz);
+    R[5] = 2 * (qy * qz - qw * qx);
+    R[6] = 2 * (qx * qz - qw * qy);
+    R[7] = 2 * (qy * qz + qw * qx);
+    R[8] = 1 - 2 * (qx * qx + qy * qy);
+    g.s2[0] = sx * sx;
+    g.s2[1] = sy * sy;
+    g.s2[2] = sz * sz;
+    // M = W R where W = r_wc^T  (W_ij = rwc[j*3+i]);  Sc = M diag(s2) M^T
+    double M[9];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int k = 0; k < 3; k++)
+            M[i * 3 + k] = rwc[0 * 3 + i] * R[0 * 3 + k] + rwc[1 * 3 + i] * R[1 * 3 + k] +
+                           rwc[2 * 3 + i] * R[2 * 3 + k];
+    double S[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = i; j < 3; j++) {
+            double s = M[i * 3 + 0] * g.s2[0] * M[j * 3 + 0] + M[i * 3 + 1] * g.s2[1] * M[j * 3 + 1] +
+                       M[i * 3 + 2] * g.s2[2] * M[j * 3 + 2];
+            S[i][j] = s;
+            S[j][i] = s;
+        }
+    g.Sc[0] = S[0][0];
+    g.Sc[1] = S[0][1];
+    g.Sc[2] = S[0][2];
+    g.Sc[3] = S[1][1];
+    g.Sc[4] = S[1][2];
+    g.Sc[5] = S[2][2];
+    // J = [[fx/z, 0, -fx x/z^2], [0, fy/z, -fy y/z^2]]
+    const double j00 = fx / z, j02 = -fx * x / (z * z);
+    const double j11 = fy / z, j12 = -fy * y / (z * z);
+    // cov2 = J Sc J^T
+    const double a00 = j00 * S[0][0] + j02 * S[2][0];
+    const double a01 = j00 * S[0][1] + j02 * S[2][1];
+    const double a02 = j00 * S[0][2] + j02 * S[2][2];
+    const double b01 = j11 * S[1][0] + j12 * S[2][0];
+    const double b11 = j11 * S[1][1] + j12 * S[2][1];
+    const double b12 = j11 * S[1][2] + j12 * S[2][2];
+    g.a = a00 * j00 + a02 * j02 + 0.3;
+    g.b = a01 * j11 + a02 * j12;
+    g.c = b11 * j11 + b12 * j12 + 0.3;
+    (void)b01;
+}
+
+int render_forward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,
+                   const sm_render_dims &dims, void *ws, int64_t ws_bytes, float *out_rgb,
+                   float *out_depth, float *out_alpha, cudaStream_t st);
+int render_backward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,
+                    const sm_render_dims &dims, void *ws, int64_t ws_bytes, const float *d_rgb,
+                    const float *d_depth, const float *d_alpha, float *grads, cudaStream_t st);
+
+}  // namespace sm

@@ -1,0 +1,358 @@
+// K5 composite backward + K6 projection backward.
+//
+// The reference is forward-only (pkg/README.md:125-129); this is the exact
+// reverse-mode derivative of the forward in render_fwd.cu (itself the
+// restatement of renderloss.py:106-218), with the reference's semantics:
+// no alpha cap, T >= 1e-10 checked before a contribution, 3-sigma box,
+// q > 9 excluded, colour clip (zero gradient outside [0,1]), final rgb/alpha
+// clip, depth = D / alpha.  Oracle: oracle/render_oracle.c or_render_bwd,
+// pinned by central differences of the reference forward.
+//
+// Per pixel the contributors are revisited back to front.  T_k is recovered
+// as T_{k+1} / (1 - alpha_k) (the last contributor's T is stored, so
+// alpha = 1 never divides by zero), the colour/depth behind k is carried
+// normalised (B_k = alpha_{k+1} c_{k+1} + (1 - alpha_{k+1}) B_{k+1}) and
+// dA/dalpha_k uses the running product P_k = prod_{j>k} (1 - alpha_j).
+// Per-Gaussian sums: a 16-wide transposed butterfly (16 shuffles, one value
+// per lane pair) per warp, shared-memory atomics across the 8 warps of the
+// tile, one global atomic per (instance, value) per tile.
+#include "render.cuh"
+
+namespace sm {
+
+__device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const bool hi = lane & 16;
+        const float send = hi ? v[k] : v[k + 8];
+        const float keep = hi ? v[k + 8] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const bool hi = lane & 8;
+        const float send = hi ? v[k] : v[k + 4];
+        const float keep = hi ? v[k + 4] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        const bool hi = lane & 4;
+        const float send = hi ? v[k] : v[k + 2];
+        const float keep = hi ? v[k + 2] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    {
+        const bool hi = lane & 2;
+        const float send = hi ? v[0] : v[1];
+        const float keep = hi ? v[1] : v[0];
+        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+    return v[0];   // value index ((lane>>4)&1)*8 + ((lane>>3)&1)*4 + ((lane>>2)&1)*2 + ((lane>>1)&1)
+}
+
+__global__ void __launch_bounds__(kTilePx)
+composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ikeys,
+              uint32_t rank_mask, const ProjRec *__restrict__ recs,
+              const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
+              int height, int tiles_x, const float *__restrict__ d_rgb,
+              const float *__restrict__ d_depth, const float *__restrict__ d_alpha,
+              const float4 *__restrict__ st_cd, const float *__restrict__ st_t,
+              const float *__restrict__ st_tlast, const int32_t *__restrict__ st_last,
+              float *__restrict__ g2d) {
+    __shared__ ProjRec s_rec[kTilePx];
+    __shared__ uint32_t s_rank[kTilePx];
+    __shared__ float s_grad[kTilePx][10];
+    __shared__ int s_maxlast;
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int px = (tile % tiles_x) * kTile + (threadIdx.x & (kTile - 1));
+    const int py = (tile / tiles_x) * kTile + (threadIdx.x / kTile);
+    const bool inside = px < width && py < height;
+    const int start = (int)ranges[2 * tile];
+    float gCr = 0.f, gCg = 0.f, gCb = 0.f, gD = 0.f, gA = 0.f, T = 0.f, tlast = 0.f;
+    int last = -1;
+    if (inside) {
+        const int64_t p = (int64_t)py * width + px;
+        const float4 cd = st_cd[p];
+        T = st_t[p];
+        tlast = st_tlast[p];
+        last = st_last[p];
+        const float A = 1.f - T;
+        if (d_rgb) {
+            gCr = (cd.x >= 0.f && cd.x <= 1.f) ? d_rgb[3 * p + 0] : 0.f;
+            gCg = (cd.y >= 0.f && cd.y <= 1.f) ? d_rgb[3 * p + 1] : 0.f;
+            gCb = (cd.z >= 0.f && cd.z <= 1.f) ? d_rgb[3 * p + 2] : 0.f;
+        }
+        if (d_alpha && A >= 0.f && A <= 1.f) gA = d_alpha[p];
+        if (d_depth && A > 0.f) {
+            const float dd = d_depth[p];
+            gD = dd / A;
+            gA += -dd * cd.w / (A * A);
+        }
+    }
+    if (threadIdx.x == 0) s_maxlast = -1;
+    __syncthreads();
+    int wmax = last;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    if (lane == 0) atomicMax(&s_maxlast, wmax);
+    __syncthreads();
+    const int maxlast = s_maxlast;
+    float Br = 0.f, Bg = 0.f, Bb = 0.f, Bz = 0.f, P = 1.f;
+    for (int bend = maxlast + 1; bend > start; bend -= kTilePx) {
+        const int bstart = max(start, bend - kTilePx);
+        const int idx = bstart + (int)threadIdx.x;
+        if (idx < bend) {
+            const uint32_t rk = ikeys[idx] & rank_mask;
+            s_rank[threadIdx.x] = rk;
+            s_rec[threadIdx.x] = recs[rk];
+#pragma unroll
+            for (int k = 0; k < 10; k++) s_grad[threadIdx.x][k] = 0.f;
+        }
+        __syncthreads();
+        const int jtop = min(bend - 1, wmax) - bstart;
+        for (int j = jtop; j >= 0; j--) {
+            const ProjRec &g = s_rec[j];
+            const int k = bstart + j;
+            float v[16];
+#pragma unroll
+            for (int t = 0; t < 16; t++) v[t] = 0.f;
+            bool hit = false;
+            if (k <= last) {
+                const int x0 = rec_x0(g), y0 = rec_y0(g);
+                if ((unsigned)(px - x0) <= (unsigned)(rec_x1(g) - x0) &&
+                    (unsigned)(py - y0) <= (unsigned)(rec_y1(g) - y0)) {
+                    const float dx = (float)(px - x0) + g.ox;
+                    const float dy = (float)(py - y0) + g.oy;
+                    const float q = dx * (g.ia * dx + 2.f * g.ib * dy) + g.ic * dy * dy;
+                    const float dq = q - 9.f;
+                    bool over;
+                    if (fabsf(dq) <= g.eps)
+                        over = quad_q64(p64[order[s_rank[j]]], px, py) > 9.0;
+                    else
+                        over = dq > 0.f;
+                    if (!over) {
+                        hit = true;
+                        const float G = __expf(-0.5f * q);
+                        const float alpha = g.op * G;
+                        const float oma = 1.f - alpha;
+                        const float Tk = (k == last) ? tlast : T / oma;
+                        float ga = (g.r - Br) * gCr + (g.g - Bg) * gCg + (g.b - Bb) * gCb +
+                                   (g.z - Bz) * gD;
+                        ga = Tk * (ga + gA * P);
+                        const float wt = Tk * alpha;
+                        v[6] = wt * gCr;
+                        v[7] = wt * gCg;
+                        v[8] = wt * gCb;
+                        v[9] = wt * gD;
+                        v[5] = ga * G;
+                        const float gq = -0.5f * alpha * ga;
+                        v[2] = gq * dx * dx;
+                        v[3] = gq * 2.f * dx * dy;
+                        v[4] = gq * dy * dy;
+                        v[0] = -gq * (2.f * g.ia * dx + 2.f * g.ib * dy);
+                        v[1] = -gq * (2.f * g.ib * dx + 2.f * g.ic * dy);
+                        Br = alpha * g.r + oma * Br;
+                        Bg = alpha * g.g + oma * Bg;
+                        Bb = alpha * g.b + oma * Bb;
+                        Bz = alpha * g.z + oma * Bz;
+                        P *= oma;
+                        T = Tk;
+                    }
+                }
+            }
+            if (__any_sync(0xffffffffu, hit)) {
+                const float s = transpose_reduce16(v, lane);
+                const int vi = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
+                               ((lane >> 1) & 1);
+                if (!(lane & 1) && vi < 10 && s != 0.f) atomicAdd(&s_grad[j][vi], s);
+            }
+        }
+        __syncthreads();
+        if (idx < bend) {
+            float *dst = g2d + (int64_t)s_rank[threadIdx.x] * kG2dStride;
+#pragma unroll
+            for (int k = 0; k < 10; k++) {
+                const float s = s_grad[threadIdx.x][k];
+                if (s != 0.f) atomicAdd(dst + k, s);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+struct CamBwd {
+    double r[9];
+    double t[3];
+    double fx, fy, cx, cy;
+};
+
+// K6: per depth rank, chain the 2D grads through the fp64 projection and
+// accumulate the 14 parameter grads into the slot-indexed grad records.
+__global__ void __launch_bounds__(256)
+project_bwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots, int64_t n,
+            CamBwd cam, const uint32_t *__restrict__ order, const uint32_t *__restrict__ tcount_r,
+            const float *__restrict__ g2d, float *__restrict__ grads) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n || tcount_r[r] == 0) return;
+    const uint32_t i = order[r];
+    const int64_t slot = slots ? (int64_t)slots[i] : (int64_t)i;
+    const float4 A = params[slot * 4 + 0];
+    const float4 B = params[slot * 4 + 1];
+    const float4 C = params[slot * 4 + 2];
+    const float4 D = params[slot * 4 + 3];
+    const float *gk = g2d + r * kG2dStride;
+    const double gu = gk[0], gv = gk[1], gia = gk[2], gib = gk[3], gic = gk[4], gop = gk[5];
+    const double gcol[3] = {gk[6], gk[7], gk[8]};
+    const double gdep = gk[9];
+    ProjGeom g;
+    const double qw = A.w, qx = B.x, qy = B.y, qz = B.z;
+    const double s[3] = {B.w, C.x, C.y};
+    project_geometry(A.x, A.y, A.z, qw, qx, qy, qz, s[0], s[1], s[2], cam.r, cam.t, cam.fx, cam.fy,
+                     cam.cx, cam.cy, g);
+    const double fx = cam.fx, fy = cam.fy;
+    const double x = g.x, y = g.y, z = g.z;
+    // colour
+    const double sh[3] = {C.w, D.x, D.y};
+    double gsh[3];
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        const double raw = SM_SH_C0 * sh[k] + 0.5;
+        gsh[k] = (raw >= 0.0 && raw <= 1.0) ? SM_SH_C0 * gcol[k] : 0.0;
+    }
+    // conic -> (a, b, c)
+    const double a = g.a, b = g.b, c = g.c;
+    const double det = a * c - b * b, d2 = det * det;
+    const double ga_ = gia * (-c * c / d2) + gib * (b * c / d2) + gic * (-b * b / d2);
+    const double gb_ = gia * (2.0 * b * c / d2) + gib * (-1.0 / det - 2.0 * b * b / d2) +
+                       gic * (2.0 * a * b / d2);
+    const double gc_ = gia * (-b * b / d2) + gib * (a * b / d2) + gic * (-a * a / d2);
+    const double G2[4] = {ga_, 0.5 * gb_, 0.5 * gb_, gc_};
+    const double J[6] = {fx / z, 0.0, -fx * x / (z * z), 0.0, fy / z, -fy * y / (z * z)};
+    const double Sc[9] = {g.Sc[0], g.Sc[1], g.Sc[2], g.Sc[1], g.Sc[3], g.Sc[4], g.Sc[2], g.Sc[4], g.Sc[5]};
+    double G2J[6];
+#pragma unroll
+    for (int i2 = 0; i2 < 2; i2++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) G2J[i2 * 3 + j] = G2[i2 * 2 + 0] * J[j] + G2[i2 * 2 + 1] * J[3 + j];
+    double gSc[9];
+#pragma unroll
+    for (int rr = 0; rr < 3; rr++)
+#pragma unroll
+        for (int cc = 0; cc < 3; cc++) gSc[rr * 3 + cc] = J[rr] * G2J[cc] + J[3 + rr] * G2J[3 + cc];
+    double gJ[6];
+#pragma unroll
+    for (int i2 = 0; i2 < 2; i2++)
+#pragma unroll
+        for (int j = 0; j < 3; j++)
+            gJ[i2 * 3 + j] = 2.0 * (G2J[i2 * 3 + 0] * Sc[j] + G2J[i2 * 3 + 1] * Sc[3 + j] +
+                                    G2J[i2 * 3 + 2] * Sc[6 + j]);
+    double gx = gu * fx / z, gy = gv * fy / z;
+    double gz = gu * (-fx * x / (z * z)) + gv * (-fy * y / (z * z)) + gdep;
+    gz += gJ[0] * (-fx / (z * z));
+    gx += gJ[2] * (-fx / (z * z));
+    gz += gJ[2] * (2.0 * fx * x / (z * z * z));
+    gz += gJ[4] * (-fy / (z * z));
+    gy += gJ[5] * (-fy / (z * z));
+    gz += gJ[5] * (2.0 * fy * y / (z * z * z));
+    const double *rw = cam.r;
+    double gpos[3];
+#pragma unroll
+    for (int k = 0; k < 3; k++) gpos[k] = rw[k * 3 + 0] * gx + rw[k * 3 + 1] * gy + rw[k * 3 + 2] * gz;
+    // gSw = r_wc gSc r_wc^T
+    double T1[9], gSw[9];
+#pragma unroll
+    for (int i2 = 0; i2 < 3; i2++)
+#pragma unroll
+        for (int j = 0; j < 3; j++)
+            T1[i2 * 3 + j] = rw[i2 * 3 + 0] * gSc[0 * 3 + j] + rw[i2 * 3 + 1] * gSc[1 * 3 + j] +
+                             rw[i2 * 3 + 2] * gSc[2 * 3 + j];
+#pragma unroll
+    for (int i2 = 0; i2 < 3; i2++)
+#pragma unroll
+        for (int j = 0; j < 3; j++)
+            gSw[i2 * 3 + j] = T1[i2 * 3 + 0] * rw[j * 3 + 0] + T1[i2 * 3 + 1] * rw[j * 3 + 1] +
+                              T1[i2 * 3 + 2] * rw[j * 3 + 2];
+    const double *R = g.R;
+    double gR[9], gsc[3];
+#pragma unroll
+    for (int k2 = 0; k2 < 3; k2++) {
+        double acc = 0.0;
+#pragma unroll
+        for (int rr = 0; rr < 3; rr++) {
+            double col = gSw[rr * 3 + 0] * R[0 * 3 + k2] + gSw[rr * 3 + 1] * R[1 * 3 + k2] +
+                         gSw[rr * 3 + 2] * R[2 * 3 + k2];
+            gR[rr * 3 + k2] = 2.0 * col * g.s2[k2];
+            acc += R[rr * 3 + k2] * col;
+        }
+        gsc[k2] = 2.0 * s[k2] * acc;
+    }
+    const double gw = 2.0 * (-qz * gR[1] + qy * gR[2] + qz * gR[3] - qx * gR[5] - qy * gR[6] + qx * gR[7]);
+    const double gqx = 2.0 * (qy * gR[1] + qz * gR[2] + qy * gR[3] - 2.0 * qx * gR[4] - qw * gR[5] +
+                              qz * gR[6] + qw * gR[7] - 2.0 * qx * gR[8]);
+    const double gqy = 2.0 * (-2.0 * qy * gR[0] + qx * gR[1] + qw * gR[2] + qx * gR[3] + qz * gR[5] -
+                              qw * gR[6] + qz * gR[7] - 2.0 * qy * gR[8]);
+    const double gqz = 2.0 * (-2.0 * qz * gR[0] - qw * gR[1] + qx * gR[2] + qw * gR[3] -
+                              2.0 * qz * gR[4] + qy * gR[5] + qx * gR[6] + qy * gR[7]);
+    float4 *dst = reinterpret_cast<float4 *>(grads) + slot * 4;
+    float4 o0 = dst[0], o1 = dst[1], o2 = dst[2], o3 = dst[3];
+    o0.x += (float)gpos[0];
+    o0.y += (float)gpos[1];
+    o0.z += (float)gpos[2];
+    o0.w += (float)gw;
+    o1.x += (float)gqx;
+    o1.y += (float)gqy;
+    o1.z += (float)gqz;
+    o1.w += (float)gsc[0];
+    o2.x += (float)gsc[1];
+    o2.y += (float)gsc[2];
+    o2.z += (float)gop;
+    o2.w += (float)gsh[0];
+    o3.x += (float)gsh[1];
+    o3.y += (float)gsh[2];
+    dst[0] = o0;
+    dst[1] = o1;
+    dst[2] = o2;
+    dst[3] = o3;
+}
+
+int render_backward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,
+                    const sm_render_dims &dims, void *ws, int64_t ws_bytes, const float *d_rgb,
+                    const float *d_depth, const float *d_alpha, float *grads, cudaStream_t st) {
+    const RenderLayout L = render_layout(dims);
+    if (ws_bytes < L.total) {
+        set_error("render workspace too small: %lld < %lld", (long long)ws_bytes, (long long)L.total);
+        return SM_ERR_WORKSPACE;
+    }
+    if (n < 0 || n > dims.max_gaussians) {
+        set_error("n=%lld outside [0, max_gaussians]", (long long)n);
+        return SM_ERR_INVALID;
+    }
+    if (cam.width != dims.width || cam.height != dims.height) {
+        set_error("camera does not match workspace");
+        return SM_ERR_DIMENSION;
+    }
+    if (n == 0) return SM_OK;
+    RenderBufs b = render_bufs(ws, L);
+    cudaMemsetAsync(b.g2d, 0, n * (int64_t)sizeof(float) * kG2dStride, st);
+    const uint32_t rank_mask = (uint32_t)((1ull << L.rank_bits) - 1ull);
+    composite_bwd<<<(unsigned)L.n_tiles, kTilePx, 0, st>>>(
+        b.ranges, L.tile_passes & 1 ? b.ikey1 : b.ikey0, rank_mask, b.rec_sorted, b.p64, b.order0,
+        dims.width, dims.height, L.tiles_x, d_rgb, d_depth, d_alpha, b.pix_cd, b.pix_t, b.pix_tlast,
+        b.pix_last, b.g2d);
+    CamBwd cb;
+    for (int k = 0; k < 9; k++) cb.r[k] = cam.r_wc[k];
+    for (int k = 0; k < 3; k++) cb.t[k] = cam.t[k];
+    cb.fx = cam.fx;
+    cb.fy = cam.fy;
+    cb.cx = cam.cx;
+    cb.cy = cam.cy;
+    project_bwd<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+        reinterpret_cast<const float4 *>(params), slots, n, cb, b.order0, b.tcount_r, b.g2d, grads);
+    SM_CHECK_LAUNCH("render_backward");
+    return SM_OK;
+}
+
+}  // namespace sm

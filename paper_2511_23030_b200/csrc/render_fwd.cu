@@ -1,0 +1,355 @@
+// K2 projection, K3 depth order + tile binning, K4 front-to-back compositing.
+//
+// Restates renderloss.render_arrays (renderloss.py:170-218) and the numba
+// _composite kernel (renderloss.py:106-152) for sm_100a:
+//   * projection in fp64 (it is HBM-bound: 64 B/Gaussian in, 104 B out), so
+//     means, conics and the 3-sigma bboxes are the reference's own numbers;
+//   * one global stable radix sort of the visible Gaussians on the fp64 bit
+//     pattern of z (z >= near > 0, so bits order like values) = np.argsort(z,
+//     kind="stable") over the sorted-chunk-id concatenation;
+//   * instances are emitted in depth-rank order and radix-sorted on the tile
+//     bits only (stable), giving each 16x16 tile its Gaussians front to back;
+//   * compositing in fp32 with the q > 9 decision taken in fp64 whenever the
+//     fp32 q lies within a per-Gaussian error band of 9.
+#include <cstdio>
+
+#include "render.cuh"
+#include "sort.cuh"
+
+namespace sm {
+
+// ---------------------------------------------------------------- layout
+RenderLayout render_layout(const sm_render_dims &d) {
+    RenderLayout L;
+    const int64_t G = d.max_gaussians > 0 ? d.max_gaussians : 1;
+    const int64_t I = d.max_instances > 0 ? d.max_instances : 1;
+    L.tiles_x = (int)ceil_div(d.width, kTile);
+    L.tiles_y = (int)ceil_div(d.height, kTile);
+    L.n_tiles = (int64_t)L.tiles_x * L.tiles_y;
+    const int64_t npx = (int64_t)d.width * d.height;
+    int rb = 1;
+    while ((1ll << rb) < G) rb++;
+    int tb = 1;
+    while ((1ll << tb) < L.n_tiles) tb++;
+    L.rank_bits = rb;
+    L.tile_bits = tb;
+    L.depth_passes = ceil_div(64, kRadixBits);
+    L.tile_passes = (int)ceil_div(tb, kRadixBits);
+    L.sort_blocks = ceil_div(G > I ? G : I, kSortTile);
+    int64_t off = 0;
+    auto take = [&](int64_t bytes) {
+        int64_t o = off;
+        off += align_up(bytes > 0 ? bytes : 1, 256);
+        return o;
+    };
+    L.o_counters = take(sizeof(sm_render_counters));
+    L.o_rec = take(G * (int64_t)sizeof(ProjRec));
+    L.o_rec_sorted = take(G * (int64_t)sizeof(ProjRec));
+    L.o_p64 = take(G * (int64_t)sizeof(Proj64));
+    L.o_dkey0 = take(G * 8);
+    L.o_dkey1 = take(G * 8);
+    L.o_order0 = take(G * 4);
+    L.o_order1 = take(G * 4);
+    L.o_tcount = take(G * 4);
+    L.o_tcount_r = take(G * 4);
+    L.o_toff = take(G * 4);
+    L.o_ikey0 = take(I * 4);
+    L.o_ikey1 = take(I * 4);
+    L.o_ranges = take(L.n_tiles * 8);
+    L.o_pix_cd = take(npx * 16);
+    L.o_pix_t = take(npx * 4);
+    L.o_pix_tlast = take(npx * 4);
+    L.o_pix_last = take(npx * 4);
+    L.o_g2d = take(G * (int64_t)sizeof(float) * kG2dStride);
+    L.o_sort_hist = take(sort_scratch_bytes(G > I ? G : I));
+    L.o_scan = take(scan_scratch_bytes(G));
+    L.total = off;
+    return L;
+}
+
+// ------------------------------------------------------------- projection
+struct CamDev {
+    double r[9];
+    double t[3];
+    double fx, fy, cx, cy, near_plane;
+    int width, height, tiles_x, tiles_y;
+};
+
+__global__ void __launch_bounds__(256)
+project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots, int64_t n,
+            CamDev cam, ProjRec *__restrict__ rec, Proj64 *__restrict__ p64,
+            unsigned long long *__restrict__ dkey, uint32_t *__restrict__ order,
+            uint32_t *__restrict__ tcount) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t slot = slots ? (int64_t)slots[i] : i;
+    const float4 A = params[slot * 4 + 0];   // px py pz qw
+    const float4 B = params[slot * 4 + 1];   // qx qy qz sx
+    const float4 C = params[slot * 4 + 2];   // sy sz op sh0r
+    const float4 D = params[slot * 4 + 3];   // sh0g sh0b - -
+    order[i] = (uint32_t)i;
+    ProjGeom g;
+    project_geometry((double)A.x, (double)A.y, (double)A.z, (double)A.w, (double)B.x,
+                     (double)B.y, (double)B.z, (double)B.w, (double)C.x, (double)C.y, cam.r,
+                     cam.t, cam.fx, cam.fy, cam.cx, cam.cy, g);
+    if (!(g.z >= cam.near_plane)) {   // renderloss.py:179 keep = z >= near
+        dkey[i] = ~0ull;
+        tcount[i] = 0;
+        return;
+    }
+    dkey[i] = (unsigned long long)__double_as_longlong(g.z);
+    // renderloss.py:110-135: conic and clamped 3-sigma bbox (fp64)
+    const double a = g.a, b = g.b, c = g.c;
+    const double det = a * c - b * b;
+    ProjRec r;
+    r.op = C.z;
+    r.z = (float)g.z;
+    const double sh[3] = {(double)C.w, (double)D.x, (double)D.y};
+    float col[3];
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        double v = SM_SH_C0 * sh[k] + 0.5;
+        col[k] = (float)(v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v));
+    }
+    r.r = col[0];
+    r.g = col[1];
+    r.b = col[2];
+    r.spare[0] = r.spare[1] = r.spare[2] = 0.f;
+    if (det <= 0.0 || a <= 0.0 || c <= 0.0) {
+        tcount[i] = 0;
+        r.x0y0 = 0;
+        r.x1y1 = (int32_t)0xffffffff;   // empty box
+        r.ox = r.oy = r.ia = r.ib = r.ic = r.eps = 0.f;
+        rec[i] = r;
+        return;
+    }
+    const double ia = c / det, ib = -b / det, ic = a / det;
+    const double rx = 3.0 * sqrt(a), ry = 3.0 * sqrt(c);
+    double fx0 = ceil(g.u - rx), fx1 = floor(g.u + rx);
+    double fy0 = ceil(g.v - ry), fy1 = floor(g.v + ry);
+    fx0 = fmin(fmax(fx0, 0.0), (double)cam.width);
+    fy0 = fmin(fmax(fy0, 0.0), (double)cam.height);
+    fx1 = fmax(fmin(fx1, (double)(cam.width - 1)), -1.0);
+    fy1 = fmax(fmin(fy1, (double)(cam.height - 1)), -1.0);
+    const int x0 = (int)fx0, x1 = (int)fx1, y0 = (int)fy0, y1 = (int)fy1;
+    r.ox = (float)((double)x0 - g.u);
+    r.oy = (float)((double)y0 - g.v);
+    r.ia = (float)ia;
+    r.ib = (float)ib;
+    r.ic = (float)ic;
+    // fp32 q error bound near q = 9 scales with K = ac/det (anisotropy).
+    const double K = a * c / det;
+    r.eps = (float)(1e-4 * (1.0 + K));
+    r.x0y0 = (int32_t)(((uint32_t)y0 << 16) | ((uint32_t)x0 & 0xffffu));
+    r.x1y1 = (int32_t)(((uint32_t)(y1 & 0xffff) << 16) | ((uint32_t)x1 & 0xffffu));
+    rec[i] = r;
+    Proj64 q;
+    q.u = g.u;
+    q.v = g.v;
+    q.ia = ia;
+    q.ib = ib;
+    q.ic = ic;
+    p64[i] = q;
+    if (x1 < x0 || y1 < y0) {
+        tcount[i] = 0;
+        return;
+    }
+    const int tx0 = x0 / kTile, tx1 = x1 / kTile, ty0 = y0 / kTile, ty1 = y1 / kTile;
+    tcount[i] = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+}
+
+__global__ void __launch_bounds__(256)
+gather_by_rank(const uint32_t *__restrict__ order, int64_t n, const ProjRec *__restrict__ rec,
+               const uint32_t *__restrict__ tcount, ProjRec *__restrict__ rec_sorted,
+               uint32_t *__restrict__ tcount_r) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint32_t i = order[r];
+    const uint32_t c = tcount[i];
+    tcount_r[r] = c;
+    if (c) rec_sorted[r] = rec[i];
+}
+
+__global__ void check_instances(sm_render_counters *ctr, int64_t max_instances) {
+    const uint32_t n = ctr->n_instances;
+    const bool of = (int64_t)n > max_instances;
+    ctr->overflow = of ? 1u : 0u;
+    ctr->reserved[0] = of ? 0u : n;   // count the sort / ranges see
+}
+
+__global__ void __launch_bounds__(256)
+emit_instances(const ProjRec *__restrict__ rec_sorted, const uint32_t *__restrict__ tcount_r,
+               const uint32_t *__restrict__ toff, int64_t n, const sm_render_counters *ctr,
+               int rank_bits, int tiles_x, uint32_t *__restrict__ ikeys) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n || ctr->overflow) return;
+    const uint32_t cnt = tcount_r[r];
+    if (!cnt) return;
+    const ProjRec g = rec_sorted[r];
+    const int tx0 = rec_x0(g) / kTile, tx1 = rec_x1(g) / kTile;
+    const int ty0 = rec_y0(g) / kTile, ty1 = rec_y1(g) / kTile;
+    uint32_t o = toff[r];
+    for (int ty = ty0; ty <= ty1; ty++)
+        for (int tx = tx0; tx <= tx1; tx++)
+            ikeys[o++] = ((uint32_t)(ty * tiles_x + tx) << rank_bits) | (uint32_t)r;
+}
+
+__global__ void __launch_bounds__(256)
+tile_ranges(const uint32_t *__restrict__ ikeys, const sm_render_counters *ctr, int rank_bits,
+            uint32_t *__restrict__ ranges) {
+    const int64_t n = ctr->reserved[0];
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const uint32_t t = ikeys[p] >> rank_bits;
+    if (p == 0 || (ikeys[p - 1] >> rank_bits) != t) ranges[2 * t] = (uint32_t)p;
+    if (p == n - 1 || (ikeys[p + 1] >> rank_bits) != t) ranges[2 * t + 1] = (uint32_t)(p + 1);
+}
+
+// ------------------------------------------------------------ compositing
+__global__ void __launch_bounds__(kTilePx)
+composite_fwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ikeys,
+              uint32_t rank_mask, const ProjRec *__restrict__ recs,
+              const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
+              int height, int tiles_x, float *__restrict__ out_rgb, float *__restrict__ out_depth,
+              float *__restrict__ out_alpha, float4 *__restrict__ st_cd, float *__restrict__ st_t,
+              float *__restrict__ st_tlast, int32_t *__restrict__ st_last) {
+    __shared__ ProjRec s_rec[kTilePx];
+    __shared__ uint32_t s_rank[kTilePx];
+    const int tile = blockIdx.x;
+    const int px = (tile % tiles_x) * kTile + (threadIdx.x & (kTile - 1));
+    const int py = (tile / tiles_x) * kTile + (threadIdx.x / kTile);
+    const bool inside = px < width && py < height;
+    const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
+    float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f, cd = 0.f, tlast = 1.f;
+    int32_t last = -1;
+    bool done = !inside;
+    for (uint32_t base = start; base < end; base += kTilePx) {
+        if (__syncthreads_count(done) == kTilePx) break;
+        const uint32_t idx = base + threadIdx.x;
+        if (idx < end) {
+            const uint32_t rk = ikeys[idx] & rank_mask;
+            s_rank[threadIdx.x] = rk;
+            s_rec[threadIdx.x] = recs[rk];
+        }
+        __syncthreads();
+        const int cnt = (int)min((uint32_t)kTilePx, end - base);
+        if (!done) {
+            for (int j = 0; j < cnt; j++) {
+                const ProjRec &g = s_rec[j];
+                const int x0 = rec_x0(g), y0 = rec_y0(g);
+                if ((unsigned)(px - x0) > (unsigned)(rec_x1(g) - x0) ||
+                    (unsigned)(py - y0) > (unsigned)(rec_y1(g) - y0))
+                    continue;
+                const float dx = (float)(px - x0) + g.ox;
+                const float dy = (float)(py - y0) + g.oy;
+                const float q = dx * (g.ia * dx + 2.f * g.ib * dy) + g.ic * dy * dy;
+                const float dq = q - 9.f;
+                bool over;
+                if (fabsf(dq) <= g.eps)
+                    over = quad_q64(p64[order[s_rank[j]]], px, py) > 9.0;
+                else
+                    over = dq > 0.f;
+                if (over) continue;
+                const float alpha = g.op * __expf(-0.5f * q);
+                const float w = T * alpha;
+                cr += w * g.r;
+                cg += w * g.g;
+                cb += w * g.b;
+                cd += w * g.z;
+                tlast = T;
+                last = (int32_t)(base + j);
+                T = T * (1.f - alpha);
+                if (T < (float)SM_MIN_T) {
+                    done = true;
+                    break;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (!inside) return;
+    const int64_t p = (int64_t)py * width + px;
+    // renderloss.py:216-218 finalize
+    const float A = 1.f - T;
+    out_rgb[3 * p + 0] = fminf(fmaxf(cr, 0.f), 1.f);
+    out_rgb[3 * p + 1] = fminf(fmaxf(cg, 0.f), 1.f);
+    out_rgb[3 * p + 2] = fminf(fmaxf(cb, 0.f), 1.f);
+    out_depth[p] = A > 0.f ? cd / A : 0.f;
+    out_alpha[p] = fminf(fmaxf(A, 0.f), 1.f);
+    st_cd[p] = make_float4(cr, cg, cb, cd);
+    st_t[p] = T;
+    st_tlast[p] = tlast;
+    st_last[p] = last;
+}
+
+CamDev make_cam(const sm_camera &c, const RenderLayout &L) {
+    CamDev d;
+    for (int k = 0; k < 9; k++) d.r[k] = c.r_wc[k];
+    for (int k = 0; k < 3; k++) d.t[k] = c.t[k];
+    d.fx = c.fx;
+    d.fy = c.fy;
+    d.cx = c.cx;
+    d.cy = c.cy;
+    d.near_plane = c.near_plane;
+    d.width = c.width;
+    d.height = c.height;
+    d.tiles_x = L.tiles_x;
+    d.tiles_y = L.tiles_y;
+    return d;
+}
+
+int render_forward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,
+                   const sm_render_dims &dims, void *ws, int64_t ws_bytes, float *out_rgb,
+                   float *out_depth, float *out_alpha, cudaStream_t st) {
+    const RenderLayout L = render_layout(dims);
+    if (ws_bytes < L.total) {
+        set_error("render workspace too small: %lld < %lld", (long long)ws_bytes, (long long)L.total);
+        return SM_ERR_WORKSPACE;
+    }
+    if (n < 0 || n > dims.max_gaussians) {
+        set_error("n=%lld outside [0, max_gaussians=%lld]", (long long)n, (long long)dims.max_gaussians);
+        return SM_ERR_INVALID;
+    }
+    if (cam.width != dims.width || cam.height != dims.height || cam.width < 1 || cam.height < 1) {
+        set_error("camera %dx%d does not match workspace %dx%d", cam.width, cam.height, dims.width,
+                  dims.height);
+        return SM_ERR_DIMENSION;
+    }
+    if (L.rank_bits + L.tile_bits > 32) {
+        set_error("rank bits %d + tile bits %d exceed 32", L.rank_bits, L.tile_bits);
+        return SM_ERR_INVALID;
+    }
+    RenderBufs b = render_bufs(ws, L);
+    CamDev cd = make_cam(cam, L);
+    cudaMemsetAsync(b.ctr, 0, sizeof(sm_render_counters), st);
+    cudaMemsetAsync(b.ranges, 0, L.n_tiles * 8, st);
+    if (n > 0) {
+        const unsigned gb = (unsigned)ceil_div(n, 256);
+        project_fwd<<<gb, 256, 0, st>>>(reinterpret_cast<const float4 *>(params), slots, n, cd,
+                                        b.rec, b.p64, b.dkey0, b.order0, b.tcount);
+        SortScratch ss{b.sort_hist, b.sort_hist + (int64_t)kRadix * L.sort_blocks, L.sort_blocks};
+        // global stable depth order (8 passes over the 64-bit key -> buffer 0)
+        radix_sort<unsigned long long, true>(b.dkey0, b.order0, b.dkey1, b.order1, nullptr, n, n, 0,
+                                             64, ss, st);
+        gather_by_rank<<<gb, 256, 0, st>>>(b.order0, n, b.rec, b.tcount, b.rec_sorted, b.tcount_r);
+        exclusive_scan(b.tcount_r, b.toff, n, b.scan, &b.ctr->n_instances, st);
+        check_instances<<<1, 1, 0, st>>>(b.ctr, dims.max_instances);
+        emit_instances<<<gb, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.toff, n, b.ctr, L.rank_bits,
+                                           L.tiles_x, b.ikey0);
+        const int cur = radix_sort<uint32_t, false>(
+            b.ikey0, nullptr, b.ikey1, nullptr, &b.ctr->reserved[0], 0, dims.max_instances,
+            L.rank_bits, L.rank_bits + L.tile_bits, ss, st);
+        uint32_t *ik = cur ? b.ikey1 : b.ikey0;
+        tile_ranges<<<(unsigned)ceil_div(dims.max_instances > 0 ? dims.max_instances : 1, 256), 256, 0,
+                      st>>>(ik, b.ctr, L.rank_bits, b.ranges);
+    }
+    const uint32_t rank_mask = (uint32_t)((1ull << L.rank_bits) - 1ull);
+    composite_fwd<<<(unsigned)L.n_tiles, kTilePx, 0, st>>>(
+        b.ranges, L.tile_passes & 1 ? b.ikey1 : b.ikey0, rank_mask, b.rec_sorted, b.p64, b.order0,
+        dims.width, dims.height, L.tiles_x, out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t,
+        b.pix_tlast, b.pix_last);
+    SM_CHECK_LAUNCH("render_forward");
+    return SM_OK;
+}
+
+}  // namespace sm

@@ -1,0 +1,323 @@
+// K1 chunk culling + active-set expansion, K7 fused Adam, K8/K9 chunk codec,
+// and the bit-exact chunk-id encoder.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace sm {
+
+// ------------------------------------------------------------------ K7
+struct AdamDev {
+    float lr[14];
+    float b1, b2, eps, min_scale;
+};
+
+__global__ void __launch_bounds__(256)
+adam_kernel(float4 *__restrict__ params, float4 *__restrict__ m, float4 *__restrict__ v,
+            float4 *__restrict__ grads, const int32_t *__restrict__ slots, int64_t n, AdamDev c,
+            const uint32_t *__restrict__ skip) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (skip && *skip) return;
+    const int64_t s = slots ? (int64_t)slots[i] : i;
+    float p[16], g[16], mm[16], vv[16];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const float4 a = params[s * 4 + k], b = grads[s * 4 + k], cm = m[s * 4 + k], cv = v[s * 4 + k];
+        p[4 * k] = a.x, p[4 * k + 1] = a.y, p[4 * k + 2] = a.z, p[4 * k + 3] = a.w;
+        g[4 * k] = b.x, g[4 * k + 1] = b.y, g[4 * k + 2] = b.z, g[4 * k + 3] = b.w;
+        mm[4 * k] = cm.x, mm[4 * k + 1] = cm.y, mm[4 * k + 2] = cm.z, mm[4 * k + 3] = cm.w;
+        vv[4 * k] = cv.x, vv[4 * k + 1] = cv.y, vv[4 * k + 2] = cv.z, vv[4 * k + 3] = cv.w;
+    }
+    const float step = mm[14] + 1.f;   // per-Gaussian step count
+    mm[14] = step;
+    const float bc1 = 1.f - powf(c.b1, step);
+    const float bc2s = sqrtf(1.f - powf(c.b2, step));
+#pragma unroll
+    for (int k = 0; k < 14; k++) {
+        mm[k] = c.b1 * mm[k] + (1.f - c.b1) * g[k];
+        vv[k] = c.b2 * vv[k] + (1.f - c.b2) * g[k] * g[k];
+        p[k] -= (c.lr[k] / bc1) * mm[k] / (sqrtf(vv[k]) / bc2s + c.eps);
+    }
+    // store invariants (core.py:186-190): unit quaternion, scale > 0, opacity in [0,1]
+    const float qn = sqrtf(p[3] * p[3] + p[4] * p[4] + p[5] * p[5] + p[6] * p[6]);
+    if (qn > 0.f) {
+        const float inv = 1.f / qn;
+        p[3] *= inv, p[4] *= inv, p[5] *= inv, p[6] *= inv;
+    } else {
+        p[3] = 1.f, p[4] = p[5] = p[6] = 0.f;
+    }
+    p[7] = fmaxf(p[7], c.min_scale);
+    p[8] = fmaxf(p[8], c.min_scale);
+    p[9] = fmaxf(p[9], c.min_scale);
+    p[10] = fminf(fmaxf(p[10], 0.f), 1.f);
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        params[s * 4 + k] = make_float4(p[4 * k], p[4 * k + 1], p[4 * k + 2], p[4 * k + 3]);
+        m[s * 4 + k] = make_float4(mm[4 * k], mm[4 * k + 1], mm[4 * k + 2], mm[4 * k + 3]);
+        v[s * 4 + k] = make_float4(vv[4 * k], vv[4 * k + 1], vv[4 * k + 2], vv[4 * k + 3]);
+        grads[s * 4 + k] = z;
+    }
+}
+
+int adam_step(float *params, float *m, float *v, float *grads, const int32_t *slots, int64_t n,
+              const sm_adam_config &cfg, const uint32_t *skip, cudaStream_t st) {
+    if (n < 0) {
+        set_error("negative n");
+        return SM_ERR_INVALID;
+    }
+    if (n == 0) return SM_OK;
+    AdamDev d;
+    for (int k = 0; k < 14; k++) d.lr[k] = cfg.lr[k];
+    d.b1 = cfg.beta1;
+    d.b2 = cfg.beta2;
+    d.eps = cfg.eps;
+    d.min_scale = cfg.min_scale;
+    adam_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+        reinterpret_cast<float4 *>(params), reinterpret_cast<float4 *>(m),
+        reinterpret_cast<float4 *>(v), reinterpret_cast<float4 *>(grads), slots, n, d, skip);
+    SM_CHECK_LAUNCH("adam_step");
+    return SM_OK;
+}
+
+// ------------------------------------------------------------------ K1
+struct CullDev {
+    double planes[24];
+    double cam[3];
+    double maxd, s, half;
+};
+
+// culling.py:104-131 in fp64 with every op rounded separately (the reference
+// evaluates these with NumPy scalars, one rounding per operation).
+__global__ void __launch_bounds__(256)
+cull_kernel(const int32_t *__restrict__ coords, int64_t n, CullDev c, uint8_t *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double mn[3], mx[3];
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        const double ctr = __dmul_rn((double)coords[3 * i + k], c.s);   // grid.py:106
+        mn[k] = __dsub_rn(ctr, c.half);
+        mx[k] = __dadd_rn(ctr, c.half);
+    }
+    // _nearest_distance: || p - clip(p, min, max) ||
+    double d2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        const double nearest = fmin(fmax(c.cam[k], mn[k]), mx[k]);
+        const double d = __dsub_rn(c.cam[k], nearest);
+        d2 = __dadd_rn(d2, __dmul_rn(d, d));
+    }
+    bool vis = !(__dsqrt_rn(d2) > c.maxd);
+    // aabb_in_frustum p-vertex OUTSIDE test
+#pragma unroll
+    for (int pl = 0; pl < 6; pl++) {
+        const double nx = c.planes[4 * pl], ny = c.planes[4 * pl + 1], nz = c.planes[4 * pl + 2],
+                     d = c.planes[4 * pl + 3];
+        const double px = nx >= 0 ? mx[0] : mn[0];
+        const double py = ny >= 0 ? mx[1] : mn[1];
+        const double pz = nz >= 0 ? mx[2] : mn[2];
+        const double val =
+            __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(nx, px), __dmul_rn(ny, py)), __dmul_rn(nz, pz)), d);
+        if (val < 0.0) vis = false;
+    }
+    out[i] = vis ? 1 : 0;
+}
+
+int cull_chunks(const int32_t *coords, int64_t n, const double *planes, const double *cam,
+                double maxd, double s, uint8_t *out, cudaStream_t st) {
+    if (n < 0 || s <= 0) {
+        set_error("bad cull arguments");
+        return SM_ERR_INVALID;
+    }
+    if (n == 0) return SM_OK;
+    CullDev c;
+    for (int k = 0; k < 24; k++) c.planes[k] = planes[k];
+    for (int k = 0; k < 3; k++) c.cam[k] = cam[k];
+    c.maxd = maxd;
+    c.s = s;
+    c.half = s / 2.0;
+    cull_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(coords, n, c, out);
+    SM_CHECK_LAUNCH("cull_chunks");
+    return SM_OK;
+}
+
+// grid.py:110-121 encode_positions: floor((p + s/2) / s) per axis in fp64.
+__global__ void __launch_bounds__(256)
+encode_kernel(const float *__restrict__ params, int64_t n, double s, double half,
+              unsigned long long *__restrict__ ids, unsigned long long *__restrict__ err) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    unsigned long long id = 0;
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        const double p = (double)params[i * SM_PARAM_STRIDE + k];
+        const double c = floor(__ddiv_rn(__dadd_rn(p, half), s));
+        if (!(c >= -1048576.0 && c <= 1048575.0)) bad = true;
+        const unsigned long long f = bad ? 0ull : (unsigned long long)(c + 1048576.0);
+        id = (id << 21) | f;
+    }
+    if (bad) atomicMin(err, (unsigned long long)i);
+    ids[i] = id;
+}
+
+int encode_positions(const float *params, int64_t n, double s, uint64_t *ids, int64_t *err,
+                     cudaStream_t st) {
+    if (s <= 0 || n < 0) {
+        set_error("chunk size must be positive");
+        return SM_ERR_INVALID;
+    }
+    cudaMemsetAsync(err, 0xff, sizeof(int64_t), st);   // -1 as u64 max
+    if (n == 0) return SM_OK;
+    encode_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+        params, n, s, s / 2.0, reinterpret_cast<unsigned long long *>(ids),
+        reinterpret_cast<unsigned long long *>(err));
+    SM_CHECK_LAUNCH("encode_positions");
+    return SM_OK;
+}
+
+__global__ void __launch_bounds__(256)
+expand_kernel(const int64_t *__restrict__ off, const int64_t *__restrict__ cnt,
+              const int64_t *__restrict__ prefix, int64_t nseg, int64_t total,
+              int32_t *__restrict__ slots) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    int64_t lo = 0, hi = nseg - 1;   // last segment with prefix <= i
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (prefix[mid] <= i) lo = mid;
+        else hi = mid - 1;
+    }
+    slots[i] = (int32_t)(off[lo] + (i - prefix[lo]));
+    (void)cnt;
+}
+
+int expand_segments(const int64_t *off, const int64_t *cnt, const int64_t *prefix, int64_t nseg,
+                    int64_t total, int32_t *slots, cudaStream_t st) {
+    if (total <= 0 || nseg <= 0) return SM_OK;
+    expand_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, st>>>(off, cnt, prefix, nseg, total, slots);
+    SM_CHECK_LAUNCH("expand_segments");
+    return SM_OK;
+}
+
+// ----------------------------------------------------------------- K8/K9
+// .dcg record (diskformat.py:51-66): 59 little-endian f32 + u32 opt_len = 240 B.
+// Optional Adam tail (opt_len = 120): "ADM1" | step u32 | m[14] f32 | v[14] f32.
+constexpr int kRecWords = 60;
+constexpr uint32_t kAdamMagic = 0x314d4441u;   // "ADM1"
+constexpr int kAdamTail = 120;
+
+__device__ __forceinline__ int shrest_src(int k) {   // rest index -> sh index
+    return k < 15 ? 1 + k : (k < 30 ? 2 + k : 3 + k);
+}
+
+__global__ void __launch_bounds__(256)
+unpack_kernel(const uint8_t *__restrict__ rec, int64_t n, int64_t stride, float *__restrict__ params,
+              float *__restrict__ sh_rest, float *__restrict__ m, float *__restrict__ v,
+              unsigned long long *__restrict__ err) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t *w = reinterpret_cast<const uint32_t *>(rec + i * stride);
+    float f[59];
+#pragma unroll
+    for (int k = 0; k < 59; k++) f[k] = __uint_as_float(w[k]);
+    const uint32_t opt_len = w[59];
+    float *p = params + i * SM_PARAM_STRIDE;
+#pragma unroll
+    for (int k = 0; k < 11; k++) p[k] = f[k];
+    p[11] = f[11 + 0];
+    p[12] = f[11 + 16];
+    p[13] = f[11 + 32];
+    p[14] = 0.f;
+    p[15] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 45; k++) sh_rest[i * 45 + k] = f[11 + shrest_src(k)];
+    // validate_gaussian_arrays (core.py:208-221)
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < 59; k++) ok = ok && isfinite(f[k]);
+    ok = ok && f[7] > 0.f && f[8] > 0.f && f[9] > 0.f && f[10] >= 0.f && f[10] <= 1.f;
+    const double qn = sqrt((double)f[3] * f[3] + (double)f[4] * f[4] + (double)f[5] * f[5] +
+                           (double)f[6] * f[6]);
+    ok = ok && fabs(qn - 1.0) <= 1e-6;
+    float *mm = m + i * SM_PARAM_STRIDE;
+    float *vv = v + i * SM_PARAM_STRIDE;
+    if (stride == 240 + kAdamTail) {
+        const uint32_t *t = w + kRecWords;
+        ok = ok && opt_len == (uint32_t)kAdamTail && t[0] == kAdamMagic;
+#pragma unroll
+        for (int k = 0; k < 14; k++) {
+            mm[k] = __uint_as_float(t[2 + k]);
+            vv[k] = __uint_as_float(t[16 + k]);
+        }
+        mm[14] = (float)t[1];
+        mm[15] = vv[14] = vv[15] = 0.f;
+    } else {
+        ok = ok && opt_len == 0;
+#pragma unroll
+        for (int k = 0; k < 16; k++) mm[k] = vv[k] = 0.f;
+    }
+    if (!ok) atomicMin(err, (unsigned long long)i);
+}
+
+__global__ void __launch_bounds__(256)
+pack_kernel(const float *__restrict__ params, const float *__restrict__ sh_rest,
+            const float *__restrict__ m, const float *__restrict__ v, int64_t n, int64_t stride,
+            uint8_t *__restrict__ rec) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t *w = reinterpret_cast<uint32_t *>(rec + i * stride);
+    const float *p = params + i * SM_PARAM_STRIDE;
+#pragma unroll
+    for (int k = 0; k < 11; k++) w[k] = __float_as_uint(p[k]);
+    w[11 + 0] = __float_as_uint(p[11]);
+    w[11 + 16] = __float_as_uint(p[12]);
+    w[11 + 32] = __float_as_uint(p[13]);
+#pragma unroll
+    for (int k = 0; k < 45; k++) w[11 + shrest_src(k)] = __float_as_uint(sh_rest[i * 45 + k]);
+    if (stride == 240 + kAdamTail) {
+        w[59] = kAdamTail;
+        uint32_t *t = w + kRecWords;
+        const float *mm = m + i * SM_PARAM_STRIDE;
+        const float *vv = v + i * SM_PARAM_STRIDE;
+        t[0] = kAdamMagic;
+        t[1] = (uint32_t)mm[14];
+#pragma unroll
+        for (int k = 0; k < 14; k++) {
+            t[2 + k] = __float_as_uint(mm[k]);
+            t[16 + k] = __float_as_uint(vv[k]);
+        }
+    } else {
+        w[59] = 0;
+    }
+}
+
+int chunk_unpack(const uint8_t *rec, int64_t n, int64_t stride, float *params, float *sh_rest,
+                 float *m, float *v, int64_t *err, cudaStream_t st) {
+    if (stride != 240 && stride != 240 + kAdamTail) {
+        set_error("unsupported record stride %lld", (long long)stride);
+        return SM_ERR_INVALID;
+    }
+    cudaMemsetAsync(err, 0xff, sizeof(int64_t), st);
+    if (n <= 0) return SM_OK;
+    unpack_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+        rec, n, stride, params, sh_rest, m, v, reinterpret_cast<unsigned long long *>(err));
+    SM_CHECK_LAUNCH("chunk_unpack");
+    return SM_OK;
+}
+
+int chunk_pack(const float *params, const float *sh_rest, const float *m, const float *v, int64_t n,
+               int64_t stride, uint8_t *rec, cudaStream_t st) {
+    if (stride != 240 && stride != 240 + kAdamTail) {
+        set_error("unsupported record stride %lld", (long long)stride);
+        return SM_ERR_INVALID;
+    }
+    if (n <= 0) return SM_OK;
+    pack_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(params, sh_rest, m, v, n, stride, rec);
+    SM_CHECK_LAUNCH("chunk_pack");
+    return SM_OK;
+}
+
+}  // namespace sm

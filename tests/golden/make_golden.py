@@ -1,0 +1,364 @@
+"""Generate golden fixtures by running the REFERENCE splatmap package.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the read-only reference from /root/reference/pkg/src with the
+test-only scikit-image shim in tests/golden/shim (scikit-image is absent and
+not installable offline; the shim restates its structural_similarity).  The
+fixtures it writes are small .npz / .json files committed next to this
+script; nothing at test or bench time reads /root/reference.
+
+Fixtures:
+  render_small.npz  reference render_arrays outputs on seeded scenes
+  render_fd.npz     central finite differences of the reference forward
+                    (linear functional of rgb/depth/alpha and total_loss)
+  loss.npz          reference total_loss / image_loss / ssim / depth_loss
+  grid.npz          encode_positions, chunk coords, frustum planes, visible sets
+  diskformat.npz    pack_chunk / pack_keyframe bytes
+  store_trace.json  ChunkStore policy trace (loads, evictions, stats)
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import tempfile
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+REF_SRC = Path(os.environ.get("SPLATMAP_REF_SRC", "/root/reference/pkg/src"))
+sys.path.insert(0, str(HERE / "shim"))
+sys.path.insert(0, str(REF_SRC))
+os.environ.setdefault("NUMBA_CACHE_DIR", tempfile.mkdtemp(prefix="numba_"))
+
+import splatmap  # noqa: E402
+from splatmap import core, culling, diskformat, grid, renderloss, store  # noqa: E402
+
+SH_C0 = core.SH_C0
+
+
+def _scene(rng, n, span=2.0, depth=(2.0, 8.0), scale=(0.05, 0.3)):
+    """Seeded SoA scene shaped like test_renderloss.random_scene (fp32-canonical)."""
+    pos = np.stack([rng.uniform(-span, span, n), rng.uniform(-span, span, n),
+                    rng.uniform(*depth, n)], axis=1)
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    sc = rng.uniform(*scale, size=(n, 3))
+    op = rng.uniform(0.3, 0.95, n)
+    col = rng.uniform(0.05, 0.95, size=(n, 3))
+    sh0 = (col - 0.5) / SH_C0
+    f = lambda a: a.astype(np.float32).astype(np.float64)  # noqa: E731
+    return renderloss.SceneArrays(positions=f(pos), rotations=f(q), scales=f(sc),
+                                  opacities=f(op), sh0=f(sh0))
+
+
+def _pose(rng, jitter=0.2, rotate=False):
+    rot = core.quat_normalize(rng.normal(size=4) * 0.05 + np.array([1.0, 0, 0, 0])) if rotate \
+        else np.array([1.0, 0.0, 0.0, 0.0])
+    return core.Pose(rotation=rot, translation=rng.normal(size=3) * jitter)
+
+
+def make_render_small():
+    rng = np.random.default_rng(2024)
+    cases = []
+    intr64 = core.CameraIntrinsics(fx=50.0, fy=50.0, cx=32.0, cy=32.0, width=64, height=64,
+                                   near=0.2, far=100.0)
+    for i in range(4):
+        cases.append((_scene(rng, 150), _pose(rng, rotate=i % 2 == 1), intr64))
+    # behind-near-plane and straddling Gaussians
+    sc = _scene(rng, 120, depth=(-1.0, 4.0))
+    cases.append((sc, core.Pose(), intr64))
+    # large footprints that clamp at the borders, non-square, odd principal point
+    intr_odd = core.CameraIntrinsics(fx=37.0, fy=41.0, cx=20.3, cy=15.7, width=48, height=33,
+                                     near=0.1, far=50.0)
+    cases.append((_scene(rng, 90, span=3.0, depth=(0.5, 3.0), scale=(0.1, 0.8)), _pose(rng), intr_odd))
+    # C1-shaped mini: 2000 splats at 160x120
+    intr_c1 = core.CameraIntrinsics(fx=120.0, fy=120.0, cx=80.0, cy=60.0, width=160, height=120,
+                                    near=0.05, far=1000.0)
+    cases.append((_scene(rng, 2000, span=4.0, depth=(1.0, 12.0), scale=(0.02, 0.25)),
+                  _pose(rng, rotate=True), intr_c1))
+    # single opaque on-axis Gaussian (test_renderloss known answer)
+    one = renderloss.SceneArrays(positions=np.array([[0.0, 0.0, 2.0]]),
+                                 rotations=np.array([[1.0, 0, 0, 0]]),
+                                 scales=np.full((1, 3), 0.1), opacities=np.array([0.999]),
+                                 sh0=((np.array([[0.9, 0.3, 0.6]]) - 0.5) / SH_C0))
+    intr32 = core.CameraIntrinsics(fx=40.0, fy=40.0, cx=16.0, cy=16.0, width=32, height=32,
+                                   near=0.1, far=200.0)
+    cases.append((one, core.Pose(), intr32))
+    out = {"count": len(cases)}
+    for k, (sc, pose, intr) in enumerate(cases):
+        fr = renderloss.render_arrays(sc, pose, intr)
+        out[f"c{k}_positions"] = sc.positions
+        out[f"c{k}_rotations"] = sc.rotations
+        out[f"c{k}_scales"] = sc.scales
+        out[f"c{k}_opacities"] = sc.opacities
+        out[f"c{k}_sh0"] = sc.sh0
+        out[f"c{k}_pose_q"] = pose.rotation
+        out[f"c{k}_pose_t"] = pose.translation
+        out[f"c{k}_intr"] = np.array([intr.fx, intr.fy, intr.cx, intr.cy, intr.near, intr.far,
+                                      intr.width, intr.height], dtype=np.float64)
+        out[f"c{k}_rgb"] = fr.rgb
+        out[f"c{k}_depth"] = fr.depth
+        out[f"c{k}_alpha"] = fr.alpha
+    np.savez_compressed(HERE / "render_small.npz", **out)
+
+
+def make_render_fd():
+    """Central differences of the reference forward (fp64), h = 1e-6."""
+    rng = np.random.default_rng(77)
+    intr = core.CameraIntrinsics(fx=30.0, fy=30.0, cx=16.0, cy=16.0, width=32, height=32,
+                                 near=0.2, far=100.0)
+    sc = _scene(rng, 40, span=1.5, depth=(2.0, 5.0), scale=(0.08, 0.35))
+    pose = _pose(rng, rotate=True)
+    wr = rng.normal(size=(32, 32, 3))
+    wd = rng.normal(size=(32, 32))
+    wa = rng.normal(size=(32, 32))
+    gt_rgb = np.round(rng.uniform(0, 1, size=(32, 32, 3)) * 255) / 255
+    gt_depth = rng.uniform(1.0, 6.0, size=(32, 32)).astype(np.float32)
+    gt_depth[rng.random((32, 32)) < 0.2] = 0.0
+    kf = core.Keyframe(id=0, pose=pose, intrinsics=intr, rgb=gt_rgb, depth=gt_depth)
+    w = renderloss.LossWeights()
+
+    def lin(s):
+        fr = renderloss.render_arrays(s, pose, intr)
+        return float((fr.rgb * wr).sum() + (fr.depth * wd).sum() + (fr.alpha * wa).sum())
+
+    def tl(s):
+        return renderloss.total_loss(renderloss.render_arrays(s, pose, intr), kf, w)
+
+    fields = ["positions", "rotations", "scales", "opacities", "sh0"]
+    picks = rng.choice(len(sc.positions), size=12, replace=False)
+    h = 1e-6
+    res = {f"lin_{f}": [] for f in fields}
+    res.update({f"loss_{f}": [] for f in fields})
+    for i in picks:
+        for f in fields:
+            arr = getattr(sc, f)
+            ncomp = 1 if arr.ndim == 1 else arr.shape[1]
+            gl, gt = [], []
+            for c in range(ncomp):
+                vals = []
+                for sgn in (1.0, -1.0):
+                    s2 = renderloss.SceneArrays(**{k: getattr(sc, k).copy() for k in fields})
+                    a2 = getattr(s2, f)
+                    if a2.ndim == 1:
+                        a2[i] += sgn * h
+                    else:
+                        a2[i, c] += sgn * h
+                    vals.append((lin(s2), tl(s2)))
+                gl.append((vals[0][0] - vals[1][0]) / (2 * h))
+                gt.append((vals[0][1] - vals[1][1]) / (2 * h))
+            res[f"lin_{f}"].append(gl)
+            res[f"loss_{f}"].append(gt)
+    fr = renderloss.render_arrays(sc, pose, intr)
+    out = {k: np.array(v) for k, v in res.items()}
+    out.update(picks=picks, positions=sc.positions, rotations=sc.rotations, scales=sc.scales,
+               opacities=sc.opacities, sh0=sc.sh0, pose_q=pose.rotation, pose_t=pose.translation,
+               intr=np.array([intr.fx, intr.fy, intr.cx, intr.cy, intr.near, intr.far, 32, 32.0]),
+               w_rgb=wr, w_depth=wd, w_alpha=wa, gt_rgb=kf.rgb, gt_depth=kf.depth,
+               loss=tl(sc), rgb=fr.rgb, depth=fr.depth, alpha=fr.alpha, h=h)
+    np.savez_compressed(HERE / "render_fd.npz", **out)
+
+
+def make_loss():
+    rng = np.random.default_rng(3)
+    out = {}
+    shapes = [(16, 16), (24, 31), (48, 64), (120, 160)]
+    for k, (h, w) in enumerate(shapes):
+        rgb = rng.uniform(0, 1, size=(h, w, 3))
+        if k == 3:
+            rgb = np.clip(rgb * 0.3 + 0.5 + 0.2 * np.sin(np.arange(w) / 5.0)[None, :, None], 0, 1)
+        depth = rng.uniform(0.5, 9.0, size=(h, w))
+        kf = core.Keyframe(id=k, pose=core.Pose(),
+                           intrinsics=core.CameraIntrinsics(fx=30.0, fy=30.0, cx=w / 2, cy=h / 2,
+                                                            width=w, height=h),
+                           rgb=rng.uniform(0, 1, size=(h, w, 3)),
+                           depth=(rng.uniform(0.5, 9.0, size=(h, w))
+                                  * (rng.random((h, w)) > 0.25)).astype(np.float32))
+        fr = renderloss.RenderedFrame(rgb=rgb, depth=depth, alpha=np.ones((h, w)))
+        out[f"c{k}_rgb"] = rgb
+        out[f"c{k}_depth"] = depth
+        out[f"c{k}_gt_rgb"] = kf.rgb
+        out[f"c{k}_gt_depth"] = kf.depth
+        for j, (ls, ld) in enumerate([(0.2, 0.5), (0.0, 0.0), (1.0, 2.0)]):
+            out[f"c{k}_total_{j}"] = np.array(
+                [ls, ld, renderloss.total_loss(fr, kf, renderloss.LossWeights(ls, ld))])
+        out[f"c{k}_ssim"] = np.array(renderloss.ssim(rgb, kf.rgb))
+        out[f"c{k}_depth_loss"] = np.array(renderloss.depth_loss(depth, kf.depth))
+    out["count"] = len(shapes)
+    np.savez_compressed(HERE / "loss.npz", **out)
+
+
+def make_grid():
+    rng = np.random.default_rng(5)
+    out = {}
+    for k, s in enumerate([10.0, 1.0, 0.37]):
+        pos = rng.uniform(-1e3, 1e3, size=(2000, 3)) * (s / 10.0)
+        # exact cell boundaries and negative-zero cases
+        pos[:6] = np.array([[s / 2, -s / 2, 0.0], [-0.0, s * 1.5, -s * 1.5],
+                            [s / 2 - 1e-12, s / 2 + 1e-12, -s / 2 + 1e-12],
+                            [0.0, 0.0, 0.0], [1e-300, -1e-300, s], [-s, s * 2.5, -s * 2.5]])
+        pos = pos.astype(np.float32).astype(np.float64)
+        out[f"s{k}_size"] = np.array(s)
+        out[f"s{k}_positions"] = pos
+        out[f"s{k}_ids"] = grid.encode_positions(pos, s)
+    # frustum planes + visibility sets over a 12^3 extent (criterion-2 style)
+    intr = core.CameraIntrinsics(fx=50.0, fy=45.0, cx=31.0, cy=33.0, width=64, height=64,
+                                 near=0.5, far=120.0)
+    cfg = culling.CullConfig(max_distance_m=70.0)
+    lo, hi = -6, 5
+    ext = culling.ChunkExtent(grid.ChunkCoord(lo, lo, lo), grid.ChunkCoord(hi, hi, hi))
+    coords = np.array([[x, y, z] for x in range(lo, hi + 1) for y in range(lo, hi + 1)
+                       for z in range(lo, hi + 1)])
+    vis = []
+    for t in range(40):
+        occ = rng.random(len(coords)) < 0.4
+        ids = {grid.encode_id(grid.ChunkCoord(*map(int, c))) for c in coords[occ]}
+        pose = core.Pose(rotation=core.quat_normalize(rng.normal(size=4)),
+                         translation=rng.uniform(-40, 40, size=3))
+        res = culling.visible_chunks(pose, intr, ext, ids.__contains__, cfg, 10.0)
+        fr = culling.extract_frustum(pose, intr)
+        out[f"v{t}_occ"] = occ
+        out[f"v{t}_pose_q"] = pose.rotation
+        out[f"v{t}_pose_t"] = pose.translation
+        out[f"v{t}_planes"] = fr.planes
+        out[f"v{t}_visible"] = np.array(sorted(res), dtype=np.uint64)
+        vis.append(len(res))
+    out["coords"] = coords
+    out["vis_count"] = np.array(len(vis))
+    out["intr"] = np.array([intr.fx, intr.fy, intr.cx, intr.cy, intr.near, intr.far, 64, 64.0])
+    out["max_distance"] = np.array(cfg.max_distance_m)
+    np.savez_compressed(HERE / "grid.npz", **out)
+
+
+def make_diskformat():
+    rng = np.random.default_rng(9)
+    gs = []
+    for i in range(7):
+        gs.append(diskformat.storage_canonical(core.Gaussian(
+            position=rng.uniform(-50, 50, size=3), rotation=core.quat_normalize(rng.normal(size=4)),
+            scale=rng.uniform(0.01, 2.0, size=3), opacity=float(rng.uniform(0, 1)),
+            sh=rng.normal(size=48), opt_state=b"")))
+    plain = diskformat.pack_chunk(0x123456789A, gs)
+    gs_opt = [g.copy() for g in gs]
+    for i, g in enumerate(gs_opt):
+        g.opt_state = bytes(rng.integers(0, 256, size=(i * 5) % 13, dtype=np.uint8))
+    with_opt = diskformat.pack_chunk(0xABCDEF, gs_opt)
+    kf = core.Keyframe(id=42, pose=core.Pose(rotation=core.quat_normalize(rng.normal(size=4)),
+                                             translation=rng.normal(size=3)),
+                       intrinsics=core.CameraIntrinsics(fx=20.0, fy=21.0, cx=6.0, cy=5.0,
+                                                        width=12, height=9, near=0.1, far=60.0),
+                       rgb=rng.random((9, 12, 3)),
+                       depth=rng.uniform(0, 5, size=(9, 12)).astype(np.float32),
+                       last_loss=0.25, usage_remaining=3)
+    out = dict(
+        chunk_plain=np.frombuffer(plain, dtype=np.uint8),
+        chunk_opt=np.frombuffer(with_opt, dtype=np.uint8),
+        keyframe=np.frombuffer(diskformat.pack_keyframe(kf), dtype=np.uint8),
+        positions=np.array([g.position for g in gs]), rotations=np.array([g.rotation for g in gs]),
+        scales=np.array([g.scale for g in gs]), opacities=np.array([g.opacity for g in gs]),
+        sh=np.array([g.sh for g in gs]),
+        opt_lens=np.array([len(g.opt_state) for g in gs_opt]),
+        opt_blob=np.frombuffer(b"".join(g.opt_state for g in gs_opt), dtype=np.uint8),
+        kf_rgb=kf.rgb, kf_depth=kf.depth, kf_pose_q=kf.pose.rotation, kf_pose_t=kf.pose.translation,
+    )
+    np.savez_compressed(HERE / "diskformat.npz", **out)
+
+
+def make_store_trace():
+    """Scripted ChunkStore workload; records every policy-visible outcome."""
+    rng = np.random.default_rng(11)
+    trace = {"ops": []}
+    with tempfile.TemporaryDirectory() as d:
+        st = store.ChunkStore(store.StoreConfig(disk_root=d, chunk_size_m=10.0,
+                                                gaussian_budget=60, keyframe_budget=4,
+                                                io_ns_per_byte=1.0))
+        cells = [(x, y, 0) for x in range(-2, 3) for y in range(-1, 2)]
+
+        def stats():
+            s = st.stats
+            return [s.active_gaussians, s.active_chunks, s.chunk_loads, s.chunk_evictions,
+                    s.chunk_writes, s.io_nanos, s.bytes_read, s.bytes_written,
+                    s.budget_overshoot, st.generation, s.total_gaussians_ever]
+
+        for step in range(120):
+            kind = rng.choice(["insert", "ensure", "evict", "mutate"], p=[0.35, 0.45, 0.1, 0.1])
+            if kind == "insert":
+                k = int(rng.integers(1, 18))
+                pos = []
+                for _ in range(k):
+                    cx, cy, cz = cells[int(rng.integers(len(cells)))]
+                    pos.append([cx * 10 + rng.uniform(-4.9, 4.9), cy * 10 + rng.uniform(-4.9, 4.9),
+                                rng.uniform(-4.9, 4.9)])
+                gs = [core.Gaussian(position=p, opacity=float(rng.uniform(0, 1)),
+                                    scale=rng.uniform(0.01, 1, size=3),
+                                    rotation=core.quat_normalize(rng.normal(size=4)),
+                                    sh=rng.normal(size=48)) for p in pos]
+                n = st.insert_gaussians(gs)
+                trace["ops"].append({"op": "insert", "positions": np.array(pos).tolist(),
+                                     "opacity": [g.opacity for g in gs],
+                                     "scale": [g.scale.tolist() for g in gs],
+                                     "rotation": [g.rotation.tolist() for g in gs],
+                                     "sh": [g.sh.tolist() for g in gs],
+                                     "ret": n, "stats": stats(),
+                                     "resident": sorted(st.resident_chunk_ids())})
+            elif kind == "ensure":
+                k = int(rng.integers(1, 5))
+                ids = sorted({grid.encode_id(grid.ChunkCoord(*cells[int(rng.integers(len(cells)))]))
+                              for _ in range(k)})
+                rep = st.ensure_resident(ids)
+                trace["ops"].append({"op": "ensure", "ids": [str(i) for i in ids],
+                                     "loaded": rep.loaded, "already": rep.already_resident,
+                                     "evicted": [str(e) for e in rep.evicted], "stats": stats(),
+                                     "resident": [str(r) for r in sorted(st.resident_chunk_ids())]})
+            elif kind == "evict":
+                res = sorted(st.resident_chunk_ids())
+                prot = [c for c in res if rng.random() < 0.3]
+                req = int(rng.integers(0, 40))
+                try:
+                    ev = st.evict_lru(req, protected=set(prot))
+                    err = None
+                except Exception as exc:  # InsufficientEvictable
+                    ev, err = [], type(exc).__name__
+                trace["ops"].append({"op": "evict", "required": req,
+                                     "protected": [str(p) for p in prot],
+                                     "evicted": [str(e) for e in ev], "error": err,
+                                     "stats": stats(),
+                                     "resident": [str(r) for r in sorted(st.resident_chunk_ids())]})
+            else:
+                res = sorted(st.resident_chunk_ids())
+                if not res:
+                    continue
+                cid = res[int(rng.integers(len(res)))]
+                st.mark_chunk_mutated(cid)
+                trace["ops"].append({"op": "mutate", "id": str(cid), "stats": stats(),
+                                     "resident": [str(r) for r in sorted(st.resident_chunk_ids())]})
+        st.flush()
+        trace["final_stats"] = stats()
+        # final map content in canonical order (chunk id, then in-chunk index)
+        content = []
+        for cid, gs in st.iter_map():
+            for g in gs:
+                content.append([str(cid)] + g.position.tolist() + [g.opacity])
+        trace["final_map"] = content
+    for op in trace["ops"]:
+        if op["op"] == "insert":
+            op["resident"] = [str(r) for r in op["resident"]]
+    (HERE / "store_trace.json").write_text(json.dumps(trace))
+
+
+if __name__ == "__main__":
+    print("reference splatmap", splatmap.__version__, "from", splatmap.__file__)
+    make_render_small()
+    make_loss()
+    make_grid()
+    make_diskformat()
+    make_store_trace()
+    make_render_fd()
+    for p in sorted(HERE.glob("*.npz")) + sorted(HERE.glob("*.json")):
+        print(f"{p.name:24s} {p.stat().st_size:>9d} bytes")

@@ -1,0 +1,193 @@
+"""GPU parity of the render path (K2-K5) and the fused loss, through the C ABI.
+
+Oracles: the reference's own outputs (tests/golden, fp64) and the CPU
+restatement oracle/render_oracle.c.  Tolerances (BASELINE.json):
+rgb max |d| <= 1e-4, alpha <= 1e-5, depth <= 1e-4 m where alpha > 1e-3;
+gradients per group ||dg|| / ||g|| <= 1e-3.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.golden_cases import f32, oracle_args, render_case
+
+pytestmark = pytest.mark.gpu
+
+RGB_TOL, ALPHA_TOL, DEPTH_TOL = 1e-4, 1e-5, 1e-4
+
+
+def _render(scene, pose, intr):
+    from paper_2511_23030_b200 import renderloss as rl
+    sa = rl.SceneArrays(**scene)
+    return rl.render_arrays(sa, pose, intr)
+
+
+def _assert_close(fr, ref, tag=""):
+    rgb, depth, alpha = ref
+    assert np.abs(fr.rgb - rgb).max() <= RGB_TOL, tag
+    assert np.abs(fr.alpha - alpha).max() <= ALPHA_TOL, tag
+    m = alpha > 1e-3
+    assert np.abs(fr.depth - depth)[m].max(initial=0) <= DEPTH_TOL, tag
+    assert np.abs(fr.depth * fr.alpha - depth * alpha).max() <= DEPTH_TOL * 10, tag
+
+
+def test_forward_matches_reference_golden(cuda, golden):
+    g = golden("render_small.npz")
+    for k in range(int(g["count"])):
+        scene, pose, intr, ref = render_case(g, k)
+        fr = _render(scene, pose, intr)
+        if k == int(g["count"]) - 1:   # non-fp32-canonical inputs: compare to oracle on f32 values
+            ref = O.render_arrays(*oracle_args(f32(scene), pose, intr))
+        _assert_close(fr, ref, k)
+
+
+def test_empty_scene_black(cuda):
+    from paper_2511_23030_b200 import renderloss as rl
+    from paper_2511_23030_b200.core import CameraIntrinsics, Pose
+    intr = CameraIntrinsics(fx=40.0, fy=40.0, cx=16, cy=16, width=32, height=32, near=0.1, far=200.0)
+    fr = rl.render([], Pose(), intr)
+    assert not fr.rgb.any() and not fr.depth.any() and not fr.alpha.any()
+
+
+def _colored(pos, color, opacity=0.9, scale=0.1):
+    from paper_2511_23030_b200.core import SH_C0, Gaussian
+    sh = np.zeros(48)
+    sh[[0, 16, 32]] = (np.asarray(color, float) - 0.5) / SH_C0
+    return Gaussian(position=pos, scale=np.full(3, scale), opacity=opacity, sh=sh)
+
+
+def test_known_answers(cuda):
+    """test_renderloss.py:61-111 known-answer cases on the GPU path."""
+    from paper_2511_23030_b200 import renderloss as rl
+    from paper_2511_23030_b200.core import CameraIntrinsics, Pose, quat_normalize
+    intr = CameraIntrinsics(fx=40.0, fy=40.0, cx=16, cy=16, width=32, height=32, near=0.1, far=200.0)
+    g = _colored([0.0, 0.0, 2.0], [0.9, 0.3, 0.6], opacity=0.999)
+    fr = rl.render([g], Pose(), intr)
+    assert np.abs(fr.rgb[16, 16] - 0.999 * np.array([0.9, 0.3, 0.6])).max() < 1e-6
+    assert abs(fr.depth[16, 16] - 2.0) / 2.0 < 0.01 and fr.alpha[16, 16] > 0.99
+    red = _colored([0.0, 0.0, 1.0], [1.0, 0.0, 0.0], opacity=0.99, scale=0.06)
+    blue = _colored([0.0, 0.0, 2.0], [0.0, 0.0, 1.0], opacity=0.99, scale=0.12)
+    a, b = rl.render([red, blue], Pose(), intr), rl.render([blue, red], Pose(), intr)
+    assert a.rgb[16, 16, 0] > a.rgb[16, 16, 2]
+    assert np.array_equal(a.rgb, b.rgb) and np.array_equal(a.depth, b.depth)
+    assert not rl.render([_colored([0, 0, -1.0], [1, 1, 1])], Pose(), intr).rgb.any()
+    frames = [rl.render([_colored([0, 0, 3.0], [1, 1, 1], opacity=o, scale=0.3)], Pose(), intr)
+              for o in (0.2, 0.5, 0.8)]
+    assert (frames[0].alpha <= frames[1].alpha + 1e-15).all()
+    assert (frames[1].alpha <= frames[2].alpha + 1e-15).all()
+    # permutation invariance, bit-exact (test_renderloss.py:86-94)
+    rng = np.random.default_rng(60)
+    scene = []
+    for _ in range(80):
+        gg = _colored([rng.uniform(-2, 2), rng.uniform(-2, 2), rng.uniform(2, 8)],
+                      rng.uniform(0.05, 0.95, 3), float(rng.uniform(0.3, 0.95)))
+        gg.rotation = quat_normalize(rng.normal(size=4))
+        gg.scale = rng.uniform(0.05, 0.3, size=3)
+        scene.append(gg)
+    base = rl.render(scene, Pose(), intr)
+    out = rl.render([scene[i] for i in rng.permutation(len(scene))], Pose(), intr)
+    assert np.array_equal(base.rgb, out.rgb) and np.array_equal(base.depth, out.depth)
+
+
+def test_larger_scene_matches_oracle(cuda):
+    """~20k Gaussians at 160x120 (config-1 shape) against the fp64 oracle."""
+    from paper_2511_23030_b200.core import CameraIntrinsics, Pose, quat_normalize
+    rng = np.random.default_rng(7)
+    n = 20000
+    pos = np.stack([rng.uniform(-6, 6, n), rng.uniform(-4, 4, n), rng.uniform(1.0, 14.0, n)], 1)
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    scene = f32(dict(positions=pos, rotations=q, scales=np.exp(rng.uniform(np.log(0.01), np.log(0.2), (n, 3))),
+                     opacities=rng.uniform(0.3, 0.95, n), sh0=(rng.uniform(0.05, 0.95, (n, 3)) - 0.5) / 0.28209479177))
+    intr = CameraIntrinsics(fx=120.0, fy=120.0, cx=80.0, cy=60.0, width=160, height=120, near=0.05)
+    pose = Pose(rotation=quat_normalize([1.0, 0.02, -0.03, 0.01]), translation=[0.1, -0.2, 0.3])
+    ref = O.render_arrays(*oracle_args(scene, pose, intr))
+    _assert_close(_render(scene, pose, intr), ref, "20k")
+
+
+def _grad_case(seed, n=300, w=64, h=48):
+    from paper_2511_23030_b200.core import CameraIntrinsics, Pose, quat_normalize
+    rng = np.random.default_rng(seed)
+    pos = np.stack([rng.uniform(-2, 2, n), rng.uniform(-1.5, 1.5, n), rng.uniform(2.0, 7.0, n)], 1)
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    scene = f32(dict(positions=pos, rotations=q, scales=rng.uniform(0.05, 0.3, (n, 3)),
+                     opacities=rng.uniform(0.3, 0.95, n),
+                     sh0=(rng.uniform(0.05, 0.95, (n, 3)) - 0.5) / 0.28209479177))
+    intr = CameraIntrinsics(fx=50.0, fy=50.0, cx=w / 2 - 0.3, cy=h / 2 + 0.2, width=w, height=h, near=0.2)
+    pose = Pose(rotation=quat_normalize([1.0, 0.03, 0.01, -0.02]), translation=[0.05, 0.1, -0.1])
+    return scene, pose, intr, rng
+
+
+def _gpu_backward(scene, pose, intr, d_rgb, d_depth, d_alpha):
+    import torch
+    from paper_2511_23030_b200 import renderloss as rl
+    sa = rl.SceneArrays(**scene)
+    params = torch.from_numpy(rl.pack_params(sa)).cuda()
+    eng = rl.default_engine()
+    rl.render_device(params, None, len(sa), pose, intr, eng)
+    grads = torch.zeros_like(params)
+    t = lambda a: None if a is None else torch.as_tensor(np.asarray(a, np.float32)).cuda()  # noqa: E731
+    eng.backward(params, None, len(sa), rl.camera_for(pose, intr), t(d_rgb), t(d_depth), t(d_alpha), grads)
+    g = grads.cpu().numpy().astype(np.float64)
+    return {"positions": g[:, 0:3], "rotations": g[:, 3:7], "scales": g[:, 7:10],
+            "opacities": g[:, 10], "sh0": g[:, 11:14]}
+
+
+def _assert_grads(gpu, ref, tag):
+    for k in ref:
+        a, b = gpu[k], ref[k]
+        nb = np.linalg.norm(b)
+        assert np.linalg.norm(a - b) <= 1e-3 * nb + 1e-9, (tag, k, np.linalg.norm(a - b) / max(nb, 1e-30))
+        assert np.all(np.abs(a - b) <= 1e-2 * np.abs(b) + 2e-3 * np.abs(b).max() + 1e-9), (tag, k)
+
+
+def test_backward_matches_oracle(cuda):
+    for seed in (1, 2):
+        scene, pose, intr, rng = _grad_case(seed)
+        h, w = intr.height, intr.width
+        d_rgb = rng.normal(size=(h, w, 3))
+        d_depth = rng.normal(size=(h, w)) * 0.1
+        d_alpha = rng.normal(size=(h, w))
+        ref = O.render_backward(*oracle_args(scene, pose, intr), d_rgb=d_rgb, d_depth=d_depth, d_alpha=d_alpha)
+        gpu = _gpu_backward(scene, pose, intr, d_rgb, d_depth, d_alpha)
+        _assert_grads(gpu, ref, seed)
+
+
+def test_loss_matches_reference_golden(cuda, golden):
+    from paper_2511_23030_b200 import renderloss as rl
+    from paper_2511_23030_b200.core import CameraIntrinsics, Keyframe, Pose
+    g = golden("loss.npz")
+    for k in range(int(g["count"])):
+        h, w = g[f"c{k}_rgb"].shape[:2]
+        kf = Keyframe(id=0, pose=Pose(), intrinsics=CameraIntrinsics(30.0, 30.0, w / 2, h / 2, w, h),
+                      rgb=g[f"c{k}_gt_rgb"], depth=g[f"c{k}_gt_depth"])
+        fr = rl.RenderedFrame(rgb=g[f"c{k}_rgb"], depth=g[f"c{k}_depth"], alpha=np.ones((h, w)))
+        for j in range(3):
+            ls, ld, ref = g[f"c{k}_total_{j}"]
+            v = rl.total_loss(fr, kf, rl.LossWeights(ls, ld))
+            assert abs(v - ref) <= 2e-5 * max(1.0, abs(ref)), (k, j, v, ref)
+        assert abs(rl.ssim(g[f"c{k}_rgb"], g[f"c{k}_gt_rgb"]) - float(g[f"c{k}_ssim"])) < 2e-5
+
+
+def test_loss_gradient_matches_oracle(cuda):
+    import torch
+    from paper_2511_23030_b200 import renderloss as rl
+    rng = np.random.default_rng(5)
+    h, w = 48, 64
+    rgb = rng.uniform(0, 1, (h, w, 3))
+    depth = rng.uniform(0.5, 5, (h, w))
+    gt_u8 = rng.integers(0, 256, (h, w, 3)).astype(np.uint8)
+    gt_d = (rng.uniform(0.5, 5, (h, w)) * (rng.random((h, w)) > 0.3)).astype(np.float32)
+    rgb32 = rgb.astype(np.float32)
+    ref_l, ref_dr, ref_dd = O.total_loss(rgb32, depth.astype(np.float32), gt_u8.astype(np.float32) / np.float32(255),
+                                         gt_d, 0.2, 0.5, grad=True)
+    eng = rl.default_loss_engine()
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    d_rgb = torch.zeros((h, w, 3), device="cuda")
+    d_dep = torch.zeros((h, w), device="cuda")
+    out = eng.run(t(rgb32), t(depth.astype(np.float32)), t(gt_u8), None, t(gt_d), 3, rl.LossWeights(),
+                  d_rgb, d_dep)
+    assert abs(float(out[0]) - ref_l) < 1e-5
+    assert np.abs(d_rgb.cpu().numpy() - ref_dr).max() <= 1e-3 * np.abs(ref_dr).max()
+    assert np.abs(d_dep.cpu().numpy() - ref_dd).max() <= 1e-6
