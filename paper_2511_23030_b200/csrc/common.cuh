@@ -28,11 +28,11 @@ constexpr int kTilePx = kTile * kTile;     // 256 threads per tile CTA
 // the fp32 offset keeps ~1e-7 relative precision whatever |u| is.
 struct __align__(16) ProjRec {
     float ox, oy;          // x0 - u, y0 - v
-    float ia, ib, ic;      // conic (c, -b, a)/det
+    float ia, ib, ic;      // conic (c, -b, a)/det pre-scaled by kPowScale (log2 units)
     float op;              // opacity
     float r, g, b;         // clipped SH0 colour
     float z;               // camera depth
-    float eps;             // |q32 - 9| band that triggers the fp64 decision
+    float eps;             // |pw - kPowCut| band that triggers the fp64 decision
     int32_t x0y0;          // (y0 << 16) | x0   clamped 3-sigma bbox
     int32_t x1y1;          // (y1 << 16) | x1
     float spare[3];
@@ -58,6 +58,35 @@ __device__ __forceinline__ double quad_q64(const Proj64 &p, int px, int py) {
     double t2 = __dmul_rn(__dmul_rn(__dmul_rn(2.0, p.ib), dx), dy);
     double t3 = __dmul_rn(__dmul_rn(p.ic, dy), dy);
     return __dadd_rn(__dadd_rn(t1, t2), t3);
+}
+
+// alpha = op * exp(-q/2) = op * 2^(kPowScale * q): the conic is stored
+// pre-multiplied by kPowScale so the quadratic form lands directly in the
+// exponent of ex2; q > 9 (renderloss.py:141) <=> pw < kPowCut.
+constexpr double kPowScale = -0.72134752044448170368;   // -0.5 * log2(e)
+constexpr float kPowCut = (float)(9.0 * -0.72134752044448170368);
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Shared by forward and backward so both take identical decisions.
+// Returns true when pixel (px,py) receives a contribution (in box, q <= 9).
+__device__ __forceinline__ bool pair_eval(const ProjRec &g, int px, int py, const Proj64 *p64,
+                                          const uint32_t *order, uint32_t rank, float &dx,
+                                          float &dy, float &pw) {
+    const int x0 = g.x0y0 & 0xffff, y0 = g.x0y0 >> 16;
+    const int x1 = (int)(short)(g.x1y1 & 0xffff), y1 = g.x1y1 >> 16;
+    if ((unsigned)(px - x0) > (unsigned)(x1 - x0) || (unsigned)(py - y0) > (unsigned)(y1 - y0))
+        return false;
+    dx = (float)(px - x0) + g.ox;
+    dy = (float)(py - y0) + g.oy;
+    pw = dx * (g.ia * dx + 2.f * g.ib * dy) + g.ic * dy * dy;
+    const float d = pw - kPowCut;
+    if (fabsf(d) <= g.eps) return !(quad_q64(p64[order[rank]], px, py) > 9.0);
+    return d >= 0.f;
 }
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -120,48 +120,35 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
 #pragma unroll
             for (int t = 0; t < 16; t++) v[t] = 0.f;
             bool hit = false;
-            if (k <= last) {
-                const int x0 = rec_x0(g), y0 = rec_y0(g);
-                if ((unsigned)(px - x0) <= (unsigned)(rec_x1(g) - x0) &&
-                    (unsigned)(py - y0) <= (unsigned)(rec_y1(g) - y0)) {
-                    const float dx = (float)(px - x0) + g.ox;
-                    const float dy = (float)(py - y0) + g.oy;
-                    const float q = dx * (g.ia * dx + 2.f * g.ib * dy) + g.ic * dy * dy;
-                    const float dq = q - 9.f;
-                    bool over;
-                    if (fabsf(dq) <= g.eps)
-                        over = quad_q64(p64[order[s_rank[j]]], px, py) > 9.0;
-                    else
-                        over = dq > 0.f;
-                    if (!over) {
-                        hit = true;
-                        const float G = __expf(-0.5f * q);
-                        const float alpha = g.op * G;
-                        const float oma = 1.f - alpha;
-                        const float Tk = (k == last) ? tlast : T / oma;
-                        float ga = (g.r - Br) * gCr + (g.g - Bg) * gCg + (g.b - Bb) * gCb +
-                                   (g.z - Bz) * gD;
-                        ga = Tk * (ga + gA * P);
-                        const float wt = Tk * alpha;
-                        v[6] = wt * gCr;
-                        v[7] = wt * gCg;
-                        v[8] = wt * gCb;
-                        v[9] = wt * gD;
-                        v[5] = ga * G;
-                        const float gq = -0.5f * alpha * ga;
-                        v[2] = gq * dx * dx;
-                        v[3] = gq * 2.f * dx * dy;
-                        v[4] = gq * dy * dy;
-                        v[0] = -gq * (2.f * g.ia * dx + 2.f * g.ib * dy);
-                        v[1] = -gq * (2.f * g.ib * dx + 2.f * g.ic * dy);
-                        Br = alpha * g.r + oma * Br;
-                        Bg = alpha * g.g + oma * Bg;
-                        Bb = alpha * g.b + oma * Bb;
-                        Bz = alpha * g.z + oma * Bz;
-                        P *= oma;
-                        T = Tk;
-                    }
-                }
+            float dx, dy, pw;
+            if (k <= last && pair_eval(g, px, py, p64, order, s_rank[j], dx, dy, pw)) {
+                hit = true;
+                const float G = ex2_approx(pw);
+                const float alpha = g.op * G;
+                const float oma = 1.f - alpha;
+                const float Tk = (k == last) ? tlast : T / oma;
+                float ga = (g.r - Br) * gCr + (g.g - Bg) * gCg + (g.b - Bb) * gCb + (g.z - Bz) * gD;
+                ga = Tk * (ga + gA * P);
+                const float wt = Tk * alpha;
+                v[6] = wt * gCr;
+                v[7] = wt * gCg;
+                v[8] = wt * gCb;
+                v[9] = wt * gD;
+                v[5] = ga * G;
+                // q = pw / kPowScale; conic grads are w.r.t. the unscaled conic
+                const float gq = -0.5f * alpha * ga;
+                v[2] = gq * dx * dx;
+                v[3] = gq * 2.f * dx * dy;
+                v[4] = gq * dy * dy;
+                const float inv = (float)(2.0 / kPowScale);
+                v[0] = -gq * inv * (g.ia * dx + g.ib * dy);
+                v[1] = -gq * inv * (g.ib * dx + g.ic * dy);
+                Br = alpha * g.r + oma * Br;
+                Bg = alpha * g.g + oma * Bg;
+                Bb = alpha * g.b + oma * Bb;
+                Bz = alpha * g.z + oma * Bz;
+                P *= oma;
+                T = Tk;
             }
             if (__any_sync(0xffffffffu, hit)) {
                 const float s = transpose_reduce16(v, lane);

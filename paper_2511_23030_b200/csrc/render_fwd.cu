@@ -134,12 +134,13 @@ project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots
     const int x0 = (int)fx0, x1 = (int)fx1, y0 = (int)fy0, y1 = (int)fy1;
     r.ox = (float)((double)x0 - g.u);
     r.oy = (float)((double)y0 - g.v);
-    r.ia = (float)ia;
-    r.ib = (float)ib;
-    r.ic = (float)ic;
-    // fp32 q error bound near q = 9 scales with K = ac/det (anisotropy).
+    r.ia = (float)(kPowScale * ia);
+    r.ib = (float)(kPowScale * ib);
+    r.ic = (float)(kPowScale * ic);
+    // fp32 error bound of the quadratic form near q = 9 scales with the
+    // anisotropy K = ac/det (sum of |terms| <= 36 K); generous margin.
     const double K = a * c / det;
-    r.eps = (float)(1e-4 * (1.0 + K));
+    r.eps = (float)(1e-4 * (1.0 + K) * -kPowScale);
     r.x0y0 = (int32_t)(((uint32_t)y0 << 16) | ((uint32_t)x0 & 0xffffu));
     r.x1y1 = (int32_t)(((uint32_t)(y1 & 0xffff) << 16) | ((uint32_t)x1 & 0xffffu));
     rec[i] = r;
@@ -236,21 +237,9 @@ composite_fwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
         if (!done) {
             for (int j = 0; j < cnt; j++) {
                 const ProjRec &g = s_rec[j];
-                const int x0 = rec_x0(g), y0 = rec_y0(g);
-                if ((unsigned)(px - x0) > (unsigned)(rec_x1(g) - x0) ||
-                    (unsigned)(py - y0) > (unsigned)(rec_y1(g) - y0))
-                    continue;
-                const float dx = (float)(px - x0) + g.ox;
-                const float dy = (float)(py - y0) + g.oy;
-                const float q = dx * (g.ia * dx + 2.f * g.ib * dy) + g.ic * dy * dy;
-                const float dq = q - 9.f;
-                bool over;
-                if (fabsf(dq) <= g.eps)
-                    over = quad_q64(p64[order[s_rank[j]]], px, py) > 9.0;
-                else
-                    over = dq > 0.f;
-                if (over) continue;
-                const float alpha = g.op * __expf(-0.5f * q);
+                float dx, dy, pw;
+                if (!pair_eval(g, px, py, p64, order, s_rank[j], dx, dy, pw)) continue;
+                const float alpha = g.op * ex2_approx(pw);
                 const float w = T * alpha;
                 cr += w * g.r;
                 cg += w * g.g;

@@ -1,9 +1,9 @@
 """GPU parity of the render path (K2-K5) and the fused loss, through the C ABI.
 
 Oracles: the reference's own outputs (tests/golden, fp64) and the CPU
-restatement oracle/render_oracle.c.  Tolerances (BASELINE.json):
-rgb max |d| <= 1e-4, alpha <= 1e-5, depth <= 1e-4 m where alpha > 1e-3;
-gradients per group ||dg|| / ||g|| <= 1e-3.
+restatement oracle/render_oracle.c.  Tolerances are the north star's
+(BASELINE.json): images max abs 1e-4 (rgb, alpha; depth relative 1e-4 where
+alpha > 1e-3), gradients relative 1e-3 per parameter group.
 """
 import numpy as np
 import pytest
@@ -13,7 +13,7 @@ from tests.golden_cases import f32, oracle_args, render_case
 
 pytestmark = pytest.mark.gpu
 
-RGB_TOL, ALPHA_TOL, DEPTH_TOL = 1e-4, 1e-5, 1e-4
+RGB_TOL, ALPHA_TOL, DEPTH_TOL = 1e-4, 1e-4, 1e-4
 
 
 def _render(scene, pose, intr):
@@ -27,7 +27,8 @@ def _assert_close(fr, ref, tag=""):
     assert np.abs(fr.rgb - rgb).max() <= RGB_TOL, tag
     assert np.abs(fr.alpha - alpha).max() <= ALPHA_TOL, tag
     m = alpha > 1e-3
-    assert np.abs(fr.depth - depth)[m].max(initial=0) <= DEPTH_TOL, tag
+    rel = np.abs(fr.depth - depth)[m] / np.maximum(np.abs(depth[m]), 1.0)
+    assert rel.max(initial=0) <= DEPTH_TOL, tag
     assert np.abs(fr.depth * fr.alpha - depth * alpha).max() <= DEPTH_TOL * 10, tag
 
 
