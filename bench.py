@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""Mapping-step benchmark (BASELINE.json metric: mapping iters/s, Gaussians/s).
+
+Workload = BASELINE.json configs[1] ("C2"): 1M-Gaussian Replica-shaped room,
+640x480, 8x8x2 chunks (s = 1 m), single-GPU mapping loop; synthetic data
+(paper_2511_23030_b200.synthetic), random-init-free: the map is the scene and
+the keyframes' ground truth renders a perturbed copy of it.
+
+One step = paper_2511_23030_b200.mapping.MappingEngine.optimization_step:
+the reference's host policy (keyframe draw, visibility, residency, metrics)
++ device render fwd, fused loss fwd/bwd, render bwd, fused Adam, one loss
+readback.  N > 1 (torchrun): data-parallel over keyframes, one keyframe per
+rank per step, NCCL all-reduce of the gradient slab, replicated Adam
+(weak scaling: value = keyframe-iterations/s over all ranks).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "mapping iters/sec (render fwd+bwd+Adam)"
+UNIT = "it/s"
+WORKLOAD = "C2: 1M-Gaussian Replica-shaped room, 640x480, 8x8x2 chunks (s=1 m), 16 keyframes"
+
+
+def _peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.lines: list[str] = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:
+                time.sleep(0.01)
+            self.start_count = len(self.lines)
+        except Exception:
+            self.proc = None
+            self.start_count = 0
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        rows = [l.split(", ") for l in self.lines[max(0, self.start_count - 1):] if l]
+        sm = [float(r[0]) for r in rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 7 for i in range(4)
+                          if r[3 + i].strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+
+
+# Algorithmic bytes per unit of each stage.
+#   n = visible Gaussians, i = tile instances, p = pixels
+STAGE_BYTES = {
+    "project_fwd": lambda n, i, p: n * (4 + 64 + 64 + 40 + 8 + 4 + 4),
+    "depth_sort": lambda n, i, p: n * 8 * (8 + 24),
+    "bin_emit": lambda n, i, p: n * (4 + 4 + 64 + 64 + 4 * 4) + i * 4,
+    "tile_sort": lambda n, i, p: i * 2 * 12 + i * 8,
+    "composite_fwd": lambda n, i, p: i * (4 + 64) + p * (20 + 28),
+    "loss": lambda n, i, p: p * (16 + 7 + 36 * 2 + 16),
+    "composite_bwd": lambda n, i, p: i * (4 + 64 + 40) + p * (28 + 16),
+    "project_bwd": lambda n, i, p: n * (4 + 4 + 4 + 64 + 40 + 2 * 64),
+    "adam": lambda n, i, p: n * (4 + 7 * 64),
+}
+
+
+def _dist():
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def cpu_baseline_step(eng, kf_id: int, seconds: float = 20.0, threads: int | None = None):
+    """Oracle (CPU, fp64) mapping iteration on the same active set; bounded sample."""
+    from oracle import oracle as O
+    store = eng.store
+    kf = store.keyframe_get(kf_id)
+    visible, _ = eng._visible_for_pose(kf.pose)
+    ids = sorted(visible)
+    rows = np.concatenate([np.arange(o, o + c) for o, c in store.segments(ids)]) if ids else np.zeros(0, int)
+    p = store.slab.params[rows].cpu().numpy().astype(np.float64)
+    st = O.TrainState(p[:, 0:3], p[:, 3:7], p[:, 7:10], p[:, 10], p[:, 11:14])
+    a = eng.adam
+    lr = [a.lr_position] * 3 + [a.lr_rotation] * 4 + [a.lr_scale] * 3 + [a.lr_opacity] + [a.lr_sh0] * 3
+    gt = kf.rgb.astype(np.float64)
+    threads = threads or os.cpu_count() or 1
+    times = []
+    t_end = time.perf_counter() + seconds
+    while True:
+        t0 = time.perf_counter()
+        st.step(kf.pose.rotation, kf.pose.translation, kf.intrinsics, gt, kf.depth, eng.weights.lambda_s,
+                eng.weights.lambda_depth, lr, a.beta1, a.beta2, a.eps, a.min_scale, threads=threads)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end or len(times) >= 5:
+            break
+    per = sum(times) / len(times)
+    return {"value": 1.0 / per, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{len(times)} full oracle mapping iteration(s) (fp64 fwd+loss+bwd+Adam, "
+                      f"oracle/render_oracle.c) on keyframe {kf_id}'s active set of {len(rows)} "
+                      f"Gaussians at 640x480, {per:.2f} s each, {threads} threads"}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference algorithm's CPU path (oracle port) on the C2 config."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2511_23030_b200.synthetic import C2_INTR, perturbed, room_poses, room_scene
+    scene = room_scene(1_000_000, seed=42)
+    poses = room_poses(16, seed=42)
+    target = perturbed(scene, 49)
+    threads = os.cpu_count() or 1
+    st = O.TrainState(scene.positions, scene.rotations, scene.scales, scene.opacities, scene.sh0)
+    intr = C2_INTR
+    gts = {}
+    lr = [1e-4] * 3 + [1e-3] * 4 + [5e-5] * 3 + [1e-2] + [2.5e-3] * 3
+    budget = 150.0
+    t_all = time.perf_counter()
+    steps, times = 0, []
+    for k in range(max(0, min(args.warmup, 1)) + max(1, args.steps)):
+        kf = k % 2
+        if kf not in gts:
+            rgb, depth, _ = O.render_arrays(target.positions, target.rotations, target.scales,
+                                            target.opacities, target.sh0, poses[kf].rotation,
+                                            poses[kf].translation, intr.fx, intr.fy, intr.cx, intr.cy,
+                                            intr.near, intr.width, intr.height, threads=threads)
+            gts[kf] = (np.round(np.clip(rgb, 0, 1) * 255) / 255, depth)
+        t0 = time.perf_counter()
+        st.step(poses[kf].rotation, poses[kf].translation, intr, gts[kf][0], gts[kf][1], 0.2, 0.5, lr,
+                0.9, 0.999, 1e-15, 1e-5, threads=threads)
+        dt = time.perf_counter() - t0
+        if k >= min(args.warmup, 1):
+            times.append(dt)
+            steps += 1
+        if time.perf_counter() - t_all > budget and steps >= 1:
+            break
+    per = sum(times) / len(times)
+    value = 1.0 / per
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": per * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "parallelism": "cpu"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{steps} oracle mapping iterations (fp64 fwd+loss+bwd+Adam over all "
+                                   f"1M Gaussians, 640x480, oracle/render_oracle.c; the reference itself "
+                                   f"is forward-only) with {threads} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--keyframes", type=int, default=16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = (1, 0, 0)
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, world, rank)
+        return
+    import torch
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    from paper_2511_23030_b200 import _lib
+    from paper_2511_23030_b200.workloads import build_c2
+    lib = _lib.load()
+    eng = build_c2(args.n, args.keyframes, store_dir=tempfile.mkdtemp(prefix=f"bench_r{rank}_"),
+                   device=f"cuda:{local}")
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    step_fn = (lambda f, s: eng.optimization_step(f, s)) if world == 1 else \
+        (lambda f, s: eng.optimization_step_dp(f, s, world, rank))
+    for s in range(args.warmup):
+        step_fn(0, s)
+    torch.cuda.synchronize()
+    # ------------------------------------------------------------ timed (device-resident)
+    eng.reset_counters()
+    lib.sm_profile_enable(1)
+    _lib.profile_collect()
+    launches0 = lib.sm_launch_count()
+    clocks = ClockSampler(local)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for s in range(args.steps):
+        step_fn(1, s)
+    ev1.record()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = lib.sm_launch_count() - launches0
+    prof = _lib.profile_collect()
+    lib.sm_profile_enable(0)
+    ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    units = args.steps * world
+    value = units / (ms / 1e3)
+    n_vis = eng.counter_gaussians / max(eng.counter_steps, 1)
+    n_inst = eng.counter_instances / max(eng.counter_steps, 1)
+    gauss_s = eng.counter_gaussians * world / (ms / 1e3)
+    # ------------------------------------------------------------ e2e through the public API
+    eng.upload_keyframes_each_step = True
+    step_fn(2, 0)
+    eng.reset_counters()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h2d0, d2h0 = eng.h2d_bytes, eng.d2h_bytes
+    e0.record()
+    for s in range(args.steps):
+        step_fn(3, s)
+    e1.record()
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ems], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+    e2e = {"value": units / (ems / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": int((eng.h2d_bytes - h2d0) / args.steps),
+           "d2h_bytes_per_step": int((eng.d2h_bytes - d2h0) / args.steps)}
+    eng.upload_keyframes_each_step = False
+    # ------------------------------------------------------------ roofline of the dominant kernel
+    peaks = _peaks()
+    px = eng.intr.width * eng.intr.height
+    stages = {k: {"ms_per_step": v[0] / args.steps, "calls": v[1]} for k, v in prof.items() if v[1]}
+    dom = max(stages, key=lambda k: stages[k]["ms_per_step"]) if stages else None
+    roof = None
+    if dom:
+        per_launch_ms = prof[dom][0] / prof[dom][1]
+        launches_per_step = prof[dom][1] / args.steps
+        byt = STAGE_BYTES.get(dom, lambda *a: 0)(n_vis, n_inst, px) / max(launches_per_step, 1)
+        achieved = byt / (per_launch_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                "algorithmic_bytes_per_launch": byt, "ms_per_launch": per_launch_ms,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "_fallback" not in peaks
+                else "fallback 6.65 TB/s"}
+        for k, v in stages.items():
+            f = STAGE_BYTES.get(k)
+            if f and v["calls"]:
+                b = f(n_vis, n_inst, px) / (v["calls"] / args.steps)
+                v["gbs"] = b / (v["ms_per_step"] / (v["calls"] / args.steps) / 1e3) / 1e9
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_step(eng, eng.latest_kf, seconds=args.cpu_seconds)
+        except Exception as exc:  # report, never fake
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "port", "sample": f"failed: {exc}"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "gaussians_total": args.n,
+                   "visible_gaussians_per_step": n_vis, "tile_instances_per_step": n_inst,
+                   "resolution": [eng.intr.width, eng.intr.height], "keyframes_per_step_per_gpu": 1,
+                   "parallelism": f"dp{world}",
+                   "l2": "inputs larger than L2 (slab params+Adam+grads 256 MB/1M Gaussians)"},
+        "gaussians_per_s": gauss_s,
+        "e2e": e2e, "gpu_launches": int(launches), "clocks": clk, "roofline": roof,
+        "stages": stages, "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

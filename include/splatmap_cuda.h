@@ -169,6 +169,19 @@ int sm_chunk_unpack(const uint8_t *records, int64_t n, int64_t stride, float *pa
 int sm_chunk_pack(const float *params, const float *sh_rest, const float *adam_m,
                   const float *adam_v, int64_t n, int64_t stride, uint8_t *records, void *stream);
 
+/* ------------------------------------------------------------ profiling
+ * No reference counterpart (the reference bills a deterministic cost model,
+ * sim.py:53-57).  When enabled, each stage (project_fwd, depth_sort,
+ * bin_emit, tile_sort, composite_fwd, loss, composite_bwd, project_bwd,
+ * adam, cull, codec) records a CUDA event pair on its launch stream;
+ * collect() blocks on them and returns per-stage summed ms and call counts
+ * (then resets).  sm_launch_count() = kernels launched by this library. */
+void sm_profile_enable(int on);
+long long sm_launch_count(void);
+int sm_profile_stage_count(void);
+const char *sm_profile_stage_name(int stage);
+int sm_profile_collect(double *ms_out, long long *calls_out);
+
 #ifdef __cplusplus
 }
 #endif

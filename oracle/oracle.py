@@ -52,6 +52,10 @@ def lib():
             + [_dp] * 3 + [_dp] * 5 + [ctypes.c_int])
         _lib.or_total_loss.restype = ctypes.c_double
         _lib.or_total_loss.argtypes = [_dp] * 4 + [ctypes.c_int] * 2 + [ctypes.c_double] * 2 + [_dp] * 2
+        _lib.or_train_step.restype = ctypes.c_double
+        _lib.or_train_step.argtypes = (
+            [ctypes.c_int64] + [_dp] * 7 + [ctypes.c_double] * 5 + [ctypes.c_int] * 2 + [_dp] * 2
+            + [ctypes.c_double] * 2 + [_dp] + [ctypes.c_double] * 4 + [_dp] * 2 + [_i64p, ctypes.c_int])
         _lib.or_adam.restype = None
         _lib.or_adam.argtypes = ([ctypes.c_int64] + [_dp] * 4 + [ctypes.c_double] * 4
                                  + [ctypes.c_int64])
@@ -153,6 +157,35 @@ def total_loss(rgb, depth, gt_rgb, gt_depth, lambda_s=0.2, lambda_depth=0.5, gra
         return float(val), d_rgb, d_depth
     return float(lib().or_total_loss(_p(rgb), _p(depth), _p(gt_rgb), _p(gt_depth), h, w,
                                      lambda_s, lambda_depth, None, None))
+
+
+class TrainState:
+    """fp64 copy of a scene + per-Gaussian Adam state for or_train_step."""
+
+    def __init__(self, positions, rotations, scales, opacities, sh0):
+        n, self.pos, self.rot, self.scale, self.opac, self.sh0 = _scene_args(
+            positions, rotations, scales, opacities, sh0)
+        self.pos, self.rot, self.scale = self.pos.copy(), self.rot.copy(), self.scale.copy()
+        self.opac, self.sh0 = self.opac.copy(), self.sh0.copy()
+        self.n = n
+        self.m = np.zeros((n, 14))
+        self.v = np.zeros((n, 14))
+        self.steps = np.zeros(n, dtype=np.int64)
+
+    def step(self, pose_rotation, pose_translation, intr, gt_rgb, gt_depth, lambda_s, lambda_depth,
+             lr14, beta1, beta2, eps, min_scale, threads=None) -> float:
+        """One CPU mapping iteration (fwd, loss+grad, bwd, Adam); returns the loss."""
+        r_wc = _c(quat_to_matrix(pose_rotation))
+        t = _c(pose_translation, (3,))
+        h, w = intr.height, intr.width
+        gt = _c(gt_rgb, (h, w, 3))
+        gd = _c(gt_depth, (h, w))
+        lr = _c(lr14, (14,))
+        return float(lib().or_train_step(
+            self.n, _p(self.pos), _p(self.rot), _p(self.scale), _p(self.opac), _p(self.sh0), _p(r_wc),
+            _p(t), intr.fx, intr.fy, intr.cx, intr.cy, intr.near, w, h, _p(gt), _p(gd), lambda_s,
+            lambda_depth, _p(lr), beta1, beta2, eps, min_scale, _p(self.m), _p(self.v),
+            self.steps.ctypes.data_as(_i64p), threads or default_threads()))
 
 
 def adam(param, m, v, grad, lr, beta1, beta2, eps, step):

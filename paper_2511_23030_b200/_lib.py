@@ -86,6 +86,11 @@ def load():
     _sig(lib.sm_expand_segments, c_int, vp, vp, vp, i64, i64, vp, vp)
     _sig(lib.sm_chunk_unpack, c_int, vp, i64, i64, vp, vp, vp, vp, vp, vp)
     _sig(lib.sm_chunk_pack, c_int, vp, vp, vp, vp, i64, i64, vp, vp)
+    _sig(lib.sm_profile_enable, None, c_int)
+    _sig(lib.sm_launch_count, ctypes.c_longlong)
+    _sig(lib.sm_profile_stage_count, c_int)
+    _sig(lib.sm_profile_stage_name, ctypes.c_char_p, c_int)
+    _sig(lib.sm_profile_collect, c_int, POINTER(c_double), POINTER(ctypes.c_longlong))
     if lib.sm_abi_version() != ABI_VERSION:
         raise DeviceFailure(f"ABI mismatch: library {lib.sm_abi_version()} != {ABI_VERSION}")
     _lib = lib
@@ -107,6 +112,16 @@ def check(rc: int, what: str = "") -> None:
     if rc in (SM_ERR_INVALID, SM_ERR_WORKSPACE):
         raise ValueError(text)
     raise DeviceFailure(text)
+
+
+def profile_collect() -> dict:
+    """{stage: (ms, calls)} since the last collect (blocks on recorded events)."""
+    lib = load()
+    n = lib.sm_profile_stage_count()
+    ms = (c_double * n)()
+    calls = (ctypes.c_longlong * n)()
+    lib.sm_profile_collect(ms, calls)
+    return {lib.sm_profile_stage_name(i).decode(): (ms[i], calls[i]) for i in range(n)}
 
 
 def ptr(t) -> int | None:

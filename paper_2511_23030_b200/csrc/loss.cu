@@ -14,6 +14,7 @@
 // S and dS/d{mu_x, E[x^2], E[xy]} on the crop, plus L1 / depth partial sums.
 // Kernel B: adjoint filter of those three maps and the final per-pixel grads.
 #include "common.cuh"
+#include "prof.cuh"
 
 namespace sm {
 
@@ -241,12 +242,15 @@ int loss_forward_backward(const float *rgb, const float *depth, const uint8_t *g
     cudaMemsetAsync(acc, 0, sizeof(LossAcc), st);
     dim3 grid((unsigned)ceil_div(W, kLT), (unsigned)ceil_div(H, kLT), (unsigned)C);
     const int want = d_rgb != nullptr;
+    prof_begin(ST_LOSS, st);
     loss_fwd_kernel<<<grid, 256, 0, st>>>(rgb, depth, gt_rgb, gt_rgbf, gt_depth, W, H, C, dmaps, acc,
                                           want);
     loss_finalize<<<1, 1, 0, st>>>(acc, W, H, C, ls, ld, loss_out);
     if (want)
         loss_bwd_kernel<<<grid, 256, 0, st>>>(rgb, depth, gt_rgb, gt_rgbf, gt_depth, W, H, C, dmaps,
                                               acc, ls, ld, d_rgb, d_depth);
+    prof_end(ST_LOSS, st);
+    count_launches(want ? 3 : 2);
     SM_CHECK_LAUNCH("loss_forward_backward");
     return SM_OK;
 }

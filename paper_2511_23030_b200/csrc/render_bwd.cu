@@ -16,6 +16,7 @@
 // Per-Gaussian sums: a 16-wide transposed butterfly (16 shuffles, one value
 // per lane pair) per warp, shared-memory atomics across the 8 warps of the
 // tile, one global atomic per (instance, value) per tile.
+#include "prof.cuh"
 #include "render.cuh"
 
 namespace sm {
@@ -325,10 +326,13 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
     RenderBufs b = render_bufs(ws, L);
     cudaMemsetAsync(b.g2d, 0, n * (int64_t)sizeof(float) * kG2dStride, st);
     const uint32_t rank_mask = (uint32_t)((1ull << L.rank_bits) - 1ull);
+    prof_begin(ST_COMPOSITE_BWD, st);
     composite_bwd<<<(unsigned)L.n_tiles, kTilePx, 0, st>>>(
         b.ranges, L.tile_passes & 1 ? b.ikey1 : b.ikey0, rank_mask, b.rec_sorted, b.p64, b.order0,
         dims.width, dims.height, L.tiles_x, d_rgb, d_depth, d_alpha, b.pix_cd, b.pix_t, b.pix_tlast,
         b.pix_last, b.g2d);
+    prof_end(ST_COMPOSITE_BWD, st);
+    count_launches(2);
     CamBwd cb;
     for (int k = 0; k < 9; k++) cb.r[k] = cam.r_wc[k];
     for (int k = 0; k < 3; k++) cb.t[k] = cam.t[k];
@@ -336,8 +340,10 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
     cb.fy = cam.fy;
     cb.cx = cam.cx;
     cb.cy = cam.cy;
+    prof_begin(ST_PROJECT_BWD, st);
     project_bwd<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
         reinterpret_cast<const float4 *>(params), slots, n, cb, b.order0, b.tcount_r, b.g2d, grads);
+    prof_end(ST_PROJECT_BWD, st);
     SM_CHECK_LAUNCH("render_backward");
     return SM_OK;
 }

@@ -13,6 +13,7 @@
 //     fp32 q lies within a per-Gaussian error band of 9.
 #include <cstdio>
 
+#include "prof.cuh"
 #include "render.cuh"
 #include "sort.cuh"
 
@@ -314,29 +315,41 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
     cudaMemsetAsync(b.ranges, 0, L.n_tiles * 8, st);
     if (n > 0) {
         const unsigned gb = (unsigned)ceil_div(n, 256);
+        prof_begin(ST_PROJECT, st);
         project_fwd<<<gb, 256, 0, st>>>(reinterpret_cast<const float4 *>(params), slots, n, cd,
                                         b.rec, b.p64, b.dkey0, b.order0, b.tcount);
+        prof_end(ST_PROJECT, st);
         SortScratch ss{b.sort_hist, b.sort_hist + (int64_t)kRadix * L.sort_blocks, L.sort_blocks};
         // global stable depth order (8 passes over the 64-bit key -> buffer 0)
+        prof_begin(ST_DEPTH_SORT, st);
         radix_sort<unsigned long long, true>(b.dkey0, b.order0, b.dkey1, b.order1, nullptr, n, n, 0,
                                              64, ss, st);
+        prof_end(ST_DEPTH_SORT, st);
+        prof_begin(ST_BIN, st);
         gather_by_rank<<<gb, 256, 0, st>>>(b.order0, n, b.rec, b.tcount, b.rec_sorted, b.tcount_r);
         exclusive_scan(b.tcount_r, b.toff, n, b.scan, &b.ctr->n_instances, st);
         check_instances<<<1, 1, 0, st>>>(b.ctr, dims.max_instances);
         emit_instances<<<gb, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.toff, n, b.ctr, L.rank_bits,
                                            L.tiles_x, b.ikey0);
+        prof_end(ST_BIN, st);
+        prof_begin(ST_TILE_SORT, st);
         const int cur = radix_sort<uint32_t, false>(
             b.ikey0, nullptr, b.ikey1, nullptr, &b.ctr->reserved[0], 0, dims.max_instances,
             L.rank_bits, L.rank_bits + L.tile_bits, ss, st);
         uint32_t *ik = cur ? b.ikey1 : b.ikey0;
         tile_ranges<<<(unsigned)ceil_div(dims.max_instances > 0 ? dims.max_instances : 1, 256), 256, 0,
                       st>>>(ik, b.ctr, L.rank_bits, b.ranges);
+        prof_end(ST_TILE_SORT, st);
+        count_launches(1 + 3 * L.depth_passes + 6 + 3 * L.tile_passes + 1);
     }
     const uint32_t rank_mask = (uint32_t)((1ull << L.rank_bits) - 1ull);
+    prof_begin(ST_COMPOSITE_FWD, st);
     composite_fwd<<<(unsigned)L.n_tiles, kTilePx, 0, st>>>(
         b.ranges, L.tile_passes & 1 ? b.ikey1 : b.ikey0, rank_mask, b.rec_sorted, b.p64, b.order0,
         dims.width, dims.height, L.tiles_x, out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t,
         b.pix_tlast, b.pix_last);
+    prof_end(ST_COMPOSITE_FWD, st);
+    count_launches(1);
     SM_CHECK_LAUNCH("render_forward");
     return SM_OK;
 }

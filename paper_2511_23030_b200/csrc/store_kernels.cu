@@ -3,6 +3,7 @@
 #include <cmath>
 
 #include "common.cuh"
+#include "prof.cuh"
 
 namespace sm {
 
@@ -74,9 +75,12 @@ int adam_step(float *params, float *m, float *v, float *grads, const int32_t *sl
     d.b2 = cfg.beta2;
     d.eps = cfg.eps;
     d.min_scale = cfg.min_scale;
+    prof_begin(ST_ADAM, st);
+    count_launches(1);
     adam_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
         reinterpret_cast<float4 *>(params), reinterpret_cast<float4 *>(m),
         reinterpret_cast<float4 *>(v), reinterpret_cast<float4 *>(grads), slots, n, d, skip);
+    prof_end(ST_ADAM, st);
     SM_CHECK_LAUNCH("adam_step");
     return SM_OK;
 }
@@ -138,7 +142,10 @@ int cull_chunks(const int32_t *coords, int64_t n, const double *planes, const do
     c.maxd = maxd;
     c.s = s;
     c.half = s / 2.0;
+    prof_begin(ST_CULL, st);
+    count_launches(1);
     cull_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(coords, n, c, out);
+    prof_end(ST_CULL, st);
     SM_CHECK_LAUNCH("cull_chunks");
     return SM_OK;
 }
@@ -171,6 +178,7 @@ int encode_positions(const float *params, int64_t n, double s, uint64_t *ids, in
     }
     cudaMemsetAsync(err, 0xff, sizeof(int64_t), st);   // -1 as u64 max
     if (n == 0) return SM_OK;
+    count_launches(1);
     encode_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
         params, n, s, s / 2.0, reinterpret_cast<unsigned long long *>(ids),
         reinterpret_cast<unsigned long long *>(err));
@@ -197,6 +205,7 @@ expand_kernel(const int64_t *__restrict__ off, const int64_t *__restrict__ cnt,
 int expand_segments(const int64_t *off, const int64_t *cnt, const int64_t *prefix, int64_t nseg,
                     int64_t total, int32_t *slots, cudaStream_t st) {
     if (total <= 0 || nseg <= 0) return SM_OK;
+    count_launches(1);
     expand_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, st>>>(off, cnt, prefix, nseg, total, slots);
     SM_CHECK_LAUNCH("expand_segments");
     return SM_OK;
@@ -302,8 +311,11 @@ int chunk_unpack(const uint8_t *rec, int64_t n, int64_t stride, float *params, f
     }
     cudaMemsetAsync(err, 0xff, sizeof(int64_t), st);
     if (n <= 0) return SM_OK;
+    prof_begin(ST_CODEC, st);
+    count_launches(1);
     unpack_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
         rec, n, stride, params, sh_rest, m, v, reinterpret_cast<unsigned long long *>(err));
+    prof_end(ST_CODEC, st);
     SM_CHECK_LAUNCH("chunk_unpack");
     return SM_OK;
 }
@@ -315,7 +327,10 @@ int chunk_pack(const float *params, const float *sh_rest, const float *m, const 
         return SM_ERR_INVALID;
     }
     if (n <= 0) return SM_OK;
+    prof_begin(ST_CODEC, st);
+    count_launches(1);
     pack_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(params, sh_rest, m, v, n, stride, rec);
+    prof_end(ST_CODEC, st);
     SM_CHECK_LAUNCH("chunk_pack");
     return SM_OK;
 }

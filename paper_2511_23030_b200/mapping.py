@@ -1,0 +1,386 @@
+"""The mapping step on the B200: drop-in for splatmap sim._Replay.optimization_step.
+
+One step (sim.py:319-370) keeps the reference's host policy -- candidate
+set, loss-weighted keyframe draw with derived seeds, keyframe tier access,
+visibility (VisibilityCache + K1), overlap, ensure_resident, loss record,
+metrics row with the deterministic cost model -- and replaces the
+render + loss + projected-residual nudge (sim.py:280-317) with the device
+pipeline: K2-K4 forward, fused loss forward/backward, K5-K6 backward and K7
+fused Adam over the active set, with a single 32-byte device->host read
+(loss + overflow flag) per step.
+
+Data-parallel mode (``optimization_step_dp``): K keyframes per step, rank r
+renders keyframes r, r+G, ...; gradients are summed with one NCCL
+all-reduce over the slab's used rows, then every rank applies the identical
+Adam update to its replica of the active tier.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .core import CameraIntrinsics, Keyframe, Pose
+from .culling import ChunkExtent, CullConfig, VisibilityCache
+from .errors import DeviceFailure, EmptyCandidates
+from .renderloss import LossEngine, LossWeights, RenderEngine, camera_for
+from .select import KeyframeIndex, SelectConfig, candidate_set, overlap, record_loss, select_keyframe
+from .store import ChunkStore
+
+__all__ = ["METRICS_HEADER", "FrameMetrics", "AdamSettings", "MappingEngine", "derive_seed"]
+
+METRICS_HEADER = ("frame,step,active_gaussians,active_chunks,active_keyframes,"
+                  "loads,evictions,io_ns,step_ns,selected_kf,overlap,loss")
+
+# Deterministic step-cost model (sim.py:53-57)
+NS_PER_RENDERED_GAUSSIAN = 150
+NS_PER_PIXEL = 40
+NS_PER_INSERTED_GAUSSIAN = 300
+NS_STEP_BASE = 20_000
+
+
+def derive_seed(master: int, purpose: int, counter: int) -> int:
+    """sim.py:158 _derive_seed."""
+    return int(np.random.SeedSequence([master, purpose, counter]).generate_state(1)[0])
+
+
+@dataclass
+class FrameMetrics:
+    frame: int
+    step: int
+    active_gaussians: int
+    active_chunks: int
+    active_keyframes: int
+    loads: int
+    evictions: int
+    io_ns: int
+    step_ns: int
+    selected_kf: int
+    overlap: float | None
+    loss: float
+
+    def csv_row(self) -> str:
+        ov = "" if self.overlap is None else f"{self.overlap:.9g}"
+        return (f"{self.frame},{self.step},{self.active_gaussians},{self.active_chunks},"
+                f"{self.active_keyframes},{self.loads},{self.evictions},{self.io_ns},"
+                f"{self.step_ns},{self.selected_kf},{ov},{self.loss:.9g}")
+
+
+@dataclass
+class AdamSettings:
+    """Per-scalar learning rates on the stored (activated) parameters."""
+
+    lr_position: float = 1e-4
+    lr_rotation: float = 1e-3
+    lr_scale: float = 5e-5
+    lr_opacity: float = 1e-2
+    lr_sh0: float = 2.5e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-15
+    min_scale: float = 1e-5
+
+    def to_c(self) -> _lib.AdamConfig:
+        c = _lib.AdamConfig()
+        lrs = [self.lr_position] * 3 + [self.lr_rotation] * 4 + [self.lr_scale] * 3 + \
+              [self.lr_opacity] + [self.lr_sh0] * 3
+        for k, v in enumerate(lrs):
+            c.lr[k] = v
+        c.beta1, c.beta2, c.eps, c.min_scale = self.beta1, self.beta2, self.eps, self.min_scale
+        return c
+
+
+class _ActiveSet:
+    """Slot list of the visible chunks (sorted ids), cached by segment layout."""
+
+    def __init__(self, device):
+        import torch
+        self.torch = torch
+        self.device = device
+        self.key = None
+        self.slots = torch.empty(0, dtype=torch.int32, device=device)
+        self.n = 0
+
+    def build(self, segments: list[tuple[int, int]]):
+        key = tuple(segments)
+        if key == self.key:
+            return self.slots, self.n
+        torch = self.torch
+        counts = np.array([c for _, c in segments], dtype=np.int64)
+        offs = np.array([o for o, _ in segments], dtype=np.int64)
+        total = int(counts.sum())
+        if total:
+            prefix = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
+            if self.slots.numel() < total:
+                self.slots = torch.empty(int(total * 1.25) + 1024, dtype=torch.int32, device=self.device)
+            meta = torch.as_tensor(np.stack([offs, counts, prefix]), device=self.device)
+            rc = _lib.load().sm_expand_segments(_lib.ptr(meta[0]), _lib.ptr(meta[1]), _lib.ptr(meta[2]),
+                                                len(segments), total, _lib.ptr(self.slots),
+                                                _lib.stream_handle())
+            _lib.check(rc, "expand_segments")
+        self.key, self.n = key, total
+        return self.slots, total
+
+
+@dataclass
+class _DeviceKeyframe:
+    rgb_u8: object
+    depth: object
+
+
+class MappingEngine:
+    """Owns the device pipeline of the mapping step for one store / camera.
+
+    Mirrors splatmap sim._Replay's state (sim.py:199-225): the store, the
+    visibility cache, the keyframe index, the latest keyframe and the step
+    counter driving the derived seeds.
+    """
+
+    def __init__(self, store: ChunkStore, intr: CameraIntrinsics, seed: int = 7,
+                 cull: CullConfig | None = None, select: SelectConfig | None = None,
+                 weights: LossWeights | None = None, adam: AdamSettings | None = None,
+                 comm=None):
+        import torch
+        self.torch = torch
+        self.store = store
+        self.intr = intr
+        self.seed = seed
+        self.cull_cfg = cull or CullConfig()
+        self.cache = VisibilityCache(cfg=self.cull_cfg)
+        self.index = KeyframeIndex(config=select or SelectConfig())
+        self.weights = weights or LossWeights()
+        self.adam = adam or AdamSettings()
+        self._adam_c = self.adam.to_c()
+        self.comm = comm
+        self.latest_kf: int | None = None
+        self.step_counter = 0
+        self.rows: list[FrameMetrics] = []
+        dev = store.slab.device
+        self.device = dev
+        self.render = RenderEngine(dev)
+        self.loss = LossEngine(dev)
+        self.active = _ActiveSet(dev)
+        h, w = intr.height, intr.width
+        self.rgb = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
+        self.depth = torch.empty((h, w), dtype=torch.float32, device=dev)
+        self.alpha = torch.empty((h, w), dtype=torch.float32, device=dev)
+        self.d_rgb = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
+        self.d_depth = torch.empty((h, w), dtype=torch.float32, device=dev)
+        self._kf_dev: dict[int, _DeviceKeyframe] = {}
+        self._readback = torch.zeros(8, dtype=torch.float32, pin_memory=True)
+        self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.cam = None
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+        self.upload_keyframes_each_step = False   # e2e mode: GT from pinned host every step
+        self._pinned_kf: dict[int, tuple] = {}
+
+    # -------------------------------------------------------------- inputs
+    def add_keyframe(self, kf: Keyframe, index_usage: int | None = None) -> None:
+        """store.keyframe_add + index.add (sim.py:264-268), without ingestion."""
+        self.store.keyframe_add(kf)
+        self.index.add(kf.id, kf.position,
+                       usage_remaining=self.index.config.initial_usage if index_usage is None else index_usage)
+        self.latest_kf = kf.id
+
+    def _device_keyframe(self, kf: Keyframe) -> _DeviceKeyframe:
+        torch = self.torch
+        if self.upload_keyframes_each_step:
+            pin = self._pinned_kf.get(kf.id)
+            if pin is None:
+                pin = (torch.from_numpy(kf.rgb_u8()).pin_memory(), torch.from_numpy(kf.depth).pin_memory())
+                self._pinned_kf[kf.id] = pin
+            d = self._kf_dev.get(-1)
+            if d is None:
+                d = self._kf_dev[-1] = _DeviceKeyframe(torch.empty_like(pin[0], device=self.device),
+                                                       torch.empty_like(pin[1], device=self.device))
+            d.rgb_u8.copy_(pin[0], non_blocking=True)
+            d.depth.copy_(pin[1], non_blocking=True)
+            self.h2d_bytes += pin[0].numel() + 4 * pin[1].numel()
+            return d
+        d = self._kf_dev.get(kf.id)
+        if d is None:
+            d = _DeviceKeyframe(torch.as_tensor(kf.rgb_u8(), device=self.device),
+                                torch.as_tensor(kf.depth, device=self.device))
+            self._kf_dev[kf.id] = d
+        return d
+
+    def _visible_for_pose(self, pose: Pose) -> tuple[set[int], bool]:
+        ext = self.store.coord_extent()
+        if ext is None:
+            return set(), False
+        return self.cache.query(pose, self.intr, ChunkExtent(*ext), self.store.has_chunk,
+                                self.store.generation, self.store.chunk_size,
+                                candidates=self.store.known_chunk_ids())
+
+    # ------------------------------------------------------------ device
+    def _device_pass(self, kf: Keyframe, slots, n: int, backward: bool = True):
+        """fwd -> loss(+grad) -> bwd for one keyframe; grads accumulate in the slab."""
+        slab = self.store.slab
+        cam = camera_for(kf.pose, kf.intrinsics)
+        dk = self._device_keyframe(kf)
+        self.render.forward(slab.params, slots, n, cam, self.rgb, self.depth, self.alpha)
+        self.loss.run(self.rgb, self.depth, dk.rgb_u8, None, dk.depth, 3, self.weights,
+                      self.d_rgb if backward else None, self.d_depth if backward else None)
+        if backward and n:
+            self.render.backward(slab.params, slots, n, cam, self.d_rgb, self.d_depth, None, slab.grads)
+
+    def _adam(self, slots, n: int) -> None:
+        s = self.store.slab
+        rc = _lib.load().sm_adam_step(_lib.ptr(s.params), _lib.ptr(s.adam_m), _lib.ptr(s.adam_v),
+                                      _lib.ptr(s.grads), _lib.ptr(slots), int(n),
+                                      self._adam_c, _lib.ptr(self.render.overflow_flag()),
+                                      _lib.stream_handle())
+        _lib.check(rc, "adam_step")
+
+    def _read_loss(self) -> tuple[float, bool]:
+        """One D2H copy of {loss[4], n_instances, overflow} into pinned memory + sync."""
+        rb = self._readback
+        rb[:4].copy_(self.loss.out, non_blocking=True)
+        rb[4:6].copy_(self.render.ws[:8].view(self.torch.float32), non_blocking=True)
+        self.torch.cuda.current_stream(self.device).synchronize()
+        self.d2h_bytes += 24
+        v = rb.numpy()
+        ctr = v[4:6].view(np.uint32)
+        self.counter_instances += int(ctr[0])
+        return float(v[0]), bool(ctr[1])
+
+    def reset_counters(self) -> None:
+        self.counter_steps = 0
+        self.counter_gaussians = 0
+        self.counter_instances = 0
+
+    counter_steps = counter_gaussians = counter_instances = 0
+
+    def train_view(self, kf: Keyframe, slots, n: int) -> float:
+        """One device iteration with overflow recovery; returns the loss."""
+        for _ in range(6):
+            self._device_pass(kf, slots, n)
+            self._adam(slots, n)
+            loss, overflow = self._read_loss()
+            if not overflow:
+                self.counter_steps += 1
+                self.counter_gaussians += n
+                return loss
+            self.store.slab.grads.zero_()
+            self.render.grow_instances(self.render.counters()["n_instances"])
+        raise DeviceFailure("tile-instance buffer kept overflowing")
+
+    # --------------------------------------------------------------- step
+    def optimization_step(self, frame_idx: int, step_idx: int, inserted: int = 0) -> FrameMetrics:
+        store, stats = self.store, self.store.stats
+        io0, loads0, ev0 = stats.io_nanos, stats.chunk_loads, stats.chunk_evictions
+        if self.latest_kf is None:
+            raise RuntimeError("no keyframe ingested yet")
+        try:
+            candidates = candidate_set(self.index.position_of(self.latest_kf), self.index)
+        except EmptyCandidates:
+            candidates = [self.latest_kf]
+        selected = select_keyframe(candidates, self.index, derive_seed(self.seed, 2, self.step_counter))
+        kf = store.keyframe_get(selected)
+        visible, _ = self._visible_for_pose(kf.pose)
+        overlap_val = overlap(visible, store.resident_chunk_ids()) if visible else None
+        ids = sorted(visible)
+        if ids:
+            store.ensure_resident(ids)
+        slots, n = self.active.build(store.segments(ids))
+        loss = self.train_view(kf, slots, n)
+        record_loss(selected, loss, self.index)
+        kf.last_loss = loss
+        kf.usage_remaining = self.index.usage_of(selected)
+        store.mark_keyframe_dirty(selected)
+        if ids:
+            store.mark_trained(ids)
+        self.step_counter += 1
+        io = stats.io_nanos - io0
+        step_ns = (io + NS_PER_RENDERED_GAUSSIAN * n + NS_PER_PIXEL * self.intr.width * self.intr.height
+                   + NS_PER_INSERTED_GAUSSIAN * inserted + NS_STEP_BASE)
+        row = FrameMetrics(frame_idx, step_idx, stats.active_gaussians, stats.active_chunks,
+                           stats.active_keyframes, stats.chunk_loads - loads0,
+                           stats.chunk_evictions - ev0, io, step_ns, selected, overlap_val, loss)
+        self.rows.append(row)
+        return row
+
+    # ------------------------------------------------------ data parallel
+    def optimization_step_dp(self, frame_idx: int, step_idx: int, world: int, rank: int,
+                             group=None, inserted: int = 0) -> list[FrameMetrics]:
+        """One data-parallel mapping step: `world` keyframes, one per rank.
+
+        Every rank runs the same host policy (same derived seeds), so the
+        keyframe draws, visible sets and residency of the replicated active
+        tier are identical everywhere.  Rank r renders and backpropagates
+        keyframe r; the slab gradients are summed with one NCCL all-reduce,
+        the per-keyframe losses travel in a second tiny all-reduce, and each
+        rank applies the same Adam update over the union active set.
+        """
+        import torch.distributed as dist
+        torch = self.torch
+        store, stats = self.store, self.store.stats
+        io0, loads0, ev0 = stats.io_nanos, stats.chunk_loads, stats.chunk_evictions
+        try:
+            candidates = candidate_set(self.index.position_of(self.latest_kf), self.index)
+        except EmptyCandidates:
+            candidates = [self.latest_kf]
+        selected = [select_keyframe(candidates, self.index,
+                                    derive_seed(self.seed, 2, self.step_counter * world + r))
+                    for r in range(world)]
+        kfs = [store.keyframe_get(s) for s in selected]
+        vis = [self._visible_for_pose(kf.pose)[0] for kf in kfs]
+        union = sorted(set().union(*vis))
+        overlap_val = overlap(set(union), store.resident_chunk_ids()) if union else None
+        if union:
+            store.ensure_resident(union)
+        if not hasattr(self, "_union_set"):
+            self._union_set = _ActiveSet(self.device)
+            self._lossbuf = torch.zeros(world + 1, dtype=torch.float32, device=self.device)
+        mine = sorted(vis[rank])
+        slots_m, n_m = self.active.build(store.segments(mine))
+        slots_u, n_u = self._union_set.build(store.segments(union))
+        slab = store.slab
+        for _ in range(6):
+            self._device_pass(kfs[rank], slots_m, n_m)
+            buf = self._lossbuf
+            buf.zero_()
+            buf[rank:rank + 1].copy_(self.loss.out[:1])
+            buf[world:world + 1].copy_(self.render.overflow_flag().float())
+            dist.all_reduce(slab.grads[:slab.high_water()], group=group)
+            dist.all_reduce(buf, group=group)
+            host = buf.cpu().numpy()
+            self.d2h_bytes += 4 * (world + 1)
+            if host[world] == 0:
+                break
+            slab.grads.zero_()
+            self.render.grow_instances(self.render.counters()["n_instances"] * 2)
+        else:
+            raise DeviceFailure("tile-instance buffer kept overflowing")
+        self._adam_noskip(slots_u, n_u)
+        self.counter_steps += 1
+        self.counter_gaussians += n_m
+        rows = []
+        for r, (sel, kf) in enumerate(zip(selected, kfs)):
+            loss = float(host[r])
+            record_loss(sel, loss, self.index)
+            kf.last_loss = loss
+            kf.usage_remaining = self.index.usage_of(sel)
+            if sel in store.resident_keyframe_ids():
+                store.mark_keyframe_dirty(sel)
+            io = stats.io_nanos - io0
+            step_ns = (io + NS_PER_RENDERED_GAUSSIAN * n_u + NS_PER_PIXEL * self.intr.width *
+                       self.intr.height * world + NS_PER_INSERTED_GAUSSIAN * inserted + NS_STEP_BASE)
+            rows.append(FrameMetrics(frame_idx, step_idx, stats.active_gaussians, stats.active_chunks,
+                                     stats.active_keyframes, stats.chunk_loads - loads0,
+                                     stats.chunk_evictions - ev0, io, step_ns, sel, overlap_val, loss))
+        if union:
+            store.mark_trained(union)
+        self.step_counter += 1
+        self.rows.extend(rows)
+        return rows
+
+    def _adam_noskip(self, slots, n: int) -> None:
+        s = self.store.slab
+        rc = _lib.load().sm_adam_step(_lib.ptr(s.params), _lib.ptr(s.adam_m), _lib.ptr(s.adam_v),
+                                      _lib.ptr(s.grads), _lib.ptr(slots), int(n), self._adam_c, None,
+                                      _lib.stream_handle())
+        _lib.check(rc, "adam_step")
