@@ -181,6 +181,13 @@ long long sm_launch_count(void);
 int sm_profile_stage_count(void);
 const char *sm_profile_stage_name(int stage);
 int sm_profile_collect(double *ms_out, long long *calls_out);
+/* CUDA-graph capture of the step: stage events and kernel counts recorded
+ * while capturing are filed under the returned graph id; after each replay
+ * completes, sm_profile_graph_replayed(gid) accounts them again. */
+int sm_profile_capture_begin(void);
+void sm_profile_capture_end(void);
+void sm_profile_graph_replayed(int gid);
+void sm_profile_graph_free(int gid);
 
 #ifdef __cplusplus
 }

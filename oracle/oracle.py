@@ -172,20 +172,91 @@ class TrainState:
         self.v = np.zeros((n, 14))
         self.steps = np.zeros(n, dtype=np.int64)
 
+    FIELDS = ("pos", "rot", "scale", "opac", "sh0", "m", "v", "steps")
+
     def step(self, pose_rotation, pose_translation, intr, gt_rgb, gt_depth, lambda_s, lambda_depth,
-             lr14, beta1, beta2, eps, min_scale, threads=None) -> float:
-        """One CPU mapping iteration (fwd, loss+grad, bwd, Adam); returns the loss."""
+             lr14, beta1, beta2, eps, min_scale, threads=None, subset=None) -> float:
+        """One CPU mapping iteration (fwd, loss+grad, bwd, Adam); returns the loss.
+
+        subset: optional index array of the active set (sim.py:236-253 order);
+        only those Gaussians are rendered and updated.
+        """
         r_wc = _c(quat_to_matrix(pose_rotation))
         t = _c(pose_translation, (3,))
         h, w = intr.height, intr.width
         gt = _c(gt_rgb, (h, w, 3))
         gd = _c(gt_depth, (h, w))
         lr = _c(lr14, (14,))
-        return float(lib().or_train_step(
-            self.n, _p(self.pos), _p(self.rot), _p(self.scale), _p(self.opac), _p(self.sh0), _p(r_wc),
+        if subset is None:
+            a = {f: getattr(self, f) for f in self.FIELDS}
+            n = self.n
+        else:
+            a = {f: np.ascontiguousarray(getattr(self, f)[subset]) for f in self.FIELDS}
+            n = len(subset)
+        loss = float(lib().or_train_step(
+            n, _p(a["pos"]), _p(a["rot"]), _p(a["scale"]), _p(a["opac"]), _p(a["sh0"]), _p(r_wc),
             _p(t), intr.fx, intr.fy, intr.cx, intr.cy, intr.near, w, h, _p(gt), _p(gd), lambda_s,
-            lambda_depth, _p(lr), beta1, beta2, eps, min_scale, _p(self.m), _p(self.v),
-            self.steps.ctypes.data_as(_i64p), threads or default_threads()))
+            lambda_depth, _p(lr), beta1, beta2, eps, min_scale, _p(a["m"]), _p(a["v"]),
+            a["steps"].ctypes.data_as(_i64p), threads or default_threads()))
+        if subset is not None:
+            for f in self.FIELDS:
+                getattr(self, f)[subset] = a[f]
+        return loss
+
+
+def frustum_planes(pose_rotation, pose_translation, intr) -> np.ndarray:
+    """culling.py:80-101 extract_frustum (same NumPy expression sequence)."""
+    w, h = float(intr.width), float(intr.height)
+    cams = [(np.array([0.0, 0.0, 1.0]), -intr.near), (np.array([0.0, 0.0, -1.0]), intr.far),
+            (np.array([intr.fx, 0.0, intr.cx]), 0.0), (np.array([-intr.fx, 0.0, w - intr.cx]), 0.0),
+            (np.array([0.0, intr.fy, intr.cy]), 0.0), (np.array([0.0, -intr.fy, h - intr.cy]), 0.0)]
+    r = quat_to_matrix(pose_rotation)
+    t = np.asarray(pose_translation, dtype=np.float64)
+    rows = []
+    for n, d in cams:
+        nw = r @ (n / np.linalg.norm(n))
+        rows.append([*nw, d - float(nw @ t)])
+    return np.array(rows)
+
+
+def visible_chunk_mask(coords, pose_rotation, pose_translation, intr, max_distance, s) -> np.ndarray:
+    """Brute-force chunk visibility (culling.py:104-131; the reference's own
+    test oracle, test_acceptance.py:74-95): p-vertex outside test + nearest
+    AABB point distance, vectorised over an (M, 3) integer coord table."""
+    coords = np.asarray(coords, dtype=np.float64)
+    planes = frustum_planes(pose_rotation, pose_translation, intr)
+    cam = np.asarray(pose_translation, dtype=np.float64)
+    mins, maxs = coords * s - s / 2.0, coords * s + s / 2.0
+    outside = np.zeros(len(coords), dtype=bool)
+    for nx, ny, nz, d in planes:
+        px = np.where(nx >= 0, maxs[:, 0], mins[:, 0])
+        py = np.where(ny >= 0, maxs[:, 1], mins[:, 1])
+        pz = np.where(nz >= 0, maxs[:, 2], mins[:, 2])
+        outside |= (nx * px + ny * py + nz * pz + d) < 0.0
+    nearest = np.clip(cam, mins, maxs)
+    dist = np.sqrt(((cam - nearest) ** 2).sum(axis=1))
+    return ~outside & (dist <= max_distance)
+
+
+def chunk_ids(positions, s) -> np.ndarray:
+    """grid.py:110-121 encode_positions."""
+    c = np.floor((np.asarray(positions, dtype=np.float64) + s / 2.0) / s)
+    u = (c + float(1 << 20)).astype(np.uint64)
+    return (u[:, 0] << np.uint64(42)) | (u[:, 1] << np.uint64(21)) | u[:, 2]
+
+
+def active_set(positions, pose_rotation, pose_translation, intr, max_distance, s) -> np.ndarray:
+    """Indices of the Gaussians in visible chunks, in sorted-chunk-id order
+    (stable within a chunk) -- the SoA concatenation of sim.py:236-253."""
+    ids = chunk_ids(positions, s)
+    uniq, inv = np.unique(ids, return_inverse=True)
+    m = np.uint64((1 << 21) - 1)
+    coords = np.stack([(uniq >> np.uint64(42)) & m, (uniq >> np.uint64(21)) & m, uniq & m], 1)
+    coords = coords.astype(np.int64) - (1 << 20)
+    vis = visible_chunk_mask(coords, pose_rotation, pose_translation, intr, max_distance, s)
+    keep = vis[inv]
+    order = np.argsort(ids, kind="stable")
+    return order[keep[order]]
 
 
 def adam(param, m, v, grad, lr, beta1, beta2, eps, step):

@@ -91,6 +91,10 @@ def load():
     _sig(lib.sm_profile_stage_count, c_int)
     _sig(lib.sm_profile_stage_name, ctypes.c_char_p, c_int)
     _sig(lib.sm_profile_collect, c_int, POINTER(c_double), POINTER(ctypes.c_longlong))
+    _sig(lib.sm_profile_capture_begin, c_int)
+    _sig(lib.sm_profile_capture_end, None)
+    _sig(lib.sm_profile_graph_replayed, None, c_int)
+    _sig(lib.sm_profile_graph_free, None, c_int)
     if lib.sm_abi_version() != ABI_VERSION:
         raise DeviceFailure(f"ABI mismatch: library {lib.sm_abi_version()} != {ABI_VERSION}")
     _lib = lib

@@ -89,6 +89,24 @@ __device__ __forceinline__ bool pair_eval(const ProjRec &g, int px, int py, cons
     return d >= 0.f;
 }
 
+// Two-pixel variant used by the compositing kernels: the column test and dx
+// are shared by the thread's pixel pair (same px, rows py and py + 1).
+// Same expression and decision order as pair_eval, so results are identical.
+__device__ __forceinline__ bool row_eval(const ProjRec &g, float dx, int px, int py, int y0, int y1,
+                                         const Proj64 *p64, const uint32_t *order, uint32_t rank,
+                                         float &dy, float &pw) {
+    if ((unsigned)(py - y0) > (unsigned)(y1 - y0)) return false;
+    dy = (float)(py - y0) + g.oy;
+    pw = dx * (g.ia * dx + 2.f * g.ib * dy) + g.ic * dy * dy;
+    const float d = pw - kPowCut;
+    if (fabsf(d) <= g.eps) return !(quad_q64(p64[order[rank]], px, py) > 9.0);
+    return d >= 0.f;
+}
+
+// Compositing CTA: one 16x16 tile, 128 threads, each thread owns the pixel
+// pair (px, py), (px, py + 1); warp w covers tile rows 4w .. 4w + 3.
+constexpr int kCompThreads = 128;
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t align_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 

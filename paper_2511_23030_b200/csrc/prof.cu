@@ -30,6 +30,16 @@ static const char *kNames[ST_COUNT] = {"project_fwd", "depth_sort", "bin_emit", 
                                        "composite_fwd", "loss", "composite_bwd", "project_bwd",
                                        "adam", "cull", "codec"};
 
+// CUDA-graph support: while a graph is being captured, stage event pairs and
+// kernel counts are filed under the graph id; every replay re-records the
+// same events, so after a replay completes the host accumulates them again.
+struct GraphProf {
+    std::vector<Pending> pairs;
+    long long launches = 0;
+};
+static std::vector<GraphProf> g_graphs;
+static int g_capture_gid = -1;
+
 static cudaEvent_t take_event() {
     if (!g_pool.empty()) {
         cudaEvent_t e = g_pool.back();
@@ -56,8 +66,18 @@ void prof_end(Stage s, cudaStream_t st) {
     if (!g_is_open[s]) return;
     cudaEvent_t e = take_event();
     cudaEventRecord(e, st);
-    g_pending.push_back({(int)s, g_open[s], e});
+    if (g_capture_gid >= 0)
+        g_graphs[g_capture_gid].pairs.push_back({(int)s, g_open[s], e});
+    else
+        g_pending.push_back({(int)s, g_open[s], e});
     g_is_open[s] = false;
+}
+
+void count_launches(long long n) {
+    if (g_capture_gid >= 0)
+        g_graphs[g_capture_gid].launches += n;   // executed (and counted) at each replay
+    else
+        g_launches.fetch_add(n, std::memory_order_relaxed);
 }
 
 }  // namespace sm
@@ -72,6 +92,47 @@ void sm_profile_enable(int on) {
 }
 
 long long sm_launch_count(void) { return g_launches.load(); }
+
+// Begin filing stage events / launch counts under a new graph id (returned).
+int sm_profile_capture_begin(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_graphs.emplace_back();
+    g_capture_gid = (int)g_graphs.size() - 1;
+    return g_capture_gid;
+}
+
+void sm_profile_capture_end(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_capture_gid = -1;
+}
+
+// Called after a replay of graph `gid` has completed (stream synchronised):
+// adds its kernel count and, when profiling is on, its stage times.
+void sm_profile_graph_replayed(int gid) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (gid < 0 || gid >= (int)g_graphs.size()) return;
+    GraphProf &g = g_graphs[gid];
+    g_launches.fetch_add(g.launches, std::memory_order_relaxed);
+    if (!g_prof_on) return;
+    for (const Pending &p : g.pairs) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+            g_ms[p.stage] += ms;
+            g_calls[p.stage] += 1;
+        }
+    }
+}
+
+void sm_profile_graph_free(int gid) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (gid < 0 || gid >= (int)g_graphs.size()) return;
+    for (const Pending &p : g_graphs[gid].pairs) {
+        g_pool.push_back(p.a);
+        g_pool.push_back(p.b);
+    }
+    g_graphs[gid].pairs.clear();
+    g_graphs[gid].launches = 0;
+}
 
 int sm_profile_stage_count(void) { return ST_COUNT; }
 

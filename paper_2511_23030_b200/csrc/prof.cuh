@@ -25,7 +25,8 @@ extern std::atomic<long long> g_launches;
 void prof_begin(Stage s, cudaStream_t st);
 void prof_end(Stage s, cudaStream_t st);
 
-// count n kernel launches issued by this library
-inline void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+// count n kernel launches issued by this library (filed under the graph being
+// captured, if any, so replays are counted too)
+void count_launches(long long n);
 
 }  // namespace sm

@@ -53,7 +53,79 @@ __device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
     return v[0];   // value index ((lane>>4)&1)*8 + ((lane>>3)&1)*4 + ((lane>>2)&1)*2 + ((lane>>1)&1)
 }
 
-__global__ void __launch_bounds__(kTilePx)
+// Per-pixel reverse state.  T holds T_{k+1} while walking back; the stored
+// T before the last contributor seeds T_k at k == last (alpha = 1 safe).
+struct BwdPix {
+    float gCr, gCg, gCb, gD, gA;   // dL/d{C, D, A} of the raw accumulators
+    float T, tlast, Br, Bg, Bb, Bz, P;
+    int32_t last;
+
+    __device__ __forceinline__ void init(bool inside, int64_t p, const float *d_rgb,
+                                         const float *d_depth, const float *d_alpha,
+                                         const float4 *st_cd, const float *st_t,
+                                         const float *st_tlast, const int32_t *st_last) {
+        gCr = gCg = gCb = gD = gA = 0.f;
+        T = tlast = 0.f;
+        Br = Bg = Bb = Bz = 0.f;
+        P = 1.f;
+        last = -1;
+        if (!inside) return;
+        const float4 cd = st_cd[p];
+        T = st_t[p];
+        tlast = st_tlast[p];
+        last = st_last[p];
+        const float A = 1.f - T;
+        if (d_rgb) {   // rgb = clip(C) (renderloss.py:218): zero gradient outside [0,1]
+            gCr = (cd.x >= 0.f && cd.x <= 1.f) ? d_rgb[3 * p + 0] : 0.f;
+            gCg = (cd.y >= 0.f && cd.y <= 1.f) ? d_rgb[3 * p + 1] : 0.f;
+            gCb = (cd.z >= 0.f && cd.z <= 1.f) ? d_rgb[3 * p + 2] : 0.f;
+        }
+        if (d_alpha && A >= 0.f && A <= 1.f) gA = d_alpha[p];
+        if (d_depth && A > 0.f) {   // depth = D / A (renderloss.py:217)
+            const float dd = d_depth[p];
+            gD = dd / A;
+            gA += -dd * cd.w / (A * A);
+        }
+    }
+
+    // Accumulates this pixel's d{u v ia ib ic op r g b z} into v and steps back.
+    __device__ __forceinline__ void step(const ProjRec &g, float dx, float dy, float pw, int k,
+                                         float (&v)[16]) {
+        const float G = ex2_approx(pw);
+        const float alpha = g.op * G;
+        const float oma = 1.f - alpha;
+        const float Tk = (k == last) ? tlast : __fdividef(T, oma);
+        float ga = (g.r - Br) * gCr + (g.g - Bg) * gCg + (g.b - Bb) * gCb + (g.z - Bz) * gD;
+        ga = Tk * (ga + gA * P);
+        const float wt = Tk * alpha;
+        v[6] += wt * gCr;
+        v[7] += wt * gCg;
+        v[8] += wt * gCb;
+        v[9] += wt * gD;
+        v[5] += ga * G;
+        // q = pw / kPowScale; conic grads are w.r.t. the unscaled conic
+        const float gq = -0.5f * alpha * ga;
+        v[2] += gq * dx * dx;
+        v[3] += gq * 2.f * dx * dy;
+        v[4] += gq * dy * dy;
+        const float gqi = gq * (float)(-2.0 / kPowScale);
+        v[0] += gqi * (g.ia * dx + g.ib * dy);
+        v[1] += gqi * (g.ib * dx + g.ic * dy);
+        Br = alpha * g.r + oma * Br;
+        Bg = alpha * g.g + oma * Bg;
+        Bb = alpha * g.b + oma * Bb;
+        Bz = alpha * g.z + oma * Bz;
+        P *= oma;
+        T = Tk;
+    }
+};
+
+// Same tiling as composite_fwd (128 threads x 2 pixels).  Instances are
+// revisited from the block's last contributor back to the tile start, 128
+// per shared-memory batch; a warp skips splats missing its 4 rows or lying
+// past every one of its pixels' last contributor.
+template <int PIX>
+__global__ void __launch_bounds__(kTilePx / PIX)
 composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ikeys,
               uint32_t rank_mask, const ProjRec *__restrict__ recs,
               const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
@@ -62,48 +134,36 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
               const float4 *__restrict__ st_cd, const float *__restrict__ st_t,
               const float *__restrict__ st_tlast, const int32_t *__restrict__ st_last,
               float *__restrict__ g2d) {
-    __shared__ ProjRec s_rec[kTilePx];
-    __shared__ uint32_t s_rank[kTilePx];
-    __shared__ float s_grad[kTilePx][10];
+    constexpr int NT = kTilePx / PIX;
+    __shared__ ProjRec s_rec[NT];
+    __shared__ uint32_t s_rank[NT];
+    __shared__ float s_grad[NT][10];
     __shared__ int s_maxlast;
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31;
+    const int ty0 = (tile / tiles_x) * kTile;
     const int px = (tile % tiles_x) * kTile + (threadIdx.x & (kTile - 1));
-    const int py = (tile / tiles_x) * kTile + (threadIdx.x / kTile);
-    const bool inside = px < width && py < height;
+    const int py = ty0 + PIX * (threadIdx.x / kTile);
+    const int wy0 = ty0 + 2 * PIX * (threadIdx.x / 32);
     const int start = (int)ranges[2 * tile];
-    float gCr = 0.f, gCg = 0.f, gCb = 0.f, gD = 0.f, gA = 0.f, T = 0.f, tlast = 0.f;
-    int last = -1;
-    if (inside) {
-        const int64_t p = (int64_t)py * width + px;
-        const float4 cd = st_cd[p];
-        T = st_t[p];
-        tlast = st_tlast[p];
-        last = st_last[p];
-        const float A = 1.f - T;
-        if (d_rgb) {
-            gCr = (cd.x >= 0.f && cd.x <= 1.f) ? d_rgb[3 * p + 0] : 0.f;
-            gCg = (cd.y >= 0.f && cd.y <= 1.f) ? d_rgb[3 * p + 1] : 0.f;
-            gCb = (cd.z >= 0.f && cd.z <= 1.f) ? d_rgb[3 * p + 2] : 0.f;
-        }
-        if (d_alpha && A >= 0.f && A <= 1.f) gA = d_alpha[p];
-        if (d_depth && A > 0.f) {
-            const float dd = d_depth[p];
-            gD = dd / A;
-            gA += -dd * cd.w / (A * A);
-        }
+    BwdPix s[PIX];
+    int wmax = -1;
+#pragma unroll
+    for (int i = 0; i < PIX; i++) {
+        s[i].init(px < width && py + i < height, (int64_t)(py + i) * width + px, d_rgb, d_depth,
+                  d_alpha, st_cd, st_t, st_tlast, st_last);
+        wmax = max(wmax, s[i].last);
     }
     if (threadIdx.x == 0) s_maxlast = -1;
     __syncthreads();
-    int wmax = last;
 #pragma unroll
     for (int o = 16; o; o >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
     if (lane == 0) atomicMax(&s_maxlast, wmax);
     __syncthreads();
     const int maxlast = s_maxlast;
-    float Br = 0.f, Bg = 0.f, Bb = 0.f, Bz = 0.f, P = 1.f;
-    for (int bend = maxlast + 1; bend > start; bend -= kTilePx) {
-        const int bstart = max(start, bend - kTilePx);
+    const int vi = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+    for (int bend = maxlast + 1; bend > start; bend -= NT) {
+        const int bstart = max(start, bend - NT);
         const int idx = bstart + (int)threadIdx.x;
         if (idx < bend) {
             const uint32_t rk = ikeys[idx] & rank_mask;
@@ -116,45 +176,28 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
         const int jtop = min(bend - 1, wmax) - bstart;
         for (int j = jtop; j >= 0; j--) {
             const ProjRec &g = s_rec[j];
+            const int y0 = rec_y0(g), y1 = rec_y1(g);
+            if (y1 < wy0 || y0 > wy0 + 2 * PIX - 1) continue;   // warp-uniform row cull
             const int k = bstart + j;
             float v[16];
 #pragma unroll
             for (int t = 0; t < 16; t++) v[t] = 0.f;
             bool hit = false;
-            float dx, dy, pw;
-            if (k <= last && pair_eval(g, px, py, p64, order, s_rank[j], dx, dy, pw)) {
-                hit = true;
-                const float G = ex2_approx(pw);
-                const float alpha = g.op * G;
-                const float oma = 1.f - alpha;
-                const float Tk = (k == last) ? tlast : T / oma;
-                float ga = (g.r - Br) * gCr + (g.g - Bg) * gCg + (g.b - Bb) * gCb + (g.z - Bz) * gD;
-                ga = Tk * (ga + gA * P);
-                const float wt = Tk * alpha;
-                v[6] = wt * gCr;
-                v[7] = wt * gCg;
-                v[8] = wt * gCb;
-                v[9] = wt * gD;
-                v[5] = ga * G;
-                // q = pw / kPowScale; conic grads are w.r.t. the unscaled conic
-                const float gq = -0.5f * alpha * ga;
-                v[2] = gq * dx * dx;
-                v[3] = gq * 2.f * dx * dy;
-                v[4] = gq * dy * dy;
-                const float inv = (float)(2.0 / kPowScale);
-                v[0] = -gq * inv * (g.ia * dx + g.ib * dy);
-                v[1] = -gq * inv * (g.ib * dx + g.ic * dy);
-                Br = alpha * g.r + oma * Br;
-                Bg = alpha * g.g + oma * Bg;
-                Bb = alpha * g.b + oma * Bb;
-                Bz = alpha * g.z + oma * Bz;
-                P *= oma;
-                T = Tk;
+            const int x0 = rec_x0(g);
+            if ((unsigned)(px - x0) <= (unsigned)(rec_x1(g) - x0)) {
+                const float dx = (float)(px - x0) + g.ox;
+#pragma unroll
+                for (int i = 0; i < PIX; i++) {
+                    float dy, pw;
+                    if (k <= s[i].last &&
+                        row_eval(g, dx, px, py + i, y0, y1, p64, order, s_rank[j], dy, pw)) {
+                        s[i].step(g, dx, dy, pw, k, v);
+                        hit = true;
+                    }
+                }
             }
             if (__any_sync(0xffffffffu, hit)) {
                 const float s = transpose_reduce16(v, lane);
-                const int vi = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
-                               ((lane >> 1) & 1);
                 if (!(lane & 1) && vi < 10 && s != 0.f) atomicAdd(&s_grad[j][vi], s);
             }
         }
@@ -327,7 +370,13 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
     cudaMemsetAsync(b.g2d, 0, n * (int64_t)sizeof(float) * kG2dStride, st);
     const uint32_t rank_mask = (uint32_t)((1ull << L.rank_bits) - 1ull);
     prof_begin(ST_COMPOSITE_BWD, st);
-    composite_bwd<<<(unsigned)L.n_tiles, kTilePx, 0, st>>>(
+    static const int pix = [] {
+        const char *v = getenv("SM_BWD_PIX");
+        const int p = v ? atoi(v) : 2;
+        return (p == 1 || p == 4) ? p : 2;
+    }();
+    auto kern = pix == 1 ? composite_bwd<1> : (pix == 4 ? composite_bwd<4> : composite_bwd<2>);
+    kern<<<(unsigned)L.n_tiles, kTilePx / pix, 0, st>>>(
         b.ranges, L.tile_passes & 1 ? b.ikey1 : b.ikey0, rank_mask, b.rec_sorted, b.p64, b.order0,
         dims.width, dims.height, L.tiles_x, d_rgb, d_depth, d_alpha, b.pix_cd, b.pix_t, b.pix_tlast,
         b.pix_last, b.g2d);

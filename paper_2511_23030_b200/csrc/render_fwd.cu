@@ -179,54 +179,128 @@ __global__ void check_instances(sm_render_counters *ctr, int64_t max_instances) 
     ctr->reserved[0] = of ? 0u : n;   // count the sort / ranges see
 }
 
+// Instance emission, load-balanced over instances rather than Gaussians (a
+// large splat can cover hundreds of tiles): each thread owns kEmitItems
+// consecutive instance slots, finds the owning depth rank of the first by
+// binary search over the exclusive scan `toff`, then walks forward.  Keys are
+// (tile << rank_bits) | rank, written in rank order.
+constexpr int kEmitItems = 4;
+
 __global__ void __launch_bounds__(256)
-emit_instances(const ProjRec *__restrict__ rec_sorted, const uint32_t *__restrict__ tcount_r,
-               const uint32_t *__restrict__ toff, int64_t n, const sm_render_counters *ctr,
-               int rank_bits, int tiles_x, uint32_t *__restrict__ ikeys) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n || ctr->overflow) return;
-    const uint32_t cnt = tcount_r[r];
-    if (!cnt) return;
-    const ProjRec g = rec_sorted[r];
-    const int tx0 = rec_x0(g) / kTile, tx1 = rec_x1(g) / kTile;
-    const int ty0 = rec_y0(g) / kTile, ty1 = rec_y1(g) / kTile;
-    uint32_t o = toff[r];
-    for (int ty = ty0; ty <= ty1; ty++)
-        for (int tx = tx0; tx <= tx1; tx++)
-            ikeys[o++] = ((uint32_t)(ty * tiles_x + tx) << rank_bits) | (uint32_t)r;
+emit_instances(const ProjRec *__restrict__ rec_sorted, const uint32_t *__restrict__ toff, int64_t n,
+               const sm_render_counters *ctr, int rank_bits, int tiles_x,
+               uint32_t *__restrict__ ikeys) {
+    const int64_t total = ctr->reserved[0];   // 0 on overflow
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * kEmitItems;
+    for (int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kEmitItems; e0 < total;
+         e0 += stride) {
+        int64_t lo = 0, hi = n - 1;   // last rank with toff <= e0
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if ((int64_t)toff[mid] <= e0) lo = mid;
+            else hi = mid - 1;
+        }
+        int64_t r = lo;
+        int64_t next = r + 1 < n ? (int64_t)toff[r + 1] : total;
+        ProjRec g = rec_sorted[r];
+        const int64_t e1 = min(e0 + kEmitItems, total);
+        for (int64_t e = e0; e < e1; e++) {
+            while (e >= next) {   // advance to the rank owning slot e (skips zero-tile ranks)
+                r++;
+                next = r + 1 < n ? (int64_t)toff[r + 1] : total;
+                g = rec_sorted[r];
+            }
+            const int tx0 = rec_x0(g) / kTile, tx1 = rec_x1(g) / kTile, ty0 = rec_y0(g) / kTile;
+            const int ntx = tx1 - tx0 + 1;
+            const int j = (int)(e - (int64_t)toff[r]);
+            const int t = (ty0 + j / ntx) * tiles_x + tx0 + j % ntx;
+            ikeys[e] = ((uint32_t)t << rank_bits) | (uint32_t)r;
+        }
+    }
 }
 
 __global__ void __launch_bounds__(256)
 tile_ranges(const uint32_t *__restrict__ ikeys, const sm_render_counters *ctr, int rank_bits,
             uint32_t *__restrict__ ranges) {
     const int64_t n = ctr->reserved[0];
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    const uint32_t t = ikeys[p] >> rank_bits;
-    if (p == 0 || (ikeys[p - 1] >> rank_bits) != t) ranges[2 * t] = (uint32_t)p;
-    if (p == n - 1 || (ikeys[p + 1] >> rank_bits) != t) ranges[2 * t + 1] = (uint32_t)(p + 1);
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t t = ikeys[p] >> rank_bits;
+        if (p == 0 || (ikeys[p - 1] >> rank_bits) != t) ranges[2 * t] = (uint32_t)p;
+        if (p == n - 1 || (ikeys[p + 1] >> rank_bits) != t) ranges[2 * t + 1] = (uint32_t)(p + 1);
+    }
 }
 
 // ------------------------------------------------------------ compositing
-__global__ void __launch_bounds__(kTilePx)
+// Per-pixel front-to-back state (renderloss.py:136-152 loop body).
+struct FwdPix {
+    float T, cr, cg, cb, cd, tlast;
+    int32_t last;
+    bool done;
+
+    __device__ __forceinline__ void add(const ProjRec &g, float pw, int32_t k) {
+        const float alpha = g.op * ex2_approx(pw);
+        const float w = T * alpha;
+        cr += w * g.r;
+        cg += w * g.g;
+        cb += w * g.b;
+        cd += w * g.z;
+        tlast = T;
+        last = k;
+        T = T * (1.f - alpha);
+        done = T < (float)SM_MIN_T;   // later pairs would be skipped (renderloss.py:143)
+    }
+
+    __device__ __forceinline__ void store(int64_t p, float *out_rgb, float *out_depth,
+                                          float *out_alpha, float4 *st_cd, float *st_t,
+                                          float *st_tlast, int32_t *st_last) const {
+        const float A = 1.f - T;   // renderloss.py:216-218 finalize
+        out_rgb[3 * p + 0] = fminf(fmaxf(cr, 0.f), 1.f);
+        out_rgb[3 * p + 1] = fminf(fmaxf(cg, 0.f), 1.f);
+        out_rgb[3 * p + 2] = fminf(fmaxf(cb, 0.f), 1.f);
+        out_depth[p] = A > 0.f ? cd / A : 0.f;
+        out_alpha[p] = fminf(fmaxf(A, 0.f), 1.f);
+        st_cd[p] = make_float4(cr, cg, cb, cd);
+        st_t[p] = T;
+        st_tlast[p] = tlast;
+        st_last[p] = last;
+    }
+};
+
+// One CTA per 16x16 tile, 256/PIX threads, each owning PIX vertically
+// adjacent pixels (same column: the column test and dx are shared).  The
+// tile's instances (depth-rank order) are staged one CTA-width batch at a
+// time in shared memory; a warp skips a splat whose 3-sigma box misses its
+// 2*PIX rows (warp-uniform), a thread skips it when its column is outside the
+// box, and the block stops once every pixel's transmittance is below 1e-10.
+template <int PIX>
+__global__ void __launch_bounds__(kTilePx / PIX)
 composite_fwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ikeys,
               uint32_t rank_mask, const ProjRec *__restrict__ recs,
               const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
               int height, int tiles_x, float *__restrict__ out_rgb, float *__restrict__ out_depth,
               float *__restrict__ out_alpha, float4 *__restrict__ st_cd, float *__restrict__ st_t,
               float *__restrict__ st_tlast, int32_t *__restrict__ st_last) {
-    __shared__ ProjRec s_rec[kTilePx];
-    __shared__ uint32_t s_rank[kTilePx];
+    constexpr int NT = kTilePx / PIX;
+    __shared__ ProjRec s_rec[NT];
+    __shared__ uint32_t s_rank[NT];
     const int tile = blockIdx.x;
+    const int ty0 = (tile / tiles_x) * kTile;
     const int px = (tile % tiles_x) * kTile + (threadIdx.x & (kTile - 1));
-    const int py = (tile / tiles_x) * kTile + (threadIdx.x / kTile);
-    const bool inside = px < width && py < height;
+    const int py = ty0 + PIX * (threadIdx.x / kTile);
+    const int wy0 = ty0 + 2 * PIX * (threadIdx.x / 32);   // warp's first row
     const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
-    float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f, cd = 0.f, tlast = 1.f;
-    int32_t last = -1;
-    bool done = !inside;
-    for (uint32_t base = start; base < end; base += kTilePx) {
-        if (__syncthreads_count(done) == kTilePx) break;
+    FwdPix s[PIX];
+    bool in[PIX];
+    bool all_done = true;
+#pragma unroll
+    for (int i = 0; i < PIX; i++) {
+        in[i] = px < width && py + i < height;
+        s[i] = FwdPix{1.f, 0.f, 0.f, 0.f, 0.f, 1.f, -1, !in[i]};
+        all_done = all_done && s[i].done;
+    }
+    for (uint32_t base = start; base < end; base += NT) {
+        if (__syncthreads_count(all_done) == NT) break;
         const uint32_t idx = base + threadIdx.x;
         if (idx < end) {
             const uint32_t rk = ikeys[idx] & rank_mask;
@@ -234,42 +308,38 @@ composite_fwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
             s_rec[threadIdx.x] = recs[rk];
         }
         __syncthreads();
-        const int cnt = (int)min((uint32_t)kTilePx, end - base);
-        if (!done) {
+        const int cnt = (int)min((uint32_t)NT, end - base);
+        if (!all_done) {
             for (int j = 0; j < cnt; j++) {
                 const ProjRec &g = s_rec[j];
-                float dx, dy, pw;
-                if (!pair_eval(g, px, py, p64, order, s_rank[j], dx, dy, pw)) continue;
-                const float alpha = g.op * ex2_approx(pw);
-                const float w = T * alpha;
-                cr += w * g.r;
-                cg += w * g.g;
-                cb += w * g.b;
-                cd += w * g.z;
-                tlast = T;
-                last = (int32_t)(base + j);
-                T = T * (1.f - alpha);
-                if (T < (float)SM_MIN_T) {
-                    done = true;
-                    break;
+                const int y0 = rec_y0(g), y1 = rec_y1(g);
+                if (y1 < wy0 || y0 > wy0 + 2 * PIX - 1) continue;   // warp-uniform row cull
+                const int x0 = rec_x0(g);
+                if ((unsigned)(px - x0) > (unsigned)(rec_x1(g) - x0)) continue;
+                const float dx = (float)(px - x0) + g.ox;
+                all_done = true;
+#pragma unroll
+                for (int i = 0; i < PIX; i++) {
+                    float dy, pw;
+                    if (!s[i].done && row_eval(g, dx, px, py + i, y0, y1, p64, order, s_rank[j], dy, pw))
+                        s[i].add(g, pw, (int32_t)(base + j));
+                    all_done = all_done && s[i].done;
                 }
+                if (all_done) break;
             }
         }
         __syncthreads();
     }
-    if (!inside) return;
-    const int64_t p = (int64_t)py * width + px;
-    // renderloss.py:216-218 finalize
-    const float A = 1.f - T;
-    out_rgb[3 * p + 0] = fminf(fmaxf(cr, 0.f), 1.f);
-    out_rgb[3 * p + 1] = fminf(fmaxf(cg, 0.f), 1.f);
-    out_rgb[3 * p + 2] = fminf(fmaxf(cb, 0.f), 1.f);
-    out_depth[p] = A > 0.f ? cd / A : 0.f;
-    out_alpha[p] = fminf(fmaxf(A, 0.f), 1.f);
-    st_cd[p] = make_float4(cr, cg, cb, cd);
-    st_t[p] = T;
-    st_tlast[p] = tlast;
-    st_last[p] = last;
+#pragma unroll
+    for (int i = 0; i < PIX; i++)
+        if (in[i])
+            s[i].store((int64_t)(py + i) * width + px, out_rgb, out_depth, out_alpha, st_cd, st_t,
+                       st_tlast, st_last);
+}
+
+static int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v ? atoi(v) : dflt;
 }
 
 CamDev make_cam(const sm_camera &c, const RenderLayout &L) {
@@ -329,22 +399,24 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
         gather_by_rank<<<gb, 256, 0, st>>>(b.order0, n, b.rec, b.tcount, b.rec_sorted, b.tcount_r);
         exclusive_scan(b.tcount_r, b.toff, n, b.scan, &b.ctr->n_instances, st);
         check_instances<<<1, 1, 0, st>>>(b.ctr, dims.max_instances);
-        emit_instances<<<gb, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.toff, n, b.ctr, L.rank_bits,
-                                           L.tiles_x, b.ikey0);
+        const unsigned persist = (unsigned)(148 * 8);
+        emit_instances<<<persist, 256, 0, st>>>(b.rec_sorted, b.toff, n, b.ctr, L.rank_bits, L.tiles_x,
+                                                b.ikey0);
         prof_end(ST_BIN, st);
         prof_begin(ST_TILE_SORT, st);
         const int cur = radix_sort<uint32_t, false>(
             b.ikey0, nullptr, b.ikey1, nullptr, &b.ctr->reserved[0], 0, dims.max_instances,
             L.rank_bits, L.rank_bits + L.tile_bits, ss, st);
         uint32_t *ik = cur ? b.ikey1 : b.ikey0;
-        tile_ranges<<<(unsigned)ceil_div(dims.max_instances > 0 ? dims.max_instances : 1, 256), 256, 0,
-                      st>>>(ik, b.ctr, L.rank_bits, b.ranges);
+        tile_ranges<<<persist, 256, 0, st>>>(ik, b.ctr, L.rank_bits, b.ranges);
         prof_end(ST_TILE_SORT, st);
         count_launches(1 + 3 * L.depth_passes + 6 + 3 * L.tile_passes + 1);
     }
     const uint32_t rank_mask = (uint32_t)((1ull << L.rank_bits) - 1ull);
     prof_begin(ST_COMPOSITE_FWD, st);
-    composite_fwd<<<(unsigned)L.n_tiles, kTilePx, 0, st>>>(
+    static const int pix = env_int("SM_FWD_PIX", 2);
+    auto kern = pix == 1 ? composite_fwd<1> : (pix == 4 ? composite_fwd<4> : composite_fwd<2>);
+    kern<<<(unsigned)L.n_tiles, kTilePx / (pix == 1 ? 1 : (pix == 4 ? 4 : 2)), 0, st>>>(
         b.ranges, L.tile_passes & 1 ? b.ikey1 : b.ikey0, rank_mask, b.rec_sorted, b.p64, b.order0,
         dims.width, dims.height, L.tiles_x, out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t,
         b.pix_tlast, b.pix_last);

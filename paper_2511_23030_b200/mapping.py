@@ -93,35 +93,43 @@ class AdamSettings:
 
 
 class _ActiveSet:
-    """Slot list of the visible chunks (sorted ids), cached by segment layout."""
+    """Slot lists of visible-chunk sets (sorted ids -> slab rows), LRU-cached by
+    segment layout so revisited keyframes reuse their list (and CUDA graph)."""
+
+    CAPACITY = 64
 
     def __init__(self, device):
         import torch
         self.torch = torch
         self.device = device
         self.key = None
-        self.slots = torch.empty(0, dtype=torch.int32, device=device)
         self.n = 0
+        self._cache: dict = {}
 
     def build(self, segments: list[tuple[int, int]]):
         key = tuple(segments)
-        if key == self.key:
-            return self.slots, self.n
+        hit = self._cache.pop(key, None)
+        if hit is not None:
+            self._cache[key] = hit
+            self.key, self.n = key, hit[1]
+            return hit
         torch = self.torch
         counts = np.array([c for _, c in segments], dtype=np.int64)
         offs = np.array([o for o, _ in segments], dtype=np.int64)
         total = int(counts.sum())
+        slots = torch.empty(max(total, 1), dtype=torch.int32, device=self.device)
         if total:
             prefix = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
-            if self.slots.numel() < total:
-                self.slots = torch.empty(int(total * 1.25) + 1024, dtype=torch.int32, device=self.device)
             meta = torch.as_tensor(np.stack([offs, counts, prefix]), device=self.device)
             rc = _lib.load().sm_expand_segments(_lib.ptr(meta[0]), _lib.ptr(meta[1]), _lib.ptr(meta[2]),
-                                                len(segments), total, _lib.ptr(self.slots),
+                                                len(segments), total, _lib.ptr(slots),
                                                 _lib.stream_handle())
             _lib.check(rc, "expand_segments")
+        self._cache[key] = (slots, total)
+        while len(self._cache) > self.CAPACITY:
+            self._cache.pop(next(iter(self._cache)))
         self.key, self.n = key, total
-        return self.slots, total
+        return slots, total
 
 
 @dataclass
@@ -198,7 +206,6 @@ class MappingEngine:
                                                        torch.empty_like(pin[1], device=self.device))
             d.rgb_u8.copy_(pin[0], non_blocking=True)
             d.depth.copy_(pin[1], non_blocking=True)
-            self.h2d_bytes += pin[0].numel() + 4 * pin[1].numel()
             return d
         d = self._kf_dev.get(kf.id)
         if d is None:
@@ -235,14 +242,16 @@ class MappingEngine:
                                       _lib.stream_handle())
         _lib.check(rc, "adam_step")
 
-    def _read_loss(self) -> tuple[float, bool]:
-        """One D2H copy of {loss[4], n_instances, overflow} into pinned memory + sync."""
+    def _queue_readback(self) -> None:
+        """D2H copy of {loss[4], n_instances, overflow} into pinned memory (async)."""
         rb = self._readback
         rb[:4].copy_(self.loss.out, non_blocking=True)
         rb[4:6].copy_(self.render.ws[:8].view(self.torch.float32), non_blocking=True)
+
+    def _finish_readback(self) -> tuple[float, bool]:
         self.torch.cuda.current_stream(self.device).synchronize()
         self.d2h_bytes += 24
-        v = rb.numpy()
+        v = self._readback.numpy()
         ctr = v[4:6].view(np.uint32)
         self.counter_instances += int(ctr[0])
         return float(v[0]), bool(ctr[1])
@@ -253,20 +262,87 @@ class MappingEngine:
         self.counter_instances = 0
 
     counter_steps = counter_gaussians = counter_instances = 0
+    use_graphs = True
+
+    def _graph_key(self, kf: Keyframe, slots, n: int):
+        s = self.store.slab
+        return (kf.id, slots.data_ptr(), n, s.params.data_ptr(), s.grads.data_ptr(),
+                self.render.ws.data_ptr(), self.upload_keyframes_each_step)
+
+    def drop_graphs(self) -> None:
+        lib = _lib.load()
+        for _, gid in getattr(self, "_graphs", {}).values():
+            lib.sm_profile_graph_free(gid)
+        self._graphs = {}
+
+    def _capture(self, kf: Keyframe, slots, n: int):
+        """Capture fwd -> loss -> bwd -> Adam -> readback as one CUDA graph."""
+        torch, lib = self.torch, _lib.load()
+        if not hasattr(self, "_cap_stream"):
+            self._cap_stream = torch.cuda.Stream(device=self.device)
+            self._graphs = {}
+        torch.cuda.current_stream(self.device).synchronize()
+        g = torch.cuda.CUDAGraph()
+        gid = lib.sm_profile_capture_begin()
+        try:
+            with torch.cuda.graph(g, stream=self._cap_stream):
+                self._device_pass(kf, slots, n)
+                self._adam(slots, n)
+                self._queue_readback()
+        finally:
+            lib.sm_profile_capture_end()
+        self._graphs[self._graph_key(kf, slots, n)] = (g, gid)
 
     def train_view(self, kf: Keyframe, slots, n: int) -> float:
-        """One device iteration with overflow recovery; returns the loss."""
-        for _ in range(6):
-            self._device_pass(kf, slots, n)
-            self._adam(slots, n)
-            loss, overflow = self._read_loss()
+        """One device iteration with overflow recovery; returns the loss.
+
+        The first visit of a (keyframe, active set) runs eagerly and then
+        captures the whole device pass as a CUDA graph; later visits replay it
+        (one launch instead of ~45), which the B200 front end needs here.
+        """
+        if self.upload_keyframes_each_step:   # GT RGB (u8) + depth (f32) cross PCIe every step
+            self.h2d_bytes += kf.intrinsics.width * kf.intrinsics.height * 7
+        graphs = getattr(self, "_graphs", {})
+        entry = graphs.get(self._graph_key(kf, slots, n)) if self.use_graphs else None
+        if entry is not None:
+            g, gid = entry
+            g.replay()
+            loss, overflow = self._finish_readback()
+            _lib.load().sm_profile_graph_replayed(gid)
             if not overflow:
                 self.counter_steps += 1
                 self.counter_gaussians += n
                 return loss
             self.store.slab.grads.zero_()
             self.render.grow_instances(self.render.counters()["n_instances"])
+            self.drop_graphs()
+        for _ in range(6):
+            self._device_pass(kf, slots, n)
+            self._adam(slots, n)
+            self._queue_readback()
+            loss, overflow = self._finish_readback()
+            if not overflow:
+                self.counter_steps += 1
+                self.counter_gaussians += n
+                if self.use_graphs and n:
+                    self._capture(kf, slots, n)
+                return loss
+            self.store.slab.grads.zero_()
+            self.render.grow_instances(self.render.counters()["n_instances"])
+            self.drop_graphs()
         raise DeviceFailure("tile-instance buffer kept overflowing")
+
+    def warm_graphs(self) -> None:
+        """Run one device iteration per resident keyframe (capturing its graph)."""
+        for kid in sorted(self.store.resident_keyframe_ids()):
+            kf = self.store.keyframe_get(kid)
+            ids = sorted(self._visible_for_pose(kf.pose)[0])
+            if ids:
+                self.store.ensure_resident(ids)
+            slots, n = self.active.build(self.store.segments(ids))
+            self.train_view(kf, slots, n)
+            if ids:
+                self.store.mark_trained(ids)
 
     # --------------------------------------------------------------- step
     def optimization_step(self, frame_idx: int, step_idx: int, inserted: int = 0) -> FrameMetrics:
