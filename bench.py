@@ -233,36 +233,37 @@ def main():
         import torch.distributed as dist
     step_fn = (lambda f, s: eng.optimization_step(f, s)) if world == 1 else \
         (lambda f, s: eng.optimization_step_dp(f, s, world, rank))
-    lib.sm_profile_enable(1)   # before warm-up: captured step graphs carry the stage events
+    def timed(frame: int, clocks_gpu=None):
+        """barrier + sync, CUDA events around exactly args.steps steps, max over ranks."""
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        sampler = ClockSampler(clocks_gpu) if clocks_gpu is not None else None
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for s in range(args.steps):
+            step_fn(frame, s)
+        b.record()
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        clk = sampler.stop() if sampler else None
+        t_ms = a.elapsed_time(b)
+        if dist is not None:
+            t = torch.tensor([t_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_ms = float(t.item())
+        return t_ms, clk
+
     eng.warm_graphs()
     for s in range(args.warmup):
         step_fn(0, s)
     torch.cuda.synchronize()
     # ------------------------------------------------------------ timed (device-resident)
     eng.reset_counters()
-    _lib.profile_collect()
     launches0 = lib.sm_launch_count()
-    clocks = ClockSampler(local)
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    for s in range(args.steps):
-        step_fn(1, s)
-    ev1.record()
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    clk = clocks.stop()
+    ms, clk = timed(1, clocks_gpu=local)
     launches = lib.sm_launch_count() - launches0
-    prof = _lib.profile_collect()
-    lib.sm_profile_enable(0)
-    ms = ev0.elapsed_time(ev1)
-    if dist is not None:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     ms_step = ms / args.steps
     units = args.steps * world
     value = units / (ms / 1e3)
@@ -271,27 +272,25 @@ def main():
     gauss_s = eng.counter_gaussians * world / (ms / 1e3)
     # ------------------------------------------------------------ e2e through the public API
     eng.upload_keyframes_each_step = True
-    step_fn(2, 0)
+    eng.warm_graphs()
     eng.reset_counters()
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     h2d0, d2h0 = eng.h2d_bytes, eng.d2h_bytes
-    e0.record()
-    for s in range(args.steps):
-        step_fn(3, s)
-    e1.record()
-    torch.cuda.synchronize()
-    ems = e0.elapsed_time(e1)
-    if dist is not None:
-        t = torch.tensor([ems], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ems = float(t.item())
+    ems, _ = timed(3)
     e2e = {"value": units / (ems / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": int((eng.h2d_bytes - h2d0) / args.steps),
            "d2h_bytes_per_step": int((eng.d2h_bytes - d2h0) / args.steps)}
     eng.upload_keyframes_each_step = False
+    # ------------------------------------------------------------ per-kernel timing pass
+    # Same steps again with CUDA-event pairs around every stage (external event
+    # nodes inside the step graphs); kept out of the headline region because
+    # the extra nodes cost ~5%.
+    lib.sm_profile_enable(1)
+    eng.drop_graphs()
+    eng.warm_graphs()
+    _lib.profile_collect()
+    pms, _ = timed(4)
+    prof = _lib.profile_collect()
+    lib.sm_profile_enable(0)
     # ------------------------------------------------------------ roofline of the dominant kernel
     peaks = _peaks()
     px = eng.intr.width * eng.intr.height
@@ -330,7 +329,7 @@ def main():
                    "l2": "inputs larger than L2 (slab params+Adam+grads 256 MB/1M Gaussians)"},
         "gaussians_per_s": gauss_s,
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clk, "roofline": roof,
-        "stages": stages, "cpu_baseline": cpu,
+        "stages": stages, "stages_pass_ms_per_step": pms / args.steps, "cpu_baseline": cpu,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -188,6 +188,7 @@ int sm_profile_capture_begin(void);
 void sm_profile_capture_end(void);
 void sm_profile_graph_replayed(int gid);
 void sm_profile_graph_free(int gid);
+long long sm_profile_graph_timing_errors(void);
 
 #ifdef __cplusplus
 }

@@ -95,6 +95,7 @@ def load():
     _sig(lib.sm_profile_capture_end, None)
     _sig(lib.sm_profile_graph_replayed, None, c_int)
     _sig(lib.sm_profile_graph_free, None, c_int)
+    _sig(lib.sm_profile_graph_timing_errors, ctypes.c_longlong)
     if lib.sm_abi_version() != ABI_VERSION:
         raise DeviceFailure(f"ABI mismatch: library {lib.sm_abi_version()} != {ABI_VERSION}")
     _lib = lib

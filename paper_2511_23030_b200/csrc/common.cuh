@@ -108,6 +108,7 @@ __device__ __forceinline__ bool row_eval(const ProjRec &g, float dx, int px, int
 constexpr int kCompThreads = 128;
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ inline int64_t align_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
 }  // namespace sm

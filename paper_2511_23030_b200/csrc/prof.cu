@@ -39,6 +39,7 @@ struct GraphProf {
 };
 static std::vector<GraphProf> g_graphs;
 static int g_capture_gid = -1;
+static long long g_graph_timing_errors = 0;
 
 static cudaEvent_t take_event() {
     if (!g_pool.empty()) {
@@ -51,11 +52,21 @@ static cudaEvent_t take_event() {
     return e;
 }
 
+// Inside stream capture a plain record becomes an internal graph edge that
+// cannot be timed; an *external* event record node is re-recorded (and
+// timeable) at every replay.
+static void record(cudaEvent_t e, cudaStream_t st) {
+    if (g_capture_gid >= 0)
+        cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+    else
+        cudaEventRecord(e, st);
+}
+
 void prof_begin(Stage s, cudaStream_t st) {
     if (!g_prof_on) return;
     std::lock_guard<std::mutex> lk(g_mu);
     cudaEvent_t e = take_event();
-    cudaEventRecord(e, st);
+    record(e, st);
     g_open[s] = e;
     g_is_open[s] = true;
 }
@@ -65,7 +76,7 @@ void prof_end(Stage s, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g_is_open[s]) return;
     cudaEvent_t e = take_event();
-    cudaEventRecord(e, st);
+    record(e, st);
     if (g_capture_gid >= 0)
         g_graphs[g_capture_gid].pairs.push_back({(int)s, g_open[s], e});
     else
@@ -116,12 +127,18 @@ void sm_profile_graph_replayed(int gid) {
     if (!g_prof_on) return;
     for (const Pending &p : g.pairs) {
         float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+        const cudaError_t e = cudaEventElapsedTime(&ms, p.a, p.b);
+        if (e == cudaSuccess) {
             g_ms[p.stage] += ms;
             g_calls[p.stage] += 1;
+        } else {
+            g_graph_timing_errors++;
+            cudaGetLastError();   // do not leave a sticky error for later launch checks
         }
     }
 }
+
+long long sm_profile_graph_timing_errors(void) { return g_graph_timing_errors; }
 
 void sm_profile_graph_free(int gid) {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -145,9 +162,12 @@ int sm_profile_collect(double *ms_out, long long *calls_out) {
     for (const Pending &p : g_pending) {
         cudaEventSynchronize(p.b);
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, p.a, p.b);
-        g_ms[p.stage] += ms;
-        g_calls[p.stage] += 1;
+        if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+            g_ms[p.stage] += ms;
+            g_calls[p.stage] += 1;
+        } else {
+            cudaGetLastError();
+        }
         g_pool.push_back(p.a);
         g_pool.push_back(p.b);
     }

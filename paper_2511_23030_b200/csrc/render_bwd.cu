@@ -21,6 +21,42 @@
 
 namespace sm {
 
+// Warp sum of 10 per-lane values with 14 shuffles: an 8-wide transposed
+// butterfly (offsets 16, 8, 4 halve the value count, 2 and 1 finish) leaves
+// the sum of value 4*b4 + 2*b3 + b2 (bits of the lane id) in every lane; a
+// 2-wide one leaves value 8 + b4.  Returns (sa, sb).
+__device__ __forceinline__ float2 transpose_reduce10(const float (&v)[16], int lane) {
+    float a[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const bool hi = lane & 16;
+        a[k] = (hi ? v[k + 4] : v[k]) + __shfl_xor_sync(0xffffffffu, hi ? v[k] : v[k + 4], 16);
+    }
+    float b[2];
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        const bool hi = lane & 8;
+        b[k] = (hi ? a[k + 2] : a[k]) + __shfl_xor_sync(0xffffffffu, hi ? a[k] : a[k + 2], 8);
+    }
+    float c;
+    {
+        const bool hi = lane & 4;
+        c = (hi ? b[1] : b[0]) + __shfl_xor_sync(0xffffffffu, hi ? b[0] : b[1], 4);
+    }
+    c += __shfl_xor_sync(0xffffffffu, c, 2);
+    c += __shfl_xor_sync(0xffffffffu, c, 1);
+    float d;
+    {
+        const bool hi = lane & 16;
+        d = (hi ? v[9] : v[8]) + __shfl_xor_sync(0xffffffffu, hi ? v[8] : v[9], 16);
+    }
+    d += __shfl_xor_sync(0xffffffffu, d, 8);
+    d += __shfl_xor_sync(0xffffffffu, d, 4);
+    d += __shfl_xor_sync(0xffffffffu, d, 2);
+    d += __shfl_xor_sync(0xffffffffu, d, 1);
+    return make_float2(c, d);
+}
+
 __device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
 #pragma unroll
     for (int k = 0; k < 8; k++) {
@@ -161,7 +197,8 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
     if (lane == 0) atomicMax(&s_maxlast, wmax);
     __syncthreads();
     const int maxlast = s_maxlast;
-    const int vi = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+    const int via = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);   // 0..7
+    const int vib = 8 + ((lane >> 4) & 1);                                                // 8..9
     for (int bend = maxlast + 1; bend > start; bend -= NT) {
         const int bstart = max(start, bend - NT);
         const int idx = bstart + (int)threadIdx.x;
@@ -197,8 +234,9 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
                 }
             }
             if (__any_sync(0xffffffffu, hit)) {
-                const float s = transpose_reduce16(v, lane);
-                if (!(lane & 1) && vi < 10 && s != 0.f) atomicAdd(&s_grad[j][vi], s);
+                const float2 s = transpose_reduce10(v, lane);
+                if (!(lane & 3) && s.x != 0.f) atomicAdd(&s_grad[j][via], s.x);
+                if (!(lane & 15) && s.y != 0.f) atomicAdd(&s_grad[j][vib], s.y);
             }
         }
         __syncthreads();

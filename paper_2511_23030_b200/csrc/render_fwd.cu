@@ -179,43 +179,51 @@ __global__ void check_instances(sm_render_counters *ctr, int64_t max_instances) 
     ctr->reserved[0] = of ? 0u : n;   // count the sort / ranges see
 }
 
-// Instance emission, load-balanced over instances rather than Gaussians (a
-// large splat can cover hundreds of tiles): each thread owns kEmitItems
-// consecutive instance slots, finds the owning depth rank of the first by
-// binary search over the exclusive scan `toff`, then walks forward.  Keys are
-// (tile << rank_bits) | rank, written in rank order.
-constexpr int kEmitItems = 4;
+// Instance emission.  Splat footprints are heavy-tailed and the biggest
+// (nearest) ones sit together at the lowest depth ranks, so emission is split:
+// a thread per rank writes splats of <= kEmitSmall tiles directly, larger ones
+// are queued and a block per queued splat writes its tiles in parallel.
+// Keys are (tile << rank_bits) | rank at the rank's scanned offset, so the
+// array is in rank order whichever thread writes a slot.
+constexpr uint32_t kEmitSmall = 32;
+
+__device__ __forceinline__ void emit_tiles(const ProjRec &g, uint32_t r, uint32_t o, uint32_t first,
+                                           uint32_t count, uint32_t step, int rank_bits, int tiles_x,
+                                           uint32_t *ikeys) {
+    const int tx0 = rec_x0(g) / kTile, ty0 = rec_y0(g) / kTile;
+    const int ntx = rec_x1(g) / kTile - tx0 + 1;
+    for (uint32_t j = first; j < count; j += step) {
+        const int t = (ty0 + (int)j / ntx) * tiles_x + tx0 + (int)j % ntx;
+        ikeys[o + j] = ((uint32_t)t << rank_bits) | r;
+    }
+}
 
 __global__ void __launch_bounds__(256)
-emit_instances(const ProjRec *__restrict__ rec_sorted, const uint32_t *__restrict__ toff, int64_t n,
-               const sm_render_counters *ctr, int rank_bits, int tiles_x,
-               uint32_t *__restrict__ ikeys) {
-    const int64_t total = ctr->reserved[0];   // 0 on overflow
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * kEmitItems;
-    for (int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kEmitItems; e0 < total;
-         e0 += stride) {
-        int64_t lo = 0, hi = n - 1;   // last rank with toff <= e0
-        while (lo < hi) {
-            const int64_t mid = (lo + hi + 1) >> 1;
-            if ((int64_t)toff[mid] <= e0) lo = mid;
-            else hi = mid - 1;
-        }
-        int64_t r = lo;
-        int64_t next = r + 1 < n ? (int64_t)toff[r + 1] : total;
-        ProjRec g = rec_sorted[r];
-        const int64_t e1 = min(e0 + kEmitItems, total);
-        for (int64_t e = e0; e < e1; e++) {
-            while (e >= next) {   // advance to the rank owning slot e (skips zero-tile ranks)
-                r++;
-                next = r + 1 < n ? (int64_t)toff[r + 1] : total;
-                g = rec_sorted[r];
-            }
-            const int tx0 = rec_x0(g) / kTile, tx1 = rec_x1(g) / kTile, ty0 = rec_y0(g) / kTile;
-            const int ntx = tx1 - tx0 + 1;
-            const int j = (int)(e - (int64_t)toff[r]);
-            const int t = (ty0 + j / ntx) * tiles_x + tx0 + j % ntx;
-            ikeys[e] = ((uint32_t)t << rank_bits) | (uint32_t)r;
-        }
+emit_instances(const ProjRec *__restrict__ rec_sorted, const uint32_t *__restrict__ tcount_r,
+               const uint32_t *__restrict__ toff, int64_t n, sm_render_counters *ctr,
+               uint32_t *__restrict__ big, int rank_bits, int tiles_x, uint32_t *__restrict__ ikeys) {
+    if (ctr->overflow) return;
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint32_t cnt = tcount_r[r];
+    if (!cnt) return;
+    if (cnt > kEmitSmall) {
+        big[atomicAdd(&ctr->reserved[1], 1u)] = (uint32_t)r;
+        return;
+    }
+    emit_tiles(rec_sorted[r], (uint32_t)r, toff[r], 0, cnt, 1, rank_bits, tiles_x, ikeys);
+}
+
+__global__ void __launch_bounds__(256)
+emit_big(const ProjRec *__restrict__ rec_sorted, const uint32_t *__restrict__ tcount_r,
+         const uint32_t *__restrict__ toff, const sm_render_counters *ctr,
+         const uint32_t *__restrict__ big, int rank_bits, int tiles_x, uint32_t *__restrict__ ikeys) {
+    if (ctr->overflow) return;
+    const uint32_t nbig = ctr->reserved[1];
+    for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
+        const uint32_t r = big[b];
+        emit_tiles(rec_sorted[r], r, toff[r], threadIdx.x, tcount_r[r], blockDim.x, rank_bits, tiles_x,
+                   ikeys);
     }
 }
 
@@ -389,7 +397,8 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
         project_fwd<<<gb, 256, 0, st>>>(reinterpret_cast<const float4 *>(params), slots, n, cd,
                                         b.rec, b.p64, b.dkey0, b.order0, b.tcount);
         prof_end(ST_PROJECT, st);
-        SortScratch ss{b.sort_hist, b.sort_hist + (int64_t)kRadix * L.sort_blocks, L.sort_blocks};
+        const SortScratch ss = sort_scratch(b.sort_hist, dims.max_gaussians > dims.max_instances
+                                                             ? dims.max_gaussians : dims.max_instances);
         // global stable depth order (8 passes over the 64-bit key -> buffer 0)
         prof_begin(ST_DEPTH_SORT, st);
         radix_sort<unsigned long long, true>(b.dkey0, b.order0, b.dkey1, b.order1, nullptr, n, n, 0,
@@ -400,8 +409,11 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
         exclusive_scan(b.tcount_r, b.toff, n, b.scan, &b.ctr->n_instances, st);
         check_instances<<<1, 1, 0, st>>>(b.ctr, dims.max_instances);
         const unsigned persist = (unsigned)(148 * 8);
-        emit_instances<<<persist, 256, 0, st>>>(b.rec_sorted, b.toff, n, b.ctr, L.rank_bits, L.tiles_x,
-                                                b.ikey0);
+        // b.tcount (per visible index) is dead after gather_by_rank: reuse it as the big-splat queue
+        emit_instances<<<gb, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.toff, n, b.ctr, b.tcount,
+                                           L.rank_bits, L.tiles_x, b.ikey0);
+        emit_big<<<148 * 4, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.toff, b.ctr, b.tcount, L.rank_bits,
+                                          L.tiles_x, b.ikey0);
         prof_end(ST_BIN, st);
         prof_begin(ST_TILE_SORT, st);
         const int cur = radix_sort<uint32_t, false>(
@@ -410,11 +422,11 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
         uint32_t *ik = cur ? b.ikey1 : b.ikey0;
         tile_ranges<<<persist, 256, 0, st>>>(ik, b.ctr, L.rank_bits, b.ranges);
         prof_end(ST_TILE_SORT, st);
-        count_launches(1 + 3 * L.depth_passes + 6 + 3 * L.tile_passes + 1);
+        count_launches(1 + (1 + L.depth_passes) + 7 + (1 + L.tile_passes) + 1);
     }
     const uint32_t rank_mask = (uint32_t)((1ull << L.rank_bits) - 1ull);
     prof_begin(ST_COMPOSITE_FWD, st);
-    static const int pix = env_int("SM_FWD_PIX", 2);
+    static const int pix = env_int("SM_FWD_PIX", 1);
     auto kern = pix == 1 ? composite_fwd<1> : (pix == 4 ? composite_fwd<4> : composite_fwd<2>);
     kern<<<(unsigned)L.n_tiles, kTilePx / (pix == 1 ? 1 : (pix == 4 ? 4 : 2)), 0, st>>>(
         b.ranges, L.tile_passes & 1 ? b.ikey1 : b.ikey0, rank_mask, b.rec_sorted, b.p64, b.order0,

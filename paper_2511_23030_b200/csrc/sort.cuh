@@ -1,13 +1,18 @@
-// Hand-written stable LSD radix sort and exclusive scan for sm_100a.
+// Hand-written stable LSD radix sort (onesweep) and exclusive scan, sm_100a.
 //
 // Used by K3 (tile binning): a global stable depth order of the visible
 // Gaussians on their fp64 camera depth (replaces np.argsort(z, kind="stable"),
 // renderloss.py:202) and the per-tile instance sort.  Counts may live in
-// device memory (`n_dev`) so the whole render pipeline runs without a host
-// round trip; grids are sized for the capacity and idle blocks exit early.
+// device memory (`n_dev`) so the render pipeline needs no host round trip and
+// can be captured in a CUDA graph; grids are sized for the capacity and idle
+// blocks exit immediately.
 //
-// One pass = upsweep (per-block digit histogram) -> per-digit scan over blocks
-// -> downsweep (stable in-block ranking with __match_any_sync, then scatter).
+// Onesweep (decoupled look-back): one histogram kernel computes the global
+// digit counts of every pass at once; then each pass is ONE kernel.  A block
+// takes the next tile id from an atomic counter (so every earlier tile is
+// already running), ranks its keys stably in shared memory, publishes its
+// per-digit counts, then walks back over its predecessors' published counts
+// / inclusive prefixes to get its global offsets, and scatters.
 #pragma once
 #include "common.cuh"
 
@@ -15,112 +20,88 @@ namespace sm {
 
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 8;
-constexpr int kSortTile = kSortThreads * kSortItems;   // 2048 keys per block
+constexpr int kSortTile = kSortThreads * kSortItems;   // 2048 keys per tile
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kMaxPasses = 8;
+constexpr uint32_t kFlagAgg = 1u << 30;      // tile aggregate published
+constexpr uint32_t kFlagPre = 2u << 30;      // tile inclusive prefix published
+constexpr uint32_t kValMask = (1u << 30) - 1;
 
 __device__ __forceinline__ int64_t load_count(const uint32_t *n_dev, int64_t n_host) {
     return n_dev ? (int64_t)(*n_dev) : n_host;
 }
 
+// Global digit histograms of all passes: hist[p][d], p = 0..npasses-1.
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads)
-radix_upsweep(const K *__restrict__ keys, const uint32_t *n_dev, int64_t n_host, int shift,
-              int nbits, uint32_t *__restrict__ hist, int64_t hist_stride) {
-    __shared__ uint32_t h[kRadix];
+onesweep_histogram(const K *__restrict__ keys, const uint32_t *n_dev, int64_t n_host, int begin_bit,
+                   int end_bit, uint32_t *__restrict__ hist) {
+    __shared__ uint32_t h[kMaxPasses][kRadix];
     const int64_t n = load_count(n_dev, n_host);
-    const int64_t start = (int64_t)blockIdx.x * kSortTile;
-    if (start >= n) return;
-    for (int i = threadIdx.x; i < kRadix; i += kSortThreads) h[i] = 0;
+    const int npass = (end_bit - begin_bit + kRadixBits - 1) / kRadixBits;
+    for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += kSortThreads) (&h[0][0])[i] = 0;
     __syncthreads();
-    const K mask = (K)((1u << nbits) - 1u);
-    const int64_t end = min(n, start + (int64_t)kSortTile);
-    for (int64_t i = start + threadIdx.x; i < end; i += kSortThreads) {
-        uint32_t d = (uint32_t)((keys[i] >> shift) & mask);
-        atomicAdd(&h[d], 1u);
+    for (int64_t i = (int64_t)blockIdx.x * kSortThreads + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * kSortThreads) {
+        const K k = keys[i];
+        for (int p = 0; p < npass; p++) {
+            const int shift = begin_bit + p * kRadixBits;
+            const int nb = min(kRadixBits, end_bit - shift);
+            atomicAdd(&h[p][(uint32_t)(k >> shift) & ((1u << nb) - 1u)], 1u);
+        }
     }
     __syncthreads();
-    for (int d = threadIdx.x; d < kRadix; d += kSortThreads)
-        hist[(int64_t)d * hist_stride + blockIdx.x] = h[d];
-}
-
-// One CTA per digit: exclusive scan of hist[d][0:nblocks] in place; total out.
-__global__ void __launch_bounds__(1024)
-radix_scan_digits(uint32_t *__restrict__ hist, int64_t hist_stride, const uint32_t *n_dev,
-                  int64_t n_host, uint32_t *__restrict__ digit_total) {
-    __shared__ uint32_t warp_sums[32];
-    __shared__ uint32_t carry;
-    const int64_t n = load_count(n_dev, n_host);
-    const int64_t nblocks = ceil_div(n, kSortTile);
-    uint32_t *row = hist + (int64_t)blockIdx.x * hist_stride;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int64_t base = 0; base < nblocks; base += blockDim.x) {
-        int64_t i = base + threadIdx.x;
-        uint32_t v = i < nblocks ? row[i] : 0u;
-        uint32_t x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) warp_sums[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t s = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0u;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
-                if (lane >= o) s += y;
-            }
-            warp_sums[lane] = s;   // inclusive
-        }
-        __syncthreads();
-        uint32_t excl = carry + (warp ? warp_sums[warp - 1] : 0u) + x - v;
-        if (i < nblocks) row[i] = excl;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry = excl + v;
-        __syncthreads();
+    for (int i = threadIdx.x; i < npass * kRadix; i += kSortThreads) {
+        const uint32_t v = (&h[0][0])[i];
+        if (v) atomicAdd(&hist[i], v);
     }
-    if (threadIdx.x == 0) digit_total[blockIdx.x] = carry;
 }
 
-// Stable scatter.  Warp w owns the contiguous segment [w*512, w*512+512) of
-// the block's tile; lane l's item j is element w*512 + j*32 + l, so the
-// (warp, round, lane) order equals the element order.
+__device__ __forceinline__ uint32_t ld_status(const uint32_t *p) {
+    return *reinterpret_cast<const volatile uint32_t *>(p);
+}
+__device__ __forceinline__ void st_status(uint32_t *p, uint32_t v) {
+    *reinterpret_cast<volatile uint32_t *>(p) = v;
+}
+
 template <typename K, bool HAS_VAL>
 __global__ void __launch_bounds__(kSortThreads)
-radix_downsweep(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
-                K *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
-                const uint32_t *n_dev, int64_t n_host, int shift, int nbits,
-                const uint32_t *__restrict__ hist, int64_t hist_stride,
-                const uint32_t *__restrict__ digit_total) {
+onesweep_pass(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
+              K *__restrict__ keys_out, uint32_t *__restrict__ vals_out, const uint32_t *n_dev,
+              int64_t n_host, int shift, int nbits, const uint32_t *__restrict__ hist_p,
+              uint32_t *__restrict__ status_p, uint32_t *__restrict__ tile_ctr_p) {
     __shared__ uint32_t wcount[kSortWarps][kRadix];
     __shared__ uint32_t digit_base[kRadix];
+    __shared__ uint32_t tile_excl[kRadix];
     __shared__ uint32_t warp_tot[kSortWarps];
+    __shared__ uint32_t s_tile;
+    __shared__ K s_keys[kSortTile];
+    __shared__ uint32_t s_vals[HAS_VAL ? kSortTile : 1];
     const int64_t n = load_count(n_dev, n_host);
-    const int64_t start = (int64_t)blockIdx.x * kSortTile;
-    if (start >= n) return;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr_p, 1u);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&wcount[0][0])[i] = 0;
-    // digit base = exclusive scan of digit totals (256 digits, one per thread)
+    // global digit base = exclusive scan of this pass's histogram
     {
-        uint32_t v = threadIdx.x < kRadix ? digit_total[threadIdx.x] : 0u;
+        const uint32_t v = hist_p[threadIdx.x];
         uint32_t x = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x += y;
         }
         if (lane == 31) warp_tot[warp] = x;
         __syncthreads();
         uint32_t off = 0;
         for (int w = 0; w < warp; w++) off += warp_tot[w];
-        if (threadIdx.x < kRadix) digit_base[threadIdx.x] = off + x - v;
+        digit_base[threadIdx.x] = off + x - v;
     }
     __syncthreads();
+    const uint32_t tile = s_tile;
+    const int64_t start = (int64_t)tile * kSortTile;
+    if (start >= n) return;
     const K mask = (K)((1u << nbits) - 1u);
     K key[kSortItems];
     uint32_t val[kSortItems];
@@ -129,12 +110,14 @@ radix_downsweep(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals
     const int64_t seg = start + (int64_t)warp * (32 * kSortItems);
 #pragma unroll
     for (int j = 0; j < kSortItems; j++) {
-        int64_t i = seg + j * 32 + lane;
-        bool ok = i < n;
+        const int64_t i = seg + j * 32 + lane;
+        const bool ok = i < n;
         key[j] = ok ? keys_in[i] : (K)0;
         if (HAS_VAL) val[j] = ok ? vals_in[i] : 0u;
         dig[j] = ok ? (uint32_t)((key[j] >> shift) & mask) : 0xffffffffu;
     }
+    // stable in-block ranking: warp w owns the contiguous segment w*256..,
+    // item j of lane l is element w*256 + j*32 + l, processed in (j, l) order
 #pragma unroll
     for (int j = 0; j < kSortItems; j++) {
         const uint32_t d = dig[j];
@@ -148,60 +131,133 @@ radix_downsweep(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals
         local[j] = cnt + __popc(lt);
     }
     __syncthreads();
-    // exclusive prefix across warps per digit
-    for (int d = threadIdx.x; d < kRadix; d += kSortThreads) {
+    // per digit (thread d): exclusive prefix across warps, tile aggregate,
+    // publish, decoupled look-back over predecessor tiles, publish prefix
+    {
+        const int d = threadIdx.x;
         uint32_t run = 0;
 #pragma unroll
         for (int w = 0; w < kSortWarps; w++) {
-            uint32_t c = wcount[w][d];
+            const uint32_t c = wcount[w][d];
             wcount[w][d] = run;
             run += c;
         }
+        uint32_t *my = status_p + (int64_t)tile * kRadix + d;
+        if (tile == 0) {
+            st_status(my, kFlagPre | run);
+        } else {
+            st_status(my, kFlagAgg | run);
+            // look back 8 predecessors per round trip (independent loads)
+            uint32_t excl = 0;
+            bool found = false;
+            for (int64_t t = (int64_t)tile - 1; t >= 0 && !found; t -= 8) {
+                uint32_t s[8];
+#pragma unroll
+                for (int k = 0; k < 8; k++)
+                    s[k] = (t - k >= 0) ? ld_status(status_p + (t - k) * kRadix + d) : kFlagPre;
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    if (found || t - k < 0) continue;
+                    uint32_t v = s[k];
+                    while ((v & (kFlagAgg | kFlagPre)) == 0) v = ld_status(status_p + (t - k) * kRadix + d);
+                    excl += v & kValMask;
+                    found = (v & kFlagPre) != 0;
+                }
+            }
+            st_status(my, kFlagPre | (excl + run));
+            digit_base[d] += excl;
+        }
+        // tile-local exclusive prefix over digits (block scan of `run`)
+        uint32_t x = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        __syncthreads();   // warp_tot reuse
+        if (lane == 31) warp_tot[warp] = x;
+        __syncthreads();
+        uint32_t off = 0;
+        for (int w = 0; w < warp; w++) off += warp_tot[w];
+        tile_excl[d] = off + x - run;
     }
     __syncthreads();
+    // stage the tile in shared memory in digit order, then write each digit's
+    // run to consecutive global addresses (full-sector, coalesced stores)
 #pragma unroll
     for (int j = 0; j < kSortItems; j++) {
         const uint32_t d = dig[j];
         if (d == 0xffffffffu) continue;
-        const uint32_t pos = digit_base[d] + hist[(int64_t)d * hist_stride + blockIdx.x] +
-                             wcount[warp][d] + local[j];
-        keys_out[pos] = key[j];
-        if (HAS_VAL) vals_out[pos] = val[j];
+        const uint32_t lp = tile_excl[d] + wcount[warp][d] + local[j];
+        s_keys[lp] = key[j];
+        if (HAS_VAL) s_vals[lp] = val[j];
+    }
+    __syncthreads();
+    const int cnt = (int)min64(kSortTile, n - start);
+    for (int i = threadIdx.x; i < cnt; i += kSortThreads) {
+        const K k = s_keys[i];
+        const uint32_t d = (uint32_t)((k >> shift) & mask);
+        const uint32_t pos = digit_base[d] + (uint32_t)i - tile_excl[d];
+        keys_out[pos] = k;
+        if (HAS_VAL) vals_out[pos] = s_vals[i];
     }
 }
 
 struct SortScratch {
-    uint32_t *hist;          // [kRadix][max_blocks]
-    uint32_t *digit_total;   // [kRadix]
-    int64_t max_blocks;
+    uint32_t *hist;      // [kMaxPasses][kRadix]
+    uint32_t *status;    // [kMaxPasses][max_tiles][kRadix]
+    uint32_t *tile_ctr;  // [kMaxPasses]
+    int64_t max_tiles;
 };
 
+inline int64_t sort_tiles(int64_t max_n) { return ceil_div(max_n > 0 ? max_n : 1, kSortTile); }
+
 inline int64_t sort_scratch_bytes(int64_t max_n) {
-    int64_t mb = ceil_div(max_n > 0 ? max_n : 1, kSortTile);
-    return align_up((int64_t)kRadix * mb * 4, 256) + align_up(kRadix * 4, 256);
+    return align_up((int64_t)kMaxPasses * kRadix * 4, 256) +
+           align_up((int64_t)kMaxPasses * sort_tiles(max_n) * kRadix * 4, 256) +
+           align_up(kMaxPasses * 4, 256);
 }
 
-// Sorts keys (and optional u32 values) over bits [begin_bit, end_bit).
-// Ping-pongs between (k0,v0) and (k1,v1); returns 0 if the result is in
-// buffer 0, 1 if in buffer 1.
+inline SortScratch sort_scratch(void *base, int64_t max_n) {
+    char *b = static_cast<char *>(base);
+    SortScratch s;
+    s.max_tiles = sort_tiles(max_n);
+    s.hist = reinterpret_cast<uint32_t *>(b);
+    b += align_up((int64_t)kMaxPasses * kRadix * 4, 256);
+    s.status = reinterpret_cast<uint32_t *>(b);
+    b += align_up((int64_t)kMaxPasses * s.max_tiles * kRadix * 4, 256);
+    s.tile_ctr = reinterpret_cast<uint32_t *>(b);
+    return s;
+}
+
+inline int radix_passes(int begin_bit, int end_bit) {
+    return (int)ceil_div(end_bit - begin_bit, kRadixBits);
+}
+
+// Stable sort of keys (+ optional u32 values) over bits [begin_bit, end_bit).
+// Ping-pongs (k0,v0) <-> (k1,v1); returns 0 if the result is in buffer 0.
+// `max_n` bounds the count (grids, status rows); the live count is n_dev or n_host.
 template <typename K, bool HAS_VAL>
 int radix_sort(K *k0, uint32_t *v0, K *k1, uint32_t *v1, const uint32_t *n_dev, int64_t n_host,
-               int64_t max_n, int begin_bit, int end_bit, const SortScratch &s,
-               cudaStream_t st) {
-    const int64_t grid = ceil_div(max_n > 0 ? max_n : 1, kSortTile);
+               int64_t max_n, int begin_bit, int end_bit, const SortScratch &s, cudaStream_t st) {
+    const int npass = radix_passes(begin_bit, end_bit);
+    const int64_t tiles = sort_tiles(max_n);
+    cudaMemsetAsync(s.hist, 0, (size_t)npass * kRadix * 4, st);
+    cudaMemsetAsync(s.status, 0, (size_t)npass * tiles * kRadix * 4, st);
+    cudaMemsetAsync(s.tile_ctr, 0, (size_t)npass * 4, st);
+    const unsigned hgrid = (unsigned)min64(tiles * 2, 148 * 8);
+    onesweep_histogram<K><<<hgrid, kSortThreads, 0, st>>>(k0, n_dev, n_host, begin_bit, end_bit, s.hist);
     int cur = 0;
-    for (int shift = begin_bit; shift < end_bit; shift += kRadixBits) {
+    for (int p = 0; p < npass; p++) {
+        const int shift = begin_bit + p * kRadixBits;
         const int nbits = min(kRadixBits, end_bit - shift);
         K *ki = cur ? k1 : k0;
         K *ko = cur ? k0 : k1;
         uint32_t *vi = cur ? v1 : v0;
         uint32_t *vo = cur ? v0 : v1;
-        radix_upsweep<K><<<(unsigned)grid, kSortThreads, 0, st>>>(ki, n_dev, n_host, shift, nbits,
-                                                                  s.hist, s.max_blocks);
-        radix_scan_digits<<<kRadix, 1024, 0, st>>>(s.hist, s.max_blocks, n_dev, n_host,
-                                                    s.digit_total);
-        radix_downsweep<K, HAS_VAL><<<(unsigned)grid, kSortThreads, 0, st>>>(
-            ki, vi, ko, vo, n_dev, n_host, shift, nbits, s.hist, s.max_blocks, s.digit_total);
+        onesweep_pass<K, HAS_VAL><<<(unsigned)tiles, kSortThreads, 0, st>>>(
+            ki, vi, ko, vo, n_dev, n_host, shift, nbits, s.hist + p * kRadix,
+            s.status + (int64_t)p * tiles * kRadix, s.tile_ctr + p);
         cur ^= 1;
     }
     return cur;

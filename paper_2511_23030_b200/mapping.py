@@ -302,6 +302,7 @@ class MappingEngine:
         """
         if self.upload_keyframes_each_step:   # GT RGB (u8) + depth (f32) cross PCIe every step
             self.h2d_bytes += kf.intrinsics.width * kf.intrinsics.height * 7
+        self.render.ensure(n, kf.intrinsics.width, kf.intrinsics.height)
         graphs = getattr(self, "_graphs", {})
         entry = graphs.get(self._graph_key(kf, slots, n)) if self.use_graphs else None
         if entry is not None:
