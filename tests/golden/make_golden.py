@@ -352,7 +352,33 @@ def make_store_trace():
     (HERE / "store_trace.json").write_text(json.dumps(trace))
 
 
+def make_select_trace():
+    """KeyframeIndex / select_keyframe / record_loss policy trace (select.py)."""
+    from splatmap import select, sim
+    rng = np.random.default_rng(21)
+    idx = select.KeyframeIndex(config=select.SelectConfig(grid_resolution_m=50.0))
+    ops = []
+    for k in range(12):
+        pos = rng.uniform(-80, 80, size=3)
+        idx.add(k, pos)
+        ops.append({"op": "add", "id": k, "pos": pos.tolist()})
+    for step in range(200):
+        latest = int(rng.integers(0, 12))
+        try:
+            cands = select.candidate_set(idx.position_of(latest), idx)
+        except Exception:
+            cands = [latest]
+        seed = sim._derive_seed(7, 2, step)
+        chosen = select.select_keyframe(cands, idx, seed)
+        loss = float(rng.uniform(0, 2)) if step % 7 else 0.0
+        select.record_loss(chosen, loss, idx)
+        ops.append({"op": "step", "latest": latest, "cands": cands, "seed": seed, "chosen": chosen,
+                    "loss": loss, "usage": [idx.usage_of(i) for i in range(12)]})
+    (HERE / "select_trace.json").write_text(json.dumps(ops))
+
+
 if __name__ == "__main__":
+    make_select_trace()
     print("reference splatmap", splatmap.__version__, "from", splatmap.__file__)
     make_render_small()
     make_loss()

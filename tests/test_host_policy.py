@@ -1,0 +1,152 @@
+"""CPU tests of the host-side policy and formats against reference fixtures.
+
+Everything here runs without a GPU: chunk ids (grid.py), frustum planes
+(culling.py:80-101), keyframe selection (select.py), the .dcg/.dkf codecs
+(diskformat.py), and the mapping-step metrics format (sim.py:66-87).
+"""
+import json
+
+import numpy as np
+import pytest
+
+from paper_2511_23030_b200 import diskformat, grid, select
+from paper_2511_23030_b200.core import CameraIntrinsics, Gaussian, Keyframe, Pose, quat_normalize
+from paper_2511_23030_b200.culling import extract_frustum
+from paper_2511_23030_b200.errors import CorruptChunk, Malformed, OutOfRange
+from tests.conftest import GOLDEN
+
+
+def test_encode_positions_bit_exact(golden):
+    g = golden("grid.npz")
+    for k in range(3):
+        ids = grid.encode_positions(g[f"s{k}_positions"], float(g[f"s{k}_size"]))
+        assert np.array_equal(ids, g[f"s{k}_ids"])
+
+
+def test_grid_known_answers():
+    # test_grid.py / test_acceptance.py criterion 1
+    assert grid.encode_id(grid.ChunkCoord(0, 0, 0)) == 4611688217451692032
+    assert grid.encode_id(grid.ChunkCoord(grid.COORD_MIN, grid.COORD_MIN, grid.COORD_MIN)) == 0
+    c = grid.ChunkCoord(123, -456, 789)
+    assert grid.decode_id(grid.encode_id(c)) == c
+    assert grid.chunk_coord([4.999, -5.0, 5.0], 10.0) == grid.ChunkCoord(0, 0, 1)
+    with pytest.raises(OutOfRange):
+        grid.encode_id(grid.ChunkCoord(grid.COORD_MAX + 1, 0, 0))
+    with pytest.raises(Malformed):
+        grid.decode_id(1 << 63)
+    rng = np.random.default_rng(1)
+    coords = rng.integers(grid.COORD_MIN, grid.COORD_MAX + 1, size=(2000, 3))
+    ids = np.array([grid.encode_id(grid.ChunkCoord(*map(int, c))) for c in coords], dtype=np.uint64)
+    assert np.array_equal(grid.decode_ids(ids), coords)
+
+
+def test_frustum_planes_bit_exact(golden):
+    g = golden("grid.npz")
+    it = g["intr"]
+    intr = CameraIntrinsics(fx=it[0], fy=it[1], cx=it[2], cy=it[3], near=it[4], far=it[5],
+                            width=int(it[6]), height=int(it[7]))
+    for t in range(int(g["vis_count"])):
+        pose = Pose(rotation=g[f"v{t}_pose_q"], translation=g[f"v{t}_pose_t"])
+        assert np.array_equal(extract_frustum(pose, intr).planes, g[f"v{t}_planes"])
+
+
+def test_keyframe_selection_trace():
+    ops = json.loads((GOLDEN / "select_trace.json").read_text())
+    idx = select.KeyframeIndex(config=select.SelectConfig(grid_resolution_m=50.0))
+    from paper_2511_23030_b200.mapping import derive_seed
+    for op in ops:
+        if op["op"] == "add":
+            idx.add(op["id"], op["pos"])
+            continue
+        latest = op["latest"]
+        try:
+            cands = select.candidate_set(idx.position_of(latest), idx)
+        except Exception:
+            cands = [latest]
+        assert cands == op["cands"]
+        seed = derive_seed(7, 2, ops.index(op) - 12)
+        assert seed == op["seed"]
+        chosen = select.select_keyframe(cands, idx, seed)
+        assert chosen == op["chosen"]
+        select.record_loss(chosen, op["loss"], idx)
+        assert [idx.usage_of(i) for i in range(12)] == op["usage"]
+
+
+def test_chunk_codec_matches_reference_bytes(golden):
+    g = golden("diskformat.npz")
+    gs = [Gaussian(position=g["positions"][i], rotation=g["rotations"][i], scale=g["scales"][i],
+                   opacity=float(g["opacities"][i]), sh=g["sh"][i]) for i in range(len(g["positions"]))]
+    plain = diskformat.pack_chunk(0x123456789A, gs)
+    assert plain == g["chunk_plain"].tobytes()
+    blob, off = g["opt_blob"].tobytes(), 0
+    for gg, n in zip(gs, g["opt_lens"]):
+        gg.opt_state = blob[off:off + int(n)]
+        off += int(n)
+    assert diskformat.pack_chunk(0xABCDEF, gs) == g["chunk_opt"].tobytes()
+    cid, back = diskformat.unpack_chunk(g["chunk_opt"].tobytes())
+    assert cid == 0xABCDEF and [x.opt_state for x in back] == [x.opt_state for x in gs]
+    # uniform-stride zero-copy view used by the device codec
+    cid, count, recs, stride = diskformat.parse_chunk_records(plain)
+    assert (cid, count, stride) == (0x123456789A, len(gs), 240)
+    assert np.array_equal(recs["position"].astype(np.float64), g["positions"])
+    assert diskformat.parse_chunk_records(g["chunk_opt"].tobytes())[2] is None   # foreign tails
+    assert diskformat.build_chunk_file(0x123456789A, recs) == plain
+
+
+def test_keyframe_codec_matches_reference_bytes(golden):
+    g = golden("diskformat.npz")
+    kf = Keyframe(id=42, pose=Pose(rotation=g["kf_pose_q"], translation=g["kf_pose_t"]),
+                  intrinsics=CameraIntrinsics(fx=20.0, fy=21.0, cx=6.0, cy=5.0, width=12, height=9,
+                                              near=0.1, far=60.0),
+                  rgb=g["kf_rgb"], depth=g["kf_depth"], last_loss=0.25, usage_remaining=3)
+    data = diskformat.pack_keyframe(kf)
+    assert data == g["keyframe"].tobytes()
+    back = diskformat.unpack_keyframe(data)
+    assert np.array_equal(back.rgb, kf.rgb) and np.array_equal(back.depth, kf.depth)
+
+
+def test_corrupt_files_rejected():
+    data = diskformat.pack_chunk(7, [Gaussian(position=[1, 2, 3])])
+    with pytest.raises(CorruptChunk):
+        diskformat.unpack_chunk(b"BAD!" + data[4:])
+    with pytest.raises(CorruptChunk):
+        diskformat.unpack_chunk(data[:-3])
+    with pytest.raises(CorruptChunk):
+        diskformat.read_chunk_header(data[:10])
+
+
+def test_persistence_roundtrip_randomized():
+    """test_acceptance.py criterion 9 (chunk half) on this codec."""
+    rng = np.random.default_rng(109)
+    for _ in range(200):
+        gs = []
+        for _ in range(int(rng.integers(0, 6))):
+            opt = rng.bytes(int(rng.integers(1, 24))) if rng.random() < 0.5 else b""
+            gs.append(diskformat.storage_canonical(Gaussian(
+                position=rng.uniform(-500, 500, size=3), rotation=quat_normalize(rng.normal(size=4)),
+                scale=rng.uniform(0.01, 2.0, size=3), opacity=float(rng.uniform(0, 1)),
+                sh=rng.normal(size=48), opt_state=opt)))
+        cid = int(rng.integers(0, 2**63))
+        out_id, out = diskformat.unpack_chunk(diskformat.pack_chunk(cid, gs))
+        assert out_id == cid and len(out) == len(gs)
+        for a, b in zip(out, gs):
+            assert np.array_equal(a.position, b.position) and np.array_equal(a.sh, b.sh)
+            assert a.opacity == b.opacity and a.opt_state == b.opt_state
+
+
+def test_metrics_row_format():
+    from paper_2511_23030_b200.mapping import METRICS_HEADER, FrameMetrics
+    assert METRICS_HEADER.count(",") == 11
+    row = FrameMetrics(1, 2, 3, 4, 5, 6, 7, 8, 9, 10, None, 0.125).csv_row()
+    assert row == "1,2,3,4,5,6,7,8,9,10,,0.125"
+
+
+def test_synthetic_workloads_are_canonical():
+    from paper_2511_23030_b200.synthetic import room_poses, room_scene
+    s = room_scene(20000, seed=3)
+    for a in (s.positions, s.rotations, s.scales, s.opacities, s.sh):
+        assert np.array_equal(a, a.astype(np.float32).astype(np.float64))
+    assert np.abs(np.linalg.norm(s.rotations, axis=1) - 1).max() <= 1e-6
+    ids = grid.encode_positions(s.positions, 1.0)
+    assert len(np.unique(ids)) == 128        # the 8x8x2 chunk grid
+    assert len(room_poses(16)) == 16

@@ -1,0 +1,163 @@
+"""ChunkStore (HBM slab + GPU codec) against the reference store's own trace.
+
+tests/golden/store_trace.json was recorded by running the reference
+ChunkStore (store.py) through 120 seeded insert / ensure_resident /
+evict_lru / mark_chunk_mutated operations: every LoadReport, eviction list,
+stats vector (loads, evictions, writes, io_ns, bytes), resident set and the
+final flushed map must be identical here.
+"""
+import json
+
+import numpy as np
+import pytest
+
+from tests.conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def _stats(st):
+    s = st.stats
+    return [s.active_gaussians, s.active_chunks, s.chunk_loads, s.chunk_evictions, s.chunk_writes,
+            s.io_nanos, s.bytes_read, s.bytes_written, s.budget_overshoot, st.generation,
+            s.total_gaussians_ever]
+
+
+def test_store_policy_trace_matches_reference(cuda, tmp_path):
+    from paper_2511_23030_b200.core import Gaussian
+    from paper_2511_23030_b200.errors import InsufficientEvictable
+    from paper_2511_23030_b200.store import ChunkStore, StoreConfig
+    trace = json.loads((GOLDEN / "store_trace.json").read_text())
+    st = ChunkStore(StoreConfig(disk_root=tmp_path, chunk_size_m=10.0, gaussian_budget=60,
+                                keyframe_budget=4, io_ns_per_byte=1.0))
+    for k, op in enumerate(trace["ops"]):
+        if op["op"] == "insert":
+            gs = [Gaussian(position=p, opacity=o, scale=s, rotation=r, sh=sh)
+                  for p, o, s, r, sh in zip(op["positions"], op["opacity"], op["scale"],
+                                            op["rotation"], op["sh"])]
+            assert st.insert_gaussians(gs) == op["ret"], k
+        elif op["op"] == "ensure":
+            rep = st.ensure_resident([int(i) for i in op["ids"]])
+            assert (rep.loaded, rep.already_resident) == (op["loaded"], op["already"]), k
+            assert [str(e) for e in rep.evicted] == op["evicted"], k
+        elif op["op"] == "evict":
+            prot = {int(p) for p in op["protected"]}
+            if op["error"]:
+                with pytest.raises(InsufficientEvictable):
+                    st.evict_lru(op["required"], protected=prot)
+            else:
+                assert [str(e) for e in st.evict_lru(op["required"], protected=prot)] == op["evicted"], k
+        else:
+            st.mark_chunk_mutated(int(op["id"]))
+        assert _stats(st) == op["stats"], (k, op["op"])
+        assert [str(r) for r in sorted(st.resident_chunk_ids())] == [str(r) for r in op["resident"]], k
+    st.flush()
+    assert _stats(st) == trace["final_stats"]
+    content = []
+    for cid, gs in st.iter_map():
+        for g in gs:
+            content.append([str(cid)] + g.position.tolist() + [g.opacity])
+    assert content == trace["final_map"]
+
+
+def test_evict_reload_bit_exact_with_adam_state(cuda, tmp_path):
+    """Chunks written with the 120-byte Adam tail reload params + moments exactly."""
+    import torch
+
+    from paper_2511_23030_b200.core import Gaussian, quat_normalize
+    from paper_2511_23030_b200.store import ChunkStore, StoreConfig
+    rng = np.random.default_rng(4)
+    st = ChunkStore(StoreConfig(disk_root=tmp_path, chunk_size_m=10.0, gaussian_budget=10_000,
+                                io_ns_per_byte=1.0))
+    gs = [Gaussian(position=rng.uniform(-4, 4, 3), rotation=quat_normalize(rng.normal(size=4)),
+                   scale=rng.uniform(0.01, 0.2, 3), opacity=float(rng.uniform(0, 1)),
+                   sh=rng.normal(size=48)) for _ in range(300)]
+    st.insert_gaussians(gs)
+    (cid,) = st.resident_chunk_ids()
+    ch = st.chunk(cid)
+    rows = slice(ch.offset, ch.offset + ch.count)
+    st.slab.adam_m[rows] = torch.randn_like(st.slab.adam_m[rows])
+    st.slab.adam_m[rows, 14] = 5.0
+    st.slab.adam_v[rows] = torch.rand_like(st.slab.adam_v[rows])
+    st.slab.adam_v[rows, 14:] = 0.0
+    st.slab.adam_m[rows, 15] = 0.0
+    st.mark_trained([cid])
+    before = [t[rows].clone() for t in (st.slab.params, st.slab.adam_m, st.slab.adam_v, st.slab.sh_rest)]
+    assert st.evict_lru(1) == [cid]
+    st.ensure_resident([cid])
+    ch = st.chunk(cid)
+    rows = slice(ch.offset, ch.offset + ch.count)
+    after = [t[rows] for t in (st.slab.params, st.slab.adam_m, st.slab.adam_v, st.slab.sh_rest)]
+    for a, b in zip(before, after):
+        assert torch.equal(a, b)
+    data = (tmp_path / "chunks" / f"{cid:016x}.dcg").read_bytes()
+    assert len(data) == 32 + 300 * 360
+
+
+def test_foreign_opt_state_roundtrips(cuda, tmp_path):
+    """Opaque opt_state payloads of untrained splats survive paging (store.py contract)."""
+    from paper_2511_23030_b200.core import Gaussian
+    from paper_2511_23030_b200.store import ChunkStore, StoreConfig
+    st = ChunkStore(StoreConfig(disk_root=tmp_path, gaussian_budget=100, io_ns_per_byte=1.0))
+    gs = [Gaussian(position=[1.0 + i * 0.01, 2.0, 3.0], opt_state=bytes([i, i + 1, i + 2]) * (i % 3))
+          for i in range(5)]
+    st.insert_gaussians(gs)
+    (cid,) = st.resident_chunk_ids()
+    st.evict_lru(1)
+    st.ensure_resident([cid])
+    assert [g.opt_state for g in st.chunk(cid).gaussians] == [g.opt_state for g in gs]
+
+
+def test_corrupt_chunk_detected_on_device(cuda, tmp_path):
+    from paper_2511_23030_b200.core import Gaussian
+    from paper_2511_23030_b200.errors import CorruptChunk
+    from paper_2511_23030_b200.store import ChunkStore, StoreConfig
+    st = ChunkStore(StoreConfig(disk_root=tmp_path, gaussian_budget=100, io_ns_per_byte=1.0))
+    st.insert_gaussians([Gaussian(position=[1.0, 2.0, 3.0]) for _ in range(3)])
+    st.flush()
+    (cid,) = st.resident_chunk_ids()
+    st.evict_lru(1)
+    p = tmp_path / "chunks" / f"{cid:016x}.dcg"
+    data = bytearray(p.read_bytes())
+    data[32 + 40:32 + 44] = np.float32(-1.0).tobytes()   # opacity of record 0 -> -1
+    p.write_bytes(bytes(data))
+    with pytest.raises(CorruptChunk):
+        st.ensure_resident([cid])
+
+
+def test_device_encode_positions_bit_exact(cuda, golden):
+    import torch
+
+    from paper_2511_23030_b200 import _lib
+    g = golden("grid.npz")
+    lib = _lib.load()
+    for k in range(3):
+        pos = g[f"s{k}_positions"]
+        rec = np.zeros((len(pos), 16), np.float32)
+        rec[:, :3] = pos
+        t = torch.as_tensor(rec, device="cuda")
+        ids = torch.empty(len(pos), dtype=torch.int64, device="cuda")
+        err = torch.empty(1, dtype=torch.int64, device="cuda")
+        _lib.check(lib.sm_encode_positions(_lib.ptr(t), len(pos), float(g[f"s{k}_size"]), _lib.ptr(ids),
+                                           _lib.ptr(err), _lib.stream_handle()))
+        assert int(err.item()) == -1
+        assert np.array_equal(ids.cpu().numpy().view(np.uint64), g[f"s{k}_ids"])
+
+
+def test_visible_chunks_bit_exact(cuda, golden):
+    """K1 over the chunk table == the reference's visible_chunks sets (culling.py:134)."""
+    from paper_2511_23030_b200.core import CameraIntrinsics, Pose
+    from paper_2511_23030_b200.culling import ChunkExtent, CullConfig, visible_chunks
+    from paper_2511_23030_b200.grid import ChunkCoord, encode_id
+    g = golden("grid.npz")
+    it = g["intr"]
+    intr = CameraIntrinsics(fx=it[0], fy=it[1], cx=it[2], cy=it[3], near=it[4], far=it[5],
+                            width=int(it[6]), height=int(it[7]))
+    coords = g["coords"]
+    ext = ChunkExtent(ChunkCoord(*map(int, coords.min(0))), ChunkCoord(*map(int, coords.max(0))))
+    cfg = CullConfig(max_distance_m=float(g["max_distance"]))
+    for t in range(int(g["vis_count"])):
+        occ = {encode_id(ChunkCoord(*map(int, c))) for c in coords[g[f"v{t}_occ"]]}
+        pose = Pose(rotation=g[f"v{t}_pose_q"], translation=g[f"v{t}_pose_t"])
+        got = visible_chunks(pose, intr, ext, occ.__contains__, cfg, 10.0)
+        assert sorted(got) == g[f"v{t}_visible"].tolist(), t
