@@ -31,7 +31,8 @@ __global__ void __launch_bounds__(256)
 loss_fwd_kernel(const float *__restrict__ rgb, const float *__restrict__ depth,
                 const uint8_t *__restrict__ gt, const float *__restrict__ gtf,
                 const float *__restrict__ gt_depth, int W, int H, int C,
-                float *__restrict__ dmaps /* [C][3 maps][H*W] */, LossAcc *acc, int want_grad) {
+                float *__restrict__ dmaps /* [C][3 maps][H*W] */, double *__restrict__ partial,
+                int want_grad) {
     __shared__ float sx[kLH][kLH], sy[kLH][kLH];
     __shared__ float hs[5][kLH][kLT];
     __shared__ float red[4][8];
@@ -119,17 +120,38 @@ loss_fwd_kernel(const float *__restrict__ rgb, const float *__restrict__ depth,
 #pragma unroll
         for (int t = 0; t < 4; t++) red[t][threadIdx.x >> 5] = v[t];
     __syncthreads();
-    if (threadIdx.x < 4) {
+    if (threadIdx.x < 4) {   // per-block partials, summed in a fixed order by loss_finalize
         double s = 0;
         for (int w = 0; w < 8; w++) s += red[threadIdx.x][w];
-        if (threadIdx.x == 0) atomicAdd(&acc->ssim, s);
-        if (threadIdx.x == 1) atomicAdd(&acc->l1, s);
-        if (threadIdx.x == 2 && s != 0.0) atomicAdd(&acc->dsum, s);
-        if (threadIdx.x == 3 && s != 0.0) atomicAdd(&acc->dcount, s);
+        const int64_t blk = ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        partial[blk * 4 + threadIdx.x] = s;
     }
 }
 
-__global__ void loss_finalize(LossAcc *acc, int W, int H, int C, float ls, float ld, float *out) {
+// Deterministic (fixed-order) reduction of the per-block partials, then the
+// loss terms.  One block of 256 threads.
+__global__ void __launch_bounds__(256)
+loss_finalize(const double *__restrict__ partial, int64_t nblk, LossAcc *acc, int W, int H, int C,
+              float ls, float ld, float *out) {
+    __shared__ double sh[4][256];
+    double s[4] = {0, 0, 0, 0};
+    for (int64_t b = threadIdx.x; b < nblk; b += 256)
+#pragma unroll
+        for (int t = 0; t < 4; t++) s[t] += partial[b * 4 + t];
+#pragma unroll
+    for (int t = 0; t < 4; t++) sh[t][threadIdx.x] = s[t];
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if ((int)threadIdx.x < o)
+#pragma unroll
+            for (int t = 0; t < 4; t++) sh[t][threadIdx.x] += sh[t][threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x) return;
+    acc->ssim = sh[0][0];
+    acc->l1 = sh[1][0];
+    acc->dsum = sh[2][0];
+    acc->dcount = sh[3][0];
     const double N = (double)W * H;
     const double Nc = (double)(W - 10) * (H - 10);
     const double l1 = acc->l1 / ((double)C * N);
@@ -205,8 +227,11 @@ loss_bwd_kernel(const float *__restrict__ rgb, const float *__restrict__ depth,
 
 static bool g_weights_set = false;
 
+static int64_t loss_blocks(int W, int H) { return ceil_div(W, kLT) * ceil_div(H, kLT) * 4; }
+
 int64_t loss_workspace_size(int W, int H) {
-    return align_up(sizeof(LossAcc), 256) + align_up((int64_t)12 * W * H * 4, 256);
+    return align_up(sizeof(LossAcc), 256) + align_up(loss_blocks(W, H) * 4 * 8, 256) +
+           align_up((int64_t)12 * W * H * 4, 256);
 }
 
 int loss_forward_backward(const float *rgb, const float *depth, const uint8_t *gt_rgb,
@@ -237,15 +262,18 @@ int loss_forward_backward(const float *rgb, const float *depth, const uint8_t *g
         if (e != cudaSuccess) return cuda_status(e, "loss weights");
         g_weights_set = true;
     }
-    LossAcc *acc = reinterpret_cast<LossAcc *>(ws);
-    float *dmaps = reinterpret_cast<float *>(static_cast<char *>(ws) + align_up(sizeof(LossAcc), 256));
-    cudaMemsetAsync(acc, 0, sizeof(LossAcc), st);
+    char *base = static_cast<char *>(ws);
+    LossAcc *acc = reinterpret_cast<LossAcc *>(base);
+    double *partial = reinterpret_cast<double *>(base + align_up(sizeof(LossAcc), 256));
+    float *dmaps = reinterpret_cast<float *>(base + align_up(sizeof(LossAcc), 256) +
+                                             align_up(loss_blocks(W, H) * 4 * 8, 256));
     dim3 grid((unsigned)ceil_div(W, kLT), (unsigned)ceil_div(H, kLT), (unsigned)C);
+    const int64_t nblk = (int64_t)grid.x * grid.y * grid.z;
     const int want = d_rgb != nullptr;
     prof_begin(ST_LOSS, st);
-    loss_fwd_kernel<<<grid, 256, 0, st>>>(rgb, depth, gt_rgb, gt_rgbf, gt_depth, W, H, C, dmaps, acc,
-                                          want);
-    loss_finalize<<<1, 1, 0, st>>>(acc, W, H, C, ls, ld, loss_out);
+    loss_fwd_kernel<<<grid, 256, 0, st>>>(rgb, depth, gt_rgb, gt_rgbf, gt_depth, W, H, C, dmaps,
+                                          partial, want);
+    loss_finalize<<<1, 256, 0, st>>>(partial, nblk, acc, W, H, C, ls, ld, loss_out);
     if (want)
         loss_bwd_kernel<<<grid, 256, 0, st>>>(rgb, depth, gt_rgb, gt_rgbf, gt_depth, W, H, C, dmaps,
                                               acc, ls, ld, d_rgb, d_depth);

@@ -156,10 +156,17 @@ struct BwdPix {
     }
 };
 
-// Same tiling as composite_fwd (128 threads x 2 pixels).  Instances are
-// revisited from the block's last contributor back to the tile start, 128
-// per shared-memory batch; a warp skips splats missing its 4 rows or lying
+// Same tiling as composite_fwd (256/PIX threads x PIX pixels).  Instances are
+// revisited from the block's last contributor back to the tile start, one
+// CTA-width batch at a time; a warp skips splats missing its rows or lying
 // past every one of its pixels' last contributor.
+//
+// Determinism: no floating-point atomics.  Each warp's 10 sums for an
+// instance land in its own shared slot; after the batch the slots are added
+// in warp order and written to the instance's emission slot (toff[rank] + the
+// tile's index in the splat's tile rectangle); grad_gather then sums a splat's
+// instances in a fixed order.  Reruns and CUDA-graph replays are bit-identical
+// (the reference's metrics determinism contract, test_acceptance.py crit. 10).
 template <int PIX>
 __global__ void __launch_bounds__(kTilePx / PIX)
 composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ikeys,
@@ -169,12 +176,15 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
               const float *__restrict__ d_depth, const float *__restrict__ d_alpha,
               const float4 *__restrict__ st_cd, const float *__restrict__ st_t,
               const float *__restrict__ st_tlast, const int32_t *__restrict__ st_last,
-              float *__restrict__ g2d) {
+              const uint32_t *__restrict__ toff, float *__restrict__ gbuf,
+              int32_t *__restrict__ tile_hor) {
     constexpr int NT = kTilePx / PIX;
+    constexpr int NW = NT / 32;
     __shared__ ProjRec s_rec[NT];
     __shared__ uint32_t s_rank[NT];
-    __shared__ float s_grad[NT][10];
+    __shared__ float s_part[NW][NT][10];
     __shared__ int s_maxlast;
+    const int warp = threadIdx.x / 32;
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31;
     const int ty0 = (tile / tiles_x) * kTile;
@@ -197,8 +207,11 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
     if (lane == 0) atomicMax(&s_maxlast, wmax);
     __syncthreads();
     const int maxlast = s_maxlast;
+    if (threadIdx.x == 0)   // rank of the tile's last visited instance (grad_gather's horizon)
+        tile_hor[tile] = maxlast >= start ? (int32_t)(ikeys[maxlast] & rank_mask) : -1;
     const int via = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);   // 0..7
     const int vib = 8 + ((lane >> 4) & 1);                                                // 8..9
+    const int tile_x = tile % tiles_x, tile_y = tile / tiles_x;
     for (int bend = maxlast + 1; bend > start; bend -= NT) {
         const int bstart = max(start, bend - NT);
         const int idx = bstart + (int)threadIdx.x;
@@ -206,9 +219,8 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
             const uint32_t rk = ikeys[idx] & rank_mask;
             s_rank[threadIdx.x] = rk;
             s_rec[threadIdx.x] = recs[rk];
-#pragma unroll
-            for (int k = 0; k < 10; k++) s_grad[threadIdx.x][k] = 0.f;
         }
+        for (int i = threadIdx.x; i < NW * NT * 10; i += NT) (&s_part[0][0][0])[i] = 0.f;
         __syncthreads();
         const int jtop = min(bend - 1, wmax) - bstart;
         for (int j = jtop; j >= 0; j--) {
@@ -235,20 +247,76 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
             }
             if (__any_sync(0xffffffffu, hit)) {
                 const float2 s = transpose_reduce10(v, lane);
-                if (!(lane & 3) && s.x != 0.f) atomicAdd(&s_grad[j][via], s.x);
-                if (!(lane & 15) && s.y != 0.f) atomicAdd(&s_grad[j][vib], s.y);
+                if (!(lane & 3)) s_part[warp][j][via] = s.x;
+                if (!(lane & 15)) s_part[warp][j][vib] = s.y;
             }
         }
         __syncthreads();
-        if (idx < bend) {
-            float *dst = g2d + (int64_t)s_rank[threadIdx.x] * kG2dStride;
+        if (idx < bend) {   // warp-ordered sum -> the instance's emission slot
+            const ProjRec &g = s_rec[threadIdx.x];
+            const int tx0 = rec_x0(g) / kTile, ty0r = rec_y0(g) / kTile;
+            const int ntx = rec_x1(g) / kTile - tx0 + 1;
+            const uint32_t slot = toff[s_rank[threadIdx.x]] + (uint32_t)((tile_y - ty0r) * ntx + tile_x - tx0);
+            float acc[12];
 #pragma unroll
             for (int k = 0; k < 10; k++) {
-                const float s = s_grad[threadIdx.x][k];
-                if (s != 0.f) atomicAdd(dst + k, s);
+                float a = 0.f;
+#pragma unroll
+                for (int w = 0; w < NW; w++) a += s_part[w][threadIdx.x][k];
+                acc[k] = a;
             }
+            acc[10] = acc[11] = 0.f;
+            float4 *dst = reinterpret_cast<float4 *>(gbuf + (int64_t)slot * kG2dStride);
+            dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+            dst[2] = make_float4(acc[8], acc[9], 0.f, 0.f);
         }
         __syncthreads();
+    }
+}
+
+// Per depth rank: sum its instances' gradient slots (visited ones only: an
+// instance was visited iff its rank is <= the tile's horizon rank) in slot
+// order.  Eight lanes per rank, fixed butterfly -> deterministic.
+__global__ void __launch_bounds__(256)
+grad_gather(const ProjRec *__restrict__ recs, const uint32_t *__restrict__ tcount_r,
+            const uint32_t *__restrict__ toff, int64_t n, const float *__restrict__ gbuf,
+            const int32_t *__restrict__ tile_hor, int tiles_x, float *__restrict__ g2d) {
+    const int lane = threadIdx.x & 31, sub = lane & 7;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x / 8;
+    for (int64_t rb = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane) / 8; rb < n; rb += stride) {
+        const int64_t r = rb + lane / 8;
+        float acc[10];
+#pragma unroll
+        for (int k = 0; k < 10; k++) acc[k] = 0.f;
+        const uint32_t cnt = r < n ? tcount_r[r] : 0u;
+        if (cnt) {
+            const ProjRec &g = recs[r];
+            const int tx0 = rec_x0(g) / kTile, ty0 = rec_y0(g) / kTile;
+            const int ntx = rec_x1(g) / kTile - tx0 + 1;
+            const uint32_t o = toff[r];
+            for (uint32_t j = sub; j < cnt; j += 8) {
+                const int t = (ty0 + (int)j / ntx) * tiles_x + tx0 + (int)j % ntx;
+                if ((int64_t)r > (int64_t)tile_hor[t]) continue;
+                const float4 *src = reinterpret_cast<const float4 *>(gbuf + (int64_t)(o + j) * kG2dStride);
+                const float4 a = src[0], b = src[1], c = src[2];
+                acc[0] += a.x, acc[1] += a.y, acc[2] += a.z, acc[3] += a.w;
+                acc[4] += b.x, acc[5] += b.y, acc[6] += b.z, acc[7] += b.w;
+                acc[8] += c.x, acc[9] += c.y;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 10; k++) {
+            acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], 4);
+            acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], 2);
+            acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], 1);
+        }
+        if (sub == 0 && r < n) {
+            float4 *dst = reinterpret_cast<float4 *>(g2d + r * kG2dStride);
+            dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+            dst[2] = make_float4(acc[8], acc[9], 0.f, 0.f);
+        }
     }
 }
 
@@ -405,21 +473,21 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
     }
     if (n == 0) return SM_OK;
     RenderBufs b = render_bufs(ws, L);
-    cudaMemsetAsync(b.g2d, 0, n * (int64_t)sizeof(float) * kG2dStride, st);
     const uint32_t rank_mask = (uint32_t)((1ull << L.rank_bits) - 1ull);
     prof_begin(ST_COMPOSITE_BWD, st);
-    static const int pix = [] {
+    static const int pix = [] {   // per-warp shared slots: PIX = 2 (4 warps) or 4 (2 warps)
         const char *v = getenv("SM_BWD_PIX");
-        const int p = v ? atoi(v) : 2;
-        return (p == 1 || p == 4) ? p : 2;
+        return (v && atoi(v) == 4) ? 4 : 2;
     }();
-    auto kern = pix == 1 ? composite_bwd<1> : (pix == 4 ? composite_bwd<4> : composite_bwd<2>);
+    auto kern = pix == 4 ? composite_bwd<4> : composite_bwd<2>;
     kern<<<(unsigned)L.n_tiles, kTilePx / pix, 0, st>>>(
         b.ranges, L.tile_passes & 1 ? b.ikey1 : b.ikey0, rank_mask, b.rec_sorted, b.p64, b.order0,
         dims.width, dims.height, L.tiles_x, d_rgb, d_depth, d_alpha, b.pix_cd, b.pix_t, b.pix_tlast,
-        b.pix_last, b.g2d);
+        b.pix_last, b.toff, b.gbuf, b.tile_hor);
+    grad_gather<<<(unsigned)min64(ceil_div(n * 8, 256), 148 * 16), 256, 0, st>>>(
+        b.rec_sorted, b.tcount_r, b.toff, n, b.gbuf, b.tile_hor, L.tiles_x, b.g2d);
     prof_end(ST_COMPOSITE_BWD, st);
-    count_launches(2);
+    count_launches(3);
     CamBwd cb;
     for (int k = 0; k < 9; k++) cb.r[k] = cam.r_wc[k];
     for (int k = 0; k < 3; k++) cb.t[k] = cam.t[k];

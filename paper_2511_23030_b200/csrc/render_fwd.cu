@@ -64,6 +64,8 @@ RenderLayout render_layout(const sm_render_dims &d) {
     L.o_g2d = take(G * (int64_t)sizeof(float) * kG2dStride);
     L.o_sort_hist = take(sort_scratch_bytes(G > I ? G : I));
     L.o_scan = take(scan_scratch_bytes(G));
+    L.o_gbuf = take(I * (int64_t)sizeof(float) * kG2dStride);
+    L.o_tile_hor = take(L.n_tiles * 4);
     L.total = off;
     return L;
 }

@@ -156,9 +156,10 @@ def unpack_chunk(data: bytes) -> tuple[int, list[Gaussian]]:
         raise CorruptChunk(f"chunk record fails invariants: {exc}") from exc
 
 
-def build_chunk_file(encoded_id: int, records: np.ndarray) -> bytes:
-    """Header + a packed record array (240- or 360-byte stride) from K9."""
-    n = records.size if records.ndim == 1 else records.shape[0]
+def build_chunk_file(encoded_id: int, records: np.ndarray, count: int | None = None) -> bytes:
+    """Header + packed records (240- or 360-byte stride): a structured record
+    array, or raw bytes from K9 with an explicit record `count`."""
+    n = len(records) if count is None else int(count)
     return _HDR.pack(CHUNK_MAGIC, FORMAT_VERSION, encoded_id, n, 0) + records.tobytes()
 
 

@@ -91,8 +91,8 @@ def test_paging_steps_are_deterministic(cuda, tmp_path):
         out = [eng.optimization_step(f, s).csv_row() for f in range(3) for s in range(5)]
         rows.append(out)
         st = eng.store.stats
-        assert st.chunk_loads + st.chunk_evictions > 0
-        assert st.active_gaussians <= max(12_000, st.active_gaussians - st.budget_overshoot)
+        assert st.chunk_evictions > 0 and st.chunk_writes > 0
+        assert st.budget_overshoot == max(0, st.active_gaussians - 12_000)
     assert rows[0] == rows[1]
 
 
