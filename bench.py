@@ -104,6 +104,7 @@ STAGE_BYTES = {
     "composite_bwd": lambda n, i, p: i * (4 + 64 + 40) + p * (28 + 16),
     "project_bwd": lambda n, i, p: n * (4 + 4 + 4 + 64 + 40 + 2 * 64),
     "adam": lambda n, i, p: n * (4 + 7 * 64),
+    "grad_gather": lambda n, i, p: n * (4 + 4 + 64 + 48) + i * (48 + 4),
 }
 
 

@@ -28,7 +28,7 @@ static long long g_calls[ST_COUNT];
 
 static const char *kNames[ST_COUNT] = {"project_fwd", "depth_sort", "bin_emit", "tile_sort",
                                        "composite_fwd", "loss", "composite_bwd", "project_bwd",
-                                       "adam", "cull", "codec"};
+                                       "adam", "cull", "codec", "grad_gather"};
 
 // CUDA-graph support: while a graph is being captured, stage event pairs and
 // kernel counts are filed under the graph id; every replay re-records the

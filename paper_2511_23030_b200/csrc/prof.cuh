@@ -18,6 +18,7 @@ enum Stage {
     ST_ADAM,
     ST_CULL,
     ST_CODEC,
+    ST_GRAD_GATHER,
     ST_COUNT
 };
 

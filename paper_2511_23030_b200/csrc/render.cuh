@@ -5,6 +5,7 @@
 namespace sm {
 
 constexpr int kG2dStride = 12;   // per-rank 2D grads: u v ia ib ic op r g b z - -
+constexpr uint32_t kEmitSmall = 32;   // splats with more tiles are emitted / gathered per block
 
 struct RenderLayout {
     int tiles_x, tiles_y;

@@ -13,9 +13,10 @@
 // alpha = 1 never divides by zero), the colour/depth behind k is carried
 // normalised (B_k = alpha_{k+1} c_{k+1} + (1 - alpha_{k+1}) B_{k+1}) and
 // dA/dalpha_k uses the running product P_k = prod_{j>k} (1 - alpha_j).
-// Per-Gaussian sums: a 16-wide transposed butterfly (16 shuffles, one value
-// per lane pair) per warp, shared-memory atomics across the 8 warps of the
-// tile, one global atomic per (instance, value) per tile.
+// Per-splat sums without floating-point atomics (deterministic): a 10-value
+// transposed warp butterfly (14 shuffles), per-warp shared slots added in warp
+// order, one gradient slot per (splat, tile) instance, and a fixed-order sum
+// over a splat's instances (inline in project_bwd, or a warp per big splat).
 #include "prof.cuh"
 #include "render.cuh"
 
@@ -55,38 +56,6 @@ __device__ __forceinline__ float2 transpose_reduce10(const float (&v)[16], int l
     d += __shfl_xor_sync(0xffffffffu, d, 2);
     d += __shfl_xor_sync(0xffffffffu, d, 1);
     return make_float2(c, d);
-}
-
-__device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-        const bool hi = lane & 16;
-        const float send = hi ? v[k] : v[k + 8];
-        const float keep = hi ? v[k + 8] : v[k];
-        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const bool hi = lane & 8;
-        const float send = hi ? v[k] : v[k + 4];
-        const float keep = hi ? v[k + 4] : v[k];
-        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-#pragma unroll
-    for (int k = 0; k < 2; k++) {
-        const bool hi = lane & 4;
-        const float send = hi ? v[k] : v[k + 2];
-        const float keep = hi ? v[k + 2] : v[k];
-        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    {
-        const bool hi = lane & 2;
-        const float send = hi ? v[0] : v[1];
-        const float keep = hi ? v[1] : v[0];
-        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-    }
-    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-    return v[0];   // value index ((lane>>4)&1)*8 + ((lane>>3)&1)*4 + ((lane>>2)&1)*2 + ((lane>>1)&1)
 }
 
 // Per-pixel reverse state.  T holds T_{k+1} while walking back; the stored
@@ -275,47 +244,51 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
     }
 }
 
-// Per depth rank: sum its instances' gradient slots (visited ones only: an
-// instance was visited iff its rank is <= the tile's horizon rank) in slot
-// order.  Eight lanes per rank, fixed butterfly -> deterministic.
+// Sum of a splat's visited instance slots, in slot order (an instance was
+// visited iff its rank is <= its tile's horizon rank).  j = first, first +
+// step, ... so callers can split a big splat across a block.
+__device__ __forceinline__ void sum_slots(const ProjRec &g, int64_t r, uint32_t o, uint32_t first,
+                                          uint32_t cnt, uint32_t step, const float *gbuf,
+                                          const int32_t *tile_hor, int tiles_x, float (&acc)[10]) {
+    const int tx0 = rec_x0(g) / kTile, ty0 = rec_y0(g) / kTile;
+    const int ntx = rec_x1(g) / kTile - tx0 + 1;
+    for (uint32_t j = first; j < cnt; j += step) {
+        const int t = (ty0 + (int)j / ntx) * tiles_x + tx0 + (int)j % ntx;
+        if (r > (int64_t)tile_hor[t]) continue;
+        const float4 *src = reinterpret_cast<const float4 *>(gbuf + (int64_t)(o + j) * kG2dStride);
+        const float4 a = src[0], b = src[1], c = src[2];
+        acc[0] += a.x, acc[1] += a.y, acc[2] += a.z, acc[3] += a.w;
+        acc[4] += b.x, acc[5] += b.y, acc[6] += b.z, acc[7] += b.w;
+        acc[8] += c.x, acc[9] += c.y;
+    }
+}
+
+// Splats with more than kEmitSmall tiles (queued at emission, rare): one block
+// each, strided partial sums + fixed-order tree -> g2d[rank].  Smaller splats
+// are summed inline by project_bwd.  Both orders are fixed: deterministic.
 __global__ void __launch_bounds__(256)
-grad_gather(const ProjRec *__restrict__ recs, const uint32_t *__restrict__ tcount_r,
-            const uint32_t *__restrict__ toff, int64_t n, const float *__restrict__ gbuf,
-            const int32_t *__restrict__ tile_hor, int tiles_x, float *__restrict__ g2d) {
-    const int lane = threadIdx.x & 31, sub = lane & 7;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x / 8;
-    for (int64_t rb = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane) / 8; rb < n; rb += stride) {
-        const int64_t r = rb + lane / 8;
+grad_gather_big(const ProjRec *__restrict__ recs, const uint32_t *__restrict__ tcount_r,
+                const uint32_t *__restrict__ toff, const sm_render_counters *ctr,
+                const uint32_t *__restrict__ big, const float *__restrict__ gbuf,
+                const int32_t *__restrict__ tile_hor, int tiles_x, float *__restrict__ g2d) {
+    const uint32_t nbig = ctr->overflow ? 0u : ctr->reserved[1];
+    const int lane = threadIdx.x & 31;
+    const uint32_t nwarps = gridDim.x * (blockDim.x / 32);
+    for (uint32_t bi = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; bi < nbig; bi += nwarps) {
+        const uint32_t r = big[bi];   // one warp per big splat: strided lanes + fixed butterfly
         float acc[10];
 #pragma unroll
         for (int k = 0; k < 10; k++) acc[k] = 0.f;
-        const uint32_t cnt = r < n ? tcount_r[r] : 0u;
-        if (cnt) {
-            const ProjRec &g = recs[r];
-            const int tx0 = rec_x0(g) / kTile, ty0 = rec_y0(g) / kTile;
-            const int ntx = rec_x1(g) / kTile - tx0 + 1;
-            const uint32_t o = toff[r];
-            for (uint32_t j = sub; j < cnt; j += 8) {
-                const int t = (ty0 + (int)j / ntx) * tiles_x + tx0 + (int)j % ntx;
-                if ((int64_t)r > (int64_t)tile_hor[t]) continue;
-                const float4 *src = reinterpret_cast<const float4 *>(gbuf + (int64_t)(o + j) * kG2dStride);
-                const float4 a = src[0], b = src[1], c = src[2];
-                acc[0] += a.x, acc[1] += a.y, acc[2] += a.z, acc[3] += a.w;
-                acc[4] += b.x, acc[5] += b.y, acc[6] += b.z, acc[7] += b.w;
-                acc[8] += c.x, acc[9] += c.y;
-            }
-        }
+        sum_slots(recs[r], r, toff[r], lane, tcount_r[r], 32, gbuf, tile_hor, tiles_x, acc);
 #pragma unroll
-        for (int k = 0; k < 10; k++) {
-            acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], 4);
-            acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], 2);
-            acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], 1);
-        }
-        if (sub == 0 && r < n) {
-            float4 *dst = reinterpret_cast<float4 *>(g2d + r * kG2dStride);
-            dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-            dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
-            dst[2] = make_float4(acc[8], acc[9], 0.f, 0.f);
+        for (int k = 0; k < 10; k++)
+#pragma unroll
+            for (int o = 16; o; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+        if (lane < 10) {
+            float v = acc[0];
+#pragma unroll
+            for (int k = 1; k < 10; k++) v = lane == k ? acc[k] : v;
+            g2d[(int64_t)r * kG2dStride + lane] = v;
         }
     }
 }
@@ -331,16 +304,28 @@ struct CamBwd {
 __global__ void __launch_bounds__(256)
 project_bwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots, int64_t n,
             CamBwd cam, const uint32_t *__restrict__ order, const uint32_t *__restrict__ tcount_r,
+            const ProjRec *__restrict__ recs, const uint32_t *__restrict__ toff,
+            const float *__restrict__ gbuf, const int32_t *__restrict__ tile_hor, int tiles_x,
             const float *__restrict__ g2d, float *__restrict__ grads) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n || tcount_r[r] == 0) return;
+    if (r >= n) return;
+    const uint32_t cnt = tcount_r[r];
+    if (cnt == 0) return;
+    float gk[10];
+    if (cnt > kEmitSmall) {   // summed by grad_gather_big
+#pragma unroll
+        for (int k = 0; k < 10; k++) gk[k] = g2d[r * kG2dStride + k];
+    } else {
+#pragma unroll
+        for (int k = 0; k < 10; k++) gk[k] = 0.f;
+        sum_slots(recs[r], r, toff[r], 0, cnt, 1, gbuf, tile_hor, tiles_x, gk);
+    }
     const uint32_t i = order[r];
     const int64_t slot = slots ? (int64_t)slots[i] : (int64_t)i;
     const float4 A = params[slot * 4 + 0];
     const float4 B = params[slot * 4 + 1];
     const float4 C = params[slot * 4 + 2];
     const float4 D = params[slot * 4 + 3];
-    const float *gk = g2d + r * kG2dStride;
     const double gu = gk[0], gv = gk[1], gia = gk[2], gib = gk[3], gic = gk[4], gop = gk[5];
     const double gcol[3] = {gk[6], gk[7], gk[8]};
     const double gdep = gk[9];
@@ -484,9 +469,11 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
         b.ranges, L.tile_passes & 1 ? b.ikey1 : b.ikey0, rank_mask, b.rec_sorted, b.p64, b.order0,
         dims.width, dims.height, L.tiles_x, d_rgb, d_depth, d_alpha, b.pix_cd, b.pix_t, b.pix_tlast,
         b.pix_last, b.toff, b.gbuf, b.tile_hor);
-    grad_gather<<<(unsigned)min64(ceil_div(n * 8, 256), 148 * 16), 256, 0, st>>>(
-        b.rec_sorted, b.tcount_r, b.toff, n, b.gbuf, b.tile_hor, L.tiles_x, b.g2d);
     prof_end(ST_COMPOSITE_BWD, st);
+    prof_begin(ST_GRAD_GATHER, st);
+    grad_gather_big<<<148 * 4, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.toff, b.ctr, b.tcount, b.gbuf,
+                                              b.tile_hor, L.tiles_x, b.g2d);
+    prof_end(ST_GRAD_GATHER, st);
     count_launches(3);
     CamBwd cb;
     for (int k = 0; k < 9; k++) cb.r[k] = cam.r_wc[k];
@@ -497,7 +484,8 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
     cb.cy = cam.cy;
     prof_begin(ST_PROJECT_BWD, st);
     project_bwd<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
-        reinterpret_cast<const float4 *>(params), slots, n, cb, b.order0, b.tcount_r, b.g2d, grads);
+        reinterpret_cast<const float4 *>(params), slots, n, cb, b.order0, b.tcount_r, b.rec_sorted,
+        b.toff, b.gbuf, b.tile_hor, L.tiles_x, b.g2d, grads);
     prof_end(ST_PROJECT_BWD, st);
     SM_CHECK_LAUNCH("render_backward");
     return SM_OK;

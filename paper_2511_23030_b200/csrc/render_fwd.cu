@@ -187,7 +187,6 @@ __global__ void check_instances(sm_render_counters *ctr, int64_t max_instances) 
 // are queued and a block per queued splat writes its tiles in parallel.
 // Keys are (tile << rank_bits) | rank at the rank's scanned offset, so the
 // array is in rank order whichever thread writes a slot.
-constexpr uint32_t kEmitSmall = 32;
 
 __device__ __forceinline__ void emit_tiles(const ProjRec &g, uint32_t r, uint32_t o, uint32_t first,
                                            uint32_t count, uint32_t step, int rank_bits, int tiles_x,

@@ -13,6 +13,66 @@ struct AdamDev {
     float b1, b2, eps, min_scale;
 };
 
+// Four threads per Gaussian, one float4 quarter of each record each (so a
+// warp streams 8 full 64-byte records per array with 16-byte accesses and a
+// thread keeps ~30 registers instead of ~90).  Quarter q holds record scalars
+// 4q..4q+3: q0 = px py pz qw, q1 = qx qy qz sx, q2 = sy sz op sh0r,
+// q3 = sh0g sh0b - - (m.q3.z = per-Gaussian step count).  The quaternion
+// spans q0.w and q1.xyz: its norm is exchanged with one shuffle.
+__global__ void __launch_bounds__(256)
+adam_quarter_kernel(float4 *__restrict__ params, float4 *__restrict__ m, float4 *__restrict__ v,
+                    float4 *__restrict__ grads, const int32_t *__restrict__ slots, int64_t n,
+                    AdamDev c, const uint32_t *__restrict__ skip) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int q = threadIdx.x & 3;
+    const int64_t i = t >> 2;
+    const bool ok = i < n && !(skip && *skip);
+    const int64_t s = ok ? (slots ? (int64_t)slots[i] : i) : 0;
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f), g = p, mm = p, vv = p;
+    if (ok) {
+        p = params[s * 4 + q];
+        g = grads[s * 4 + q];
+        mm = m[s * 4 + q];
+        vv = v[s * 4 + q];
+    }
+    // per-Gaussian step count lives in m quarter 3, component z
+    const float step = __shfl_sync(0xffffffffu, mm.z, (threadIdx.x & 31) | 3) + 1.f;
+    const float bc1 = 1.f - powf(c.b1, step);
+    const float bc2s = sqrtf(1.f - powf(c.b2, step));
+    float pv[4] = {p.x, p.y, p.z, p.w}, gv[4] = {g.x, g.y, g.z, g.w};
+    float mv[4] = {mm.x, mm.y, mm.z, mm.w}, vvv[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int idx = 4 * q + k;
+        if (idx < 14) {
+            mv[k] = c.b1 * mv[k] + (1.f - c.b1) * gv[k];
+            vvv[k] = c.b2 * vvv[k] + (1.f - c.b2) * gv[k] * gv[k];
+            pv[k] -= (c.lr[idx] / bc1) * mv[k] / (sqrtf(vvv[k]) / bc2s + c.eps);
+        }
+    }
+    if (q == 3) mv[2] = step;
+    // quaternion renormalisation (core.py:186 unit-norm invariant)
+    const float part = q == 0 ? pv[3] * pv[3] : (q == 1 ? pv[0] * pv[0] + pv[1] * pv[1] + pv[2] * pv[2] : 0.f);
+    const float other = __shfl_xor_sync(0xffffffffu, part, 1);
+    const float qn = sqrtf(part + other);
+    if (q == 0) pv[3] = qn > 0.f ? pv[3] * (1.f / qn) : 1.f;
+    if (q == 1) {
+        const float inv = qn > 0.f ? 1.f / qn : 0.f;
+        pv[0] *= inv, pv[1] *= inv, pv[2] *= inv;
+        pv[3] = fmaxf(pv[3], c.min_scale);   // sx
+    }
+    if (q == 2) {
+        pv[0] = fmaxf(pv[0], c.min_scale);   // sy
+        pv[1] = fmaxf(pv[1], c.min_scale);   // sz
+        pv[2] = fminf(fmaxf(pv[2], 0.f), 1.f);   // opacity
+    }
+    if (!ok) return;
+    params[s * 4 + q] = make_float4(pv[0], pv[1], pv[2], pv[3]);
+    m[s * 4 + q] = make_float4(mv[0], mv[1], mv[2], mv[3]);
+    v[s * 4 + q] = make_float4(vvv[0], vvv[1], vvv[2], vvv[3]);
+    grads[s * 4 + q] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
 __global__ void __launch_bounds__(256)
 adam_kernel(float4 *__restrict__ params, float4 *__restrict__ m, float4 *__restrict__ v,
             float4 *__restrict__ grads, const int32_t *__restrict__ slots, int64_t n, AdamDev c,
@@ -77,7 +137,7 @@ int adam_step(float *params, float *m, float *v, float *grads, const int32_t *sl
     d.min_scale = cfg.min_scale;
     prof_begin(ST_ADAM, st);
     count_launches(1);
-    adam_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+    adam_quarter_kernel<<<(unsigned)ceil_div(n * 4, 256), 256, 0, st>>>(
         reinterpret_cast<float4 *>(params), reinterpret_cast<float4 *>(m),
         reinterpret_cast<float4 *>(v), reinterpret_cast<float4 *>(grads), slots, n, d, skip);
     prof_end(ST_ADAM, st);
