@@ -182,16 +182,26 @@ class VisibilityCache:
     cfg: CullConfig = field(default_factory=CullConfig)
     _entries: list = field(default_factory=list)
 
+    def _match(self, e: _CacheEntry, pose: Pose, intr, generation: int, s: float) -> bool:
+        return (e.generation == generation and e.chunk_size == s and e.intr == intr
+                and float(np.linalg.norm(e.translation - pose.translation)) < self.cfg.pose_quantum_m
+                and _rotation_angle(e.rotation, pose.rotation) < self.cfg.pose_quantum_rad)
+
     def query(self, pose: Pose, intr: CameraIntrinsics, extent: ChunkExtent,
               existing: Callable[[int], bool], generation: int, s: float,
               candidates: Iterable[int] | None = None) -> tuple[set[int], bool]:
-        for i in range(len(self._entries) - 1, -1, -1):
-            e = self._entries[i]
-            if (e.generation == generation and e.chunk_size == s and e.intr == intr
-                    and float(np.linalg.norm(e.translation - pose.translation)) < self.cfg.pose_quantum_m
-                    and _rotation_angle(e.rotation, pose.rotation) < self.cfg.pose_quantum_rad):
-                self._entries.append(self._entries.pop(i))
-                return set(e.result), True
+        # Most recent matching entry, as the reference scan (culling.py:213-229).
+        # A vectorised distance prefilter (with a relative margin) limits the
+        # exact per-entry test to plausible entries; the verdict is the exact one.
+        if self._entries:
+            tr = np.array([e.translation for e in self._entries])
+            d = np.sqrt(((tr - pose.translation) ** 2).sum(axis=1))
+            near = np.flatnonzero(d < self.cfg.pose_quantum_m * (1 + 1e-9) + 1e-300)
+            for i in near[::-1]:
+                e = self._entries[int(i)]
+                if self._match(e, pose, intr, generation, s):
+                    self._entries.append(self._entries.pop(int(i)))
+                    return set(e.result), True
         result = visible_chunks(pose, intr, extent, existing, self.cfg, s, candidates)
         self._entries.append(_CacheEntry(pose.translation.copy(), pose.rotation.copy(), intr, s,
                                          generation, frozenset(result)))

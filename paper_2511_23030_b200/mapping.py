@@ -26,7 +26,8 @@ from .core import CameraIntrinsics, Keyframe, Pose
 from .culling import ChunkExtent, CullConfig, VisibilityCache
 from .errors import DeviceFailure, EmptyCandidates
 from .renderloss import LossEngine, LossWeights, RenderEngine, camera_for
-from .select import KeyframeIndex, SelectConfig, candidate_set, overlap, record_loss, select_keyframe
+from .select import (KeyframeIndex, SelectConfig, candidate_set, draw_uniform, overlap, record_loss,
+                     select_keyframe)
 from .store import ChunkStore
 
 __all__ = ["METRICS_HEADER", "FrameMetrics", "AdamSettings", "MappingEngine", "derive_seed"]
@@ -184,6 +185,7 @@ class MappingEngine:
         self.d2h_bytes = 0
         self.upload_keyframes_each_step = False   # e2e mode: GT from pinned host every step
         self._pinned_kf: dict[int, tuple] = {}
+        self._uniforms: dict[int, float] = {}
 
     # -------------------------------------------------------------- inputs
     def add_keyframe(self, kf: Keyframe, index_usage: int | None = None) -> None:
@@ -264,6 +266,13 @@ class MappingEngine:
     counter_steps = counter_gaussians = counter_instances = 0
     use_graphs = True
 
+    def _precompute_next_draw(self) -> None:
+        """The next single-GPU step's uniform draw depends only on its derived
+        seed (not on this step's loss): compute it while the GPU works."""
+        nxt = self.step_counter + 1
+        if nxt not in self._uniforms:
+            self._uniforms = {nxt: draw_uniform(derive_seed(self.seed, 2, nxt))}
+
     def _graph_key(self, kf: Keyframe, slots, n: int):
         s = self.store.slab
         return (kf.id, slots.data_ptr(), n, s.params.data_ptr(), s.grads.data_ptr(),
@@ -308,6 +317,7 @@ class MappingEngine:
         if entry is not None:
             g, gid = entry
             g.replay()
+            self._precompute_next_draw()   # host work overlapped with the GPU pass
             loss, overflow = self._finish_readback()
             _lib.load().sm_profile_graph_replayed(gid)
             if not overflow:
@@ -355,7 +365,9 @@ class MappingEngine:
             candidates = candidate_set(self.index.position_of(self.latest_kf), self.index)
         except EmptyCandidates:
             candidates = [self.latest_kf]
-        selected = select_keyframe(candidates, self.index, derive_seed(self.seed, 2, self.step_counter))
+        pre = self._uniforms.pop(self.step_counter, None)
+        selected = select_keyframe(candidates, self.index, derive_seed(self.seed, 2, self.step_counter),
+                                   uniform=pre)
         kf = store.keyframe_get(selected)
         visible, _ = self._visible_for_pose(kf.pose)
         overlap_val = overlap(visible, store.resident_chunk_ids()) if visible else None

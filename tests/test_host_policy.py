@@ -72,6 +72,26 @@ def test_keyframe_selection_trace():
         assert [idx.usage_of(i) for i in range(12)] == op["usage"]
 
 
+def test_fast_selection_and_quantile_match_numpy():
+    """The precomputed-uniform draw and the pure-Python quantile are the
+    NumPy computations the reference uses (select.py:144-166), bit for bit."""
+    rng = np.random.default_rng(5)
+    for trial in range(3000):
+        k = int(rng.integers(1, 20))
+        w = rng.uniform(0, 3, k) * (rng.random(k) > 0.2) + (rng.random(k) < 0.1) * 1e-7
+        w = np.maximum(w, 1e-6)
+        p = w / w.sum()
+        seed = int(rng.integers(0, 2**63))
+        ref = int(np.random.default_rng(seed).choice(k, p=p))
+        u = select.draw_uniform(seed)
+        cdf = p.cumsum()
+        cdf /= cdf[-1]
+        assert int(cdf.searchsorted(u, side="right")) == ref
+        vals = list(rng.uniform(0, 2, int(rng.integers(1, 30))))
+        for q in (0.5, 0.25, 0.9, 1.0, 0.0):
+            assert select.quantile_linear(vals, q) == float(np.quantile(vals, q))
+
+
 def test_chunk_codec_matches_reference_bytes(golden):
     g = golden("diskformat.npz")
     gs = [Gaussian(position=g["positions"][i], rotation=g["rotations"][i], scale=g["scales"][i],
