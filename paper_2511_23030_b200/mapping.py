@@ -47,6 +47,29 @@ def derive_seed(master: int, purpose: int, counter: int) -> int:
     return int(np.random.SeedSequence([master, purpose, counter]).generate_state(1)[0])
 
 
+def dp_select(index: KeyframeIndex, latest_kf: int, seed: int, step_counter: int,
+              world: int) -> list[int]:
+    """Keyframes of one data-parallel step, identical on every rank: `world`
+    sequential loss-weighted draws (select.py policy) with derived seeds
+    (seed, 2, step*world + r); rank r trains keyframe r."""
+    try:
+        candidates = candidate_set(index.position_of(latest_kf), index)
+    except EmptyCandidates:
+        candidates = [latest_kf]
+    return [select_keyframe(candidates, index, derive_seed(seed, 2, step_counter * world + r))
+            for r in range(world)]
+
+
+def allreduce_step(grads, lossbuf, group=None) -> None:
+    """The DP exchange: sum the gradient slab (NCCL on GPUs, gloo in tests) and
+    the per-rank [loss..., overflow] vector."""
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return
+    dist.all_reduce(grads, group=group)
+    dist.all_reduce(lossbuf, group=group)
+
+
 @dataclass
 class FrameMetrics:
     frame: int
@@ -408,13 +431,7 @@ class MappingEngine:
         torch = self.torch
         store, stats = self.store, self.store.stats
         io0, loads0, ev0 = stats.io_nanos, stats.chunk_loads, stats.chunk_evictions
-        try:
-            candidates = candidate_set(self.index.position_of(self.latest_kf), self.index)
-        except EmptyCandidates:
-            candidates = [self.latest_kf]
-        selected = [select_keyframe(candidates, self.index,
-                                    derive_seed(self.seed, 2, self.step_counter * world + r))
-                    for r in range(world)]
+        selected = dp_select(self.index, self.latest_kf, self.seed, self.step_counter, world)
         kfs = [store.keyframe_get(s) for s in selected]
         vis = [self._visible_for_pose(kf.pose)[0] for kf in kfs]
         union = sorted(set().union(*vis))
@@ -434,8 +451,7 @@ class MappingEngine:
             buf.zero_()
             buf[rank:rank + 1].copy_(self.loss.out[:1])
             buf[world:world + 1].copy_(self.render.overflow_flag().float())
-            dist.all_reduce(slab.grads[:slab.high_water()], group=group)
-            dist.all_reduce(buf, group=group)
+            allreduce_step(slab.grads[:slab.high_water()], buf, group)
             host = buf.cpu().numpy()
             self.d2h_bytes += 4 * (world + 1)
             if host[world] == 0:

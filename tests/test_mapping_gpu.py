@@ -82,6 +82,20 @@ def test_graph_replay_equals_eager(cuda, tmp_path):
     assert torch.equal(sa.adam_m[:hw], sb.adam_m[:hw])
 
 
+def test_dp_step_world1_equals_single_step(cuda, tmp_path):
+    """optimization_step_dp with one rank = optimization_step (same draws,
+    same device pass, same Adam) -- the N>1 path minus the collectives."""
+    import torch
+    a = _c1_engine(tmp_path / "a", budget=100_000)
+    b = _c1_engine(tmp_path / "b", budget=100_000)
+    for s in range(6):
+        ra = a.optimization_step(0, s)
+        (rb,) = b.optimization_step_dp(0, s, world=1, rank=0)
+        assert ra.selected_kf == rb.selected_kf and ra.loss == rb.loss
+    hw = a.store.slab.high_water()
+    assert torch.equal(a.store.slab.params[:hw], b.store.slab.params[:hw])
+
+
 def test_paging_steps_are_deterministic(cuda, tmp_path):
     """Budget 12k < 20k splats: the steps load and evict chunks; two identical
     runs give byte-identical metrics (test_acceptance.py criterion 10)."""
