@@ -1,26 +1,55 @@
 """Chunk streamer: .dcg bytes <-> pinned host <-> HBM slab, codec on the GPU.
 
-Load:  file bytes -> pinned staging -> cudaMemcpyAsync on the copy stream ->
-       K8 sm_chunk_unpack (AoS records -> slab SoA + Adam moments) on the
-       copy stream; the compute stream waits on an event, not the host.
-Evict: K9 sm_chunk_pack (slab SoA -> AoS records) -> D2H into pinned staging
-       -> file write (diskformat.build_chunk_file).
+Replaces the reference's synchronous unpack_chunk / pack_chunk object codecs
+(diskformat.py:86-186, 82-138 MB/s on the survey host) on the paging path
+(store.py:241-272, 493-515) without changing any policy decision or the
+io_ns cost model (the store charges bytes exactly as the reference does).
 
-Replaces the reference's unpack_chunk / pack_chunk object codecs
-(diskformat.py:86-186, 82-138 MB/s on the survey host) on the chunk paging
-path (store.py:241-272).
+Load:   file bytes (or a prefetched / still-pending copy) -> pinned staging ->
+        cudaMemcpyAsync on the copy stream -> K8 sm_chunk_unpack into the
+        chunk's slab segment on the copy stream; the compute stream waits on
+        the copy stream (device-side), the host only waits for the K8 verdict.
+Evict:  K9 sm_chunk_pack on the compute stream into a device staging buffer
+        (so the slab rows can be reused immediately, stream-ordered), the D2H
+        copy into pinned memory on the copy stream, and a writer thread that
+        waits on that copy's event and writes the file: eviction write-back
+        overlaps with rendering (write-behind).  A reload of a chunk whose
+        write is still pending is served from its pinned copy.
+Prefetch: reader threads pull .dcg files into host memory ahead of use
+        (speculative: e.g. the visible sets of the other candidate keyframes);
+        a later load takes the bytes from there instead of the disk.
+flush():  drains the writer queue (the store's durability point).
 """
 
 from __future__ import annotations
 
+import queue
+import threading
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
 import numpy as np
 
 from . import _lib
-from .errors import CorruptChunk
+from .errors import CorruptChunk, IoFailure
+
+
+class _PendingWrite:
+    __slots__ = ("path", "header", "pin", "nbytes", "event", "done", "dev")
+
+    def __init__(self, path, header, pin, nbytes, event, dev):
+        self.path, self.header, self.pin, self.nbytes = path, header, pin, nbytes
+        self.event, self.dev = event, dev
+        self.done = threading.Event()
+
+    def data(self) -> bytes:
+        self.event.synchronize()
+        return self.header + self.pin[:self.nbytes].numpy().tobytes()
 
 
 class ChunkStreamer:
-    def __init__(self, slab):
+    def __init__(self, slab, write_behind: bool = True, reader_threads: int = 4,
+                 prefetch_bytes: int = 1 << 30):
         import torch
         self.torch = torch
         self.slab = slab
@@ -31,7 +60,21 @@ class ChunkStreamer:
         self._err = torch.empty(1, dtype=torch.int64, device=slab.device)
         self.bytes_h2d = 0
         self.bytes_d2h = 0
+        self.write_behind = write_behind
+        self._pending: dict[Path, _PendingWrite] = {}
+        self._lock = threading.Lock()
+        self._queue: queue.Queue = queue.Queue()
+        self._writer_error: BaseException | None = None
+        self._free_pins: list = []
+        self._free_devs: list = []
+        self._writer = threading.Thread(target=self._write_loop, daemon=True)
+        self._writer.start()
+        self._pool = ThreadPoolExecutor(max_workers=reader_threads)
+        self._prefetched: dict[Path, object] = {}
+        self._prefetch_limit = prefetch_bytes
+        self.stats = {"prefetch_hits": 0, "pending_hits": 0, "async_writes": 0}
 
+    # ---------------------------------------------------------------- staging
     def _staging(self, nbytes: int):
         torch = self.torch
         if self._dev.numel() < nbytes:
@@ -40,6 +83,49 @@ class ChunkStreamer:
             self._pin = torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, pin_memory=True)
         return self._dev, self._pin
 
+    def _take(self, pool: list, nbytes: int, pinned: bool):
+        torch = self.torch
+        with self._lock:
+            for i, t in enumerate(pool):
+                if t.numel() >= nbytes:
+                    return pool.pop(i)
+        if pinned:
+            return torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, pin_memory=True)
+        return torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, device=self.slab.device)
+
+    # ------------------------------------------------------------------- load
+    def read_file(self, path: Path) -> bytes | None:
+        """Bytes of `path` from a pending write-behind copy or the prefetch
+        tier (None: caller reads the disk).  Charged by the caller as a read."""
+        with self._lock:
+            pw = self._pending.get(path)
+            fut = self._prefetched.pop(path, None)
+        if pw is not None:
+            self.stats["pending_hits"] += 1
+            return pw.data()
+        if fut is not None:
+            try:
+                data = fut.result()
+            except OSError:
+                return None
+            self.stats["prefetch_hits"] += 1
+            return data
+
+    def prefetch(self, paths) -> None:
+        """Speculatively read chunk files into host memory (reader threads)."""
+        with self._lock:
+            budget = self._prefetch_limit - len(self._prefetched) * (1 << 20)
+            for p in paths:
+                p = Path(p)
+                if p in self._prefetched or p in self._pending or budget <= 0:
+                    continue
+                self._prefetched[p] = self._pool.submit(p.read_bytes)
+                budget -= 1 << 20
+
+    def drop_prefetch(self, path: Path) -> None:
+        with self._lock:
+            self._prefetched.pop(Path(path), None)
+
     def unpack_into(self, records: np.ndarray, stride: int, offset: int) -> None:
         n = int(records.shape[0])
         if n == 0:
@@ -47,8 +133,7 @@ class ChunkStreamer:
         nbytes = n * stride
         dev, pin = self._staging(nbytes)
         torch = self.torch
-        pin[:nbytes].numpy()[:] = np.frombuffer(records.tobytes() if not records.flags.c_contiguous
-                                                else records.view(np.uint8).reshape(-1), np.uint8)
+        pin[:nbytes].numpy()[:] = records.view(np.uint8).reshape(-1)[:nbytes]
         cur = torch.cuda.current_stream(self.slab.device)
         self.copy_stream.wait_stream(cur)   # slab rows may still be in use by queued work
         with torch.cuda.stream(self.copy_stream):
@@ -60,25 +145,91 @@ class ChunkStreamer:
                                           _lib.ptr(s.adam_v[rows]), _lib.ptr(self._err),
                                           _lib.stream_handle(self.copy_stream))
             _lib.check(rc, "chunk_unpack")
-        s.grads[offset:offset + n].zero_()
+            s.grads[offset:offset + n].zero_()
         cur.wait_stream(self.copy_stream)
         self.bytes_h2d += nbytes
-        err = int(self._err.item())   # synchronises: the policy needs the verdict
+        err = int(self._err.item())   # the policy needs the verdict (CorruptChunk)
         if err >= 0:
             raise CorruptChunk(f"chunk record {err} fails invariants")
 
-    def pack_from(self, offset: int, n: int, stride: int) -> np.ndarray:
-        if n == 0:
-            return np.zeros(0, dtype=np.uint8)
-        nbytes = n * stride
-        dev, pin = self._staging(nbytes)
+    # ------------------------------------------------------------------ evict
+    def _pack_to_device(self, offset: int, n: int, stride: int, dev):
         s = self.slab
         rows = slice(offset, offset + n)
         rc = self.lib.sm_chunk_pack(_lib.ptr(s.params[rows]), _lib.ptr(s.sh_rest[rows]),
                                     _lib.ptr(s.adam_m[rows]), _lib.ptr(s.adam_v[rows]), n, int(stride),
                                     _lib.ptr(dev), _lib.stream_handle())
         _lib.check(rc, "chunk_pack")
+
+    def pack_from(self, offset: int, n: int, stride: int) -> np.ndarray:
+        """Synchronous pack (flush, API materialisation)."""
+        if n == 0:
+            return np.zeros(0, dtype=np.uint8)
+        nbytes = n * stride
+        dev, pin = self._staging(nbytes)
+        self._pack_to_device(offset, n, stride, dev)
         pin[:nbytes].copy_(dev[:nbytes], non_blocking=True)
-        self.torch.cuda.current_stream(s.device).synchronize()
+        self.torch.cuda.current_stream(self.slab.device).synchronize()
         self.bytes_d2h += nbytes
         return pin[:nbytes].numpy().copy()
+
+    def write_async(self, path: Path, header: bytes, offset: int, n: int, stride: int) -> None:
+        """Write-behind eviction of slab rows [offset, offset+n) to `path`."""
+        torch = self.torch
+        nbytes = n * stride
+        dev = self._take(self._free_devs, max(nbytes, 1), pinned=False)
+        pin = self._take(self._free_pins, max(nbytes, 1), pinned=True)
+        if n:
+            self._pack_to_device(offset, n, stride, dev)
+        cur = torch.cuda.current_stream(self.slab.device)
+        self.copy_stream.wait_stream(cur)
+        ev = torch.cuda.Event()
+        with torch.cuda.stream(self.copy_stream):
+            if n:
+                pin[:nbytes].copy_(dev[:nbytes], non_blocking=True)
+            ev.record(self.copy_stream)
+        pw = _PendingWrite(Path(path), header, pin, nbytes, ev, dev)
+        with self._lock:
+            self._pending[pw.path] = pw
+            self._prefetched.pop(pw.path, None)
+        self.bytes_d2h += nbytes
+        self.stats["async_writes"] += 1
+        self._queue.put(pw)
+
+    def _write_loop(self) -> None:
+        while True:
+            pw = self._queue.get()
+            if pw is None:
+                return
+            try:
+                data = pw.data()
+                tmp = pw.path.with_suffix(".dcg.tmp")
+                tmp.write_bytes(data)
+                tmp.replace(pw.path)
+            except BaseException as exc:   # surfaced at the next check()/drain()
+                self._writer_error = exc
+            finally:
+                with self._lock:
+                    if self._pending.get(pw.path) is pw:
+                        del self._pending[pw.path]
+                    self._free_pins.append(pw.pin)
+                    self._free_devs.append(pw.dev)
+                pw.done.set()
+                self._queue.task_done()
+
+    def check(self) -> None:
+        if self._writer_error is not None:
+            exc, self._writer_error = self._writer_error, None
+            raise IoFailure(f"write-behind failed: {exc}") from exc
+
+    def drain(self) -> None:
+        """Block until every pending write reached the disk (flush point)."""
+        self._queue.join()
+        self.check()
+
+    def wait_path(self, path: Path) -> None:
+        with self._lock:
+            pw = self._pending.get(Path(path))
+        if pw is not None:
+            pw.done.wait()
+        self.check()

@@ -60,6 +60,33 @@ def test_store_policy_trace_matches_reference(cuda, tmp_path):
     assert content == trace["final_map"]
 
 
+@pytest.mark.parametrize("write_behind", [False, True])
+def test_policy_trace_sync_and_write_behind(cuda, tmp_path, write_behind):
+    """Same trace with synchronous and write-behind eviction: identical policy,
+    stats and flushed files (the streamer never changes a decision)."""
+    from paper_2511_23030_b200.core import Gaussian
+    from paper_2511_23030_b200.store import ChunkStore, StoreConfig
+    trace = json.loads((GOLDEN / "store_trace.json").read_text())
+    st = ChunkStore(StoreConfig(disk_root=tmp_path, chunk_size_m=10.0, gaussian_budget=60,
+                                io_ns_per_byte=1.0, write_behind=write_behind))
+    for op in trace["ops"]:
+        if op["op"] == "insert":
+            st.insert_gaussians([Gaussian(position=p, opacity=o, scale=s, rotation=r, sh=sh)
+                                 for p, o, s, r, sh in zip(op["positions"], op["opacity"], op["scale"],
+                                                           op["rotation"], op["sh"])])
+        elif op["op"] == "ensure":
+            st.ensure_resident([int(i) for i in op["ids"]])
+        elif op["op"] == "evict" and not op["error"]:
+            st.evict_lru(op["required"], protected={int(p) for p in op["protected"]})
+        elif op["op"] == "mutate":
+            st.mark_chunk_mutated(int(op["id"]))
+        assert _stats(st) == op["stats"]
+    st.flush()
+    assert _stats(st) == trace["final_stats"]
+    if write_behind:
+        assert st.streamer.stats["async_writes"] > 0
+
+
 def test_evict_reload_bit_exact_with_adam_state(cuda, tmp_path):
     """Chunks written with the 120-byte Adam tail reload params + moments exactly."""
     import torch
