@@ -104,6 +104,13 @@ int sm_render_backward(const float *params, const int32_t *slots, int64_t n,
                        const float *d_rgb, const float *d_depth, const float *d_alpha,
                        float *grads, void *stream);
 
+/* Tile binning keeps only the tiles a splat's q <= 9 ellipse reaches (on, the
+ * default) or every tile of its 3-sigma box (off).  Images and gradients are
+ * bit-identical either way (the dropped tiles are ones the compositor skips
+ * anyway); the switch exists so tests can prove that.  Process-global; takes
+ * effect at the next sm_render_forward (CUDA graphs keep their captured value). */
+void sm_set_ellipse_cull(int on);
+
 /* ------------------------------------------------------------------ loss
  * renderloss.total_loss / image_loss / ssim / depth_loss (renderloss.py:226-274):
  * (1-ls)*L1 + ls*(1-SSIM 11x11 sigma 1.5, 5-px crop, channel mean)

@@ -22,6 +22,7 @@ int cuda_status(cudaError_t e, const char *what) {
 }
 
 int64_t loss_workspace_size(int W, int H);
+extern int g_ellipse_cull;
 int loss_forward_backward(const float *, const float *, const uint8_t *, const float *, const float *,
                           int, int, int, float, float, void *, int64_t, float *, float *, float *,
                           cudaStream_t);
@@ -83,6 +84,8 @@ int sm_render_backward(const float *params, const int32_t *slots, int64_t n, con
     return render_backward(params, slots, n, *cam, *dims, workspace, workspace_bytes, d_rgb, d_depth,
                            d_alpha, grads, SM_STREAM(stream));
 }
+
+void sm_set_ellipse_cull(int on) { g_ellipse_cull = on ? 1 : 0; }
 
 int64_t sm_loss_workspace_size(int32_t width, int32_t height) { return loss_workspace_size(width, height); }
 

@@ -35,7 +35,7 @@ struct __align__(16) ProjRec {
     float eps;             // |pw - kPowCut| band that triggers the fp64 decision
     int32_t x0y0;          // (y0 << 16) | x0   clamped 3-sigma bbox
     int32_t x1y1;          // (y1 << 16) | x1
-    float spare[3];
+    float beta, G, K;      // ellipse row extent (RowSpan); K <= 0: whole bbox rows
 };
 static_assert(sizeof(ProjRec) == 64, "ProjRec must be 64 bytes");
 
@@ -48,6 +48,79 @@ __device__ __forceinline__ int rec_x0(const ProjRec &r) { return (int)(short)(r.
 __device__ __forceinline__ int rec_y0(const ProjRec &r) { return r.x0y0 >> 16; }
 __device__ __forceinline__ int rec_x1(const ProjRec &r) { return (int)(short)(r.x1y1 & 0xffff); }
 __device__ __forceinline__ int rec_y1(const ProjRec &r) { return r.x1y1 >> 16; }
+
+// Tile columns [c0, c1] of tile row ty that the splat's q <= 9 ellipse can
+// reach (c0 > c1: none).  At row offset dy the ellipse spans
+// |dx - beta dy| <= sqrt(G - K dy^2) (beta = b/c, G = 9 det/c, K = det/c^2 of
+// the dilated cov2), so over the row band [a0, a1] of pixel-row offsets the
+// extreme dx sit at dy = +-beta sqrt(G/K / (K + beta^2)) (= +-3b/sqrt(a), the
+// ellipse's side points) clamped into the band.  Widened by 1% of the radius +
+// 0.02 px, far above the fp32 evaluation error, so no pixel with q <= 9 is
+// ever dropped: the culled tiles are exactly ones the compositor would skip.
+// Projection (counts), emission, composite_bwd (slot index) and the gradient
+// gather all call this one function, so they agree tile for tile.
+struct RowSpan {
+    int x0, y0, y1, tx0, tx1, ty0, ty1;
+    float beta, G, K, dys, rad, xo, oy;
+    bool ell;
+
+    __device__ __forceinline__ explicit RowSpan(const ProjRec &g) {
+        x0 = rec_x0(g);
+        y0 = rec_y0(g);
+        y1 = rec_y1(g);
+        tx0 = x0 / SM_TILE;
+        tx1 = rec_x1(g) / SM_TILE;
+        ty0 = y0 / SM_TILE;
+        ty1 = y1 / SM_TILE;
+        beta = g.beta;
+        G = g.G;
+        K = g.K;
+        ell = K > 0.f;
+        // explicit _rn ops: no FMA contraction, so every kernel inlining this
+        // computes the same bits
+        dys = ell ? __fmul_rn(beta, __fsqrt_rn(__fdiv_rn(__fdiv_rn(G, K), __fadd_rn(K, __fmul_rn(beta, beta)))))
+                  : 0.f;
+        rad = __fsqrt_rn(fmaxf(G, 0.f));
+        xo = __fsub_rn((float)x0, g.ox);   // pixel column of dx = 0 (the splat's u)
+        oy = g.oy;
+    }
+
+    __device__ __forceinline__ float half_width(float dy) const {
+        return __fsqrt_rn(fmaxf(__fsub_rn(G, __fmul_rn(__fmul_rn(K, dy), dy)), 0.f));
+    }
+
+    __device__ __forceinline__ void row(int ty, int &c0, int &c1) const {
+        c0 = tx0;
+        c1 = tx1;
+        if (!ell) return;
+        const float a0 = __fadd_rn((float)(max(ty * SM_TILE, y0) - y0), oy);
+        const float a1 = __fadd_rn((float)(min(ty * SM_TILE + SM_TILE - 1, y1) - y0), oy);
+        const float dr = fminf(fmaxf(dys, a0), a1), dl = fminf(fmaxf(-dys, a0), a1);
+        const float xr = __fadd_rn(__fmul_rn(beta, dr), half_width(dr));
+        const float xl = __fsub_rn(__fmul_rn(beta, dl), half_width(dl));
+        const float m = __fadd_rn(
+            __fmul_rn(0.01f, __fadd_rn(rad, __fmul_rn(fabsf(beta), fmaxf(fabsf(a0), fabsf(a1))))), 0.02f);
+        const float pl = __fsub_rn(__fadd_rn(xo, xl), m), pr = __fadd_rn(__fadd_rn(xo, xr), m);
+        if (!(pl <= pr) || !(pr - pl < 1e7f)) return;   // NaN / inf guard: keep the whole row
+        c0 = max(c0, (int)floorf(__fmul_rn(pl, 1.f / SM_TILE)));
+        c1 = min(c1, (int)floorf(__fmul_rn(pr, 1.f / SM_TILE)));
+    }
+
+    __device__ __forceinline__ int count(int ty) const {
+        int c0, c1;
+        row(ty, c0, c1);
+        return c1 >= c0 ? c1 - c0 + 1 : 0;
+    }
+
+    // Index of tile (tx, ty) among the kept tiles (row-major order).
+    __device__ __forceinline__ uint32_t kept_index(int tx, int ty) const {
+        uint32_t j = 0;
+        for (int t = ty0; t < ty; t++) j += (uint32_t)count(t);
+        int c0, c1;
+        row(ty, c0, c1);
+        return j + (uint32_t)(tx - c0);
+    }
+};
 
 // Exact reference expression (renderloss.py:140) evaluated left to right in
 // fp64 with explicit round-to-nearest ops so nvcc cannot contract to FMA.

@@ -5,7 +5,55 @@
 namespace sm {
 
 constexpr int kG2dStride = 12;   // per-rank 2D grads: u v ia ib ic op r g b z - -
-constexpr uint32_t kEmitSmall = 32;   // splats with more tiles are emitted / gathered per block
+constexpr uint32_t kEmitSmall = 32;   // splats with more box tiles are emitted / gathered per warp
+
+// Tiles of the 3-sigma box.  The small / big split is taken on this count, not
+// on the kept (ellipse) count, so a splat's gradient is summed by the same
+// path, in the same order, whether or not tiles were culled.
+__device__ __forceinline__ uint32_t bbox_tiles(const ProjRec &g) {
+    return (uint32_t)((rec_x1(g) / kTile - rec_x0(g) / kTile + 1) * (rec_y1(g) / kTile - rec_y0(g) / kTile + 1));
+}
+
+// Big splats are handled by a 256-thread block: thread i evaluates tile row
+// tyb + i (RowSpan), a block scan turns the row counts into kept-index
+// offsets, then warp w walks rows w, w + 8, ... with its lanes across columns.
+constexpr int kBigThreads = 256;
+struct BigRowTable {
+    int c0[kBigThreads], c1[kBigThreads];
+    uint32_t off[kBigThreads];
+    uint32_t wsum[kBigThreads / 32];
+};
+
+// Fills rows tyb .. tyb + 255 (clipped to the box); returns base + their count.
+__device__ __forceinline__ uint32_t fill_row_table(const RowSpan &sp, int tyb, uint32_t base,
+                                                   BigRowTable &t) {
+    __syncthreads();   // the previous user of the table is done
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ty = tyb + (int)threadIdx.x;
+    int c0 = 0, c1 = -1;
+    if (ty <= sp.ty1) sp.row(ty, c0, c1);
+    const uint32_t cnt = c1 >= c0 ? (uint32_t)(c1 - c0 + 1) : 0u;
+    uint32_t x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) t.wsum[warp] = x;
+    __syncthreads();
+    uint32_t pre = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kBigThreads / 32; w++) {
+        const uint32_t s = t.wsum[w];
+        pre += w < warp ? s : 0u;
+        total += s;
+    }
+    t.c0[threadIdx.x] = c0;
+    t.c1[threadIdx.x] = c1;
+    t.off[threadIdx.x] = base + pre + x - cnt;
+    __syncthreads();
+    return base + total;
+}
 
 struct RenderLayout {
     int tiles_x, tiles_y;

@@ -16,7 +16,7 @@
 // Per-splat sums without floating-point atomics (deterministic): a 10-value
 // transposed warp butterfly (14 shuffles), per-warp shared slots added in warp
 // order, one gradient slot per (splat, tile) instance, and a fixed-order sum
-// over a splat's instances (inline in project_bwd, or a warp per big splat).
+// over a splat's instances (inline in project_bwd, or a block per big splat).
 #include "prof.cuh"
 #include "render.cuh"
 
@@ -133,7 +133,7 @@ struct BwdPix {
 // Determinism: no floating-point atomics.  Each warp's 10 sums for an
 // instance land in its own shared slot; after the batch the slots are added
 // in warp order and written to the instance's emission slot (toff[rank] + the
-// tile's index in the splat's tile rectangle); grad_gather then sums a splat's
+// tile's index among the splat's kept tiles); grad_gather then sums a splat's
 // instances in a fixed order.  Reruns and CUDA-graph replays are bit-identical
 // (the reference's metrics determinism contract, test_acceptance.py crit. 10).
 template <int PIX>
@@ -222,10 +222,8 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
         }
         __syncthreads();
         if (idx < bend) {   // warp-ordered sum -> the instance's emission slot
-            const ProjRec &g = s_rec[threadIdx.x];
-            const int tx0 = rec_x0(g) / kTile, ty0r = rec_y0(g) / kTile;
-            const int ntx = rec_x1(g) / kTile - tx0 + 1;
-            const uint32_t slot = toff[s_rank[threadIdx.x]] + (uint32_t)((tile_y - ty0r) * ntx + tile_x - tx0);
+            const uint32_t slot =
+                toff[s_rank[threadIdx.x]] + RowSpan(s_rec[threadIdx.x]).kept_index(tile_x, tile_y);
             float acc[12];
 #pragma unroll
             for (int k = 0; k < 10; k++) {
@@ -244,52 +242,81 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
     }
 }
 
-// Sum of a splat's visited instance slots, in slot order (an instance was
-// visited iff its rank is <= its tile's horizon rank).  j = first, first +
-// step, ... so callers can split a big splat across a block.
-__device__ __forceinline__ void sum_slots(const ProjRec &g, int64_t r, uint32_t o, uint32_t first,
-                                          uint32_t cnt, uint32_t step, const float *gbuf,
+// Sum of a splat's visited instance slots (an instance was visited iff its
+// rank is <= its tile's horizon rank), walking the kept tiles in emission
+// order: a culled tile only removes a zero term, so ellipse culling stays
+// bit-exact.
+__device__ __forceinline__ void sum_slots(const ProjRec &g, int64_t r, uint32_t o, const float *gbuf,
                                           const int32_t *tile_hor, int tiles_x, float (&acc)[10]) {
-    const int tx0 = rec_x0(g) / kTile, ty0 = rec_y0(g) / kTile;
-    const int ntx = rec_x1(g) / kTile - tx0 + 1;
-    for (uint32_t j = first; j < cnt; j += step) {
-        const int t = (ty0 + (int)j / ntx) * tiles_x + tx0 + (int)j % ntx;
-        if (r > (int64_t)tile_hor[t]) continue;
-        const float4 *src = reinterpret_cast<const float4 *>(gbuf + (int64_t)(o + j) * kG2dStride);
-        const float4 a = src[0], b = src[1], c = src[2];
-        acc[0] += a.x, acc[1] += a.y, acc[2] += a.z, acc[3] += a.w;
-        acc[4] += b.x, acc[5] += b.y, acc[6] += b.z, acc[7] += b.w;
-        acc[8] += c.x, acc[9] += c.y;
+    const RowSpan sp(g);
+    for (int ty = sp.ty0; ty <= sp.ty1; ty++) {
+        int c0, c1;
+        sp.row(ty, c0, c1);
+        for (int c = c0; c <= c1; c++) {
+            if (r > (int64_t)tile_hor[ty * tiles_x + c]) continue;
+            const float4 *src =
+                reinterpret_cast<const float4 *>(gbuf + (int64_t)(o + (uint32_t)(c - c0)) * kG2dStride);
+            const float4 a = src[0], b = src[1], cc = src[2];
+            acc[0] += a.x, acc[1] += a.y, acc[2] += a.z, acc[3] += a.w;
+            acc[4] += b.x, acc[5] += b.y, acc[6] += b.z, acc[7] += b.w;
+            acc[8] += cc.x, acc[9] += cc.y;
+        }
+        if (c1 >= c0) o += (uint32_t)(c1 - c0 + 1);
     }
 }
 
-// Splats with more than kEmitSmall tiles (queued at emission, rare): one block
-// each, strided partial sums + fixed-order tree -> g2d[rank].  Smaller splats
+// Splats with more than kEmitSmall box tiles (queued at emission, rare): one
+// block each, fixed-assignment partial sums + fixed-order tree -> g2d[rank].  Smaller splats
 // are summed inline by project_bwd.  Both orders are fixed: deterministic.
 __global__ void __launch_bounds__(256)
 grad_gather_big(const ProjRec *__restrict__ recs, const uint32_t *__restrict__ tcount_r,
                 const uint32_t *__restrict__ toff, const sm_render_counters *ctr,
                 const uint32_t *__restrict__ big, const float *__restrict__ gbuf,
                 const int32_t *__restrict__ tile_hor, int tiles_x, float *__restrict__ g2d) {
+    __shared__ BigRowTable tab;
+    __shared__ float s_part[kBigThreads / 32][10];
     const uint32_t nbig = ctr->overflow ? 0u : ctr->reserved[1];
-    const int lane = threadIdx.x & 31;
-    const uint32_t nwarps = gridDim.x * (blockDim.x / 32);
-    for (uint32_t bi = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; bi < nbig; bi += nwarps) {
-        const uint32_t r = big[bi];   // one warp per big splat: strided lanes + fixed butterfly
-        float acc[10];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int via = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    const int vib = 8 + ((lane >> 4) & 1);
+    for (uint32_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {   // a block per big splat
+        const int64_t r = big[bi];
+        const RowSpan sp(recs[r]);
+        const uint32_t o = toff[r];
+        float v[16];
 #pragma unroll
-        for (int k = 0; k < 10; k++) acc[k] = 0.f;
-        sum_slots(recs[r], r, toff[r], lane, tcount_r[r], 32, gbuf, tile_hor, tiles_x, acc);
-#pragma unroll
-        for (int k = 0; k < 10; k++)
-#pragma unroll
-            for (int o = 16; o; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
-        if (lane < 10) {
-            float v = acc[0];
-#pragma unroll
-            for (int k = 1; k < 10; k++) v = lane == k ? acc[k] : v;
-            g2d[(int64_t)r * kG2dStride + lane] = v;
+        for (int k = 0; k < 16; k++) v[k] = 0.f;
+        uint32_t base = 0;
+        // warp w takes box rows ty0 + w (mod 8), lane l the tiles t = l (mod 32):
+        // fixed by the box, not by the kept spans (see sum_slots)
+        for (int tyb = sp.ty0; tyb <= sp.ty1; tyb += kBigThreads) {
+            base = fill_row_table(sp, tyb, base, tab);
+            const int nrows = min(kBigThreads, sp.ty1 - tyb + 1);
+            for (int i = warp; i < nrows; i += kBigThreads / 32) {
+                const int c0 = tab.c0[i], c1 = tab.c1[i], row = (tyb + i) * tiles_x;
+                const uint32_t src0 = o + tab.off[i] - (uint32_t)c0;
+                for (int c = c0 + (((lane - row - c0) % 32) + 32) % 32; c <= c1; c += 32) {
+                    if (r > (int64_t)tile_hor[row + c]) continue;
+                    const float4 *src =
+                        reinterpret_cast<const float4 *>(gbuf + (int64_t)(src0 + (uint32_t)c) * kG2dStride);
+                    const float4 a = src[0], b = src[1], cc = src[2];
+                    v[0] += a.x, v[1] += a.y, v[2] += a.z, v[3] += a.w;
+                    v[4] += b.x, v[5] += b.y, v[6] += b.z, v[7] += b.w;
+                    v[8] += cc.x, v[9] += cc.y;
+                }
+            }
         }
+        const float2 s = transpose_reduce10(v, lane);   // fixed butterfly, then warps in order
+        if (!(lane & 3)) s_part[warp][via] = s.x;
+        if (!(lane & 15)) s_part[warp][vib] = s.y;
+        __syncthreads();
+        if (threadIdx.x < 10) {
+            float a = 0.f;
+#pragma unroll
+            for (int w = 0; w < kBigThreads / 32; w++) a += s_part[w][threadIdx.x];
+            g2d[r * kG2dStride + threadIdx.x] = a;
+        }
+        __syncthreads();
     }
 }
 
@@ -312,13 +339,14 @@ project_bwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots
     const uint32_t cnt = tcount_r[r];
     if (cnt == 0) return;
     float gk[10];
-    if (cnt > kEmitSmall) {   // summed by grad_gather_big
+    const ProjRec rec = recs[r];
+    if (bbox_tiles(rec) > kEmitSmall) {   // summed by grad_gather_big
 #pragma unroll
         for (int k = 0; k < 10; k++) gk[k] = g2d[r * kG2dStride + k];
     } else {
 #pragma unroll
         for (int k = 0; k < 10; k++) gk[k] = 0.f;
-        sum_slots(recs[r], r, toff[r], 0, cnt, 1, gbuf, tile_hor, tiles_x, gk);
+        sum_slots(rec, r, toff[r], gbuf, tile_hor, tiles_x, gk);
     }
     const uint32_t i = order[r];
     const int64_t slot = slots ? (int64_t)slots[i] : (int64_t)i;

@@ -80,7 +80,7 @@ struct CamDev {
 
 __global__ void __launch_bounds__(256)
 project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots, int64_t n,
-            CamDev cam, ProjRec *__restrict__ rec, Proj64 *__restrict__ p64,
+            CamDev cam, int cull, ProjRec *__restrict__ rec, Proj64 *__restrict__ p64,
             unsigned long long *__restrict__ dkey, uint32_t *__restrict__ order,
             uint32_t *__restrict__ tcount) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -117,12 +117,13 @@ project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots
     r.r = col[0];
     r.g = col[1];
     r.b = col[2];
-    r.spare[0] = r.spare[1] = r.spare[2] = 0.f;
     if (det <= 0.0 || a <= 0.0 || c <= 0.0) {
         tcount[i] = 0;
         r.x0y0 = 0;
         r.x1y1 = (int32_t)0xffffffff;   // empty box
         r.ox = r.oy = r.ia = r.ib = r.ic = r.eps = 0.f;
+        r.beta = r.G = 0.f;
+        r.K = -1.f;
         rec[i] = r;
         return;
     }
@@ -146,6 +147,9 @@ project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots
     r.eps = (float)(1e-4 * (1.0 + K) * -kPowScale);
     r.x0y0 = (int32_t)(((uint32_t)y0 << 16) | ((uint32_t)x0 & 0xffffu));
     r.x1y1 = (int32_t)(((uint32_t)(y1 & 0xffff) << 16) | ((uint32_t)x1 & 0xffffu));
+    r.beta = (float)(b / c);
+    r.G = (float)(9.0 * det / c);
+    r.K = cull ? (float)(det / (c * c)) : -1.f;
     rec[i] = r;
     Proj64 q;
     q.u = g.u;
@@ -158,8 +162,10 @@ project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots
         tcount[i] = 0;
         return;
     }
-    const int tx0 = x0 / kTile, tx1 = x1 / kTile, ty0 = y0 / kTile, ty1 = y1 / kTile;
-    tcount[i] = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+    uint32_t cnt = 0;   // tiles the q <= 9 ellipse reaches (RowSpan)
+    const RowSpan sp(r);
+    for (int ty = sp.ty0; ty <= sp.ty1; ty++) cnt += (uint32_t)sp.count(ty);
+    tcount[i] = cnt;
 }
 
 __global__ void __launch_bounds__(256)
@@ -184,18 +190,22 @@ __global__ void check_instances(sm_render_counters *ctr, int64_t max_instances) 
 // Instance emission.  Splat footprints are heavy-tailed and the biggest
 // (nearest) ones sit together at the lowest depth ranks, so emission is split:
 // a thread per rank writes splats of <= kEmitSmall tiles directly, larger ones
-// are queued and a block per queued splat writes its tiles in parallel.
+// are queued and a warp per queued splat writes its tiles in parallel.
 // Keys are (tile << rank_bits) | rank at the rank's scanned offset, so the
 // array is in rank order whichever thread writes a slot.
 
-__device__ __forceinline__ void emit_tiles(const ProjRec &g, uint32_t r, uint32_t o, uint32_t first,
-                                           uint32_t count, uint32_t step, int rank_bits, int tiles_x,
-                                           uint32_t *ikeys) {
-    const int tx0 = rec_x0(g) / kTile, ty0 = rec_y0(g) / kTile;
-    const int ntx = rec_x1(g) / kTile - tx0 + 1;
-    for (uint32_t j = first; j < count; j += step) {
-        const int t = (ty0 + (int)j / ntx) * tiles_x + tx0 + (int)j % ntx;
-        ikeys[o + j] = ((uint32_t)t << rank_bits) | r;
+// Kept tiles (RowSpan) in row-major order; lane `first` of `step` writes the
+// kept indices j = first (mod step).
+__device__ __forceinline__ void emit_tiles(const ProjRec &g, uint32_t r, uint32_t o, int first,
+                                           int step, int rank_bits, int tiles_x, uint32_t *ikeys) {
+    const RowSpan sp(g);
+    int j = 0;
+    for (int ty = sp.ty0; ty <= sp.ty1; ty++) {
+        int c0, c1;
+        sp.row(ty, c0, c1);
+        for (int c = c0 + ((first - j) % step + step) % step; c <= c1; c += step)
+            ikeys[o + (uint32_t)(j + c - c0)] = ((uint32_t)(ty * tiles_x + c) << rank_bits) | r;
+        if (c1 >= c0) j += c1 - c0 + 1;
     }
 }
 
@@ -208,11 +218,12 @@ emit_instances(const ProjRec *__restrict__ rec_sorted, const uint32_t *__restric
     if (r >= n) return;
     const uint32_t cnt = tcount_r[r];
     if (!cnt) return;
-    if (cnt > kEmitSmall) {
+    const ProjRec g = rec_sorted[r];
+    if (bbox_tiles(g) > kEmitSmall) {
         big[atomicAdd(&ctr->reserved[1], 1u)] = (uint32_t)r;
         return;
     }
-    emit_tiles(rec_sorted[r], (uint32_t)r, toff[r], 0, cnt, 1, rank_bits, tiles_x, ikeys);
+    emit_tiles(g, (uint32_t)r, toff[r], 0, 1, rank_bits, tiles_x, ikeys);
 }
 
 __global__ void __launch_bounds__(256)
@@ -220,11 +231,24 @@ emit_big(const ProjRec *__restrict__ rec_sorted, const uint32_t *__restrict__ tc
          const uint32_t *__restrict__ toff, const sm_render_counters *ctr,
          const uint32_t *__restrict__ big, int rank_bits, int tiles_x, uint32_t *__restrict__ ikeys) {
     if (ctr->overflow) return;
+    __shared__ BigRowTable tab;
     const uint32_t nbig = ctr->reserved[1];
-    for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {   // a block per big splat
         const uint32_t r = big[b];
-        emit_tiles(rec_sorted[r], r, toff[r], threadIdx.x, tcount_r[r], blockDim.x, rank_bits, tiles_x,
-                   ikeys);
+        const RowSpan sp(rec_sorted[r]);
+        const uint32_t o = toff[r];
+        uint32_t base = 0;
+        for (int tyb = sp.ty0; tyb <= sp.ty1; tyb += kBigThreads) {
+            base = fill_row_table(sp, tyb, base, tab);
+            const int nrows = min(kBigThreads, sp.ty1 - tyb + 1);
+            for (int i = warp; i < nrows; i += kBigThreads / 32) {
+                const int c0 = tab.c0[i], c1 = tab.c1[i], row = (tyb + i) * tiles_x;
+                const uint32_t dst = o + tab.off[i] - (uint32_t)c0;
+                for (int c = c0 + lane; c <= c1; c += 32)
+                    ikeys[dst + (uint32_t)c] = ((uint32_t)(row + c) << rank_bits) | r;
+            }
+        }
     }
 }
 
@@ -346,6 +370,8 @@ composite_fwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
                        st_tlast, st_last);
 }
 
+int g_ellipse_cull = 1;   // sm_set_ellipse_cull (tests: culled == unculled, bit for bit)
+
 static int env_int(const char *name, int dflt) {
     const char *v = getenv(name);
     return v ? atoi(v) : dflt;
@@ -396,7 +422,7 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
         const unsigned gb = (unsigned)ceil_div(n, 256);
         prof_begin(ST_PROJECT, st);
         project_fwd<<<gb, 256, 0, st>>>(reinterpret_cast<const float4 *>(params), slots, n, cd,
-                                        b.rec, b.p64, b.dkey0, b.order0, b.tcount);
+                                        g_ellipse_cull, b.rec, b.p64, b.dkey0, b.order0, b.tcount);
         prof_end(ST_PROJECT, st);
         const SortScratch ss = sort_scratch(b.sort_hist, dims.max_gaussians > dims.max_instances
                                                              ? dims.max_gaussians : dims.max_instances);

@@ -117,6 +117,7 @@ def test_evict_reload_bit_exact_with_adam_state(cuda, tmp_path):
     after = [t[rows] for t in (st.slab.params, st.slab.adam_m, st.slab.adam_v, st.slab.sh_rest)]
     for a, b in zip(before, after):
         assert torch.equal(a, b)
+    st.streamer.drain()   # the write-behind file lands asynchronously
     data = (tmp_path / "chunks" / f"{cid:016x}.dcg").read_bytes()
     assert len(data) == 32 + 300 * 360
 
