@@ -14,6 +14,21 @@ __device__ __forceinline__ uint32_t bbox_tiles(const ProjRec &g) {
     return (uint32_t)((rec_x1(g) / kTile - rec_x0(g) / kTile + 1) * (rec_y1(g) / kTile - rec_y0(g) / kTile + 1));
 }
 
+// Small splats (<= kEmitSmall box tiles) carry their kept tiles as a bit mask
+// over the box in row-major order (bit (ty - ty0) * ntx + tx - tx0), computed
+// once by the projection: emission walks the set bits, the kept index of a
+// tile is the popcount below its bit.
+__device__ __forceinline__ uint32_t small_mask(const RowSpan &sp) {
+    const int ntx = sp.tx1 - sp.tx0 + 1;
+    uint32_t m = 0;
+    for (int ty = sp.ty0, bit = 0; ty <= sp.ty1; ty++, bit += ntx) {
+        int c0, c1;
+        sp.row(ty, c0, c1);
+        if (c1 >= c0) m |= (0xffffffffu >> (31 - (c1 - c0))) << (bit + c0 - sp.tx0);
+    }
+    return m;
+}
+
 // Big splats are handled by a 256-thread block: thread i evaluates tile row
 // tyb + i (RowSpan), a block scan turns the row counts into kept-index
 // offsets, then warp w walks rows w, w + 8, ... with its lanes across columns.
@@ -62,7 +77,7 @@ struct RenderLayout {
     int depth_passes, tile_passes;
     int64_t sort_blocks;
     int64_t o_counters, o_rec, o_rec_sorted, o_p64, o_dkey0, o_dkey1, o_order0, o_order1;
-    int64_t o_tcount, o_tcount_r, o_toff, o_ikey0, o_ikey1, o_ranges;
+    int64_t o_tcount, o_tcount_r, o_tmask, o_tmask_r, o_toff, o_ikey0, o_ikey1, o_ranges;
     int64_t o_pix_cd, o_pix_t, o_pix_tlast, o_pix_last, o_g2d, o_sort_hist, o_scan;
     int64_t o_gbuf, o_tile_hor;
     int64_t total;
@@ -75,7 +90,7 @@ struct RenderBufs {
     ProjRec *rec, *rec_sorted;
     Proj64 *p64;
     unsigned long long *dkey0, *dkey1;
-    uint32_t *order0, *order1, *tcount, *tcount_r, *toff, *ikey0, *ikey1, *ranges;
+    uint32_t *order0, *order1, *tcount, *tcount_r, *tmask, *tmask_r, *toff, *ikey0, *ikey1, *ranges;
     float4 *pix_cd;
     float *pix_t, *pix_tlast;
     int32_t *pix_last;
@@ -98,6 +113,8 @@ inline RenderBufs render_bufs(void *ws, const RenderLayout &L) {
     r.order1 = reinterpret_cast<uint32_t *>(b + L.o_order1);
     r.tcount = reinterpret_cast<uint32_t *>(b + L.o_tcount);
     r.tcount_r = reinterpret_cast<uint32_t *>(b + L.o_tcount_r);
+    r.tmask = reinterpret_cast<uint32_t *>(b + L.o_tmask);
+    r.tmask_r = reinterpret_cast<uint32_t *>(b + L.o_tmask_r);
     r.toff = reinterpret_cast<uint32_t *>(b + L.o_toff);
     r.ikey0 = reinterpret_cast<uint32_t *>(b + L.o_ikey0);
     r.ikey1 = reinterpret_cast<uint32_t *>(b + L.o_ikey1);

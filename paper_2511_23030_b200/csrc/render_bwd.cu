@@ -145,8 +145,8 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
               const float *__restrict__ d_depth, const float *__restrict__ d_alpha,
               const float4 *__restrict__ st_cd, const float *__restrict__ st_t,
               const float *__restrict__ st_tlast, const int32_t *__restrict__ st_last,
-              const uint32_t *__restrict__ toff, float *__restrict__ gbuf,
-              int32_t *__restrict__ tile_hor) {
+              const uint32_t *__restrict__ toff, const uint32_t *__restrict__ tmask_r,
+              float *__restrict__ gbuf, int32_t *__restrict__ tile_hor) {
     constexpr int NT = kTilePx / PIX;
     constexpr int NW = NT / 32;
     __shared__ ProjRec s_rec[NT];
@@ -222,8 +222,17 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
         }
         __syncthreads();
         if (idx < bend) {   // warp-ordered sum -> the instance's emission slot
-            const uint32_t slot =
-                toff[s_rank[threadIdx.x]] + RowSpan(s_rec[threadIdx.x]).kept_index(tile_x, tile_y);
+            const ProjRec &g = s_rec[threadIdx.x];
+            const uint32_t rk = s_rank[threadIdx.x];
+            uint32_t kept;   // the tile's index among the splat's kept tiles
+            if (bbox_tiles(g) <= kEmitSmall) {
+                const int tx0 = rec_x0(g) / kTile, ty0r = rec_y0(g) / kTile;
+                const int bit = (tile_y - ty0r) * (rec_x1(g) / kTile - tx0 + 1) + tile_x - tx0;
+                kept = (uint32_t)__popc(tmask_r[rk] & ((1u << bit) - 1u));
+            } else {
+                kept = RowSpan(g).kept_index(tile_x, tile_y);
+            }
+            const uint32_t slot = toff[rk] + kept;
             float acc[12];
 #pragma unroll
             for (int k = 0; k < 10; k++) {
@@ -242,26 +251,22 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
     }
 }
 
-// Sum of a splat's visited instance slots (an instance was visited iff its
-// rank is <= its tile's horizon rank), walking the kept tiles in emission
-// order: a culled tile only removes a zero term, so ellipse culling stays
-// bit-exact.
-__device__ __forceinline__ void sum_slots(const ProjRec &g, int64_t r, uint32_t o, const float *gbuf,
-                                          const int32_t *tile_hor, int tiles_x, float (&acc)[10]) {
-    const RowSpan sp(g);
-    for (int ty = sp.ty0; ty <= sp.ty1; ty++) {
-        int c0, c1;
-        sp.row(ty, c0, c1);
-        for (int c = c0; c <= c1; c++) {
-            if (r > (int64_t)tile_hor[ty * tiles_x + c]) continue;
-            const float4 *src =
-                reinterpret_cast<const float4 *>(gbuf + (int64_t)(o + (uint32_t)(c - c0)) * kG2dStride);
-            const float4 a = src[0], b = src[1], cc = src[2];
-            acc[0] += a.x, acc[1] += a.y, acc[2] += a.z, acc[3] += a.w;
-            acc[4] += b.x, acc[5] += b.y, acc[6] += b.z, acc[7] += b.w;
-            acc[8] += cc.x, acc[9] += cc.y;
-        }
-        if (c1 >= c0) o += (uint32_t)(c1 - c0 + 1);
+// Sum of a small splat's visited instance slots (an instance was visited iff
+// its rank is <= its tile's horizon rank), walking the kept-tile mask in
+// emission order: a culled tile only removes a zero term, so ellipse culling
+// stays bit-exact.
+__device__ __forceinline__ void sum_slots(const ProjRec &g, uint32_t mask, int64_t r, uint32_t o,
+                                          const float *gbuf, const int32_t *tile_hor, int tiles_x,
+                                          float (&acc)[10]) {
+    const int tx0 = rec_x0(g) / kTile, ty0 = rec_y0(g) / kTile, ntx = rec_x1(g) / kTile - tx0 + 1;
+    for (uint32_t m = mask; m; m &= m - 1, o++) {
+        const int bit = __ffs(m) - 1;
+        if (r > (int64_t)tile_hor[(ty0 + bit / ntx) * tiles_x + tx0 + bit % ntx]) continue;
+        const float4 *src = reinterpret_cast<const float4 *>(gbuf + (int64_t)o * kG2dStride);
+        const float4 a = src[0], b = src[1], cc = src[2];
+        acc[0] += a.x, acc[1] += a.y, acc[2] += a.z, acc[3] += a.w;
+        acc[4] += b.x, acc[5] += b.y, acc[6] += b.z, acc[7] += b.w;
+        acc[8] += cc.x, acc[9] += cc.y;
     }
 }
 
@@ -331,6 +336,7 @@ struct CamBwd {
 __global__ void __launch_bounds__(256)
 project_bwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots, int64_t n,
             CamBwd cam, const uint32_t *__restrict__ order, const uint32_t *__restrict__ tcount_r,
+            const uint32_t *__restrict__ tmask_r,
             const ProjRec *__restrict__ recs, const uint32_t *__restrict__ toff,
             const float *__restrict__ gbuf, const int32_t *__restrict__ tile_hor, int tiles_x,
             const float *__restrict__ g2d, float *__restrict__ grads) {
@@ -346,7 +352,7 @@ project_bwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots
     } else {
 #pragma unroll
         for (int k = 0; k < 10; k++) gk[k] = 0.f;
-        sum_slots(rec, r, toff[r], gbuf, tile_hor, tiles_x, gk);
+        sum_slots(rec, tmask_r[r], r, toff[r], gbuf, tile_hor, tiles_x, gk);
     }
     const uint32_t i = order[r];
     const int64_t slot = slots ? (int64_t)slots[i] : (int64_t)i;
@@ -496,7 +502,7 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
     kern<<<(unsigned)L.n_tiles, kTilePx / pix, 0, st>>>(
         b.ranges, L.tile_passes & 1 ? b.ikey1 : b.ikey0, rank_mask, b.rec_sorted, b.p64, b.order0,
         dims.width, dims.height, L.tiles_x, d_rgb, d_depth, d_alpha, b.pix_cd, b.pix_t, b.pix_tlast,
-        b.pix_last, b.toff, b.gbuf, b.tile_hor);
+        b.pix_last, b.toff, b.tmask_r, b.gbuf, b.tile_hor);
     prof_end(ST_COMPOSITE_BWD, st);
     prof_begin(ST_GRAD_GATHER, st);
     grad_gather_big<<<148 * 4, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.toff, b.ctr, b.tcount, b.gbuf,
@@ -512,7 +518,7 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
     cb.cy = cam.cy;
     prof_begin(ST_PROJECT_BWD, st);
     project_bwd<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
-        reinterpret_cast<const float4 *>(params), slots, n, cb, b.order0, b.tcount_r, b.rec_sorted,
+        reinterpret_cast<const float4 *>(params), slots, n, cb, b.order0, b.tcount_r, b.tmask_r, b.rec_sorted,
         b.toff, b.gbuf, b.tile_hor, L.tiles_x, b.g2d, grads);
     prof_end(ST_PROJECT_BWD, st);
     SM_CHECK_LAUNCH("render_backward");

@@ -53,6 +53,8 @@ RenderLayout render_layout(const sm_render_dims &d) {
     L.o_order1 = take(G * 4);
     L.o_tcount = take(G * 4);
     L.o_tcount_r = take(G * 4);
+    L.o_tmask = take(G * 4);
+    L.o_tmask_r = take(G * 4);
     L.o_toff = take(G * 4);
     L.o_ikey0 = take(I * 4);
     L.o_ikey1 = take(I * 4);
@@ -82,7 +84,7 @@ __global__ void __launch_bounds__(256)
 project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots, int64_t n,
             CamDev cam, int cull, ProjRec *__restrict__ rec, Proj64 *__restrict__ p64,
             unsigned long long *__restrict__ dkey, uint32_t *__restrict__ order,
-            uint32_t *__restrict__ tcount) {
+            uint32_t *__restrict__ tcount, uint32_t *__restrict__ tmask) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int64_t slot = slots ? (int64_t)slots[i] : i;
@@ -162,22 +164,33 @@ project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots
         tcount[i] = 0;
         return;
     }
-    uint32_t cnt = 0;   // tiles the q <= 9 ellipse reaches (RowSpan)
+    // tiles the q <= 9 ellipse reaches (RowSpan); small splats keep them as a mask
     const RowSpan sp(r);
-    for (int ty = sp.ty0; ty <= sp.ty1; ty++) cnt += (uint32_t)sp.count(ty);
-    tcount[i] = cnt;
+    if (bbox_tiles(r) <= kEmitSmall) {
+        const uint32_t m = small_mask(sp);
+        tmask[i] = m;
+        tcount[i] = (uint32_t)__popc(m);
+    } else {
+        uint32_t cnt = 0;
+        for (int ty = sp.ty0; ty <= sp.ty1; ty++) cnt += (uint32_t)sp.count(ty);
+        tcount[i] = cnt;
+    }
 }
 
 __global__ void __launch_bounds__(256)
 gather_by_rank(const uint32_t *__restrict__ order, int64_t n, const ProjRec *__restrict__ rec,
-               const uint32_t *__restrict__ tcount, ProjRec *__restrict__ rec_sorted,
-               uint32_t *__restrict__ tcount_r) {
+               const uint32_t *__restrict__ tcount, const uint32_t *__restrict__ tmask,
+               ProjRec *__restrict__ rec_sorted, uint32_t *__restrict__ tcount_r,
+               uint32_t *__restrict__ tmask_r) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     const uint32_t i = order[r];
     const uint32_t c = tcount[i];
     tcount_r[r] = c;
-    if (c) rec_sorted[r] = rec[i];
+    if (c) {
+        rec_sorted[r] = rec[i];
+        tmask_r[r] = tmask[i];   // meaningful for small splats only
+    }
 }
 
 __global__ void check_instances(sm_render_counters *ctr, int64_t max_instances) {
@@ -194,24 +207,10 @@ __global__ void check_instances(sm_render_counters *ctr, int64_t max_instances) 
 // Keys are (tile << rank_bits) | rank at the rank's scanned offset, so the
 // array is in rank order whichever thread writes a slot.
 
-// Kept tiles (RowSpan) in row-major order; lane `first` of `step` writes the
-// kept indices j = first (mod step).
-__device__ __forceinline__ void emit_tiles(const ProjRec &g, uint32_t r, uint32_t o, int first,
-                                           int step, int rank_bits, int tiles_x, uint32_t *ikeys) {
-    const RowSpan sp(g);
-    int j = 0;
-    for (int ty = sp.ty0; ty <= sp.ty1; ty++) {
-        int c0, c1;
-        sp.row(ty, c0, c1);
-        for (int c = c0 + ((first - j) % step + step) % step; c <= c1; c += step)
-            ikeys[o + (uint32_t)(j + c - c0)] = ((uint32_t)(ty * tiles_x + c) << rank_bits) | r;
-        if (c1 >= c0) j += c1 - c0 + 1;
-    }
-}
 
 __global__ void __launch_bounds__(256)
 emit_instances(const ProjRec *__restrict__ rec_sorted, const uint32_t *__restrict__ tcount_r,
-               const uint32_t *__restrict__ toff, int64_t n, sm_render_counters *ctr,
+               const uint32_t *__restrict__ tmask_r, const uint32_t *__restrict__ toff, int64_t n, sm_render_counters *ctr,
                uint32_t *__restrict__ big, int rank_bits, int tiles_x, uint32_t *__restrict__ ikeys) {
     if (ctr->overflow) return;
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -223,7 +222,14 @@ emit_instances(const ProjRec *__restrict__ rec_sorted, const uint32_t *__restric
         big[atomicAdd(&ctr->reserved[1], 1u)] = (uint32_t)r;
         return;
     }
-    emit_tiles(g, (uint32_t)r, toff[r], 0, 1, rank_bits, tiles_x, ikeys);
+    // kept tiles = set bits of the box mask, row-major
+    const int tx0 = rec_x0(g) / kTile, ty0 = rec_y0(g) / kTile, ntx = rec_x1(g) / kTile - tx0 + 1;
+    uint32_t o = toff[r];
+    for (uint32_t m = tmask_r[r]; m; m &= m - 1) {
+        const int bit = __ffs(m) - 1;
+        const int t = (ty0 + bit / ntx) * tiles_x + tx0 + bit % ntx;
+        ikeys[o++] = ((uint32_t)t << rank_bits) | (uint32_t)r;
+    }
 }
 
 __global__ void __launch_bounds__(256)
@@ -422,7 +428,7 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
         const unsigned gb = (unsigned)ceil_div(n, 256);
         prof_begin(ST_PROJECT, st);
         project_fwd<<<gb, 256, 0, st>>>(reinterpret_cast<const float4 *>(params), slots, n, cd,
-                                        g_ellipse_cull, b.rec, b.p64, b.dkey0, b.order0, b.tcount);
+                                        g_ellipse_cull, b.rec, b.p64, b.dkey0, b.order0, b.tcount, b.tmask);
         prof_end(ST_PROJECT, st);
         const SortScratch ss = sort_scratch(b.sort_hist, dims.max_gaussians > dims.max_instances
                                                              ? dims.max_gaussians : dims.max_instances);
@@ -432,12 +438,13 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
                                              64, ss, st);
         prof_end(ST_DEPTH_SORT, st);
         prof_begin(ST_BIN, st);
-        gather_by_rank<<<gb, 256, 0, st>>>(b.order0, n, b.rec, b.tcount, b.rec_sorted, b.tcount_r);
+        gather_by_rank<<<gb, 256, 0, st>>>(b.order0, n, b.rec, b.tcount, b.tmask, b.rec_sorted,
+                                           b.tcount_r, b.tmask_r);
         exclusive_scan(b.tcount_r, b.toff, n, b.scan, &b.ctr->n_instances, st);
         check_instances<<<1, 1, 0, st>>>(b.ctr, dims.max_instances);
         const unsigned persist = (unsigned)(148 * 8);
         // b.tcount (per visible index) is dead after gather_by_rank: reuse it as the big-splat queue
-        emit_instances<<<gb, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.toff, n, b.ctr, b.tcount,
+        emit_instances<<<gb, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.tmask_r, b.toff, n, b.ctr, b.tcount,
                                            L.rank_bits, L.tiles_x, b.ikey0);
         emit_big<<<148 * 4, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.toff, b.ctr, b.tcount, L.rank_bits,
                                           L.tiles_x, b.ikey0);
