@@ -111,6 +111,14 @@ int sm_render_backward(const float *params, const int32_t *slots, int64_t n,
  * effect at the next sm_render_forward (CUDA graphs keep their captured value). */
 void sm_set_ellipse_cull(int on);
 
+/* Diagnostics: byte offset inside a render workspace of an internal buffer
+ * (SM_WS_TILE_RANGES: uint32 [n_tiles][2] instance range per tile;
+ * SM_WS_PIX_LAST: int32 [H*W] position of each pixel's last contributor in its
+ * tile's instance list), or -1.  Valid after sm_render_forward. */
+#define SM_WS_TILE_RANGES 0
+#define SM_WS_PIX_LAST 1
+int64_t sm_render_ws_offset(const sm_render_dims *dims, int which);
+
 /* ------------------------------------------------------------------ loss
  * renderloss.total_loss / image_loss / ssim / depth_loss (renderloss.py:226-274):
  * (1-ls)*L1 + ls*(1-SSIM 11x11 sigma 1.5, 5-px crop, channel mean)

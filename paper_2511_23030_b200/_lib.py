@@ -77,6 +77,7 @@ def load():
     _sig(lib.sm_render_backward, c_int, vp, vp, i64, POINTER(Camera), POINTER(RenderDims), vp, i64,
          vp, vp, vp, vp, vp)
     _sig(lib.sm_set_ellipse_cull, None, c_int)
+    _sig(lib.sm_render_ws_offset, i64, POINTER(RenderDims), c_int)
     _sig(lib.sm_loss_workspace_size, i64, i32, i32)
     _sig(lib.sm_loss_forward_backward, c_int, vp, vp, vp, vp, vp, i32, i32, i32, c_float, c_float,
          vp, i64, vp, vp, vp, vp)

@@ -47,7 +47,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         obj = objdir / (Path(src).stem + ".o")
         cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xptxas", "-v" if verbose else "-O3", "--expt-relaxed-constexpr",
-               "-I", str(HERE.parent / "include"), "-c", str(CSRC / src), "-o", str(obj)]
+               "-I", str(HERE.parent / "include"), *os.environ.get("SM_NVCC_EXTRA", "").split(),
+               "-c", str(CSRC / src), "-o", str(obj)]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(str(obj))
     failed = False

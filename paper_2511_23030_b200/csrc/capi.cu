@@ -87,6 +87,16 @@ int sm_render_backward(const float *params, const int32_t *slots, int64_t n, con
 
 void sm_set_ellipse_cull(int on) { g_ellipse_cull = on ? 1 : 0; }
 
+int64_t sm_render_ws_offset(const sm_render_dims *dims, int which) {
+    if (!dims) return -1;
+    const RenderLayout L = render_layout(*dims);
+    switch (which) {
+        case SM_WS_TILE_RANGES: return L.o_ranges;
+        case SM_WS_PIX_LAST: return L.o_pix_last;
+        default: return -1;
+    }
+}
+
 int64_t sm_loss_workspace_size(int32_t width, int32_t height) { return loss_workspace_size(width, height); }
 
 int sm_loss_forward_backward(const float *rgb, const float *depth, const uint8_t *gt_rgb_u8,

@@ -139,6 +139,15 @@ __device__ __forceinline__ double quad_q64(const Proj64 &p, int px, int py) {
 constexpr double kPowScale = -0.72134752044448170368;   // -0.5 * log2(e)
 constexpr float kPowCut = (float)(9.0 * -0.72134752044448170368);
 
+// Packed fp32x2 arithmetic (sm_100 FFMA2 / FMUL2 / FADD2): two pixels' math
+// per issue slot in the compositing kernels.
+__device__ __forceinline__ float2 f2s(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float hsum(float2 a) { return a.x + a.y; }
+
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -58,11 +58,12 @@ __device__ __forceinline__ float2 transpose_reduce10(const float (&v)[16], int l
     return make_float2(c, d);
 }
 
-// Per-pixel reverse state.  T holds T_{k+1} while walking back; the stored
-// T before the last contributor seeds T_k at k == last (alpha = 1 safe).
+// Per-pixel reverse state, initialised from the forward's stored per-pixel
+// values.  T holds T_{k+1} while walking back; the stored T before the last
+// contributor seeds T_k at k == last (alpha = 1 safe).
 struct BwdPix {
     float gCr, gCg, gCb, gD, gA;   // dL/d{C, D, A} of the raw accumulators
-    float T, tlast, Br, Bg, Bb, Bz, P;
+    float T, tlast;
     int32_t last;
 
     __device__ __forceinline__ void init(bool inside, int64_t p, const float *d_rgb,
@@ -71,8 +72,6 @@ struct BwdPix {
                                          const float *st_tlast, const int32_t *st_last) {
         gCr = gCg = gCb = gD = gA = 0.f;
         T = tlast = 0.f;
-        Br = Bg = Bb = Bz = 0.f;
-        P = 1.f;
         last = -1;
         if (!inside) return;
         const float4 cd = st_cd[p];
@@ -92,43 +91,76 @@ struct BwdPix {
             gA += -dd * cd.w / (A * A);
         }
     }
+};
 
-    // Accumulates this pixel's d{u v ia ib ic op r g b z} into v and steps back.
-    __device__ __forceinline__ void step(const ProjRec &g, float dx, float dy, float pw, int k,
-                                         float (&v)[16]) {
-        const float G = ex2_approx(pw);
-        const float alpha = g.op * G;
-        const float oma = 1.f - alpha;
-        const float Tk = (k == last) ? tlast : __fdividef(T, oma);
-        float ga = (g.r - Br) * gCr + (g.g - Bg) * gCg + (g.b - Bb) * gCb + (g.z - Bz) * gD;
-        ga = Tk * (ga + gA * P);
-        const float wt = Tk * alpha;
-        v[6] += wt * gCr;
-        v[7] += wt * gCg;
-        v[8] += wt * gCb;
-        v[9] += wt * gD;
-        v[5] += ga * G;
+// A thread's two pixels (same column, rows py and py + 1) walked back
+// together in packed fp32x2: .x is row py, .y row py + 1.  A pixel the splat
+// does not reach gets G = 0, which makes every contribution exactly zero and
+// leaves T, B and P unchanged (1 - 0 = 1), so the step is branch-free.
+struct BwdPair {
+    float2 gCr, gCg, gCb, gD, gA;
+    float2 T, tlast, Br, Bg, Bb, Bz, P;
+    int32_t last0, last1;
+
+    __device__ __forceinline__ void init(const BwdPix &a, const BwdPix &b) {
+        gCr = make_float2(a.gCr, b.gCr);
+        gCg = make_float2(a.gCg, b.gCg);
+        gCb = make_float2(a.gCb, b.gCb);
+        gD = make_float2(a.gD, b.gD);
+        gA = make_float2(a.gA, b.gA);
+        T = make_float2(a.T, b.T);
+        tlast = make_float2(a.tlast, b.tlast);
+        Br = Bg = Bb = Bz = f2s(0.f);
+        P = f2s(1.f);
+        last0 = a.last;
+        last1 = b.last;
+    }
+
+    // d{u v ia ib ic op r g b z} of splat g (instance position k) summed over
+    // the pair into v[0..9]; then one step back.
+    __device__ __forceinline__ void step(const ProjRec &g, float dx, float2 dy, float2 pw, bool h0,
+                                         bool h1, int k, float (&v)[16]) {
+        const float2 G = make_float2(h0 ? ex2_approx(pw.x) : 0.f, h1 ? ex2_approx(pw.y) : 0.f);
+        const float2 alpha = mul2(G, f2s(g.op));
+        const float2 oma = sub2(f2s(1.f), alpha);
+        float2 Tk;
+        Tk.x = !h0 ? T.x : (k == last0 ? tlast.x : __fdividef(T.x, oma.x));
+        Tk.y = !h1 ? T.y : (k == last1 ? tlast.y : __fdividef(T.y, oma.y));
+        float2 ga = mul2(sub2(f2s(g.r), Br), gCr);
+        ga = fma2(sub2(f2s(g.g), Bg), gCg, ga);
+        ga = fma2(sub2(f2s(g.b), Bb), gCb, ga);
+        ga = fma2(sub2(f2s(g.z), Bz), gD, ga);
+        ga = mul2(Tk, fma2(gA, P, ga));
+        const float2 wt = mul2(Tk, alpha);
+        v[6] = hsum(mul2(wt, gCr));
+        v[7] = hsum(mul2(wt, gCg));
+        v[8] = hsum(mul2(wt, gCb));
+        v[9] = hsum(mul2(wt, gD));
+        v[5] = hsum(mul2(ga, G));
         // q = pw / kPowScale; conic grads are w.r.t. the unscaled conic
-        const float gq = -0.5f * alpha * ga;
-        v[2] += gq * dx * dx;
-        v[3] += gq * 2.f * dx * dy;
-        v[4] += gq * dy * dy;
-        const float gqi = gq * (float)(-2.0 / kPowScale);
-        v[0] += gqi * (g.ia * dx + g.ib * dy);
-        v[1] += gqi * (g.ib * dx + g.ic * dy);
-        Br = alpha * g.r + oma * Br;
-        Bg = alpha * g.g + oma * Bg;
-        Bb = alpha * g.b + oma * Bb;
-        Bz = alpha * g.z + oma * Bz;
-        P *= oma;
+        const float2 gq = mul2(f2s(-0.5f), mul2(alpha, ga));
+        const float2 gqdx = mul2(gq, f2s(dx));
+        v[2] = hsum(mul2(gqdx, f2s(dx)));
+        v[3] = hsum(mul2(mul2(gqdx, f2s(2.f)), dy));
+        v[4] = hsum(mul2(mul2(gq, dy), dy));
+        const float2 gqi = mul2(gq, f2s((float)(-2.0 / kPowScale)));
+        v[0] = hsum(mul2(gqi, fma2(f2s(g.ib), dy, f2s(g.ia * dx))));
+        v[1] = hsum(mul2(gqi, fma2(f2s(g.ic), dy, f2s(g.ib * dx))));
+        Br = fma2(alpha, f2s(g.r), mul2(oma, Br));
+        Bg = fma2(alpha, f2s(g.g), mul2(oma, Bg));
+        Bb = fma2(alpha, f2s(g.b), mul2(oma, Bb));
+        Bz = fma2(alpha, f2s(g.z), mul2(oma, Bz));
+        P = mul2(P, oma);
         T = Tk;
     }
 };
 
-// Same tiling as composite_fwd (256/PIX threads x PIX pixels).  Instances are
-// revisited from the block's last contributor back to the tile start, one
-// CTA-width batch at a time; a warp skips splats missing its rows or lying
-// past every one of its pixels' last contributor.
+// Same tiling as composite_fwd: one CTA per 16x16 tile, 128 threads, each
+// owning a pixel pair (BwdPair); warp w covers tile rows 4w .. 4w + 3.
+// Instances are revisited from the block's last contributor back to the tile
+// start, one CTA-width batch at a time; a warp skips splats missing its rows,
+// lying past every one of its pixels' last contributor, or reaching none of
+// its pixels.
 //
 // Determinism: no floating-point atomics.  Each warp's 10 sums for an
 // instance land in its own shared slot; after the batch the slots are added
@@ -136,8 +168,12 @@ struct BwdPix {
 // tile's index among the splat's kept tiles); grad_gather then sums a splat's
 // instances in a fixed order.  Reruns and CUDA-graph replays are bit-identical
 // (the reference's metrics determinism contract, test_acceptance.py crit. 10).
-template <int PIX>
-__global__ void __launch_bounds__(kTilePx / PIX)
+constexpr int kBwdThreads = kTilePx / 2;
+#ifndef SM_BWD_MINB
+#define SM_BWD_MINB 5   // 5 CTAs x 4 warps per SM: measured best (register cap 102)
+#endif
+
+__global__ void __launch_bounds__(kBwdThreads, SM_BWD_MINB)
 composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ikeys,
               uint32_t rank_mask, const ProjRec *__restrict__ recs,
               const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
@@ -147,7 +183,7 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
               const float *__restrict__ st_tlast, const int32_t *__restrict__ st_last,
               const uint32_t *__restrict__ toff, const uint32_t *__restrict__ tmask_r,
               float *__restrict__ gbuf, int32_t *__restrict__ tile_hor) {
-    constexpr int NT = kTilePx / PIX;
+    constexpr int NT = kBwdThreads;
     constexpr int NW = NT / 32;
     __shared__ ProjRec s_rec[NT];
     __shared__ uint32_t s_rank[NT];
@@ -158,17 +194,19 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
     const int lane = threadIdx.x & 31;
     const int ty0 = (tile / tiles_x) * kTile;
     const int px = (tile % tiles_x) * kTile + (threadIdx.x & (kTile - 1));
-    const int py = ty0 + PIX * (threadIdx.x / kTile);
-    const int wy0 = ty0 + 2 * PIX * (threadIdx.x / 32);
+    const int py = ty0 + 2 * (threadIdx.x / kTile);
+    const int wy0 = ty0 + 4 * (threadIdx.x / 32);
     const int start = (int)ranges[2 * tile];
-    BwdPix s[PIX];
-    int wmax = -1;
-#pragma unroll
-    for (int i = 0; i < PIX; i++) {
-        s[i].init(px < width && py + i < height, (int64_t)(py + i) * width + px, d_rgb, d_depth,
-                  d_alpha, st_cd, st_t, st_tlast, st_last);
-        wmax = max(wmax, s[i].last);
+    BwdPair pp;
+    {
+        BwdPix a, b;
+        a.init(px < width && py < height, (int64_t)py * width + px, d_rgb, d_depth, d_alpha, st_cd,
+               st_t, st_tlast, st_last);
+        b.init(px < width && py + 1 < height, (int64_t)(py + 1) * width + px, d_rgb, d_depth, d_alpha,
+               st_cd, st_t, st_tlast, st_last);
+        pp.init(a, b);
     }
+    int wmax = max(pp.last0, pp.last1);
     if (threadIdx.x == 0) s_maxlast = -1;
     __syncthreads();
 #pragma unroll
@@ -195,30 +233,23 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
         for (int j = jtop; j >= 0; j--) {
             const ProjRec &g = s_rec[j];
             const int y0 = rec_y0(g), y1 = rec_y1(g);
-            if (y1 < wy0 || y0 > wy0 + 2 * PIX - 1) continue;   // warp-uniform row cull
+            if (y1 < wy0 || y0 > wy0 + 3) continue;   // warp-uniform row cull
             const int k = bstart + j;
-            float v[16];
-#pragma unroll
-            for (int t = 0; t < 16; t++) v[t] = 0.f;
-            bool hit = false;
             const int x0 = rec_x0(g);
+            bool h0 = false, h1 = false;
+            float dx = 0.f;
+            float2 dy = f2s(0.f), pw = f2s(0.f);
             if ((unsigned)(px - x0) <= (unsigned)(rec_x1(g) - x0)) {
-                const float dx = (float)(px - x0) + g.ox;
-#pragma unroll
-                for (int i = 0; i < PIX; i++) {
-                    float dy, pw;
-                    if (k <= s[i].last &&
-                        row_eval(g, dx, px, py + i, y0, y1, p64, order, s_rank[j], dy, pw)) {
-                        s[i].step(g, dx, dy, pw, k, v);
-                        hit = true;
-                    }
-                }
+                dx = (float)(px - x0) + g.ox;
+                h0 = k <= pp.last0 && row_eval(g, dx, px, py, y0, y1, p64, order, s_rank[j], dy.x, pw.x);
+                h1 = k <= pp.last1 && row_eval(g, dx, px, py + 1, y0, y1, p64, order, s_rank[j], dy.y, pw.y);
             }
-            if (__any_sync(0xffffffffu, hit)) {
-                const float2 s = transpose_reduce10(v, lane);
-                if (!(lane & 3)) s_part[warp][j][via] = s.x;
-                if (!(lane & 15)) s_part[warp][j][vib] = s.y;
-            }
+            if (!__any_sync(0xffffffffu, h0 || h1)) continue;
+            float v[16];
+            pp.step(g, dx, dy, pw, h0, h1, k, v);
+            const float2 s = transpose_reduce10(v, lane);
+            if (!(lane & 3)) s_part[warp][j][via] = s.x;
+            if (!(lane & 15)) s_part[warp][j][vib] = s.y;
         }
         __syncthreads();
         if (idx < bend) {   // warp-ordered sum -> the instance's emission slot
@@ -233,7 +264,7 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
                 kept = RowSpan(g).kept_index(tile_x, tile_y);
             }
             const uint32_t slot = toff[rk] + kept;
-            float acc[12];
+            float acc[10];
 #pragma unroll
             for (int k = 0; k < 10; k++) {
                 float a = 0.f;
@@ -241,7 +272,6 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
                 for (int w = 0; w < NW; w++) a += s_part[w][threadIdx.x][k];
                 acc[k] = a;
             }
-            acc[10] = acc[11] = 0.f;
             float4 *dst = reinterpret_cast<float4 *>(gbuf + (int64_t)slot * kG2dStride);
             dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
             dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
@@ -494,12 +524,7 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
     RenderBufs b = render_bufs(ws, L);
     const uint32_t rank_mask = (uint32_t)((1ull << L.rank_bits) - 1ull);
     prof_begin(ST_COMPOSITE_BWD, st);
-    static const int pix = [] {   // per-warp shared slots: PIX = 2 (4 warps) or 4 (2 warps)
-        const char *v = getenv("SM_BWD_PIX");
-        return (v && atoi(v) == 4) ? 4 : 2;
-    }();
-    auto kern = pix == 4 ? composite_bwd<4> : composite_bwd<2>;
-    kern<<<(unsigned)L.n_tiles, kTilePx / pix, 0, st>>>(
+    composite_bwd<<<(unsigned)L.n_tiles, kBwdThreads, 0, st>>>(
         b.ranges, L.tile_passes & 1 ? b.ikey1 : b.ikey0, rank_mask, b.rec_sorted, b.p64, b.order0,
         dims.width, dims.height, L.tiles_x, d_rgb, d_depth, d_alpha, b.pix_cd, b.pix_t, b.pix_tlast,
         b.pix_last, b.toff, b.tmask_r, b.gbuf, b.tile_hor);

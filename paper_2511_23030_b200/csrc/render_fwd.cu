@@ -306,38 +306,30 @@ struct FwdPix {
     }
 };
 
-// One CTA per 16x16 tile, 256/PIX threads, each owning PIX vertically
-// adjacent pixels (same column: the column test and dx are shared).  The
-// tile's instances (depth-rank order) are staged one CTA-width batch at a
-// time in shared memory; a warp skips a splat whose 3-sigma box misses its
-// 2*PIX rows (warp-uniform), a thread skips it when its column is outside the
-// box, and the block stops once every pixel's transmittance is below 1e-10.
-template <int PIX>
-__global__ void __launch_bounds__(kTilePx / PIX)
+// One CTA per 16x16 tile, 256 threads, a pixel each.  The tile's instances
+// (depth-rank order) are staged one CTA-width batch at a time in shared
+// memory; a warp skips a splat whose 3-sigma box misses its 2 rows
+// (warp-uniform), a thread skips it when its column is outside the box, and
+// the block stops once every pixel's transmittance is below 1e-10.
+__global__ void __launch_bounds__(kTilePx)
 composite_fwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ikeys,
               uint32_t rank_mask, const ProjRec *__restrict__ recs,
               const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
               int height, int tiles_x, float *__restrict__ out_rgb, float *__restrict__ out_depth,
               float *__restrict__ out_alpha, float4 *__restrict__ st_cd, float *__restrict__ st_t,
               float *__restrict__ st_tlast, int32_t *__restrict__ st_last) {
-    constexpr int NT = kTilePx / PIX;
+    constexpr int NT = kTilePx;
     __shared__ ProjRec s_rec[NT];
     __shared__ uint32_t s_rank[NT];
     const int tile = blockIdx.x;
     const int ty0 = (tile / tiles_x) * kTile;
     const int px = (tile % tiles_x) * kTile + (threadIdx.x & (kTile - 1));
-    const int py = ty0 + PIX * (threadIdx.x / kTile);
-    const int wy0 = ty0 + 2 * PIX * (threadIdx.x / 32);   // warp's first row
+    const int py = ty0 + threadIdx.x / kTile;
+    const int wy0 = ty0 + 2 * (threadIdx.x / 32);   // warp's first row
     const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
-    FwdPix s[PIX];
-    bool in[PIX];
-    bool all_done = true;
-#pragma unroll
-    for (int i = 0; i < PIX; i++) {
-        in[i] = px < width && py + i < height;
-        s[i] = FwdPix{1.f, 0.f, 0.f, 0.f, 0.f, 1.f, -1, !in[i]};
-        all_done = all_done && s[i].done;
-    }
+    const bool in = px < width && py < height;
+    FwdPix s = FwdPix{1.f, 0.f, 0.f, 0.f, 0.f, 1.f, -1, !in};
+    bool all_done = s.done;
     for (uint32_t base = start; base < end; base += NT) {
         if (__syncthreads_count(all_done) == NT) break;
         const uint32_t idx = base + threadIdx.x;
@@ -352,28 +344,98 @@ composite_fwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
             for (int j = 0; j < cnt; j++) {
                 const ProjRec &g = s_rec[j];
                 const int y0 = rec_y0(g), y1 = rec_y1(g);
-                if (y1 < wy0 || y0 > wy0 + 2 * PIX - 1) continue;   // warp-uniform row cull
+                if (y1 < wy0 || y0 > wy0 + 1) continue;   // warp-uniform row cull
                 const int x0 = rec_x0(g);
                 if ((unsigned)(px - x0) > (unsigned)(rec_x1(g) - x0)) continue;
                 const float dx = (float)(px - x0) + g.ox;
-                all_done = true;
-#pragma unroll
-                for (int i = 0; i < PIX; i++) {
-                    float dy, pw;
-                    if (!s[i].done && row_eval(g, dx, px, py + i, y0, y1, p64, order, s_rank[j], dy, pw))
-                        s[i].add(g, pw, (int32_t)(base + j));
-                    all_done = all_done && s[i].done;
+                float dy, pw;
+                if (row_eval(g, dx, px, py, y0, y1, p64, order, s_rank[j], dy, pw)) {
+                    s.add(g, pw, (int32_t)(base + j));
+                    if (s.done) {
+                        all_done = true;
+                        break;
+                    }
                 }
-                if (all_done) break;
             }
         }
         __syncthreads();
     }
-#pragma unroll
-    for (int i = 0; i < PIX; i++)
-        if (in[i])
-            s[i].store((int64_t)(py + i) * width + px, out_rgb, out_depth, out_alpha, st_cd, st_t,
-                       st_tlast, st_last);
+    if (in)
+        s.store((int64_t)py * width + px, out_rgb, out_depth, out_alpha, st_cd, st_t, st_tlast, st_last);
+}
+
+// Pixel-pair variant: 128 threads, each owning (px, py) and (px, py + 1),
+// the pair's arithmetic in packed fp32x2 (.x row py, .y row py + 1).  A pixel
+// the splat does not reach gets alpha = 0: its accumulators and T are left
+// unchanged, so the pair update is branch-free.  Same decisions, same
+// per-pixel expression order as composite_fwd.
+__global__ void __launch_bounds__(kTilePx / 2)
+composite_fwd_pair(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ikeys,
+                   uint32_t rank_mask, const ProjRec *__restrict__ recs,
+                   const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
+                   int height, int tiles_x, float *__restrict__ out_rgb, float *__restrict__ out_depth,
+                   float *__restrict__ out_alpha, float4 *__restrict__ st_cd, float *__restrict__ st_t,
+                   float *__restrict__ st_tlast, int32_t *__restrict__ st_last) {
+    constexpr int NT = kTilePx / 2;
+    __shared__ ProjRec s_rec[NT];
+    __shared__ uint32_t s_rank[NT];
+    const int tile = blockIdx.x;
+    const int ty0 = (tile / tiles_x) * kTile;
+    const int px = (tile % tiles_x) * kTile + (threadIdx.x & (kTile - 1));
+    const int py = ty0 + 2 * (threadIdx.x / kTile);
+    const int wy0 = ty0 + 4 * (threadIdx.x / 32);   // warp's first row
+    const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
+    const bool in0 = px < width && py < height, in1 = px < width && py + 1 < height;
+    float2 T = f2s(1.f), cr = f2s(0.f), cg = f2s(0.f), cb = f2s(0.f), cd = f2s(0.f), tlast = f2s(1.f);
+    int32_t last0 = -1, last1 = -1;
+    bool done0 = !in0, done1 = !in1;
+    for (uint32_t base = start; base < end; base += NT) {
+        if (__syncthreads_count(done0 && done1) == NT) break;
+        const uint32_t idx = base + threadIdx.x;
+        if (idx < end) {
+            const uint32_t rk = ikeys[idx] & rank_mask;
+            s_rank[threadIdx.x] = rk;
+            s_rec[threadIdx.x] = recs[rk];
+        }
+        __syncthreads();
+        const int cnt = (int)min((uint32_t)NT, end - base);
+        if (!(done0 && done1)) {
+            for (int j = 0; j < cnt; j++) {
+                const ProjRec &g = s_rec[j];
+                const int y0 = rec_y0(g), y1 = rec_y1(g);
+                if (y1 < wy0 || y0 > wy0 + 3) continue;   // warp-uniform row cull
+                const int x0 = rec_x0(g);
+                if ((unsigned)(px - x0) > (unsigned)(rec_x1(g) - x0)) continue;
+                const float dx = (float)(px - x0) + g.ox;
+                float dy, pw0, pw1;
+                const bool h0 = !done0 && row_eval(g, dx, px, py, y0, y1, p64, order, s_rank[j], dy, pw0);
+                const bool h1 = !done1 && row_eval(g, dx, px, py + 1, y0, y1, p64, order, s_rank[j], dy, pw1);
+                if (!(h0 || h1)) continue;
+                const int32_t k = (int32_t)(base + j);
+                const float2 alpha = mul2(f2s(g.op), make_float2(h0 ? ex2_approx(pw0) : 0.f,
+                                                                 h1 ? ex2_approx(pw1) : 0.f));
+                const float2 w = mul2(T, alpha);
+                cr = fma2(w, f2s(g.r), cr);
+                cg = fma2(w, f2s(g.g), cg);
+                cb = fma2(w, f2s(g.b), cb);
+                cd = fma2(w, f2s(g.z), cd);
+                tlast.x = h0 ? T.x : tlast.x;
+                tlast.y = h1 ? T.y : tlast.y;
+                last0 = h0 ? k : last0;
+                last1 = h1 ? k : last1;
+                T = mul2(T, sub2(f2s(1.f), alpha));
+                done0 = done0 || T.x < (float)SM_MIN_T;   // later pairs would be skipped (renderloss.py:143)
+                done1 = done1 || T.y < (float)SM_MIN_T;
+                if (done0 && done1) break;
+            }
+        }
+        __syncthreads();
+    }
+    FwdPix a{T.x, cr.x, cg.x, cb.x, cd.x, tlast.x, last0, done0};
+    FwdPix b{T.y, cr.y, cg.y, cb.y, cd.y, tlast.y, last1, done1};
+    if (in0) a.store((int64_t)py * width + px, out_rgb, out_depth, out_alpha, st_cd, st_t, st_tlast, st_last);
+    if (in1) b.store((int64_t)(py + 1) * width + px, out_rgb, out_depth, out_alpha, st_cd, st_t, st_tlast,
+                     st_last);
 }
 
 int g_ellipse_cull = 1;   // sm_set_ellipse_cull (tests: culled == unculled, bit for bit)
@@ -460,9 +522,9 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
     }
     const uint32_t rank_mask = (uint32_t)((1ull << L.rank_bits) - 1ull);
     prof_begin(ST_COMPOSITE_FWD, st);
-    static const int pix = env_int("SM_FWD_PIX", 1);
-    auto kern = pix == 1 ? composite_fwd<1> : (pix == 4 ? composite_fwd<4> : composite_fwd<2>);
-    kern<<<(unsigned)L.n_tiles, kTilePx / (pix == 1 ? 1 : (pix == 4 ? 4 : 2)), 0, st>>>(
+    static const int pair = env_int("SM_FWD_PAIR", 0);
+    auto kern = pair ? composite_fwd_pair : composite_fwd;
+    kern<<<(unsigned)L.n_tiles, pair ? kTilePx / 2 : kTilePx, 0, st>>>(
         b.ranges, L.tile_passes & 1 ? b.ikey1 : b.ikey0, rank_mask, b.rec_sorted, b.p64, b.order0,
         dims.width, dims.height, L.tiles_x, out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t,
         b.pix_tlast, b.pix_last);
