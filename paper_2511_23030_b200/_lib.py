@@ -8,6 +8,7 @@ the library in-tree (nvcc, sm_100a) when it is missing and nvcc is present.
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import POINTER, c_double, c_float, c_int, c_int32, c_int64, c_uint32, c_void_p
 from pathlib import Path
 
@@ -16,6 +17,8 @@ import numpy as np
 from .errors import CorruptChunk, DeviceFailure, DimensionMismatch, OutOfRange
 
 LIB_PATH = Path(__file__).resolve().parent / "libsplatmap_cuda.so"
+if os.environ.get("SM_LIB_VARIANT"):   # A/B experiments: libsplatmap_cuda.<variant>.so next to it
+    LIB_PATH = LIB_PATH.with_name(f"libsplatmap_cuda.{os.environ['SM_LIB_VARIANT']}.so")
 ABI_VERSION = 1
 PARAM_STRIDE = 16
 TILE = 16

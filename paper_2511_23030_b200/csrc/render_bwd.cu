@@ -123,9 +123,12 @@ struct BwdPair {
         const float2 G = make_float2(h0 ? ex2_approx(pw.x) : 0.f, h1 ? ex2_approx(pw.y) : 0.f);
         const float2 alpha = mul2(G, f2s(g.op));
         const float2 oma = sub2(f2s(1.f), alpha);
+        // T_k = T_{k+1} / (1 - alpha_k); 1 - alpha >= 2^-24 unless k is the
+        // pixel's last contributor (stored T).  Non-hits keep T.
+        const float2 Tq = mul2(T, make_float2(rcp_approx(oma.x), rcp_approx(oma.y)));
         float2 Tk;
-        Tk.x = !h0 ? T.x : (k == last0 ? tlast.x : __fdividef(T.x, oma.x));
-        Tk.y = !h1 ? T.y : (k == last1 ? tlast.y : __fdividef(T.y, oma.y));
+        Tk.x = !h0 ? T.x : (k == last0 ? tlast.x : Tq.x);
+        Tk.y = !h1 ? T.y : (k == last1 ? tlast.y : Tq.y);
         float2 ga = mul2(sub2(f2s(g.r), Br), gCr);
         ga = fma2(sub2(f2s(g.g), Bg), gCg, ga);
         ga = fma2(sub2(f2s(g.b), Bb), gCb, ga);
@@ -236,13 +239,24 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
             if (y1 < wy0 || y0 > wy0 + 3) continue;   // warp-uniform row cull
             const int k = bstart + j;
             const int x0 = rec_x0(g);
-            bool h0 = false, h1 = false;
-            float dx = 0.f;
-            float2 dy = f2s(0.f), pw = f2s(0.f);
-            if ((unsigned)(px - x0) <= (unsigned)(rec_x1(g) - x0)) {
-                dx = (float)(px - x0) + g.ox;
-                h0 = k <= pp.last0 && row_eval(g, dx, px, py, y0, y1, p64, order, s_rank[j], dy.x, pw.x);
-                h1 = k <= pp.last1 && row_eval(g, dx, px, py + 1, y0, y1, p64, order, s_rank[j], dy.y, pw.y);
+            // both rows at once; the same q <= 9 decisions as the forward's
+            // row_eval (an fp32 q outside the error band decides alike)
+            const float dx = (float)(px - x0) + g.ox;
+            const float2 dy = make_float2((float)(py - y0) + g.oy, (float)(py + 1 - y0) + g.oy);
+            const float2 pw = fma2(dy, fma2(f2s(g.ic), dy, f2s(2.f * g.ib * dx)), f2s(g.ia * dx * dx));
+            const float2 d = sub2(pw, f2s(kPowCut));
+            const bool col = (unsigned)(px - x0) <= (unsigned)(rec_x1(g) - x0);
+            bool h0 = col && (unsigned)(py - y0) <= (unsigned)(y1 - y0) && k <= pp.last0;
+            bool h1 = col && (unsigned)(py + 1 - y0) <= (unsigned)(y1 - y0) && k <= pp.last1;
+            if ((h0 && fabsf(d.x) <= g.eps) || (h1 && fabsf(d.y) <= g.eps)) {   // rare: fp64
+                const Proj64 q = p64[order[s_rank[j]]];
+                if (h0 && fabsf(d.x) <= g.eps) h0 = !(quad_q64(q, px, py) > 9.0);
+                else h0 = h0 && d.x >= 0.f;
+                if (h1 && fabsf(d.y) <= g.eps) h1 = !(quad_q64(q, px, py + 1) > 9.0);
+                else h1 = h1 && d.y >= 0.f;
+            } else {
+                h0 = h0 && d.x >= 0.f;
+                h1 = h1 && d.y >= 0.f;
             }
             if (!__any_sync(0xffffffffu, h0 || h1)) continue;
             float v[16];
