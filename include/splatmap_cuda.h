@@ -114,9 +114,12 @@ void sm_set_ellipse_cull(int on);
 /* Diagnostics: byte offset inside a render workspace of an internal buffer
  * (SM_WS_TILE_RANGES: uint32 [n_tiles][2] instance range per tile;
  * SM_WS_PIX_LAST: int32 [H*W] position of each pixel's last contributor in its
- * tile's instance list), or -1.  Valid after sm_render_forward. */
+ * tile's instance list; SM_WS_DEPTH_ORDER: the stable depth order, kept
+ * Gaussians first = np.argsort(z, kind="stable"), renderloss.py:202), or -1.
+ * Valid after sm_render_forward. */
 #define SM_WS_TILE_RANGES 0
 #define SM_WS_PIX_LAST 1
+#define SM_WS_DEPTH_ORDER 2   /* uint32 [n]: depth rank -> visible index */
 int64_t sm_render_ws_offset(const sm_render_dims *dims, int which);
 
 /* ------------------------------------------------------------------ loss

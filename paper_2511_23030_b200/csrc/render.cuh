@@ -151,7 +151,9 @@ __device__ __forceinline__ void project_geometry(double px, double py, double pz
     // cam = (p - t) @ r_wc
     g.x = d0 * rwc[0] + d1 * rwc[3] + d2 * rwc[6];
     g.y = d0 * rwc[1] + d1 * rwc[4] + d2 * rwc[7];
-    g.z = d0 * rwc[2] + d1 * rwc[5] + d2 * rwc[8];
+    // z without FMA contraction: (d0 r02 + d1 r12) + d2 r22, the depth-order
+    // key, reproducible on the host (tests compare the order bit for bit)
+    g.z = __dadd_rn(__dadd_rn(__dmul_rn(d0, rwc[2]), __dmul_rn(d1, rwc[5])), __dmul_rn(d2, rwc[8]));
     const double x = g.x, y = g.y, z = g.z;
     g.u = fx * x / z + cx;
     g.v = fy * y / z + cy;

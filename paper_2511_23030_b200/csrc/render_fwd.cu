@@ -4,9 +4,10 @@
 // _composite kernel (renderloss.py:106-152) for sm_100a:
 //   * projection in fp64 (it is HBM-bound: 64 B/Gaussian in, 104 B out), so
 //     means, conics and the 3-sigma bboxes are the reference's own numbers;
-//   * one global stable radix sort of the visible Gaussians on the fp64 bit
-//     pattern of z (z >= near > 0, so bits order like values) = np.argsort(z,
-//     kind="stable") over the sorted-chunk-id concatenation;
+//   * one global stable order of the visible Gaussians by z = np.argsort(z,
+//     kind="stable") over the sorted-chunk-id concatenation: a 4-pass radix
+//     sort on the fp32-rounded z (z >= near > 0, so the bits order like the
+//     values), then runs of equal fp32 keys re-sorted on the fp64 bits;
 //   * instances are emitted in depth-rank order and radix-sorted on the tile
 //     bits only (stable), giving each 16x16 tile its Gaussians front to back;
 //   * compositing in fp32 with the q > 9 decision taken in fp64 whenever the
@@ -34,7 +35,7 @@ RenderLayout render_layout(const sm_render_dims &d) {
     while ((1ll << tb) < L.n_tiles) tb++;
     L.rank_bits = rb;
     L.tile_bits = tb;
-    L.depth_passes = ceil_div(64, kRadixBits);
+    L.depth_passes = ceil_div(32, kRadixBits);   // fp32 key + fp64 tie fixup
     L.tile_passes = (int)ceil_div(tb, kRadixBits);
     L.sort_blocks = ceil_div(G > I ? G : I, kSortTile);
     int64_t off = 0;
@@ -83,7 +84,8 @@ struct CamDev {
 __global__ void __launch_bounds__(256)
 project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots, int64_t n,
             CamDev cam, int cull, ProjRec *__restrict__ rec, Proj64 *__restrict__ p64,
-            unsigned long long *__restrict__ dkey, uint32_t *__restrict__ order,
+            uint32_t *__restrict__ dkey, unsigned long long *__restrict__ zbits,
+            uint32_t *__restrict__ order,
             uint32_t *__restrict__ tcount, uint32_t *__restrict__ tmask) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -98,11 +100,14 @@ project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots
                      (double)B.y, (double)B.z, (double)B.w, (double)C.x, (double)C.y, cam.r,
                      cam.t, cam.fx, cam.fy, cam.cx, cam.cy, g);
     if (!(g.z >= cam.near_plane)) {   // renderloss.py:179 keep = z >= near
-        dkey[i] = ~0ull;
+        dkey[i] = ~0u;                   // after every kept depth, index order
         tcount[i] = 0;
         return;
     }
-    dkey[i] = (unsigned long long)__double_as_longlong(g.z);
+    // depth order key: fp32 z (monotone rounding of z > 0, ordered as uint);
+    // ties are resolved on the exact fp64 bits by depth_tie_fixup
+    dkey[i] = __float_as_uint((float)g.z);
+    zbits[i] = (unsigned long long)__double_as_longlong(g.z);
     // renderloss.py:110-135: conic and clamped 3-sigma bbox (fp64)
     const double a = g.a, b = g.b, c = g.c;
     const double det = a * c - b * b;
@@ -174,6 +179,39 @@ project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots
         uint32_t cnt = 0;
         for (int ty = sp.ty0; ty <= sp.ty1; ty++) cnt += (uint32_t)sp.count(ty);
         tcount[i] = cnt;
+    }
+}
+
+// The 32-bit depth sort is stable, so within a run of equal fp32 keys the
+// Gaussians are in index order; np.argsort(z, kind="stable") orders them by
+// the fp64 z first.  The run's first thread re-sorts the run (stable
+// insertion sort on the fp64 bits) when it holds an inversion -- runs are a
+// few elements long (distinct fp64 depths within one fp32 ulp).
+__global__ void __launch_bounds__(256)
+depth_tie_fixup(const uint32_t *__restrict__ key, uint32_t *__restrict__ order, int64_t n,
+                const unsigned long long *__restrict__ zbits) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r + 1 >= n) return;
+    const uint32_t k = key[r];
+    if (k == ~0u || key[r + 1] != k || (r > 0 && key[r - 1] == k)) return;   // not a run head
+    int64_t e = r + 1;
+    bool inv = false;
+    unsigned long long prev = zbits[order[r]];
+    for (; e < n && key[e] == k; e++) {
+        const unsigned long long z = zbits[order[e]];
+        inv |= z < prev;
+        prev = z;
+    }
+    if (!inv) return;
+    for (int64_t a = r + 1; a < e; a++) {   // stable insertion sort of order[r, e) by zbits
+        const uint32_t oa = order[a];
+        const unsigned long long za = zbits[oa];
+        int64_t b = a - 1;
+        while (b >= r && zbits[order[b]] > za) {
+            order[b + 1] = order[b];
+            b--;
+        }
+        order[b + 1] = oa;
     }
 }
 
@@ -488,16 +526,20 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
     cudaMemsetAsync(b.ranges, 0, L.n_tiles * 8, st);
     if (n > 0) {
         const unsigned gb = (unsigned)ceil_div(n, 256);
+        // 32-bit depth keys, ping-pong halves of the dkey0 region; fp64 z bits in dkey1
+        uint32_t *dk = reinterpret_cast<uint32_t *>(b.dkey0);
         prof_begin(ST_PROJECT, st);
         project_fwd<<<gb, 256, 0, st>>>(reinterpret_cast<const float4 *>(params), slots, n, cd,
-                                        g_ellipse_cull, b.rec, b.p64, b.dkey0, b.order0, b.tcount, b.tmask);
+                                        g_ellipse_cull, b.rec, b.p64, dk, b.dkey1, b.order0, b.tcount, b.tmask);
         prof_end(ST_PROJECT, st);
         const SortScratch ss = sort_scratch(b.sort_hist, dims.max_gaussians > dims.max_instances
                                                              ? dims.max_gaussians : dims.max_instances);
-        // global stable depth order (8 passes over the 64-bit key -> buffer 0)
+        // global stable depth order: 4 passes over the fp32 key + fp64 tie fixup
         prof_begin(ST_DEPTH_SORT, st);
-        radix_sort<unsigned long long, true>(b.dkey0, b.order0, b.dkey1, b.order1, nullptr, n, n, 0,
-                                             64, ss, st);
+        const int dcur = radix_sort<uint32_t, true>(dk, b.order0, dk + dims.max_gaussians, b.order1,
+                                                    nullptr, n, n, 0, 32, ss, st);
+        (void)dcur;   // 4 passes: keys and order end in buffer 0
+        depth_tie_fixup<<<gb, 256, 0, st>>>(dk, b.order0, n, b.dkey1);
         prof_end(ST_DEPTH_SORT, st);
         prof_begin(ST_BIN, st);
         gather_by_rank<<<gb, 256, 0, st>>>(b.order0, n, b.rec, b.tcount, b.tmask, b.rec_sorted,
@@ -518,7 +560,7 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
         uint32_t *ik = cur ? b.ikey1 : b.ikey0;
         tile_ranges<<<persist, 256, 0, st>>>(ik, b.ctr, L.rank_bits, b.ranges);
         prof_end(ST_TILE_SORT, st);
-        count_launches(1 + (1 + L.depth_passes) + 7 + (1 + L.tile_passes) + 1);
+        count_launches(1 + (1 + L.depth_passes) + 1 + 7 + (1 + L.tile_passes) + 1);
     }
     const uint32_t rank_mask = (uint32_t)((1ull << L.rank_bits) - 1ull);
     prof_begin(ST_COMPOSITE_FWD, st);

@@ -204,6 +204,65 @@ def test_ellipse_tile_cull_is_exact(cuda):
         lib.sm_set_ellipse_cull(1)
 
 
+def _gpu_depth_order(scene, pose, intr):
+    import torch
+
+    from paper_2511_23030_b200 import _lib
+    from paper_2511_23030_b200 import renderloss as rl
+    sa = rl.SceneArrays(**scene)
+    params = torch.from_numpy(rl.pack_params(sa)).cuda()
+    eng = rl.default_engine()
+    rl.render_device(params, None, len(sa), pose, intr, eng)
+    torch.cuda.synchronize()
+    off = _lib.load().sm_render_ws_offset(eng.dims, 2)
+    order = eng.ws[off:off + 4 * len(sa)].view(torch.int32).cpu().numpy().view(np.uint32)
+    cam = rl.camera_for(pose, intr)
+    r = np.array(list(cam.r_wc)).reshape(3, 3)
+    t = np.array(list(cam.t))
+    d = scene["positions"].astype(np.float64) - t
+    z = (d[:, 0] * r[0, 2] + d[:, 1] * r[1, 2]) + d[:, 2] * r[2, 2]   # the kernel's exact expression
+    return order.astype(np.int64), z, d @ r, intr.near
+
+
+def test_depth_order_bit_exact(cuda):
+    """The global depth order equals np.argsort(z, kind="stable") over the
+    kept Gaussians (renderloss.py:179, 202), element for element: a random
+    scene (also against the reference's matmul z), and a tie stress scene
+    where hundreds of Gaussians share one fp32 depth but differ in fp64 (a
+    tiny camera roll spreads z below one fp32 ulp), in shuffled index order,
+    so the fp64 tie fixup after the 32-bit radix sort decides the order."""
+    from paper_2511_23030_b200.core import CameraIntrinsics, Pose, quat_normalize
+    rng = np.random.default_rng(21)
+    n = 20000
+    pos = np.stack([rng.uniform(-6, 6, n), rng.uniform(-4, 4, n), rng.uniform(-1.0, 14.0, n)], 1)
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    scene = f32(dict(positions=pos, rotations=q, scales=rng.uniform(0.01, 0.2, (n, 3)),
+                     opacities=rng.uniform(0.3, 0.95, n), sh0=rng.normal(size=(n, 3))))
+    intr = CameraIntrinsics(fx=120.0, fy=120.0, cx=80.0, cy=60.0, width=160, height=120, near=0.05)
+    pose = Pose(rotation=quat_normalize([1.0, 0.02, -0.03, 0.01]), translation=[0.1, -0.2, 0.3])
+    order, z, cam_ref, near = _gpu_depth_order(scene, pose, intr)
+    keep = np.flatnonzero(z >= near)
+    want = keep[np.argsort(z[keep], kind="stable")]
+    assert np.array_equal(order[:len(keep)], want)
+    assert np.array_equal(np.sort(order[len(keep):]), np.flatnonzero(~(z >= near)))
+    zr = cam_ref[:, 2]   # the reference's own (BLAS) z gives the same order here
+    keep_r = np.flatnonzero(zr >= near)
+    assert np.array_equal(order[:len(keep_r)], keep_r[np.argsort(zr[keep_r], kind="stable")])
+
+    # tie stress: 600 splats on one depth plane, camera rolled by ~1e-9 rad
+    m = 600
+    pos = np.stack([rng.uniform(-1, 1, m), rng.uniform(-0.5, 0.5, m), np.full(m, 5.0)], 1)
+    scene = f32(dict(positions=pos, rotations=np.tile([1.0, 0, 0, 0], (m, 1)),
+                     scales=np.full((m, 3), 0.05), opacities=np.full(m, 0.5), sh0=np.zeros((m, 3))))
+    pose = Pose(rotation=quat_normalize([1.0, 0.0, 3e-9, 0.0]), translation=[0.0, 0.0, 0.25])
+    order, z, _, near = _gpu_depth_order(scene, pose, intr)
+    zf = z.astype(np.float32)
+    assert len(np.unique(zf)) < m // 10 and len(np.unique(z)) > m // 2   # the ties are real
+    want = np.argsort(z, kind="stable")
+    assert np.array_equal(order, want)
+
+
 def test_loss_matches_reference_golden(cuda, golden):
     from paper_2511_23030_b200 import renderloss as rl
     from paper_2511_23030_b200.core import CameraIntrinsics, Keyframe, Pose
