@@ -120,6 +120,7 @@ void sm_set_ellipse_cull(int on);
 #define SM_WS_TILE_RANGES 0
 #define SM_WS_PIX_LAST 1
 #define SM_WS_DEPTH_ORDER 2   /* uint32 [n]: depth rank -> visible index */
+#define SM_WS_RANK_TILES 3    /* uint32 [n]: kept tiles per depth rank   */
 int64_t sm_render_ws_offset(const sm_render_dims *dims, int which);
 
 /* ------------------------------------------------------------------ loss

@@ -94,6 +94,7 @@ int64_t sm_render_ws_offset(const sm_render_dims *dims, int which) {
         case SM_WS_TILE_RANGES: return L.o_ranges;
         case SM_WS_PIX_LAST: return L.o_pix_last;
         case SM_WS_DEPTH_ORDER: return L.o_order0;
+        case SM_WS_RANK_TILES: return L.o_tcount_r;
         default: return -1;
     }
 }

@@ -160,6 +160,7 @@ class _ActiveSet:
 class _DeviceKeyframe:
     rgb_u8: object
     depth: object
+    pending: object = None   # side stream still uploading (e2e mode)
 
 
 class MappingEngine:
@@ -229,8 +230,16 @@ class MappingEngine:
             if d is None:
                 d = self._kf_dev[-1] = _DeviceKeyframe(torch.empty_like(pin[0], device=self.device),
                                                        torch.empty_like(pin[1], device=self.device))
-            d.rgb_u8.copy_(pin[0], non_blocking=True)
-            d.depth.copy_(pin[1], non_blocking=True)
+            # H2D on a side stream, overlapped with the forward render (which
+            # does not read the ground truth); the loss waits for it
+            cur = torch.cuda.current_stream(self.device)
+            if not hasattr(self, "_up_stream"):
+                self._up_stream = torch.cuda.Stream(device=self.device)
+            self._up_stream.wait_stream(cur)   # the previous step's loss is done with d
+            with torch.cuda.stream(self._up_stream):
+                d.rgb_u8.copy_(pin[0], non_blocking=True)
+                d.depth.copy_(pin[1], non_blocking=True)
+            d.pending = self._up_stream
             return d
         d = self._kf_dev.get(kf.id)
         if d is None:
@@ -254,6 +263,9 @@ class MappingEngine:
         cam = camera_for(kf.pose, kf.intrinsics)
         dk = self._device_keyframe(kf)
         self.render.forward(slab.params, slots, n, cam, self.rgb, self.depth, self.alpha)
+        if getattr(dk, "pending", None) is not None:   # join the side-stream upload
+            self.torch.cuda.current_stream(self.device).wait_stream(dk.pending)
+            dk.pending = None
         self.loss.run(self.rgb, self.depth, dk.rgb_u8, None, dk.depth, 3, self.weights,
                       self.d_rgb if backward else None, self.d_depth if backward else None)
         if backward and n:
@@ -335,6 +347,7 @@ class MappingEngine:
         if self.upload_keyframes_each_step:   # GT RGB (u8) + depth (f32) cross PCIe every step
             self.h2d_bytes += kf.intrinsics.width * kf.intrinsics.height * 7
         self.render.ensure(n, kf.intrinsics.width, kf.intrinsics.height)
+        self.last_n = n
         graphs = getattr(self, "_graphs", {})
         entry = graphs.get(self._graph_key(kf, slots, n)) if self.use_graphs else None
         if entry is not None:

@@ -48,12 +48,18 @@ def main():
         L = (ranges[:, 1].astype(np.int64) - ranges[:, 0])
         V = np.where(maxlast >= 0, maxlast - ranges[:, 0].astype(np.int64) + 1, 0)
         srt = np.sort(V)[::-1]
+        o_t = lib.sm_render_ws_offset(d, 3)
+        cnt = ws[o_t:o_t + 4 * eng.last_n].view(torch.int32).cpu().numpy()
+        big = cnt[cnt > 32]
         out.append({
             "keyframe_step": k, "tiles": int(len(L)), "instances": int(L.sum()), "visited": int(V.sum()),
             "L_mean": float(L.mean()), "L_max": int(L.max()), "L_p99": float(np.percentile(L, 99)),
             "V_mean": float(V.mean()), "V_max": int(V.max()), "V_p99": float(np.percentile(V, 99)),
             "V_top10": srt[:10].tolist(),
             "V_max_over_mean": float(V.max() / max(V.mean(), 1)),
+            "big_splats": int(len(big)), "big_instances": int(big.sum()),
+            "big_max": int(big.max()) if len(big) else 0,
+            "big_hist": np.histogram(big, bins=[33, 64, 128, 256, 512, 1024, 4096])[0].tolist(),
         })
     for o in out:
         print(json.dumps(o))
