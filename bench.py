@@ -94,18 +94,29 @@ class ClockSampler:
 
 # Algorithmic bytes per unit of each stage.
 #   n = visible Gaussians, i = tile instances, p = pixels
+# Algorithmic bytes per step and stage (n visible Gaussians, i tile instances,
+# p pixels, v instances the compositing revisits = the backward's horizon sum):
 STAGE_BYTES = {
-    "project_fwd": lambda n, i, p: n * (4 + 64 + 64 + 40 + 8 + 4 + 4),
-    "depth_sort": lambda n, i, p: n * 8 * (8 + 24),
-    "bin_emit": lambda n, i, p: n * (4 + 4 + 64 + 64 + 4 * 4) + i * 4,
-    "tile_sort": lambda n, i, p: i * 2 * 12 + i * 8,
-    "composite_fwd": lambda n, i, p: i * (4 + 64) + p * (20 + 28),
-    "loss": lambda n, i, p: p * (16 + 7 + 36 * 2 + 16),
-    "composite_bwd": lambda n, i, p: i * (4 + 64 + 40) + p * (28 + 16),
-    "project_bwd": lambda n, i, p: n * (4 + 4 + 4 + 64 + 40 + 2 * 64),
-    "adam": lambda n, i, p: n * (4 + 7 * 64),
-    "grad_gather": lambda n, i, p: n * (4 + 4 + 64 + 48) + i * (48 + 4),
+    "project_fwd": lambda n, i, p, v: n * (4 + 64 + 64 + 40 + 8 + 4 + 4),
+    "depth_sort": lambda n, i, p, v: n * 8 * 4 * 2 + n * 8,
+    "bin_emit": lambda n, i, p, v: n * (4 + 4 + 64 + 64 + 4 * 4) + i * 4,
+    "tile_sort": lambda n, i, p, v: i * 2 * 12 + i * 8,
+    "composite_fwd": lambda n, i, p, v: v * (4 + 64) + p * (20 + 28),
+    "loss": lambda n, i, p, v: p * (16 + 7 + 36 * 2 + 16),
+    "composite_bwd": lambda n, i, p, v: v * (4 + 64 + 48) + p * (28 + 16),
+    "project_bwd": lambda n, i, p, v: n * (4 + 4 + 4 + 64 + 40 + 2 * 64),
+    "adam": lambda n, i, p, v: n * (4 + 7 * 64),
+    "grad_gather": lambda n, i, p, v: n * (4 + 4 + 64 + 48) + v * (48 + 4),
 }
+NCU_SUMMARY = Path(__file__).resolve().parent / "profiles" / "r01_ncu_full.json"
+
+
+def _ncu_kernel(name: str):
+    """Counters of `name` from the committed `ncu --set full` summary (same build)."""
+    try:
+        return json.loads(NCU_SUMMARY.read_text())["kernels"].get(name)
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 def _dist():
@@ -270,6 +281,7 @@ def main():
     value = units / (ms / 1e3)
     n_vis = eng.counter_gaussians / max(eng.counter_steps, 1)
     n_inst = eng.counter_instances / max(eng.counter_steps, 1)
+    n_visit = eng.counter_visited / max(eng.counter_steps, 1)
     gauss_s = eng.counter_gaussians * world / (ms / 1e3)
     # ------------------------------------------------------------ e2e through the public API
     eng.upload_keyframes_each_step = True
@@ -301,17 +313,23 @@ def main():
     if dom:
         per_launch_ms = prof[dom][0] / prof[dom][1]
         launches_per_step = prof[dom][1] / args.steps
-        byt = STAGE_BYTES.get(dom, lambda *a: 0)(n_vis, n_inst, px) / max(launches_per_step, 1)
+        byt = STAGE_BYTES.get(dom, lambda *a: 0)(n_vis, n_inst, px, n_visit) / max(launches_per_step, 1)
         achieved = byt / (per_launch_ms / 1e3) / 1e9
+        nk = _ncu_kernel(dom)
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                "traffic": nk.get("traffic_bytes") if nk else None,
+                "traffic_source": f"profiles/{NCU_SUMMARY.name} (ncu --set full, dram read+write per launch)",
                 "algorithmic_bytes_per_launch": byt, "ms_per_launch": per_launch_ms,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "_fallback" not in peaks
-                else "fallback 6.65 TB/s"}
+                else "fallback 6.65 TB/s",
+                # the compositing kernels are issue / FP32-pipe bound, not HBM bound
+                "issue_active_pct": nk.get("issue_pct") if nk else None,
+                "sm_throughput_pct": nk.get("sm_pct") if nk else None}
         for k, v in stages.items():
             f = STAGE_BYTES.get(k)
             if f and v["calls"]:
-                b = f(n_vis, n_inst, px) / (v["calls"] / args.steps)
+                b = f(n_vis, n_inst, px, n_visit) / (v["calls"] / args.steps)
                 v["gbs"] = b / (v["ms_per_step"] / (v["calls"] / args.steps) / 1e3) / 1e9
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -325,6 +343,7 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "gaussians_total": args.n,
                    "visible_gaussians_per_step": n_vis, "tile_instances_per_step": n_inst,
+                   "revisited_instances_per_step": n_visit,
                    "resolution": [eng.intr.width, eng.intr.height], "keyframes_per_step_per_gpu": 1,
                    "parallelism": f"dp{world}",
                    "l2": "inputs larger than L2 (slab params+Adam+grads 256 MB/1M Gaussians)"},

@@ -68,7 +68,8 @@ typedef struct sm_render_counters {
     uint32_t overflow;       /* 1 if n_instances > max_instances (no image)  */
     uint32_t n_visible;      /* Gaussians with >= 1 tile                     */
     uint32_t n_fallback;     /* not maintained (reserved)                    */
-    uint32_t reserved[12];
+    uint32_t reserved[12];   /* [0] sort count, [1] big-splat queue length,
+                              * [2] instances the last backward revisited    */
 } sm_render_counters;
 
 typedef struct sm_adam_config {

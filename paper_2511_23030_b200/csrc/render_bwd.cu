@@ -185,7 +185,7 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
               const float4 *__restrict__ st_cd, const float *__restrict__ st_t,
               const float *__restrict__ st_tlast, const int32_t *__restrict__ st_last,
               const uint32_t *__restrict__ toff, const uint32_t *__restrict__ tmask_r,
-              float *__restrict__ gbuf, int32_t *__restrict__ tile_hor) {
+              float *__restrict__ gbuf, int32_t *__restrict__ tile_hor, sm_render_counters *ctr) {
     constexpr int NT = kBwdThreads;
     constexpr int NW = NT / 32;
     __shared__ ProjRec s_rec[NT];
@@ -217,8 +217,10 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
     if (lane == 0) atomicMax(&s_maxlast, wmax);
     __syncthreads();
     const int maxlast = s_maxlast;
-    if (threadIdx.x == 0)   // rank of the tile's last visited instance (grad_gather's horizon)
+    if (threadIdx.x == 0) {   // rank of the tile's last visited instance (grad_gather's horizon)
         tile_hor[tile] = maxlast >= start ? (int32_t)(ikeys[maxlast] & rank_mask) : -1;
+        if (maxlast >= start) atomicAdd(&ctr->reserved[2], (uint32_t)(maxlast - start + 1));
+    }
     const int via = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);   // 0..7
     const int vib = 8 + ((lane >> 4) & 1);                                                // 8..9
     const int tile_x = tile % tiles_x, tile_y = tile / tiles_x;
@@ -541,7 +543,7 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
     composite_bwd<<<(unsigned)L.n_tiles, kBwdThreads, 0, st>>>(
         b.ranges, L.tile_passes & 1 ? b.ikey1 : b.ikey0, rank_mask, b.rec_sorted, b.p64, b.order0,
         dims.width, dims.height, L.tiles_x, d_rgb, d_depth, d_alpha, b.pix_cd, b.pix_t, b.pix_tlast,
-        b.pix_last, b.toff, b.tmask_r, b.gbuf, b.tile_hor);
+        b.pix_last, b.toff, b.tmask_r, b.gbuf, b.tile_hor, b.ctr);
     prof_end(ST_COMPOSITE_BWD, st);
     prof_begin(ST_GRAD_GATHER, st);
     grad_gather_big<<<148 * 4, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.toff, b.ctr, b.tcount, b.gbuf,

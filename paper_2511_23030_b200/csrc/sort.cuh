@@ -81,6 +81,10 @@ onesweep_pass(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals_i
     __shared__ uint32_t s_vals[HAS_VAL ? kSortTile : 1];
     const int64_t n = load_count(n_dev, n_host);
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr_p, 1u);
+    __syncthreads();
+    // tiles are handed out in launch order: blocks past the live count (the
+    // grid is sized for the capacity) leave before doing any work
+    if ((int64_t)s_tile * kSortTile >= n) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&wcount[0][0])[i] = 0;
     // global digit base = exclusive scan of this pass's histogram
@@ -101,7 +105,6 @@ onesweep_pass(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals_i
     __syncthreads();
     const uint32_t tile = s_tile;
     const int64_t start = (int64_t)tile * kSortTile;
-    if (start >= n) return;
     const K mask = (K)((1u << nbits) - 1u);
     K key[kSortItems];
     uint32_t val[kSortItems];

@@ -202,7 +202,7 @@ class MappingEngine:
         self.d_rgb = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
         self.d_depth = torch.empty((h, w), dtype=torch.float32, device=dev)
         self._kf_dev: dict[int, _DeviceKeyframe] = {}
-        self._readback = torch.zeros(8, dtype=torch.float32, pin_memory=True)
+        self._readback = torch.zeros(12, dtype=torch.float32, pin_memory=True)
         self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
         self.cam = None
         self.h2d_bytes = 0
@@ -283,22 +283,24 @@ class MappingEngine:
         """D2H copy of {loss[4], n_instances, overflow} into pinned memory (async)."""
         rb = self._readback
         rb[:4].copy_(self.loss.out, non_blocking=True)
-        rb[4:6].copy_(self.render.ws[:8].view(self.torch.float32), non_blocking=True)
+        rb[4:11].copy_(self.render.ws[:28].view(self.torch.float32), non_blocking=True)
 
     def _finish_readback(self) -> tuple[float, bool]:
         self.torch.cuda.current_stream(self.device).synchronize()
-        self.d2h_bytes += 24
+        self.d2h_bytes += 44
         v = self._readback.numpy()
-        ctr = v[4:6].view(np.uint32)
+        ctr = v[4:11].view(np.uint32)   # sm_render_counters[0:7]
         self.counter_instances += int(ctr[0])
+        self.counter_visited += int(ctr[6])   # instances the backward revisited
         return float(v[0]), bool(ctr[1])
 
     def reset_counters(self) -> None:
         self.counter_steps = 0
         self.counter_gaussians = 0
         self.counter_instances = 0
+        self.counter_visited = 0
 
-    counter_steps = counter_gaussians = counter_instances = 0
+    counter_steps = counter_gaussians = counter_instances = counter_visited = 0
     use_graphs = True
 
     def _precompute_next_draw(self) -> None:

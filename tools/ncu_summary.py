@@ -51,8 +51,8 @@ def main():
         rec = {"kernel": r[kcol].split("(")[0].replace("void ", "")}
         for m, c in col.items():
             v = _num(r[c])
-            if m == "gpu__time_duration.sum" and units[c].strip() == "ns":
-                v = v / 1e3 if v is not None else v
+            if m == "gpu__time_duration.sum" and v is not None:
+                v *= {"ns": 1e-3, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3}.get(units[c].strip(), 1.0)
             if m.startswith("dram__bytes") and v is not None:
                 unit = units[c].strip()
                 v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
