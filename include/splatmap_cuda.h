@@ -182,8 +182,10 @@ int sm_expand_segments(const int64_t *seg_offset, const int64_t *seg_count,
  * loopclose.py:241); stride 360: a 120-byte opt_state tail
  * "ADM1" | step u32 | m[14] f32 | v[14] f32.  Unpack validates the record
  * invariants (diskformat.py:153 -> core.py:208-221) and the tail; err_out
- * (device int64) receives the first bad record index or -1.  Foreign
- * opt_state payloads take the host path. */
+ * (device int64) receives the first bad record index or -1.  With params,
+ * sh_rest, adam_m and adam_v all NULL it only validates (the streamer checks
+ * a staged chunk on its copy stream, then queues the unpack behind the
+ * render).  Foreign opt_state payloads take the host path. */
 int sm_chunk_unpack(const uint8_t *records, int64_t n, int64_t stride, float *params,
                     float *sh_rest, float *adam_m, float *adam_v, int64_t *err_out, void *stream);
 int sm_chunk_pack(const float *params, const float *sh_rest, const float *adam_m,

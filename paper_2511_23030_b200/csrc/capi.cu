@@ -151,7 +151,8 @@ int sm_expand_segments(const int64_t *seg_offset, const int64_t *seg_count, cons
 
 int sm_chunk_unpack(const uint8_t *records, int64_t n, int64_t stride, float *params, float *sh_rest,
                     float *adam_m, float *adam_v, int64_t *err_out, void *stream) {
-    if (!err_out || (n > 0 && (!records || !params || !sh_rest || !adam_m || !adam_v))) {
+    const bool validate_only = !params && !sh_rest && !adam_m && !adam_v;
+    if (!err_out || (n > 0 && (!records || (!validate_only && (!params || !sh_rest || !adam_m || !adam_v))))) {
         set_error("sm_chunk_unpack: null argument");
         return SM_ERR_INVALID;
     }

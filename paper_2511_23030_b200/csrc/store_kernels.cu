@@ -282,6 +282,9 @@ __device__ __forceinline__ int shrest_src(int k) {   // rest index -> sh index
     return k < 15 ? 1 + k : (k < 30 ? 2 + k : 3 + k);
 }
 
+// WRITE = false: validation only (the streamer checks a staged chunk on its
+// copy stream before the unpack is queued behind the render).
+template <bool WRITE>
 __global__ void __launch_bounds__(256)
 unpack_kernel(const uint8_t *__restrict__ rec, int64_t n, int64_t stride, float *__restrict__ params,
               float *__restrict__ sh_rest, float *__restrict__ m, float *__restrict__ v,
@@ -293,6 +296,22 @@ unpack_kernel(const uint8_t *__restrict__ rec, int64_t n, int64_t stride, float 
 #pragma unroll
     for (int k = 0; k < 59; k++) f[k] = __uint_as_float(w[k]);
     const uint32_t opt_len = w[59];
+    // validate_gaussian_arrays (core.py:208-221)
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < 59; k++) ok = ok && isfinite(f[k]);
+    ok = ok && f[7] > 0.f && f[8] > 0.f && f[9] > 0.f && f[10] >= 0.f && f[10] <= 1.f;
+    const double qn = sqrt((double)f[3] * f[3] + (double)f[4] * f[4] + (double)f[5] * f[5] +
+                           (double)f[6] * f[6]);
+    ok = ok && fabs(qn - 1.0) <= 1e-6;
+    if (stride == 240 + kAdamTail) {
+        const uint32_t *t = w + kRecWords;
+        ok = ok && opt_len == (uint32_t)kAdamTail && t[0] == kAdamMagic;
+    } else {
+        ok = ok && opt_len == 0;
+    }
+    if (!ok) atomicMin(err, (unsigned long long)i);
+    if (!WRITE) return;
     float *p = params + i * SM_PARAM_STRIDE;
 #pragma unroll
     for (int k = 0; k < 11; k++) p[k] = f[k];
@@ -303,19 +322,10 @@ unpack_kernel(const uint8_t *__restrict__ rec, int64_t n, int64_t stride, float 
     p[15] = 0.f;
 #pragma unroll
     for (int k = 0; k < 45; k++) sh_rest[i * 45 + k] = f[11 + shrest_src(k)];
-    // validate_gaussian_arrays (core.py:208-221)
-    bool ok = true;
-#pragma unroll
-    for (int k = 0; k < 59; k++) ok = ok && isfinite(f[k]);
-    ok = ok && f[7] > 0.f && f[8] > 0.f && f[9] > 0.f && f[10] >= 0.f && f[10] <= 1.f;
-    const double qn = sqrt((double)f[3] * f[3] + (double)f[4] * f[4] + (double)f[5] * f[5] +
-                           (double)f[6] * f[6]);
-    ok = ok && fabs(qn - 1.0) <= 1e-6;
     float *mm = m + i * SM_PARAM_STRIDE;
     float *vv = v + i * SM_PARAM_STRIDE;
     if (stride == 240 + kAdamTail) {
         const uint32_t *t = w + kRecWords;
-        ok = ok && opt_len == (uint32_t)kAdamTail && t[0] == kAdamMagic;
 #pragma unroll
         for (int k = 0; k < 14; k++) {
             mm[k] = __uint_as_float(t[2 + k]);
@@ -324,11 +334,9 @@ unpack_kernel(const uint8_t *__restrict__ rec, int64_t n, int64_t stride, float 
         mm[14] = (float)t[1];
         mm[15] = vv[14] = vv[15] = 0.f;
     } else {
-        ok = ok && opt_len == 0;
 #pragma unroll
         for (int k = 0; k < 16; k++) mm[k] = vv[k] = 0.f;
     }
-    if (!ok) atomicMin(err, (unsigned long long)i);
 }
 
 __global__ void __launch_bounds__(256)
@@ -373,8 +381,12 @@ int chunk_unpack(const uint8_t *rec, int64_t n, int64_t stride, float *params, f
     if (n <= 0) return SM_OK;
     prof_begin(ST_CODEC, st);
     count_launches(1);
-    unpack_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
-        rec, n, stride, params, sh_rest, m, v, reinterpret_cast<unsigned long long *>(err));
+    if (params)
+        unpack_kernel<true><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+            rec, n, stride, params, sh_rest, m, v, reinterpret_cast<unsigned long long *>(err));
+    else   // validation only
+        unpack_kernel<false><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+            rec, n, stride, nullptr, nullptr, nullptr, nullptr, reinterpret_cast<unsigned long long *>(err));
     prof_end(ST_CODEC, st);
     SM_CHECK_LAUNCH("chunk_unpack");
     return SM_OK;

@@ -91,7 +91,7 @@ def pack_chunk(encoded_id: int, gaussians: list[Gaussian]) -> bytes:
 def _header(data: bytes, magic: bytes, size: int, kind: str) -> None:
     if len(data) < size:
         raise CorruptChunk(f"{kind} file truncated before header end")
-    if data[:4] != magic:
+    if bytes(data[:4]) != magic:
         raise CorruptChunk(f"bad {kind} magic {data[:4]!r}")
 
 

@@ -210,6 +210,7 @@ class MappingEngine:
         self.upload_keyframes_each_step = False   # e2e mode: GT from pinned host every step
         self._pinned_kf: dict[int, tuple] = {}
         self._uniforms: dict[int, float] = {}
+        self._eager_seen: dict = {}
 
     # -------------------------------------------------------------- inputs
     def add_keyframe(self, kf: Keyframe, index_usage: int | None = None) -> None:
@@ -301,7 +302,9 @@ class MappingEngine:
         self.counter_visited = 0
 
     counter_steps = counter_gaussians = counter_instances = counter_visited = 0
+    counter_replays = counter_eager = 0
     use_graphs = True
+    capture_after = 2   # eager visits of a (keyframe, active set) before its graph is captured
 
     def _precompute_next_draw(self) -> None:
         """The next single-GPU step's uniform draw depends only on its derived
@@ -355,6 +358,7 @@ class MappingEngine:
         if entry is not None:
             g, gid = entry
             g.replay()
+            self.counter_replays += 1
             self._precompute_next_draw()   # host work overlapped with the GPU pass
             loss, overflow = self._finish_readback()
             _lib.load().sm_profile_graph_replayed(gid)
@@ -366,6 +370,7 @@ class MappingEngine:
             self.render.grow_instances(self.render.counters()["n_instances"])
             self.drop_graphs()
         for _ in range(6):
+            self.counter_eager += 1
             self._device_pass(kf, slots, n)
             self._adam(slots, n)
             self._queue_readback()
@@ -374,7 +379,17 @@ class MappingEngine:
                 self.counter_steps += 1
                 self.counter_gaussians += n
                 if self.use_graphs and n:
-                    self._capture(kf, slots, n)
+                    # capture on the second eager visit of a (keyframe, active
+                    # set): one-off sets (a moving camera paging chunks in and
+                    # out) never pay the capture
+                    key = self._graph_key(kf, slots, n)
+                    seen = self._eager_seen.get(key, 0) + 1
+                    self._eager_seen[key] = seen
+                    if seen >= self.capture_after:
+                        self._capture(kf, slots, n)
+                        self._eager_seen.pop(key, None)
+                    elif len(self._eager_seen) > 4096:
+                        self._eager_seen.clear()
                 return loss
             self.store.slab.grads.zero_()
             self.render.grow_instances(self.render.counters()["n_instances"])
@@ -383,15 +398,19 @@ class MappingEngine:
 
     def warm_graphs(self) -> None:
         """Run one device iteration per resident keyframe (capturing its graph)."""
-        for kid in sorted(self.store.resident_keyframe_ids()):
-            kf = self.store.keyframe_get(kid)
-            ids = sorted(self._visible_for_pose(kf.pose)[0])
-            if ids:
-                self.store.ensure_resident(ids)
-            slots, n = self.active.build(self.store.segments(ids))
-            self.train_view(kf, slots, n)
-            if ids:
-                self.store.mark_trained(ids)
+        after, self.capture_after = self.capture_after, 1
+        try:
+            for kid in sorted(self.store.resident_keyframe_ids()):
+                kf = self.store.keyframe_get(kid)
+                ids = sorted(self._visible_for_pose(kf.pose)[0])
+                if ids:
+                    self.store.ensure_resident(ids)
+                slots, n = self.active.build(self.store.segments(ids))
+                self.train_view(kf, slots, n)
+                if ids:
+                    self.store.mark_trained(ids)
+        finally:
+            self.capture_after = after
 
     # --------------------------------------------------------------- step
     def optimization_step(self, frame_idx: int, step_idx: int, inserted: int = 0) -> FrameMetrics:

@@ -5,19 +5,20 @@ Replaces the reference's synchronous unpack_chunk / pack_chunk object codecs
 (store.py:241-272, 493-515) without changing any policy decision or the
 io_ns cost model (the store charges bytes exactly as the reference does).
 
-Load:   file bytes (or a prefetched / still-pending copy) -> pinned staging ->
-        cudaMemcpyAsync on the copy stream -> K8 sm_chunk_unpack into the
-        chunk's slab segment on the copy stream; the compute stream waits on
-        the copy stream (device-side), the host only waits for the K8 verdict.
-Evict:  K9 sm_chunk_pack on the compute stream into a device staging buffer
-        (so the slab rows can be reused immediately, stream-ordered), the D2H
-        copy into pinned memory on the copy stream, and a writer thread that
+Load:   the file is read straight into a pinned buffer (readinto; reader
+        threads do it ahead of use for prefetched chunks); the copy stream
+        moves it into a device staging slot and validates the records there
+        (the host waits for that verdict only -- CorruptChunk is raised inside
+        ensure_resident like the reference); the K8 unpack into the chunk's
+        slab rows is queued on the compute stream behind the work already
+        there, so a load never waits for the render in flight.
+        A chunk whose eviction write is still pending is unpacked straight
+        from the device buffer it was packed into (no host round trip).
+Evict:  K9 sm_chunk_pack on the compute stream into a device buffer (so the
+        slab rows can be reused immediately, stream-ordered), the D2H copy
+        into pinned memory on the copy stream, and a writer thread that
         waits on that copy's event and writes the file: eviction write-back
-        overlaps with rendering (write-behind).  A reload of a chunk whose
-        write is still pending is served from its pinned copy.
-Prefetch: reader threads pull .dcg files into host memory ahead of use
-        (speculative: e.g. the visible sets of the other candidate keyframes);
-        a later load takes the bytes from there instead of the disk.
+        overlaps with rendering (write-behind).
 flush():  drains the writer queue (the store's durability point).
 """
 
@@ -25,6 +26,8 @@ from __future__ import annotations
 
 import queue
 import threading
+import time
+from collections import OrderedDict
 from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
@@ -35,11 +38,11 @@ from .errors import CorruptChunk, IoFailure
 
 
 class _PendingWrite:
-    __slots__ = ("path", "header", "pin", "nbytes", "event", "done", "dev")
+    __slots__ = ("path", "header", "pin", "nbytes", "event", "done", "dev", "stride")
 
-    def __init__(self, path, header, pin, nbytes, event, dev):
+    def __init__(self, path, header, pin, nbytes, event, dev, stride):
         self.path, self.header, self.pin, self.nbytes = path, header, pin, nbytes
-        self.event, self.dev = event, dev
+        self.event, self.dev, self.stride = event, dev, stride
         self.done = threading.Event()
 
     def data(self) -> bytes:
@@ -47,9 +50,28 @@ class _PendingWrite:
         return self.header + self.pin[:self.nbytes].numpy().tobytes()
 
 
+class PinnedFile:
+    """A chunk file's bytes in pinned host memory (`view()` = the file)."""
+    __slots__ = ("pin", "size")
+
+    def __init__(self, pin, size: int):
+        self.pin, self.size = pin, size
+
+    def view(self) -> np.ndarray:
+        return self.pin[:self.size].numpy()
+
+
+class DeviceRecords:
+    """A chunk whose write-behind is pending: header + packed records on device."""
+    __slots__ = ("header", "dev", "nbytes", "stride")
+
+    def __init__(self, header: bytes, dev, nbytes: int, stride: int):
+        self.header, self.dev, self.nbytes, self.stride = header, dev, nbytes, stride
+
+
 class ChunkStreamer:
     def __init__(self, slab, write_behind: bool = True, reader_threads: int = 4,
-                 prefetch_bytes: int = 1 << 30):
+                 writer_threads: int = 4, prefetch_bytes: int = 1 << 30, victim_bytes: int = 4 << 30):
         import torch
         self.torch = torch
         self.slab = slab
@@ -58,6 +80,10 @@ class ChunkStreamer:
         self._dev = torch.empty(0, dtype=torch.uint8, device=slab.device)
         self._pin = torch.empty(0, dtype=torch.uint8, pin_memory=True)
         self._err = torch.empty(1, dtype=torch.int64, device=slab.device)
+        self._err_unpack = torch.empty(1, dtype=torch.int64, device=slab.device)
+        self._err_host = torch.empty(1, dtype=torch.int64, pin_memory=True)
+        self._slots = [{"buf": None, "event": None} for _ in range(4)]   # device staging ring
+        self._slot_i = 0
         self.bytes_h2d = 0
         self.bytes_d2h = 0
         self.write_behind = write_behind
@@ -66,13 +92,23 @@ class ChunkStreamer:
         self._queue: queue.Queue = queue.Queue()
         self._writer_error: BaseException | None = None
         self._free_pins: list = []
+        self._arena_ready = False
+        # device victim cache: packed records of chunks whose write-behind
+        # landed, kept in HBM so a reload is one K8 (the OS page cache, one
+        # level up); never changes a policy decision or a charged byte
+        self._victims: "OrderedDict[Path, DeviceRecords]" = OrderedDict()
+        self._victim_bytes = 0
+        self.victim_limit = victim_bytes
         self._free_devs: list = []
-        self._writer = threading.Thread(target=self._write_loop, daemon=True)
-        self._writer.start()
+        self._writers = [threading.Thread(target=self._write_loop, daemon=True) for _ in range(writer_threads)]
+        for t in self._writers:
+            t.start()
         self._pool = ThreadPoolExecutor(max_workers=reader_threads)
         self._prefetched: dict[Path, object] = {}
         self._prefetch_limit = prefetch_bytes
-        self.stats = {"prefetch_hits": 0, "pending_hits": 0, "async_writes": 0}
+        self.stats = {"prefetch_hits": 0, "pending_hits": 0, "victim_hits": 0, "async_writes": 0, "alloc_pinned": 0,
+                      "alloc_device": 0, "alloc_s": 0.0, "read_s": 0.0, "stage_wait_s": 0.0,
+                      "validate_wait_s": 0.0}
 
     # ---------------------------------------------------------------- staging
     def _staging(self, nbytes: int):
@@ -83,74 +119,180 @@ class ChunkStreamer:
             self._pin = torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, pin_memory=True)
         return self._dev, self._pin
 
+    _QUANTUM = 8 << 20   # pooled buffers are whole multiples: any freed one fits the next chunk
+    PINNED_SLOTS = 48    # pre-registered pinned buffers (page-locking on demand costs ~10 ms per buffer)
+    DEVICE_SLOTS = 24    # device pack buffers of pending write-behinds
+    PINNED_SLOT_BYTES = 32 << 20
+
+    def _ensure_arena(self) -> None:
+        """Page-lock the pinned staging pool once, on the first paging operation."""
+        if self._arena_ready:
+            return
+        self._arena_ready = True
+        torch = self.torch
+        t0 = time.perf_counter()
+        bufs = [torch.empty(self.PINNED_SLOT_BYTES, dtype=torch.uint8, pin_memory=True)
+                for _ in range(self.PINNED_SLOTS)]
+        devs = [torch.empty(self.PINNED_SLOT_BYTES, dtype=torch.uint8, device=self.slab.device)
+                for _ in range(self.DEVICE_SLOTS if self.write_behind else 0)]
+        with self._lock:
+            self._free_pins.extend(bufs)
+            self._free_devs.extend(devs)
+            self.stats["arena_s"] = time.perf_counter() - t0
+
+    def warm(self) -> None:
+        """Allocate the staging pools now (else on the first paging operation)."""
+        self._ensure_arena()
+
+    def _pinned_free(self) -> int:
+        with self._lock:
+            return len(self._free_pins)
+
     def _take(self, pool: list, nbytes: int, pinned: bool):
         torch = self.torch
+        self._ensure_arena()
         with self._lock:
-            for i, t in enumerate(pool):
-                if t.numel() >= nbytes:
-                    return pool.pop(i)
+            best = None
+            for i, t in enumerate(pool):   # smallest buffer that fits
+                if t.numel() >= nbytes and (best is None or t.numel() < pool[best].numel()):
+                    best = i
+            if best is not None:
+                return pool.pop(best)
+        size = -(-(nbytes + 4096) // self._QUANTUM) * self._QUANTUM
+        t0 = time.perf_counter()
         if pinned:
-            return torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, pin_memory=True)
-        return torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, device=self.slab.device)
+            buf = torch.empty(size, dtype=torch.uint8, pin_memory=True)
+        else:
+            buf = torch.empty(size, dtype=torch.uint8, device=self.slab.device)
+        with self._lock:
+            self.stats["alloc_pinned" if pinned else "alloc_device"] += 1
+            self.stats["alloc_s"] += time.perf_counter() - t0
+        return buf
 
     # ------------------------------------------------------------------- load
-    def read_file(self, path: Path) -> bytes | None:
-        """Bytes of `path` from a pending write-behind copy or the prefetch
-        tier (None: caller reads the disk).  Charged by the caller as a read."""
+    def _read_pinned(self, path: Path) -> PinnedFile:
+        size = path.stat().st_size
+        pin = self._take(self._free_pins, max(size, 1), pinned=True)
+        t0 = time.perf_counter()
+        with open(path, "rb", buffering=0) as f:
+            got = f.readinto(memoryview(pin.numpy())[:size])
+        with self._lock:
+            self.stats["read_s"] += time.perf_counter() - t0
+        if got != size:
+            raise OSError(f"short read of {path}: {got} of {size} bytes")
+        return PinnedFile(pin, size)
+
+    def release(self, src) -> None:
+        """Return a PinnedFile's buffer to the pool (after its H2D completed)."""
+        if isinstance(src, PinnedFile):
+            with self._lock:
+                self._free_pins.append(src.pin)
+
+    def read_file(self, path: Path):
+        """PinnedFile of `path` from the prefetch tier or the disk, or a
+        DeviceRecords if its eviction write is still pending."""
+        path = Path(path)
         with self._lock:
             pw = self._pending.get(path)
-            fut = self._prefetched.pop(path, None)
+            vic = self._victims.get(path)
+            if vic is not None:
+                self._victims.move_to_end(path)
+            fut = self._prefetched.pop(path, None) if pw is None and vic is None else None
         if pw is not None:
             self.stats["pending_hits"] += 1
-            return pw.data()
+            return DeviceRecords(pw.header, pw.dev, pw.nbytes, pw.stride)
+        if vic is not None:
+            self.stats["victim_hits"] += 1
+            return vic
         if fut is not None:
             try:
-                data = fut.result()
+                src = fut.result()
+                self.stats["prefetch_hits"] += 1
+                return src
             except OSError:
-                return None
-            self.stats["prefetch_hits"] += 1
-            return data
+                pass
+        return self._read_pinned(path)
 
     def prefetch(self, paths) -> None:
-        """Speculatively read chunk files into host memory (reader threads)."""
+        """Speculatively read chunk files into pinned memory (reader threads);
+        never takes the last pinned buffers a load or eviction needs."""
+        self._ensure_arena()
+        reserve = 8
         with self._lock:
-            budget = self._prefetch_limit - len(self._prefetched) * (1 << 20)
+            spare = len(self._free_pins) - reserve
             for p in paths:
                 p = Path(p)
-                if p in self._prefetched or p in self._pending or budget <= 0:
+                if p in self._prefetched or p in self._pending or spare <= 0:
                     continue
-                self._prefetched[p] = self._pool.submit(p.read_bytes)
-                budget -= 1 << 20
+                self._prefetched[p] = self._pool.submit(self._read_pinned, p)
+                spare -= 1
 
     def drop_prefetch(self, path: Path) -> None:
         with self._lock:
-            self._prefetched.pop(Path(path), None)
+            fut = self._prefetched.pop(Path(path), None)
+        if fut is not None:
+            fut.add_done_callback(lambda f: f.exception() is None and self.release(f.result()))
 
-    def unpack_into(self, records: np.ndarray, stride: int, offset: int) -> None:
-        n = int(records.shape[0])
-        if n == 0:
-            return
-        nbytes = n * stride
-        dev, pin = self._staging(nbytes)
+    def _stage_slot(self, nbytes: int):
+        """A device staging buffer whose previous unpack has completed."""
         torch = self.torch
-        pin[:nbytes].numpy()[:] = records.view(np.uint8).reshape(-1)[:nbytes]
+        slot = self._slots[self._slot_i]
+        self._slot_i = (self._slot_i + 1) % len(self._slots)
+        if slot["event"] is not None:
+            t0 = time.perf_counter()
+            slot["event"].synchronize()
+            self.stats["stage_wait_s"] += time.perf_counter() - t0
+        if slot["buf"] is None or slot["buf"].numel() < nbytes:
+            slot["buf"] = torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, device=self.slab.device)
+        return slot
+
+    def unpack_into(self, src, records: np.ndarray | None, n: int, stride: int, offset: int) -> None:
+        """Chunk records -> slab rows [offset, offset + n) (K8)."""
+        if n == 0:
+            self.release(src)
+            return
+        torch = self.torch
+        nbytes = n * stride
+        s = self.slab
+        rows = slice(offset, offset + n)
         cur = torch.cuda.current_stream(self.slab.device)
-        self.copy_stream.wait_stream(cur)   # slab rows may still be in use by queued work
-        with torch.cuda.stream(self.copy_stream):
-            dev[:nbytes].copy_(pin[:nbytes], non_blocking=True)
-            s = self.slab
-            rows = slice(offset, offset + n)
-            rc = self.lib.sm_chunk_unpack(_lib.ptr(dev), n, int(stride), _lib.ptr(s.params[rows]),
-                                          _lib.ptr(s.sh_rest[rows]), _lib.ptr(s.adam_m[rows]),
-                                          _lib.ptr(s.adam_v[rows]), _lib.ptr(self._err),
-                                          _lib.stream_handle(self.copy_stream))
-            _lib.check(rc, "chunk_unpack")
-            s.grads[offset:offset + n].zero_()
-        cur.wait_stream(self.copy_stream)
+        if isinstance(src, DeviceRecords):   # our own packed bytes, still on the device
+            dev = src.dev
+        else:
+            slot = self._stage_slot(nbytes)
+            dev = slot["buf"]
+            if isinstance(src, PinnedFile):
+                host = src.pin[records.ctypes.data - src.pin.data_ptr():][:nbytes]
+            else:   # plain bytes (API callers): through the pinned staging buffer
+                _, host = self._staging(nbytes)
+                host[:nbytes].numpy()[:] = records.view(np.uint8).reshape(-1)[:nbytes]
+                host = host[:nbytes]
+            with torch.cuda.stream(self.copy_stream):
+                dev[:nbytes].copy_(host, non_blocking=True)
+                rc = self.lib.sm_chunk_unpack(_lib.ptr(dev), n, int(stride), None, None, None, None,
+                                              _lib.ptr(self._err), _lib.stream_handle(self.copy_stream))
+                _lib.check(rc, "chunk_validate")
+                self._err_host.copy_(self._err, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.copy_stream)
+            t0 = time.perf_counter()
+            ev.synchronize()   # H2D + validation only; the render keeps running
+            self.stats["validate_wait_s"] += time.perf_counter() - t0
+            self.release(src)
+            err = int(self._err_host[0])
+            if err >= 0:
+                raise CorruptChunk(f"chunk record {err} fails invariants")
+            cur.wait_event(ev)
+        rc = self.lib.sm_chunk_unpack(_lib.ptr(dev), n, int(stride), _lib.ptr(s.params[rows]),
+                                      _lib.ptr(s.sh_rest[rows]), _lib.ptr(s.adam_m[rows]),
+                                      _lib.ptr(s.adam_v[rows]), _lib.ptr(self._err_unpack),
+                                      _lib.stream_handle(cur))
+        _lib.check(rc, "chunk_unpack")
+        s.grads[offset:offset + n].zero_()
+        if not isinstance(src, DeviceRecords):
+            slot["event"] = torch.cuda.Event()
+            slot["event"].record(cur)
         self.bytes_h2d += nbytes
-        err = int(self._err.item())   # the policy needs the verdict (CorruptChunk)
-        if err >= 0:
-            raise CorruptChunk(f"chunk record {err} fails invariants")
 
     # ------------------------------------------------------------------ evict
     def _pack_to_device(self, offset: int, n: int, stride: int, dev):
@@ -188,10 +330,13 @@ class ChunkStreamer:
             if n:
                 pin[:nbytes].copy_(dev[:nbytes], non_blocking=True)
             ev.record(self.copy_stream)
-        pw = _PendingWrite(Path(path), header, pin, nbytes, ev, dev)
+        pw = _PendingWrite(Path(path), header, pin, nbytes, ev, dev, stride)
         with self._lock:
             self._pending[pw.path] = pw
-            self._prefetched.pop(pw.path, None)
+            self._drop_victim(pw.path)
+            fut = self._prefetched.pop(pw.path, None)
+        if fut is not None:
+            fut.add_done_callback(lambda f: f.exception() is None and self.release(f.result()))
         self.bytes_d2h += nbytes
         self.stats["async_writes"] += 1
         self._queue.put(pw)
@@ -202,20 +347,54 @@ class ChunkStreamer:
             if pw is None:
                 return
             try:
-                data = pw.data()
-                tmp = pw.path.with_suffix(".dcg.tmp")
-                tmp.write_bytes(data)
-                tmp.replace(pw.path)
+                pw.event.synchronize()   # the D2H copy of the packed records
+                tmp = pw.path.with_name(f"{pw.path.name}.{threading.get_ident()}.tmp")
+                with open(tmp, "wb") as f:   # straight from pinned memory, no bytes copy
+                    f.write(pw.header)
+                    f.write(memoryview(pw.pin.numpy())[:pw.nbytes])
+                with self._lock:   # several writers: only the newest write of a path lands
+                    current = self._pending.get(pw.path) is pw
+                    if current:
+                        tmp.replace(pw.path)
+                if not current:
+                    tmp.unlink(missing_ok=True)
             except BaseException as exc:   # surfaced at the next check()/drain()
                 self._writer_error = exc
             finally:
                 with self._lock:
+                    landed = self._pending.get(pw.path) is pw and self._writer_error is None
                     if self._pending.get(pw.path) is pw:
                         del self._pending[pw.path]
                     self._free_pins.append(pw.pin)
-                    self._free_devs.append(pw.dev)
+                    if landed and self.victim_limit > 0:   # keep the packed bytes in HBM
+                        self._drop_victim(pw.path)
+                        self._victims[pw.path] = DeviceRecords(pw.header, pw.dev, pw.nbytes, pw.stride)
+                        self._victim_bytes += pw.dev.numel()
+                        while self._victim_bytes > self.victim_limit and self._victims:
+                            _, old = self._victims.popitem(last=False)
+                            self._victim_bytes -= old.dev.numel()
+                            self._free_devs.append(old.dev)
+                    else:
+                        self._free_devs.append(pw.dev)
                 pw.done.set()
                 self._queue.task_done()
+
+    def _drop_victim(self, path: Path) -> None:   # caller holds the lock
+        old = self._victims.pop(path, None)
+        if old is not None:
+            self._victim_bytes -= old.dev.numel()
+            self._free_devs.append(old.dev)
+
+    def forget(self, path: Path) -> None:
+        """The store is about to rewrite or delete `path`: let a pending write
+        land first and drop every cached copy of the old bytes."""
+        path = Path(path)
+        self.wait_path(path)
+        with self._lock:
+            self._drop_victim(path)
+            fut = self._prefetched.pop(path, None)
+        if fut is not None:
+            fut.add_done_callback(lambda f: f.exception() is None and self.release(f.result()))
 
     def check(self) -> None:
         if self._writer_error is not None:

@@ -24,11 +24,13 @@ import numpy as np
 
 from .core import SH_C0, CameraIntrinsics, Pose, quat_multiply, quat_normalize
 
-__all__ = ["SceneData", "uniform_scene", "room_scene", "room_poses", "C1_INTR", "C2_INTR",
-           "perturbed"]
+__all__ = ["SceneData", "uniform_scene", "room_scene", "room_poses", "corridor_scene",
+           "corridor_poses", "C1_INTR", "C2_INTR", "C4_INTR", "perturbed"]
 
 C1_INTR = CameraIntrinsics(fx=120.0, fy=120.0, cx=80.0, cy=60.0, width=160, height=120, near=0.05)
 C2_INTR = CameraIntrinsics(fx=525.0, fy=525.0, cx=319.5, cy=239.5, width=640, height=480, near=0.05)
+# KITTI-00
+C4_INTR = CameraIntrinsics(fx=718.856, fy=718.856, cx=607.19, cy=185.22, width=1241, height=376, near=0.05)
 _BASE_Q = quat_normalize(np.array([0.5, -0.5, 0.5, -0.5]))   # cam z -> +x, cam y -> -z
 
 
@@ -134,6 +136,52 @@ def room_poses(k: int, seed: int = 42, size=(8.0, 8.0, 2.0), chunk: float = 1.0,
         # back the camera away from the wall it faces so the frustum sees the room
         fwd = np.array([math.cos(yaw), math.sin(yaw), 0.0])
         poses.append(Pose(rotation=rot, translation=c - 1.2 * fwd))
+    return poses
+
+
+def corridor_scene(n: int, length: float = 200.0, width: float = 40.0, seed: int = 7,
+                   scale_lo=0.02, scale_hi=0.2) -> SceneData:
+    """C4-shaped street corridor along +x (20k splats per metre,
+    s = 10 m chunks, 4 chunks across): road surface, two building facades,
+    and boxes (parked cars / street furniture) along the kerbs."""
+    rng = np.random.default_rng(seed)
+    half = width / 2.0 - 0.05
+    n_road, n_wall = int(n * 0.35), int(n * 0.4)
+    n_box = n - n_road - n_wall
+    road = np.stack([rng.uniform(0.05, length - 0.05, n_road), rng.uniform(-half, half, n_road),
+                     np.full(n_road, -1.6) + rng.normal(scale=0.01, size=n_road)], 1)
+    side = rng.integers(0, 2, n_wall)
+    wall = np.stack([rng.uniform(0.05, length - 0.05, n_wall),
+                     np.where(side == 0, -12.0, 12.0) + rng.normal(scale=0.05, size=n_wall),
+                     rng.uniform(-1.6, 4.9, n_wall)], 1)
+    nb = max(1, int(length / 4))
+    bx = rng.uniform(0.5, length - 0.5, nb)
+    by = np.where(rng.integers(0, 2, nb) == 0, -6.0, 6.0) + rng.uniform(-1.0, 1.0, nb)
+    bsz = rng.uniform([1.5, 0.8, 0.8], [4.5, 2.0, 1.8], size=(nb, 3))
+    which = rng.integers(0, nb, n_box)
+    cmin = np.stack([bx[which] - bsz[which, 0] / 2, by[which] - bsz[which, 1] / 2, np.full(n_box, -1.6)], 1)
+    cp = cmin + rng.uniform(size=(n_box, 3)) * bsz[which]
+    face = rng.integers(0, 5, n_box)
+    axis = np.array([0, 0, 1, 1, 2])[face]
+    top = np.array([0, 1, 0, 1, 1])[face]
+    rows = np.arange(n_box)
+    cp[rows, axis] = cmin[rows, axis] + top * bsz[which][rows, axis]
+    pos = np.concatenate([road, wall, cp], 0)
+    pos = np.clip(pos, [0.01, -half, -4.9], [length - 0.01, half, 4.9])
+    pos = pos[rng.permutation(n)]
+    q, sc, o, sh = _attributes(rng, n, scale_lo, scale_hi)
+    return SceneData(_c(pos), q, sc, o, sh)
+
+
+def corridor_poses(k: int, spacing: float = 2.0, seed: int = 7) -> list[Pose]:
+    """A car driving along +x at 1.5 m above the road, slight lateral wander."""
+    rng = np.random.default_rng(seed + 1)
+    poses = []
+    for i in range(k):
+        yaw = rng.uniform(-0.05, 0.05)
+        qz = np.array([math.cos(yaw / 2), 0.0, 0.0, math.sin(yaw / 2)])
+        rot = quat_normalize(quat_multiply(qz, _BASE_Q))
+        poses.append(Pose(rotation=rot, translation=np.array([1.0 + i * spacing, rng.uniform(-1.0, 1.0), 0.0])))
     return poses
 
 

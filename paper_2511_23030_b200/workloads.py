@@ -19,7 +19,8 @@ from .culling import CullConfig
 from .mapping import MappingEngine
 from .renderloss import SceneArrays, default_engine, pack_params, render_device
 from .store import ChunkStore, StoreConfig
-from .synthetic import C1_INTR, C2_INTR, SceneData, perturbed, room_poses, room_scene, uniform_scene
+from .synthetic import (C1_INTR, C2_INTR, C4_INTR, SceneData, corridor_poses, corridor_scene, perturbed,
+                        room_poses, room_scene, uniform_scene)
 
 
 def _gt_frames(target: SceneData, poses, intr, device):
@@ -72,3 +73,13 @@ def c1_poses(k: int = 10):
 def build_c1(n: int = 20_000, keyframes: int = 10, budget: int = 12_000, store_dir=None,
              device=None) -> MappingEngine:
     return build_engine(c1_scene(n), c1_poses(keyframes), C1_INTR, 10.0, budget, store_dir, device)
+
+
+def build_c4lite(n: int = 4_000_000, length: float = 200.0, keyframes: int = 100, budget: int = 1_500_000,
+                 store_dir=None, device=None, max_distance: float = 50.0) -> MappingEngine:
+    """Out-of-core C4 shape at 1/5 length: a street corridor
+    with C4's density (20k splats/m, s = 10 m, 4 chunks across), KITTI
+    intrinsics, a 1.5M-splat HBM budget, keyframes every 2 m."""
+    scene = corridor_scene(n, length=length, seed=7)
+    return build_engine(scene, corridor_poses(keyframes, spacing=length / keyframes), C4_INTR, 10.0, budget,
+                        store_dir, device, max_distance=max_distance)
