@@ -76,7 +76,8 @@ class ChunkStreamer:
         self.torch = torch
         self.slab = slab
         self.lib = _lib.load()
-        self.copy_stream = torch.cuda.Stream(device=slab.device)
+        self.copy_stream = torch.cuda.Stream(device=slab.device)   # H2D + validation of loads
+        self.d2h_stream = torch.cuda.Stream(device=slab.device)    # write-behind D2H (own copy engine)
         self._dev = torch.empty(0, dtype=torch.uint8, device=slab.device)
         self._pin = torch.empty(0, dtype=torch.uint8, pin_memory=True)
         self._err = torch.empty(1, dtype=torch.int64, device=slab.device)
@@ -324,12 +325,12 @@ class ChunkStreamer:
         if n:
             self._pack_to_device(offset, n, stride, dev)
         cur = torch.cuda.current_stream(self.slab.device)
-        self.copy_stream.wait_stream(cur)
+        self.d2h_stream.wait_stream(cur)
         ev = torch.cuda.Event()
-        with torch.cuda.stream(self.copy_stream):
+        with torch.cuda.stream(self.d2h_stream):
             if n:
                 pin[:nbytes].copy_(dev[:nbytes], non_blocking=True)
-            ev.record(self.copy_stream)
+            ev.record(self.d2h_stream)
         pw = _PendingWrite(Path(path), header, pin, nbytes, ev, dev, stride)
         with self._lock:
             self._pending[pw.path] = pw
