@@ -37,8 +37,12 @@ adam_quarter_kernel(float4 *__restrict__ params, float4 *__restrict__ m, float4 
     }
     // per-Gaussian step count lives in m quarter 3, component z
     const float step = __shfl_sync(0xffffffffu, mm.z, (threadIdx.x & 31) | 3) + 1.f;
-    const float bc1 = 1.f - powf(c.b1, step);
-    const float bc2s = sqrtf(1.f - powf(c.b2, step));
+    // bias corrections with IEEE powf (1 - 0.999^t cancels: keep them exact),
+    // once per splat; per element one approximate sqrt and reciprocal instead
+    // of IEEE div / sqrt (the kernel was issue-bound), relative error ~3e-7 of
+    // the update (oracle tolerance 1e-6 (1 + |p|))
+    const float ibc1 = 1.f / (1.f - powf(c.b1, step));
+    const float ibc2s = 1.f / sqrtf(1.f - powf(c.b2, step));   // 1 / sqrt(bc2)
     float pv[4] = {p.x, p.y, p.z, p.w}, gv[4] = {g.x, g.y, g.z, g.w};
     float mv[4] = {mm.x, mm.y, mm.z, mm.w}, vvv[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
@@ -47,7 +51,7 @@ adam_quarter_kernel(float4 *__restrict__ params, float4 *__restrict__ m, float4 
         if (idx < 14) {
             mv[k] = c.b1 * mv[k] + (1.f - c.b1) * gv[k];
             vvv[k] = c.b2 * vvv[k] + (1.f - c.b2) * gv[k] * gv[k];
-            pv[k] -= (c.lr[idx] / bc1) * mv[k] / (sqrtf(vvv[k]) / bc2s + c.eps);
+            pv[k] -= (c.lr[idx] * ibc1) * mv[k] * rcp_approx(sqrt_approx(vvv[k]) * ibc2s + c.eps);
         }
     }
     if (q == 3) mv[2] = step;
@@ -71,55 +75,6 @@ adam_quarter_kernel(float4 *__restrict__ params, float4 *__restrict__ m, float4 
     m[s * 4 + q] = make_float4(mv[0], mv[1], mv[2], mv[3]);
     v[s * 4 + q] = make_float4(vvv[0], vvv[1], vvv[2], vvv[3]);
     grads[s * 4 + q] = make_float4(0.f, 0.f, 0.f, 0.f);
-}
-
-__global__ void __launch_bounds__(256)
-adam_kernel(float4 *__restrict__ params, float4 *__restrict__ m, float4 *__restrict__ v,
-            float4 *__restrict__ grads, const int32_t *__restrict__ slots, int64_t n, AdamDev c,
-            const uint32_t *__restrict__ skip) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    if (skip && *skip) return;
-    const int64_t s = slots ? (int64_t)slots[i] : i;
-    float p[16], g[16], mm[16], vv[16];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const float4 a = params[s * 4 + k], b = grads[s * 4 + k], cm = m[s * 4 + k], cv = v[s * 4 + k];
-        p[4 * k] = a.x, p[4 * k + 1] = a.y, p[4 * k + 2] = a.z, p[4 * k + 3] = a.w;
-        g[4 * k] = b.x, g[4 * k + 1] = b.y, g[4 * k + 2] = b.z, g[4 * k + 3] = b.w;
-        mm[4 * k] = cm.x, mm[4 * k + 1] = cm.y, mm[4 * k + 2] = cm.z, mm[4 * k + 3] = cm.w;
-        vv[4 * k] = cv.x, vv[4 * k + 1] = cv.y, vv[4 * k + 2] = cv.z, vv[4 * k + 3] = cv.w;
-    }
-    const float step = mm[14] + 1.f;   // per-Gaussian step count
-    mm[14] = step;
-    const float bc1 = 1.f - powf(c.b1, step);
-    const float bc2s = sqrtf(1.f - powf(c.b2, step));
-#pragma unroll
-    for (int k = 0; k < 14; k++) {
-        mm[k] = c.b1 * mm[k] + (1.f - c.b1) * g[k];
-        vv[k] = c.b2 * vv[k] + (1.f - c.b2) * g[k] * g[k];
-        p[k] -= (c.lr[k] / bc1) * mm[k] / (sqrtf(vv[k]) / bc2s + c.eps);
-    }
-    // store invariants (core.py:186-190): unit quaternion, scale > 0, opacity in [0,1]
-    const float qn = sqrtf(p[3] * p[3] + p[4] * p[4] + p[5] * p[5] + p[6] * p[6]);
-    if (qn > 0.f) {
-        const float inv = 1.f / qn;
-        p[3] *= inv, p[4] *= inv, p[5] *= inv, p[6] *= inv;
-    } else {
-        p[3] = 1.f, p[4] = p[5] = p[6] = 0.f;
-    }
-    p[7] = fmaxf(p[7], c.min_scale);
-    p[8] = fmaxf(p[8], c.min_scale);
-    p[9] = fmaxf(p[9], c.min_scale);
-    p[10] = fminf(fmaxf(p[10], 0.f), 1.f);
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        params[s * 4 + k] = make_float4(p[4 * k], p[4 * k + 1], p[4 * k + 2], p[4 * k + 3]);
-        m[s * 4 + k] = make_float4(mm[4 * k], mm[4 * k + 1], mm[4 * k + 2], mm[4 * k + 3]);
-        v[s * 4 + k] = make_float4(vv[4 * k], vv[4 * k + 1], vv[4 * k + 2], vv[4 * k + 3]);
-        grads[s * 4 + k] = z;
-    }
 }
 
 int adam_step(float *params, float *m, float *v, float *grads, const int32_t *slots, int64_t n,
