@@ -10,99 +10,124 @@
 // the value or the gradient.  gt rgb arrives as the keyframe's 8-bit values
 // (core.py:262-267 keeps k/255 in float32; u8 / 255.f reproduces it exactly).
 //
-// Kernel A (per 16x16 tile and channel, separable filter in shared memory):
-// S and dS/d{mu_x, E[x^2], E[xy]} on the crop, plus L1 / depth partial sums.
-// Kernel B: adjoint filter of those three maps and the final per-pixel grads.
+// Kernel A (per 32x16 tile and channel): separable 11-tap filter of
+// x, y, x^2, y^2, xy in shared memory, register-blocked (a thread produces 4
+// horizontal or 2 vertical outputs from one window load, ~5x fewer shared
+// loads than one output per thread); S and dS/d{mu_x, E[x^2], E[xy]} on the
+// crop, L1 / depth partial sums; the last block sums the partials in a fixed
+// order (deterministic) and finalises the loss.
+// Kernel B: the adjoint filter of those three maps (same blocking) and the
+// per-pixel gradients; the depth gradient reads the finished valid count.
 #include "common.cuh"
 #include "prof.cuh"
 
 namespace sm {
 
-constexpr int kLT = 16;            // output tile
-constexpr int kLH = kLT + 10;      // tile + halo
+constexpr int kLW = 32, kLH = 16;   // output tile (columns x rows)
+constexpr int kHW = kLW + 10, kHH = kLH + 10;   // + 5-px halo each side
 __constant__ float c_gw[11];
 
 struct LossAcc {
     double l1, ssim, dsum, dcount;
-    float out[4];
+    uint32_t done;   // blocks of kernel A finished (the last one finalises)
 };
+
+__device__ __forceinline__ float load_gt(const uint8_t *gt, const float *gtf, int64_t i) {
+    return gt ? (float)gt[i] / 255.f : gtf[i];
+}
 
 __global__ void __launch_bounds__(256)
 loss_fwd_kernel(const float *__restrict__ rgb, const float *__restrict__ depth,
                 const uint8_t *__restrict__ gt, const float *__restrict__ gtf,
-                const float *__restrict__ gt_depth, int W, int H, int C,
-                float *__restrict__ dmaps /* [C][3 maps][H*W] */, double *__restrict__ partial,
-                int want_grad) {
-    __shared__ float sx[kLH][kLH], sy[kLH][kLH];
-    __shared__ float hs[5][kLH][kLT];
+                const float *__restrict__ gt_depth, int W, int H, int C, float ls, float ld,
+                float *__restrict__ dmaps /* [C][3][H*W] */, double *__restrict__ partial,
+                LossAcc *acc, float *__restrict__ out, int want_grad) {
+    __shared__ float sx[kHH][kHW], sy[kHH][kHW];
+    __shared__ float hs[5][kHH][kLW];
     __shared__ float red[4][8];
+    __shared__ bool s_last;
     const int ch = blockIdx.z;
-    const int tx0 = blockIdx.x * kLT, ty0 = blockIdx.y * kLT;
+    const int tx0 = blockIdx.x * kLW, ty0 = blockIdx.y * kLH;
     const int64_t N = (int64_t)W * H;
-    for (int i = threadIdx.x; i < kLH * kLH; i += 256) {
-        const int yy = ty0 - 5 + i / kLH, xx = tx0 - 5 + i % kLH;
+    for (int i = threadIdx.x; i < kHH * kHW; i += 256) {
+        const int yy = ty0 - 5 + i / kHW, xx = tx0 - 5 + i % kHW;
         float xv = 0.f, yv = 0.f;
         if (yy >= 0 && yy < H && xx >= 0 && xx < W) {
             const int64_t p = (int64_t)yy * W + xx;
             xv = rgb[C * p + ch];
-            yv = gt ? (float)gt[C * p + ch] / 255.f : gtf[C * p + ch];
+            yv = load_gt(gt, gtf, C * p + ch);
         }
-        sx[i / kLH][i % kLH] = xv;
-        sy[i / kLH][i % kLH] = yv;
+        sx[i / kHW][i % kHW] = xv;
+        sy[i / kHW][i % kHW] = yv;
     }
     __syncthreads();
-    // horizontal pass: rows of the haloed tile, 16 output columns
-    for (int i = threadIdx.x; i < kLH * kLT; i += 256) {
-        const int r = i / kLT, c = i % kLT;
-        float a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+    // horizontal: 26 rows x 32 centres, 4 consecutive centres per thread
+    for (int it = threadIdx.x; it < kHH * (kLW / 4); it += 256) {
+        const int r = it / (kLW / 4), c0 = 4 * (it % (kLW / 4));
+        float a[5][4];
 #pragma unroll
-        for (int k = 0; k < 11; k++) {
-            const float w = c_gw[k], xv = sx[r][c + k], yv = sy[r][c + k];
-            a0 += w * xv;
-            a1 += w * yv;
-            a2 += w * xv * xv;
-            a3 += w * yv * yv;
-            a4 += w * xv * yv;
+        for (int t = 0; t < 5; t++)
+#pragma unroll
+            for (int o = 0; o < 4; o++) a[t][o] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 14; k++) {
+            const float xv = sx[r][c0 + k], yv = sy[r][c0 + k];
+            const float v[5] = {xv, yv, xv * xv, yv * yv, xv * yv};
+#pragma unroll
+            for (int o = 0; o < 4; o++) {
+                if (k - o >= 0 && k - o < 11) {
+                    const float w = c_gw[k - o];
+#pragma unroll
+                    for (int t = 0; t < 5; t++) a[t][o] += w * v[t];
+                }
+            }
         }
-        hs[0][r][c] = a0;
-        hs[1][r][c] = a1;
-        hs[2][r][c] = a2;
-        hs[3][r][c] = a3;
-        hs[4][r][c] = a4;
+#pragma unroll
+        for (int t = 0; t < 5; t++)
+#pragma unroll
+            for (int o = 0; o < 4; o++) hs[t][r][c0 + o] = a[t][o];
     }
     __syncthreads();
-    const int lx = threadIdx.x % kLT, ly = threadIdx.x / kLT;
-    const int x = tx0 + lx, y = ty0 + ly;
+    // vertical: 16 x 32 outputs, 2 rows per thread
+    const int lx = threadIdx.x % kLW, ly0 = 2 * (threadIdx.x / kLW);
+    float m[2][5];
+#pragma unroll
+    for (int o = 0; o < 2; o++)
+#pragma unroll
+        for (int t = 0; t < 5; t++) m[o][t] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 12; k++) {
+#pragma unroll
+        for (int t = 0; t < 5; t++) {
+            const float h = hs[t][ly0 + k][lx];
+            if (k < 11) m[0][t] += c_gw[k] * h;
+            if (k >= 1) m[1][t] += c_gw[k - 1] * h;
+        }
+    }
     float s_val = 0.f, l1 = 0.f, dsum = 0.f, dcnt = 0.f;
-    if (x < W && y < H) {
+#pragma unroll
+    for (int o = 0; o < 2; o++) {
+        const int x = tx0 + lx, y = ty0 + ly0 + o;
+        if (x >= W || y >= H) continue;
         const int64_t p = (int64_t)y * W + x;
-        l1 = fabsf(sx[ly + 5][lx + 5] - sy[ly + 5][lx + 5]);
+        l1 += fabsf(sx[ly0 + o + 5][lx + 5] - sy[ly0 + o + 5][lx + 5]);
         if (ch == 0 && gt_depth && depth && gt_depth[p] > 0.f) {
-            dsum = fabsf(depth[p] - gt_depth[p]);
-            dcnt = 1.f;
+            dsum += fabsf(depth[p] - gt_depth[p]);
+            dcnt += 1.f;
         }
         float dmu = 0.f, dxx = 0.f, dxy = 0.f;
         if (x >= 5 && x < W - 5 && y >= 5 && y < H - 5) {
-            float m[5] = {0, 0, 0, 0, 0};
-#pragma unroll
-            for (int k = 0; k < 11; k++) {
-                const float w = c_gw[k];
-#pragma unroll
-                for (int t = 0; t < 5; t++) m[t] += w * hs[t][ly + k][lx];
-            }
             const float C1 = 1e-4f, C2 = 9e-4f;
-            const float mx = m[0], my = m[1];
-            const float vx = m[2] - mx * mx, vy = m[3] - my * my, vxy = m[4] - mx * my;
+            const float mx = m[o][0], my = m[o][1];
+            const float vx = m[o][2] - mx * mx, vy = m[o][3] - my * my, vxy = m[o][4] - mx * my;
             const float A1 = 2.f * mx * my + C1, A2 = 2.f * vxy + C2;
             const float B1 = mx * mx + my * my + C1, B2 = vx + vy + C2;
             const float inv = 1.f / (B1 * B2);
             const float S = A1 * A2 * inv;
-            s_val = S;
-            if (want_grad) {
-                dmu = (2.f * my * A2 - 2.f * my * A1) * inv - S * (2.f * mx / B1 - 2.f * mx / B2);
-                dxx = -S / B2;
-                dxy = 2.f * A1 * inv;
-            }
+            s_val += S;
+            dmu = (2.f * my * A2 - 2.f * my * A1) * inv - S * (2.f * mx / B1 - 2.f * mx / B2);
+            dxx = -S / B2;
+            dxy = 2.f * A1 * inv;
         }
         if (want_grad) {
             dmaps[(int64_t)(ch * 3 + 0) * N + p] = dmu;
@@ -110,7 +135,7 @@ loss_fwd_kernel(const float *__restrict__ rgb, const float *__restrict__ depth,
             dmaps[(int64_t)(ch * 3 + 2) * N + p] = dxy;
         }
     }
-    // block reduction of the four partial sums
+    // block partials, then the last block sums every block's in a fixed order
     float v[4] = {s_val, l1, dsum, dcnt};
 #pragma unroll
     for (int t = 0; t < 4; t++)
@@ -120,46 +145,45 @@ loss_fwd_kernel(const float *__restrict__ rgb, const float *__restrict__ depth,
 #pragma unroll
         for (int t = 0; t < 4; t++) red[t][threadIdx.x >> 5] = v[t];
     __syncthreads();
-    if (threadIdx.x < 4) {   // per-block partials, summed in a fixed order by loss_finalize
-        double s = 0;
-        for (int w = 0; w < 8; w++) s += red[threadIdx.x][w];
+    const uint32_t nblk = gridDim.x * gridDim.y * gridDim.z;
+    if (threadIdx.x < 4) {
+        double sacc = 0;
+        for (int w = 0; w < 8; w++) sacc += red[threadIdx.x][w];
         const int64_t blk = ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-        partial[blk * 4 + threadIdx.x] = s;
+        partial[blk * 4 + threadIdx.x] = sacc;
+        __threadfence();
     }
-}
-
-// Deterministic (fixed-order) reduction of the per-block partials, then the
-// loss terms.  One block of 256 threads.
-__global__ void __launch_bounds__(256)
-loss_finalize(const double *__restrict__ partial, int64_t nblk, LossAcc *acc, int W, int H, int C,
-              float ls, float ld, float *out) {
-    __shared__ double sh[4][256];
-    double s[4] = {0, 0, 0, 0};
-    for (int64_t b = threadIdx.x; b < nblk; b += 256)
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&acc->done, 1u) == nblk - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double *sh = reinterpret_cast<double *>(&hs[0][0][0]);   // [4][256], reused
+    double s4[4] = {0, 0, 0, 0};
+    for (uint32_t b = threadIdx.x; b < nblk; b += 256)
 #pragma unroll
-        for (int t = 0; t < 4; t++) s[t] += partial[b * 4 + t];
+        for (int t = 0; t < 4; t++) s4[t] += __ldcg(&partial[(int64_t)b * 4 + t]);
 #pragma unroll
-    for (int t = 0; t < 4; t++) sh[t][threadIdx.x] = s[t];
+    for (int t = 0; t < 4; t++) sh[t * 256 + threadIdx.x] = s4[t];
     __syncthreads();
     for (int o = 128; o; o >>= 1) {
         if ((int)threadIdx.x < o)
 #pragma unroll
-            for (int t = 0; t < 4; t++) sh[t][threadIdx.x] += sh[t][threadIdx.x + o];
+            for (int t = 0; t < 4; t++) sh[t * 256 + threadIdx.x] += sh[t * 256 + threadIdx.x + o];
         __syncthreads();
     }
     if (threadIdx.x) return;
-    acc->ssim = sh[0][0];
-    acc->l1 = sh[1][0];
-    acc->dsum = sh[2][0];
-    acc->dcount = sh[3][0];
-    const double N = (double)W * H;
+    acc->ssim = sh[0];
+    acc->l1 = sh[256];
+    acc->dsum = sh[512];
+    acc->dcount = sh[768];
+    const double Np = (double)W * H;
     const double Nc = (double)(W - 10) * (H - 10);
-    const double l1 = acc->l1 / ((double)C * N);
-    const double ssim = acc->ssim / ((double)C * Nc);
-    const double dl = acc->dcount > 0 ? acc->dsum / acc->dcount : 0.0;
-    const double total = (1.0 - ls) * l1 + ls * (1.0 - ssim) + ld * dl;
-    out[0] = (float)total;
-    out[1] = (float)l1;
+    const double l1v = sh[256] / ((double)C * Np);
+    const double ssim = sh[0] / ((double)C * Nc);
+    const double dl = sh[768] > 0 ? sh[512] / sh[768] : 0.0;
+    out[0] = (float)((1.0 - ls) * l1v + ls * (1.0 - ssim) + ld * dl);
+    out[1] = (float)l1v;
     out[2] = (float)ssim;
     out[3] = (float)dl;
 }
@@ -170,64 +194,89 @@ loss_bwd_kernel(const float *__restrict__ rgb, const float *__restrict__ depth,
                 const float *__restrict__ gt_depth, int W, int H, int C,
                 const float *__restrict__ dmaps, const LossAcc *acc, float ls, float ld,
                 float *__restrict__ d_rgb, float *__restrict__ d_depth) {
-    __shared__ float sm3[3][kLH][kLH];
-    __shared__ float hs[3][kLH][kLT];
+    __shared__ float sm3[3][kHH][kHW];
+    __shared__ float ha[3][kHH][kLW];
     const int ch = blockIdx.z;
-    const int tx0 = blockIdx.x * kLT, ty0 = blockIdx.y * kLT;
+    const int tx0 = blockIdx.x * kLW, ty0 = blockIdx.y * kLH;
     const int64_t N = (int64_t)W * H;
-    for (int i = threadIdx.x; i < kLH * kLH; i += 256) {
-        const int yy = ty0 - 5 + i / kLH, xx = tx0 - 5 + i % kLH;
+    for (int i = threadIdx.x; i < kHH * kHW; i += 256) {
+        const int yy = ty0 - 5 + i / kHW, xx = tx0 - 5 + i % kHW;
         const bool ok = yy >= 0 && yy < H && xx >= 0 && xx < W;
         const int64_t p = (int64_t)yy * W + xx;
 #pragma unroll
-        for (int t = 0; t < 3; t++) sm3[t][i / kLH][i % kLH] = ok ? dmaps[(int64_t)(ch * 3 + t) * N + p] : 0.f;
+        for (int t = 0; t < 3; t++) sm3[t][i / kHW][i % kHW] = ok ? dmaps[(int64_t)(ch * 3 + t) * N + p] : 0.f;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < kLH * kLT; i += 256) {
-        const int r = i / kLT, c = i % kLT;
-        float a[3] = {0, 0, 0};
+    for (int it = threadIdx.x; it < kHH * (kLW / 4); it += 256) {   // adjoint, horizontal
+        const int r = it / (kLW / 4), c0 = 4 * (it % (kLW / 4));
+        float a[3][4];
 #pragma unroll
-        for (int k = 0; k < 11; k++) {
-            const float w = c_gw[k];   // symmetric kernel: adjoint = same taps
+        for (int t = 0; t < 3; t++)
 #pragma unroll
-            for (int t = 0; t < 3; t++) a[t] += w * sm3[t][r][c + k];
+            for (int o = 0; o < 4; o++) a[t][o] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 14; k++) {
+            float v[3];
+#pragma unroll
+            for (int t = 0; t < 3; t++) v[t] = sm3[t][r][c0 + k];
+#pragma unroll
+            for (int o = 0; o < 4; o++) {
+                if (k - o >= 0 && k - o < 11) {
+                    const float w = c_gw[k - o];   // symmetric kernel: adjoint = same taps
+#pragma unroll
+                    for (int t = 0; t < 3; t++) a[t][o] += w * v[t];
+                }
+            }
         }
 #pragma unroll
-        for (int t = 0; t < 3; t++) hs[t][r][c] = a[t];
+        for (int t = 0; t < 3; t++)
+#pragma unroll
+            for (int o = 0; o < 4; o++) ha[t][r][c0 + o] = a[t][o];
     }
     __syncthreads();
-    const int lx = threadIdx.x % kLT, ly = threadIdx.x / kLT;
-    const int x = tx0 + lx, y = ty0 + ly;
-    if (x >= W || y >= H) return;
-    float a[3] = {0, 0, 0};
+    const int lx = threadIdx.x % kLW, ly0 = 2 * (threadIdx.x / kLW);
+    float a[2][3];
 #pragma unroll
-    for (int k = 0; k < 11; k++) {
-        const float w = c_gw[k];
+    for (int o = 0; o < 2; o++)
 #pragma unroll
-        for (int t = 0; t < 3; t++) a[t] += w * hs[t][ly + k][lx];
+        for (int t = 0; t < 3; t++) a[o][t] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 12; k++) {
+#pragma unroll
+        for (int t = 0; t < 3; t++) {
+            const float h = ha[t][ly0 + k][lx];
+            if (k < 11) a[0][t] += c_gw[k] * h;
+            if (k >= 1) a[1][t] += c_gw[k - 1] * h;
+        }
     }
-    const int64_t p = (int64_t)y * W + x;
-    const float xv = rgb[C * p + ch];
-    const float yv = gt ? (float)gt[C * p + ch] / 255.f : gtf[C * p + ch];
+    const float Nf = (float)((double)W * H);
     const float Nc = (float)((double)(W - 10) * (H - 10));
-    const float dssim = (a[0] + 2.f * xv * a[1] + yv * a[2]) / Nc;
-    const float diff = xv - yv;
-    const float sg = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
-    d_rgb[C * p + ch] = (1.f - ls) * sg / (float)((double)C * N) - ls * dssim / (float)C;
-    if (ch == 0 && d_depth) {
-        float g = 0.f;
-        const double nv = acc->dcount;
-        if (nv > 0 && gt_depth && depth && gt_depth[p] > 0.f) {
-            const float dd = depth[p] - gt_depth[p];
-            g = ld * (dd > 0.f ? 1.f : (dd < 0.f ? -1.f : 0.f)) / (float)nv;
+    const double nv = acc->dcount;
+#pragma unroll
+    for (int o = 0; o < 2; o++) {
+        const int x = tx0 + lx, y = ty0 + ly0 + o;
+        if (x >= W || y >= H) continue;
+        const int64_t p = (int64_t)y * W + x;
+        const float xv = rgb[C * p + ch];
+        const float yv = load_gt(gt, gtf, C * p + ch);
+        const float dssim = (a[o][0] + 2.f * xv * a[o][1] + yv * a[o][2]) / Nc;
+        const float diff = xv - yv;
+        const float sg = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
+        d_rgb[C * p + ch] = (1.f - ls) * sg / (float)((double)C * Nf) - ls * dssim / (float)C;
+        if (ch == 0 && d_depth) {
+            float g = 0.f;
+            if (nv > 0 && gt_depth && depth && gt_depth[p] > 0.f) {
+                const float dd = depth[p] - gt_depth[p];
+                g = ld * (dd > 0.f ? 1.f : (dd < 0.f ? -1.f : 0.f)) / (float)nv;
+            }
+            d_depth[p] = g;
         }
-        d_depth[p] = g;
     }
 }
 
 static bool g_weights_set = false;
 
-static int64_t loss_blocks(int W, int H) { return ceil_div(W, kLT) * ceil_div(H, kLT) * 4; }
+static int64_t loss_blocks(int W, int H) { return ceil_div(W, kLW) * ceil_div(H, kLH) * 4; }
 
 int64_t loss_workspace_size(int W, int H) {
     return align_up(sizeof(LossAcc), 256) + align_up(loss_blocks(W, H) * 4 * 8, 256) +
@@ -267,18 +316,17 @@ int loss_forward_backward(const float *rgb, const float *depth, const uint8_t *g
     double *partial = reinterpret_cast<double *>(base + align_up(sizeof(LossAcc), 256));
     float *dmaps = reinterpret_cast<float *>(base + align_up(sizeof(LossAcc), 256) +
                                              align_up(loss_blocks(W, H) * 4 * 8, 256));
-    dim3 grid((unsigned)ceil_div(W, kLT), (unsigned)ceil_div(H, kLT), (unsigned)C);
-    const int64_t nblk = (int64_t)grid.x * grid.y * grid.z;
+    dim3 grid((unsigned)ceil_div(W, kLW), (unsigned)ceil_div(H, kLH), (unsigned)C);
     const int want = d_rgb != nullptr;
     prof_begin(ST_LOSS, st);
-    loss_fwd_kernel<<<grid, 256, 0, st>>>(rgb, depth, gt_rgb, gt_rgbf, gt_depth, W, H, C, dmaps,
-                                          partial, want);
-    loss_finalize<<<1, 256, 0, st>>>(partial, nblk, acc, W, H, C, ls, ld, loss_out);
+    cudaMemsetAsync(&acc->done, 0, sizeof(uint32_t), st);   // block counter (any workspace state)
+    loss_fwd_kernel<<<grid, 256, 0, st>>>(rgb, depth, gt_rgb, gt_rgbf, gt_depth, W, H, C, ls, ld, dmaps,
+                                          partial, acc, loss_out, want);
     if (want)
         loss_bwd_kernel<<<grid, 256, 0, st>>>(rgb, depth, gt_rgb, gt_rgbf, gt_depth, W, H, C, dmaps,
                                               acc, ls, ld, d_rgb, d_depth);
     prof_end(ST_LOSS, st);
-    count_launches(want ? 3 : 2);
+    count_launches(want ? 2 : 1);
     SM_CHECK_LAUNCH("loss_forward_backward");
     return SM_OK;
 }
