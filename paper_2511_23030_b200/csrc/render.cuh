@@ -74,6 +74,7 @@ struct RenderLayout {
     int tiles_x, tiles_y;
     int64_t n_tiles;
     int rank_bits, tile_bits;
+    int key_bytes;   // tile-instance keys: 4 while rank_bits + tile_bits <= 32, else 8
     int depth_passes, tile_passes;
     int64_t sort_blocks;
     int64_t o_counters, o_rec, o_rec_sorted, o_p64, o_dkey0, o_dkey1, o_order0, o_order1;
@@ -90,7 +91,8 @@ struct RenderBufs {
     ProjRec *rec, *rec_sorted;
     Proj64 *p64;
     unsigned long long *dkey0, *dkey1;
-    uint32_t *order0, *order1, *tcount, *tcount_r, *tmask, *tmask_r, *toff, *ikey0, *ikey1, *ranges;
+    uint32_t *order0, *order1, *tcount, *tcount_r, *tmask, *tmask_r, *toff, *ranges;
+    void *ikey0, *ikey1;   // uint32_t or unsigned long long (key_bytes)
     float4 *pix_cd;
     float *pix_t, *pix_tlast;
     int32_t *pix_last;
@@ -116,8 +118,8 @@ inline RenderBufs render_bufs(void *ws, const RenderLayout &L) {
     r.tmask = reinterpret_cast<uint32_t *>(b + L.o_tmask);
     r.tmask_r = reinterpret_cast<uint32_t *>(b + L.o_tmask_r);
     r.toff = reinterpret_cast<uint32_t *>(b + L.o_toff);
-    r.ikey0 = reinterpret_cast<uint32_t *>(b + L.o_ikey0);
-    r.ikey1 = reinterpret_cast<uint32_t *>(b + L.o_ikey1);
+    r.ikey0 = b + L.o_ikey0;
+    r.ikey1 = b + L.o_ikey1;
     r.ranges = reinterpret_cast<uint32_t *>(b + L.o_ranges);
     r.pix_cd = reinterpret_cast<float4 *>(b + L.o_pix_cd);
     r.pix_t = reinterpret_cast<float *>(b + L.o_pix_t);

@@ -176,9 +176,10 @@ constexpr int kBwdThreads = kTilePx / 2;
 #define SM_BWD_MINB 5   // 5 CTAs x 4 warps per SM: measured best (register cap 102)
 #endif
 
+template <typename KeyT>
 __global__ void __launch_bounds__(kBwdThreads, SM_BWD_MINB)
-composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ikeys,
-              uint32_t rank_mask, const ProjRec *__restrict__ recs,
+composite_bwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikeys,
+              KeyT rank_mask, const ProjRec *__restrict__ recs,
               const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
               int height, int tiles_x, const float *__restrict__ d_rgb,
               const float *__restrict__ d_depth, const float *__restrict__ d_alpha,
@@ -218,7 +219,7 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
     __syncthreads();
     const int maxlast = s_maxlast;
     if (threadIdx.x == 0) {   // rank of the tile's last visited instance (grad_gather's horizon)
-        tile_hor[tile] = maxlast >= start ? (int32_t)(ikeys[maxlast] & rank_mask) : -1;
+        tile_hor[tile] = maxlast >= start ? (int32_t)(uint32_t)(ikeys[maxlast] & rank_mask) : -1;
         if (maxlast >= start) atomicAdd(&ctr->reserved[2], (uint32_t)(maxlast - start + 1));
     }
     const int via = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);   // 0..7
@@ -228,7 +229,7 @@ composite_bwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
         const int bstart = max(start, bend - NT);
         const int idx = bstart + (int)threadIdx.x;
         if (idx < bend) {
-            const uint32_t rk = ikeys[idx] & rank_mask;
+            const uint32_t rk = (uint32_t)(ikeys[idx] & rank_mask);
             s_rank[threadIdx.x] = rk;
             s_rec[threadIdx.x] = recs[rk];
         }
@@ -520,6 +521,18 @@ project_bwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots
     dst[3] = o3;
 }
 
+template <typename KeyT>
+static void launch_composite_bwd(const RenderBufs &b, const RenderLayout &L, const sm_render_dims &dims,
+                                 const float *d_rgb, const float *d_depth, const float *d_alpha,
+                                 cudaStream_t st) {
+    const KeyT rank_mask = (KeyT)((1ull << L.rank_bits) - 1ull);
+    const KeyT *ik = static_cast<const KeyT *>(L.tile_passes & 1 ? b.ikey1 : b.ikey0);
+    composite_bwd<KeyT><<<(unsigned)L.n_tiles, kBwdThreads, 0, st>>>(
+        b.ranges, ik, rank_mask, b.rec_sorted, b.p64, b.order0, dims.width, dims.height, L.tiles_x, d_rgb,
+        d_depth, d_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, b.toff, b.tmask_r, b.gbuf, b.tile_hor,
+        b.ctr);
+}
+
 int render_backward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,
                     const sm_render_dims &dims, void *ws, int64_t ws_bytes, const float *d_rgb,
                     const float *d_depth, const float *d_alpha, float *grads, cudaStream_t st) {
@@ -538,12 +551,11 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
     }
     if (n == 0) return SM_OK;
     RenderBufs b = render_bufs(ws, L);
-    const uint32_t rank_mask = (uint32_t)((1ull << L.rank_bits) - 1ull);
     prof_begin(ST_COMPOSITE_BWD, st);
-    composite_bwd<<<(unsigned)L.n_tiles, kBwdThreads, 0, st>>>(
-        b.ranges, L.tile_passes & 1 ? b.ikey1 : b.ikey0, rank_mask, b.rec_sorted, b.p64, b.order0,
-        dims.width, dims.height, L.tiles_x, d_rgb, d_depth, d_alpha, b.pix_cd, b.pix_t, b.pix_tlast,
-        b.pix_last, b.toff, b.tmask_r, b.gbuf, b.tile_hor, b.ctr);
+    if (L.key_bytes == 8)
+        launch_composite_bwd<unsigned long long>(b, L, dims, d_rgb, d_depth, d_alpha, st);
+    else
+        launch_composite_bwd<uint32_t>(b, L, dims, d_rgb, d_depth, d_alpha, st);
     prof_end(ST_COMPOSITE_BWD, st);
     prof_begin(ST_GRAD_GATHER, st);
     grad_gather_big<<<148 * 4, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.toff, b.ctr, b.tcount, b.gbuf,

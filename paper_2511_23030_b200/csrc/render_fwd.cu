@@ -35,6 +35,7 @@ RenderLayout render_layout(const sm_render_dims &d) {
     while ((1ll << tb) < L.n_tiles) tb++;
     L.rank_bits = rb;
     L.tile_bits = tb;
+    L.key_bytes = rb + tb > 32 ? 8 : 4;
     L.depth_passes = ceil_div(32, kRadixBits);   // fp32 key + fp64 tie fixup
     L.tile_passes = (int)ceil_div(tb, kRadixBits);
     L.sort_blocks = ceil_div(G > I ? G : I, kSortTile);
@@ -57,8 +58,8 @@ RenderLayout render_layout(const sm_render_dims &d) {
     L.o_tmask = take(G * 4);
     L.o_tmask_r = take(G * 4);
     L.o_toff = take(G * 4);
-    L.o_ikey0 = take(I * 4);
-    L.o_ikey1 = take(I * 4);
+    L.o_ikey0 = take(I * L.key_bytes);
+    L.o_ikey1 = take(I * L.key_bytes);
     L.o_ranges = take(L.n_tiles * 8);
     L.o_pix_cd = take(npx * 16);
     L.o_pix_t = take(npx * 4);
@@ -243,13 +244,14 @@ __global__ void check_instances(sm_render_counters *ctr, int64_t max_instances) 
 // a thread per rank writes splats of <= kEmitSmall tiles directly, larger ones
 // are queued and a warp per queued splat writes its tiles in parallel.
 // Keys are (tile << rank_bits) | rank at the rank's scanned offset, so the
-// array is in rank order whichever thread writes a slot.
-
-
+// array is in rank order whichever thread writes a slot.  KeyT is uint32_t
+// while rank_bits + tile_bits <= 32 (up to 2M visible splats at 2048 tiles),
+// else 64-bit (the sort then reads twice the bytes).
+template <typename KeyT>
 __global__ void __launch_bounds__(256)
 emit_instances(const ProjRec *__restrict__ rec_sorted, const uint32_t *__restrict__ tcount_r,
                const uint32_t *__restrict__ tmask_r, const uint32_t *__restrict__ toff, int64_t n, sm_render_counters *ctr,
-               uint32_t *__restrict__ big, int rank_bits, int tiles_x, uint32_t *__restrict__ ikeys) {
+               uint32_t *__restrict__ big, int rank_bits, int tiles_x, KeyT *__restrict__ ikeys) {
     if (ctr->overflow) return;
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
@@ -266,14 +268,15 @@ emit_instances(const ProjRec *__restrict__ rec_sorted, const uint32_t *__restric
     for (uint32_t m = tmask_r[r]; m; m &= m - 1) {
         const int bit = __ffs(m) - 1;
         const int t = (ty0 + bit / ntx) * tiles_x + tx0 + bit % ntx;
-        ikeys[o++] = ((uint32_t)t << rank_bits) | (uint32_t)r;
+        ikeys[o++] = ((KeyT)t << rank_bits) | (KeyT)r;
     }
 }
 
+template <typename KeyT>
 __global__ void __launch_bounds__(256)
 emit_big(const ProjRec *__restrict__ rec_sorted, const uint32_t *__restrict__ tcount_r,
          const uint32_t *__restrict__ toff, const sm_render_counters *ctr,
-         const uint32_t *__restrict__ big, int rank_bits, int tiles_x, uint32_t *__restrict__ ikeys) {
+         const uint32_t *__restrict__ big, int rank_bits, int tiles_x, KeyT *__restrict__ ikeys) {
     if (ctr->overflow) return;
     __shared__ BigRowTable tab;
     const uint32_t nbig = ctr->reserved[1];
@@ -290,19 +293,20 @@ emit_big(const ProjRec *__restrict__ rec_sorted, const uint32_t *__restrict__ tc
                 const int c0 = tab.c0[i], c1 = tab.c1[i], row = (tyb + i) * tiles_x;
                 const uint32_t dst = o + tab.off[i] - (uint32_t)c0;
                 for (int c = c0 + lane; c <= c1; c += 32)
-                    ikeys[dst + (uint32_t)c] = ((uint32_t)(row + c) << rank_bits) | r;
+                    ikeys[dst + (uint32_t)c] = ((KeyT)(row + c) << rank_bits) | (KeyT)r;
             }
         }
     }
 }
 
+template <typename KeyT>
 __global__ void __launch_bounds__(256)
-tile_ranges(const uint32_t *__restrict__ ikeys, const sm_render_counters *ctr, int rank_bits,
+tile_ranges(const KeyT *__restrict__ ikeys, const sm_render_counters *ctr, int rank_bits,
             uint32_t *__restrict__ ranges) {
     const int64_t n = ctr->reserved[0];
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t t = ikeys[p] >> rank_bits;
+        const uint32_t t = (uint32_t)(ikeys[p] >> rank_bits);
         if (p == 0 || (ikeys[p - 1] >> rank_bits) != t) ranges[2 * t] = (uint32_t)p;
         if (p == n - 1 || (ikeys[p + 1] >> rank_bits) != t) ranges[2 * t + 1] = (uint32_t)(p + 1);
     }
@@ -349,9 +353,10 @@ struct FwdPix {
 // memory; a warp skips a splat whose 3-sigma box misses its 2 rows
 // (warp-uniform), a thread skips it when its column is outside the box, and
 // the block stops once every pixel's transmittance is below 1e-10.
+template <typename KeyT>
 __global__ void __launch_bounds__(kTilePx)
-composite_fwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ikeys,
-              uint32_t rank_mask, const ProjRec *__restrict__ recs,
+composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikeys,
+              KeyT rank_mask, const ProjRec *__restrict__ recs,
               const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
               int height, int tiles_x, float *__restrict__ out_rgb, float *__restrict__ out_depth,
               float *__restrict__ out_alpha, float4 *__restrict__ st_cd, float *__restrict__ st_t,
@@ -372,7 +377,7 @@ composite_fwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
         if (__syncthreads_count(all_done) == NT) break;
         const uint32_t idx = base + threadIdx.x;
         if (idx < end) {
-            const uint32_t rk = ikeys[idx] & rank_mask;
+            const uint32_t rk = (uint32_t)(ikeys[idx] & rank_mask);
             s_rank[threadIdx.x] = rk;
             s_rec[threadIdx.x] = recs[rk];
         }
@@ -402,86 +407,7 @@ composite_fwd(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ 
         s.store((int64_t)py * width + px, out_rgb, out_depth, out_alpha, st_cd, st_t, st_tlast, st_last);
 }
 
-// Pixel-pair variant: 128 threads, each owning (px, py) and (px, py + 1),
-// the pair's arithmetic in packed fp32x2 (.x row py, .y row py + 1).  A pixel
-// the splat does not reach gets alpha = 0: its accumulators and T are left
-// unchanged, so the pair update is branch-free.  Same decisions, same
-// per-pixel expression order as composite_fwd.
-__global__ void __launch_bounds__(kTilePx / 2)
-composite_fwd_pair(const uint32_t *__restrict__ ranges, const uint32_t *__restrict__ ikeys,
-                   uint32_t rank_mask, const ProjRec *__restrict__ recs,
-                   const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
-                   int height, int tiles_x, float *__restrict__ out_rgb, float *__restrict__ out_depth,
-                   float *__restrict__ out_alpha, float4 *__restrict__ st_cd, float *__restrict__ st_t,
-                   float *__restrict__ st_tlast, int32_t *__restrict__ st_last) {
-    constexpr int NT = kTilePx / 2;
-    __shared__ ProjRec s_rec[NT];
-    __shared__ uint32_t s_rank[NT];
-    const int tile = blockIdx.x;
-    const int ty0 = (tile / tiles_x) * kTile;
-    const int px = (tile % tiles_x) * kTile + (threadIdx.x & (kTile - 1));
-    const int py = ty0 + 2 * (threadIdx.x / kTile);
-    const int wy0 = ty0 + 4 * (threadIdx.x / 32);   // warp's first row
-    const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
-    const bool in0 = px < width && py < height, in1 = px < width && py + 1 < height;
-    float2 T = f2s(1.f), cr = f2s(0.f), cg = f2s(0.f), cb = f2s(0.f), cd = f2s(0.f), tlast = f2s(1.f);
-    int32_t last0 = -1, last1 = -1;
-    bool done0 = !in0, done1 = !in1;
-    for (uint32_t base = start; base < end; base += NT) {
-        if (__syncthreads_count(done0 && done1) == NT) break;
-        const uint32_t idx = base + threadIdx.x;
-        if (idx < end) {
-            const uint32_t rk = ikeys[idx] & rank_mask;
-            s_rank[threadIdx.x] = rk;
-            s_rec[threadIdx.x] = recs[rk];
-        }
-        __syncthreads();
-        const int cnt = (int)min((uint32_t)NT, end - base);
-        if (!(done0 && done1)) {
-            for (int j = 0; j < cnt; j++) {
-                const ProjRec &g = s_rec[j];
-                const int y0 = rec_y0(g), y1 = rec_y1(g);
-                if (y1 < wy0 || y0 > wy0 + 3) continue;   // warp-uniform row cull
-                const int x0 = rec_x0(g);
-                if ((unsigned)(px - x0) > (unsigned)(rec_x1(g) - x0)) continue;
-                const float dx = (float)(px - x0) + g.ox;
-                float dy, pw0, pw1;
-                const bool h0 = !done0 && row_eval(g, dx, px, py, y0, y1, p64, order, s_rank[j], dy, pw0);
-                const bool h1 = !done1 && row_eval(g, dx, px, py + 1, y0, y1, p64, order, s_rank[j], dy, pw1);
-                if (!(h0 || h1)) continue;
-                const int32_t k = (int32_t)(base + j);
-                const float2 alpha = mul2(f2s(g.op), make_float2(h0 ? ex2_approx(pw0) : 0.f,
-                                                                 h1 ? ex2_approx(pw1) : 0.f));
-                const float2 w = mul2(T, alpha);
-                cr = fma2(w, f2s(g.r), cr);
-                cg = fma2(w, f2s(g.g), cg);
-                cb = fma2(w, f2s(g.b), cb);
-                cd = fma2(w, f2s(g.z), cd);
-                tlast.x = h0 ? T.x : tlast.x;
-                tlast.y = h1 ? T.y : tlast.y;
-                last0 = h0 ? k : last0;
-                last1 = h1 ? k : last1;
-                T = mul2(T, sub2(f2s(1.f), alpha));
-                done0 = done0 || T.x < (float)SM_MIN_T;   // later pairs would be skipped (renderloss.py:143)
-                done1 = done1 || T.y < (float)SM_MIN_T;
-                if (done0 && done1) break;
-            }
-        }
-        __syncthreads();
-    }
-    FwdPix a{T.x, cr.x, cg.x, cb.x, cd.x, tlast.x, last0, done0};
-    FwdPix b{T.y, cr.y, cg.y, cb.y, cd.y, tlast.y, last1, done1};
-    if (in0) a.store((int64_t)py * width + px, out_rgb, out_depth, out_alpha, st_cd, st_t, st_tlast, st_last);
-    if (in1) b.store((int64_t)(py + 1) * width + px, out_rgb, out_depth, out_alpha, st_cd, st_t, st_tlast,
-                     st_last);
-}
-
 int g_ellipse_cull = 1;   // sm_set_ellipse_cull (tests: culled == unculled, bit for bit)
-
-static int env_int(const char *name, int dflt) {
-    const char *v = getenv(name);
-    return v ? atoi(v) : dflt;
-}
 
 CamDev make_cam(const sm_camera &c, const RenderLayout &L) {
     CamDev d;
@@ -497,6 +423,39 @@ CamDev make_cam(const sm_camera &c, const RenderLayout &L) {
     d.tiles_x = L.tiles_x;
     d.tiles_y = L.tiles_y;
     return d;
+}
+
+// Emission + tile sort + ranges for one key width.
+template <typename KeyT>
+static void bin_tiles(const RenderBufs &b, const RenderLayout &L, const sm_render_dims &dims, int64_t n,
+                      unsigned gb, const SortScratch &ss, cudaStream_t st) {
+    KeyT *k0 = static_cast<KeyT *>(b.ikey0), *k1 = static_cast<KeyT *>(b.ikey1);
+    prof_begin(ST_BIN, st);
+    gather_by_rank<<<gb, 256, 0, st>>>(b.order0, n, b.rec, b.tcount, b.tmask, b.rec_sorted, b.tcount_r,
+                                       b.tmask_r);
+    exclusive_scan(b.tcount_r, b.toff, n, b.scan, &b.ctr->n_instances, st);
+    check_instances<<<1, 1, 0, st>>>(b.ctr, dims.max_instances);
+    // b.tcount (per visible index) is dead after gather_by_rank: reuse it as the big-splat queue
+    emit_instances<KeyT><<<gb, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.tmask_r, b.toff, n, b.ctr, b.tcount,
+                                             L.rank_bits, L.tiles_x, k0);
+    emit_big<KeyT><<<148 * 4, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.toff, b.ctr, b.tcount, L.rank_bits,
+                                            L.tiles_x, k0);
+    prof_end(ST_BIN, st);
+    prof_begin(ST_TILE_SORT, st);
+    const int cur = radix_sort<KeyT, false>(k0, nullptr, k1, nullptr, &b.ctr->reserved[0], 0,
+                                            dims.max_instances, L.rank_bits, L.rank_bits + L.tile_bits, ss, st);
+    tile_ranges<KeyT><<<148 * 8, 256, 0, st>>>(cur ? k1 : k0, b.ctr, L.rank_bits, b.ranges);
+    prof_end(ST_TILE_SORT, st);
+}
+
+template <typename KeyT>
+static void launch_composite_fwd(const RenderBufs &b, const RenderLayout &L, const sm_render_dims &dims,
+                                 float *out_rgb, float *out_depth, float *out_alpha, cudaStream_t st) {
+    const KeyT rank_mask = (KeyT)((1ull << L.rank_bits) - 1ull);
+    const KeyT *ik = static_cast<const KeyT *>(L.tile_passes & 1 ? b.ikey1 : b.ikey0);
+    composite_fwd<KeyT><<<(unsigned)L.n_tiles, kTilePx, 0, st>>>(
+        b.ranges, ik, rank_mask, b.rec_sorted, b.p64, b.order0, dims.width, dims.height, L.tiles_x,
+        out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last);
 }
 
 int render_forward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,
@@ -516,8 +475,8 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
                   dims.height);
         return SM_ERR_DIMENSION;
     }
-    if (L.rank_bits + L.tile_bits > 32) {
-        set_error("rank bits %d + tile bits %d exceed 32", L.rank_bits, L.tile_bits);
+    if (L.rank_bits + L.tile_bits > 64) {
+        set_error("rank bits %d + tile bits %d exceed 64", L.rank_bits, L.tile_bits);
         return SM_ERR_INVALID;
     }
     RenderBufs b = render_bufs(ws, L);
@@ -541,35 +500,17 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
         (void)dcur;   // 4 passes: keys and order end in buffer 0
         depth_tie_fixup<<<gb, 256, 0, st>>>(dk, b.order0, n, b.dkey1);
         prof_end(ST_DEPTH_SORT, st);
-        prof_begin(ST_BIN, st);
-        gather_by_rank<<<gb, 256, 0, st>>>(b.order0, n, b.rec, b.tcount, b.tmask, b.rec_sorted,
-                                           b.tcount_r, b.tmask_r);
-        exclusive_scan(b.tcount_r, b.toff, n, b.scan, &b.ctr->n_instances, st);
-        check_instances<<<1, 1, 0, st>>>(b.ctr, dims.max_instances);
-        const unsigned persist = (unsigned)(148 * 8);
-        // b.tcount (per visible index) is dead after gather_by_rank: reuse it as the big-splat queue
-        emit_instances<<<gb, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.tmask_r, b.toff, n, b.ctr, b.tcount,
-                                           L.rank_bits, L.tiles_x, b.ikey0);
-        emit_big<<<148 * 4, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.toff, b.ctr, b.tcount, L.rank_bits,
-                                          L.tiles_x, b.ikey0);
-        prof_end(ST_BIN, st);
-        prof_begin(ST_TILE_SORT, st);
-        const int cur = radix_sort<uint32_t, false>(
-            b.ikey0, nullptr, b.ikey1, nullptr, &b.ctr->reserved[0], 0, dims.max_instances,
-            L.rank_bits, L.rank_bits + L.tile_bits, ss, st);
-        uint32_t *ik = cur ? b.ikey1 : b.ikey0;
-        tile_ranges<<<persist, 256, 0, st>>>(ik, b.ctr, L.rank_bits, b.ranges);
-        prof_end(ST_TILE_SORT, st);
+        if (L.key_bytes == 8)
+            bin_tiles<unsigned long long>(b, L, dims, n, gb, ss, st);
+        else
+            bin_tiles<uint32_t>(b, L, dims, n, gb, ss, st);
         count_launches(1 + (1 + L.depth_passes) + 1 + 7 + (1 + L.tile_passes) + 1);
     }
-    const uint32_t rank_mask = (uint32_t)((1ull << L.rank_bits) - 1ull);
     prof_begin(ST_COMPOSITE_FWD, st);
-    static const int pair = env_int("SM_FWD_PAIR", 0);
-    auto kern = pair ? composite_fwd_pair : composite_fwd;
-    kern<<<(unsigned)L.n_tiles, pair ? kTilePx / 2 : kTilePx, 0, st>>>(
-        b.ranges, L.tile_passes & 1 ? b.ikey1 : b.ikey0, rank_mask, b.rec_sorted, b.p64, b.order0,
-        dims.width, dims.height, L.tiles_x, out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t,
-        b.pix_tlast, b.pix_last);
+    if (L.key_bytes == 8)
+        launch_composite_fwd<unsigned long long>(b, L, dims, out_rgb, out_depth, out_alpha, st);
+    else
+        launch_composite_fwd<uint32_t>(b, L, dims, out_rgb, out_depth, out_alpha, st);
     prof_end(ST_COMPOSITE_FWD, st);
     count_launches(1);
     SM_CHECK_LAUNCH("render_forward");

@@ -204,6 +204,38 @@ def test_ellipse_tile_cull_is_exact(cuda):
         lib.sm_set_ellipse_cull(1)
 
 
+def test_wide_instance_keys_bit_identical(cuda):
+    """Workspaces sized for > 2M splats pack (tile, rank) into 64-bit instance
+    keys (rank bits + tile bits > 32); images and gradients are bit-identical
+    to the 32-bit path on the same scene."""
+    import torch
+
+    from paper_2511_23030_b200 import renderloss as rl
+    scene, pose, intr, rng = _grad_case(5, n=3000, w=640, h=480)
+    sa = rl.SceneArrays(**scene)
+    params = torch.from_numpy(rl.pack_params(sa)).cuda()
+    cam = rl.camera_for(pose, intr)
+    h, w = intr.height, intr.width
+    d_rgb = torch.as_tensor(rng.normal(size=(h, w, 3)), dtype=torch.float32).cuda()
+    d_depth = torch.as_tensor(rng.normal(size=(h, w)) * 0.1, dtype=torch.float32).cuda()
+    outs = []
+    for cap in (len(sa), 3_000_000):
+        eng = rl.RenderEngine()
+        eng.ensure(cap, w, h)
+        rgb = torch.empty((h, w, 3), device="cuda")
+        depth = torch.empty((h, w), device="cuda")
+        alpha = torch.empty((h, w), device="cuda")
+        eng.forward(params, None, len(sa), cam, rgb, depth, alpha)
+        assert not eng.counters()["overflow"]
+        grads = torch.zeros_like(params)
+        eng.backward(params, None, len(sa), cam, d_rgb, d_depth, None, grads)
+        torch.cuda.synchronize()
+        outs.append((rgb, depth, alpha, grads))
+        del eng
+    for name, a, b in zip(("rgb", "depth", "alpha", "grads"), *outs):
+        assert torch.equal(a, b), name
+
+
 def _gpu_depth_order(scene, pose, intr):
     import torch
 
