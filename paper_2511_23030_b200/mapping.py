@@ -201,7 +201,11 @@ class MappingEngine:
         self.alpha = torch.empty((h, w), dtype=torch.float32, device=dev)
         self.d_rgb = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
         self.d_depth = torch.empty((h, w), dtype=torch.float32, device=dev)
+        # HBM keyframe tier: ground-truth RGB (u8) + depth (f32) of the store's
+        # resident keyframes (store.py:427-489 LRU), dropped when the store
+        # evicts the keyframe (its .dkf write-back is the store's)
         self._kf_dev: dict[int, _DeviceKeyframe] = {}
+        store.keyframe_evict_hooks.append(self._drop_device_keyframe)
         self._readback = torch.zeros(12, dtype=torch.float32, pin_memory=True)
         self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
         self.cam = None
@@ -219,6 +223,12 @@ class MappingEngine:
         self.index.add(kf.id, kf.position,
                        usage_remaining=self.index.config.initial_usage if index_usage is None else index_usage)
         self.latest_kf = kf.id
+
+    def _drop_device_keyframe(self, kid: int) -> None:
+        self._kf_dev.pop(kid, None)
+
+    def device_keyframe_ids(self) -> set[int]:
+        return {k for k in self._kf_dev if k >= 0}
 
     def _device_keyframe(self, kf: Keyframe) -> _DeviceKeyframe:
         torch = self.torch

@@ -38,12 +38,13 @@ def _gt_frames(target: SceneData, poses, intr, device):
 
 def build_engine(scene: SceneData, poses, intr, chunk_size: float, budget: int,
                  store_dir: Path | None = None, device=None, seed: int = 7,
-                 max_distance: float = 200.0, target_seed: int = 49) -> MappingEngine:
+                 max_distance: float = 200.0, target_seed: int = 49,
+                 keyframe_budget: int = 400) -> MappingEngine:
     import torch
     device = torch.device(device if device is not None else "cuda")
     store_dir = Path(store_dir or tempfile.mkdtemp(prefix="splatmap_b200_"))
     store = ChunkStore(StoreConfig(disk_root=store_dir, chunk_size_m=chunk_size,
-                                   gaussian_budget=budget, keyframe_budget=400, io_ns_per_byte=1.0,
+                                   gaussian_budget=budget, keyframe_budget=keyframe_budget, io_ns_per_byte=1.0,
                                    device=str(device)))
     store.insert_arrays(scene.positions, scene.rotations, scene.scales, scene.opacities, scene.sh)
     eng = MappingEngine(store, intr, seed=seed, cull=CullConfig(max_distance_m=max_distance))
@@ -71,8 +72,9 @@ def c1_poses(k: int = 10):
 
 
 def build_c1(n: int = 20_000, keyframes: int = 10, budget: int = 12_000, store_dir=None,
-             device=None) -> MappingEngine:
-    return build_engine(c1_scene(n), c1_poses(keyframes), C1_INTR, 10.0, budget, store_dir, device)
+             device=None, keyframe_budget: int = 400) -> MappingEngine:
+    return build_engine(c1_scene(n), c1_poses(keyframes), C1_INTR, 10.0, budget, store_dir, device,
+                        keyframe_budget=keyframe_budget)
 
 
 def build_c4lite(n: int = 4_000_000, length: float = 200.0, keyframes: int = 100, budget: int = 1_500_000,

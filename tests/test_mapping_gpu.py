@@ -50,9 +50,9 @@ def test_adam_kernel_matches_oracle(cuda):
     assert np.all(m.cpu().numpy()[:, 14] == 3.0)
 
 
-def _c1_engine(tmp_path, budget=12_000, n=20_000, use_graphs=True):
+def _c1_engine(tmp_path, budget=12_000, n=20_000, use_graphs=True, keyframe_budget=400):
     from paper_2511_23030_b200.workloads import build_c1
-    eng = build_c1(n=n, keyframes=10, budget=budget, store_dir=tmp_path)
+    eng = build_c1(n=n, keyframes=10, budget=budget, store_dir=tmp_path, keyframe_budget=keyframe_budget)
     eng.use_graphs = use_graphs
     return eng
 
@@ -131,3 +131,32 @@ def test_render_through_store_matches_oracle(cuda, tmp_path):
                           kf.pose.translation, i.fx, i.fy, i.cx, i.cy, i.near, i.width, i.height)
     assert np.abs(eng.rgb.cpu().numpy() - ref[0]).max() <= 1e-4
     assert np.abs(eng.alpha.cpu().numpy() - ref[2]).max() <= 1e-4
+
+
+def test_device_keyframe_tier_follows_store_lru(cuda, tmp_path):
+    """The HBM keyframe tier holds ground truth only for the store's resident
+    keyframes (store.py:427-489 LRU): keyframes the store evicts (and writes
+    as .dkf) leave HBM, reloads come back from disk bit-exact, so training is
+    identical to an unbounded keyframe tier."""
+    import torch
+    a = _c1_engine(tmp_path / "a", budget=100_000, keyframe_budget=3)
+    b = _c1_engine(tmp_path / "b", budget=100_000)
+    for s in range(16):
+        ra = a.optimization_step(0, s)
+        rb = b.optimization_step(0, s)
+        assert ra.selected_kf == rb.selected_kf and ra.loss == rb.loss
+        assert a.device_keyframe_ids() <= a.store.resident_keyframe_ids()
+        assert len(a.store.resident_keyframe_ids()) <= 3
+    for kid in (0, 1, 2):   # evicted keyframes come back from their .dkf files
+        losses = []
+        for e in (a, b):
+            kf = e.store.keyframe_get(kid)
+            ids = sorted(e._visible_for_pose(kf.pose)[0])
+            e.store.ensure_resident(ids)
+            slots, n = e.active.build(e.store.segments(ids))
+            losses.append(e.train_view(kf, slots, n))
+        assert losses[0] == losses[1], kid
+        assert a.device_keyframe_ids() <= a.store.resident_keyframe_ids()
+    assert a.store.stats.keyframe_writes > 0 and a.store.stats.keyframe_loads > 0
+    hw = a.store.slab.high_water()
+    assert torch.equal(a.store.slab.params[:hw], b.store.slab.params[:hw])
