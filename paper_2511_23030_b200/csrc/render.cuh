@@ -80,7 +80,7 @@ struct RenderLayout {
     int64_t o_counters, o_rec, o_rec_sorted, o_p64, o_dkey0, o_dkey1, o_order0, o_order1;
     int64_t o_tcount, o_tcount_r, o_tmask, o_tmask_r, o_toff, o_ikey0, o_ikey1, o_ranges;
     int64_t o_pix_cd, o_pix_t, o_pix_tlast, o_pix_last, o_g2d, o_sort_hist, o_scan;
-    int64_t o_gbuf, o_tile_hor;
+    int64_t o_gbuf, o_tile_hor, o_tile_work, o_tile_order;
     int64_t total;
 };
 
@@ -100,6 +100,8 @@ struct RenderBufs {
     uint32_t *sort_hist, *scan;
     float *gbuf;         // per-instance gradient slots [max_instances][12] (backward)
     int32_t *tile_hor;   // per-tile horizon rank (backward)
+    uint32_t *tile_work;    // per-tile instances the forward composited (backward's work)
+    uint32_t *tile_order;   // tiles by descending work: the backward's launch order
 };
 
 inline RenderBufs render_bufs(void *ws, const RenderLayout &L) {
@@ -130,6 +132,8 @@ inline RenderBufs render_bufs(void *ws, const RenderLayout &L) {
     r.scan = reinterpret_cast<uint32_t *>(b + L.o_scan);
     r.gbuf = reinterpret_cast<float *>(b + L.o_gbuf);
     r.tile_hor = reinterpret_cast<int32_t *>(b + L.o_tile_hor);
+    r.tile_work = reinterpret_cast<uint32_t *>(b + L.o_tile_work);
+    r.tile_order = reinterpret_cast<uint32_t *>(b + L.o_tile_order);
     return r;
 }
 

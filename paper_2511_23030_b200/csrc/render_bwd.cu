@@ -186,7 +186,8 @@ composite_bwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
               const float4 *__restrict__ st_cd, const float *__restrict__ st_t,
               const float *__restrict__ st_tlast, const int32_t *__restrict__ st_last,
               const uint32_t *__restrict__ toff, const uint32_t *__restrict__ tmask_r,
-              float *__restrict__ gbuf, int32_t *__restrict__ tile_hor, sm_render_counters *ctr) {
+              float *__restrict__ gbuf, int32_t *__restrict__ tile_hor, sm_render_counters *ctr,
+              const uint32_t *__restrict__ tile_order) {
     constexpr int NT = kBwdThreads;
     constexpr int NW = NT / 32;
     __shared__ ProjRec s_rec[NT];
@@ -194,7 +195,7 @@ composite_bwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
     __shared__ float s_part[NW][NT][10];
     __shared__ int s_maxlast;
     const int warp = threadIdx.x / 32;
-    const int tile = blockIdx.x;
+    const int tile = (int)tile_order[blockIdx.x];   // heaviest tiles first
     const int lane = threadIdx.x & 31;
     const int ty0 = (tile / tiles_x) * kTile;
     const int px = (tile % tiles_x) * kTile + (threadIdx.x & (kTile - 1));
@@ -530,7 +531,7 @@ static void launch_composite_bwd(const RenderBufs &b, const RenderLayout &L, con
     composite_bwd<KeyT><<<(unsigned)L.n_tiles, kBwdThreads, 0, st>>>(
         b.ranges, ik, rank_mask, b.rec_sorted, b.p64, b.order0, dims.width, dims.height, L.tiles_x, d_rgb,
         d_depth, d_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, b.toff, b.tmask_r, b.gbuf, b.tile_hor,
-        b.ctr);
+        b.ctr, b.tile_order);
 }
 
 int render_backward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,

@@ -70,6 +70,8 @@ RenderLayout render_layout(const sm_render_dims &d) {
     L.o_scan = take(scan_scratch_bytes(G));
     L.o_gbuf = take(I * (int64_t)sizeof(float) * kG2dStride);
     L.o_tile_hor = take(L.n_tiles * 4);
+    L.o_tile_work = take(L.n_tiles * 4);
+    L.o_tile_order = take(L.n_tiles * 4);
     L.total = off;
     return L;
 }
@@ -360,10 +362,11 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
               const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
               int height, int tiles_x, float *__restrict__ out_rgb, float *__restrict__ out_depth,
               float *__restrict__ out_alpha, float4 *__restrict__ st_cd, float *__restrict__ st_t,
-              float *__restrict__ st_tlast, int32_t *__restrict__ st_last) {
+              float *__restrict__ st_tlast, int32_t *__restrict__ st_last, uint32_t *__restrict__ tile_work) {
     constexpr int NT = kTilePx;
     __shared__ ProjRec s_rec[NT];
     __shared__ uint32_t s_rank[NT];
+    __shared__ int s_maxlast;
     const int tile = blockIdx.x;
     const int ty0 = (tile / tiles_x) * kTile;
     const int px = (tile % tiles_x) * kTile + (threadIdx.x & (kTile - 1));
@@ -405,6 +408,44 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
     }
     if (in)
         s.store((int64_t)py * width + px, out_rgb, out_depth, out_alpha, st_cd, st_t, st_tlast, st_last);
+    // the backward revisits [start, max last]: its work estimate for scheduling
+    if (threadIdx.x == 0) s_maxlast = -1;
+    __syncthreads();
+    const int wl = __reduce_max_sync(0xffffffffu, s.last);
+    if ((threadIdx.x & 31) == 0) atomicMax(&s_maxlast, wl);
+    __syncthreads();
+    if (threadIdx.x == 0) tile_work[tile] = s_maxlast >= (int)start ? (uint32_t)(s_maxlast - (int)start + 1) : 0u;
+}
+
+// Longest-first launch order of the tiles for the backward: a counting sort
+// of the tiles into 64 work buckets, heaviest bucket first (one block).  The
+// backward's CTAs then start heavy tiles first and light ones fill in behind
+// them (LPT), shortening the tail.  Order inside a bucket is arbitrary: tiles
+// are independent, so results do not depend on it.
+constexpr int kWorkBuckets = 64;
+__global__ void __launch_bounds__(1024)
+order_tiles(const uint32_t *__restrict__ work, int n_tiles, uint32_t *__restrict__ order) {
+    __shared__ uint32_t hist[kWorkBuckets], base[kWorkBuckets];
+    __shared__ uint32_t wmax;
+    if (threadIdx.x < kWorkBuckets) hist[threadIdx.x] = 0;
+    if (threadIdx.x == 0) wmax = 1;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) atomicMax(&wmax, work[i]);
+    __syncthreads();
+    const uint32_t div = (wmax + kWorkBuckets - 1) / kWorkBuckets;
+    for (int i = threadIdx.x; i < n_tiles; i += blockDim.x)
+        atomicAdd(&hist[kWorkBuckets - 1 - min(work[i] / div, (uint32_t)kWorkBuckets - 1)], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int b = 0; b < kWorkBuckets; b++) {
+            base[b] = run;
+            run += hist[b];
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_tiles; i += blockDim.x)
+        order[atomicAdd(&base[kWorkBuckets - 1 - min(work[i] / div, (uint32_t)kWorkBuckets - 1)], 1u)] = (uint32_t)i;
 }
 
 int g_ellipse_cull = 1;   // sm_set_ellipse_cull (tests: culled == unculled, bit for bit)
@@ -455,7 +496,8 @@ static void launch_composite_fwd(const RenderBufs &b, const RenderLayout &L, con
     const KeyT *ik = static_cast<const KeyT *>(L.tile_passes & 1 ? b.ikey1 : b.ikey0);
     composite_fwd<KeyT><<<(unsigned)L.n_tiles, kTilePx, 0, st>>>(
         b.ranges, ik, rank_mask, b.rec_sorted, b.p64, b.order0, dims.width, dims.height, L.tiles_x,
-        out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last);
+        out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, b.tile_work);
+    order_tiles<<<1, 1024, 0, st>>>(b.tile_work, (int)L.n_tiles, b.tile_order);
 }
 
 int render_forward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,
@@ -512,7 +554,7 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
     else
         launch_composite_fwd<uint32_t>(b, L, dims, out_rgb, out_depth, out_alpha, st);
     prof_end(ST_COMPOSITE_FWD, st);
-    count_launches(1);
+    count_launches(2);
     SM_CHECK_LAUNCH("render_forward");
     return SM_OK;
 }
