@@ -48,7 +48,7 @@ def main():
     kcol = head.index("Kernel Name")
     recs = []
     for r in data:
-        rec = {"kernel": r[kcol].split("(")[0].replace("void ", "")}
+        rec = {"kernel": r[kcol].split("(")[0].replace("void ", "").split("<")[0]}
         for m, c in col.items():
             v = _num(r[c])
             if m == "gpu__time_duration.sum" and v is not None:
