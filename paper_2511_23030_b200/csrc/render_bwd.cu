@@ -381,7 +381,10 @@ struct CamBwd {
 
 // K6: per depth rank, chain the 2D grads through the fp64 projection and
 // accumulate the 14 parameter grads into the slot-indexed grad records.
-__global__ void __launch_bounds__(256)
+#ifndef SM_PBWD_MINB
+#define SM_PBWD_MINB 3   // 3 x 256 threads per SM (<= 85 registers): measured best of 1-3
+#endif
+__global__ void __launch_bounds__(256, SM_PBWD_MINB)
 project_bwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots, int64_t n,
             CamBwd cam, const uint32_t *__restrict__ order, const uint32_t *__restrict__ tcount_r,
             const uint32_t *__restrict__ tmask_r,

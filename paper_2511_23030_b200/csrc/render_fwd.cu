@@ -483,7 +483,7 @@ static void bin_tiles(const RenderBufs &b, const RenderLayout &L, const sm_rende
                                             L.tiles_x, k0);
     prof_end(ST_BIN, st);
     prof_begin(ST_TILE_SORT, st);
-    const int cur = radix_sort<KeyT, false>(k0, nullptr, k1, nullptr, &b.ctr->reserved[0], 0,
+    const int cur = radix_sort<KeyT, false, kSortItemsWide>(k0, nullptr, k1, nullptr, &b.ctr->reserved[0], 0,
                                             dims.max_instances, L.rank_bits, L.rank_bits + L.tile_bits, ss, st);
     tile_ranges<KeyT><<<148 * 8, 256, 0, st>>>(cur ? k1 : k0, b.ctr, L.rank_bits, b.ranges);
     prof_end(ST_TILE_SORT, st);

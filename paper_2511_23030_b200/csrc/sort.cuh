@@ -19,8 +19,12 @@
 namespace sm {
 
 constexpr int kSortThreads = 256;
+// Keys per thread: 8 (2048-key tiles) for the depth sort's ~0.4M keys --
+// enough tiles to fill 148 SMs -- and 16 (4096-key tiles, half the look-back
+// chain) for the tile sort's ~2M keys (measured best for each).
 constexpr int kSortItems = 8;
-constexpr int kSortTile = kSortThreads * kSortItems;   // 2048 keys per tile
+constexpr int kSortItemsWide = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;   // smallest tile: sizes the scratch
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 constexpr int kSortWarps = kSortThreads / 32;
@@ -66,7 +70,7 @@ __device__ __forceinline__ void st_status(uint32_t *p, uint32_t v) {
     *reinterpret_cast<volatile uint32_t *>(p) = v;
 }
 
-template <typename K, bool HAS_VAL>
+template <typename K, bool HAS_VAL, int ITEMS>
 __global__ void __launch_bounds__(kSortThreads)
 onesweep_pass(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
               K *__restrict__ keys_out, uint32_t *__restrict__ vals_out, const uint32_t *n_dev,
@@ -77,14 +81,14 @@ onesweep_pass(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals_i
     __shared__ uint32_t tile_excl[kRadix];
     __shared__ uint32_t warp_tot[kSortWarps];
     __shared__ uint32_t s_tile;
-    __shared__ K s_keys[kSortTile];
-    __shared__ uint32_t s_vals[HAS_VAL ? kSortTile : 1];
+    __shared__ K s_keys[(kSortThreads * ITEMS)];
+    __shared__ uint32_t s_vals[HAS_VAL ? (kSortThreads * ITEMS) : 1];
     const int64_t n = load_count(n_dev, n_host);
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr_p, 1u);
     __syncthreads();
     // tiles are handed out in launch order: blocks past the live count (the
     // grid is sized for the capacity) leave before doing any work
-    if ((int64_t)s_tile * kSortTile >= n) return;
+    if ((int64_t)s_tile * (kSortThreads * ITEMS) >= n) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&wcount[0][0])[i] = 0;
     // global digit base = exclusive scan of this pass's histogram
@@ -104,15 +108,15 @@ onesweep_pass(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals_i
     }
     __syncthreads();
     const uint32_t tile = s_tile;
-    const int64_t start = (int64_t)tile * kSortTile;
+    const int64_t start = (int64_t)tile * (kSortThreads * ITEMS);
     const K mask = (K)((1u << nbits) - 1u);
-    K key[kSortItems];
-    uint32_t val[kSortItems];
-    uint32_t local[kSortItems];
-    uint32_t dig[kSortItems];
-    const int64_t seg = start + (int64_t)warp * (32 * kSortItems);
+    K key[ITEMS];
+    uint32_t val[ITEMS];
+    uint32_t local[ITEMS];
+    uint32_t dig[ITEMS];
+    const int64_t seg = start + (int64_t)warp * (32 * ITEMS);
 #pragma unroll
-    for (int j = 0; j < kSortItems; j++) {
+    for (int j = 0; j < ITEMS; j++) {
         const int64_t i = seg + j * 32 + lane;
         const bool ok = i < n;
         key[j] = ok ? keys_in[i] : (K)0;
@@ -122,7 +126,7 @@ onesweep_pass(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals_i
     // stable in-block ranking: warp w owns the contiguous segment w*256..,
     // item j of lane l is element w*256 + j*32 + l, processed in (j, l) order
 #pragma unroll
-    for (int j = 0; j < kSortItems; j++) {
+    for (int j = 0; j < ITEMS; j++) {
         const uint32_t d = dig[j];
         const unsigned peers = __match_any_sync(0xffffffffu, d);
         const unsigned lt = peers & ((1u << lane) - 1u);
@@ -188,7 +192,7 @@ onesweep_pass(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals_i
     // stage the tile in shared memory in digit order, then write each digit's
     // run to consecutive global addresses (full-sector, coalesced stores)
 #pragma unroll
-    for (int j = 0; j < kSortItems; j++) {
+    for (int j = 0; j < ITEMS; j++) {
         const uint32_t d = dig[j];
         if (d == 0xffffffffu) continue;
         const uint32_t lp = tile_excl[d] + wcount[warp][d] + local[j];
@@ -196,7 +200,7 @@ onesweep_pass(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals_i
         if (HAS_VAL) s_vals[lp] = val[j];
     }
     __syncthreads();
-    const int cnt = (int)min64(kSortTile, n - start);
+    const int cnt = (int)min64((kSortThreads * ITEMS), n - start);
     for (int i = threadIdx.x; i < cnt; i += kSortThreads) {
         const K k = s_keys[i];
         const uint32_t d = (uint32_t)((k >> shift) & mask);
@@ -240,11 +244,11 @@ inline int radix_passes(int begin_bit, int end_bit) {
 // Stable sort of keys (+ optional u32 values) over bits [begin_bit, end_bit).
 // Ping-pongs (k0,v0) <-> (k1,v1); returns 0 if the result is in buffer 0.
 // `max_n` bounds the count (grids, status rows); the live count is n_dev or n_host.
-template <typename K, bool HAS_VAL>
+template <typename K, bool HAS_VAL, int ITEMS = kSortItems>
 int radix_sort(K *k0, uint32_t *v0, K *k1, uint32_t *v1, const uint32_t *n_dev, int64_t n_host,
                int64_t max_n, int begin_bit, int end_bit, const SortScratch &s, cudaStream_t st) {
     const int npass = radix_passes(begin_bit, end_bit);
-    const int64_t tiles = sort_tiles(max_n);
+    const int64_t tiles = ceil_div(max_n > 0 ? max_n : 1, (int64_t)kSortThreads * ITEMS);
     cudaMemsetAsync(s.hist, 0, (size_t)npass * kRadix * 4, st);
     cudaMemsetAsync(s.status, 0, (size_t)npass * tiles * kRadix * 4, st);
     cudaMemsetAsync(s.tile_ctr, 0, (size_t)npass * 4, st);
@@ -258,7 +262,7 @@ int radix_sort(K *k0, uint32_t *v0, K *k1, uint32_t *v1, const uint32_t *n_dev, 
         K *ko = cur ? k0 : k1;
         uint32_t *vi = cur ? v1 : v0;
         uint32_t *vo = cur ? v0 : v1;
-        onesweep_pass<K, HAS_VAL><<<(unsigned)tiles, kSortThreads, 0, st>>>(
+        onesweep_pass<K, HAS_VAL, ITEMS><<<(unsigned)tiles, kSortThreads, 0, st>>>(
             ki, vi, ko, vo, n_dev, n_host, shift, nbits, s.hist + p * kRadix,
             s.status + (int64_t)p * tiles * kRadix, s.tile_ctr + p);
         cur ^= 1;
