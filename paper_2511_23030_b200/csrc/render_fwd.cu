@@ -89,8 +89,12 @@ project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots
             CamDev cam, int cull, ProjRec *__restrict__ rec, Proj64 *__restrict__ p64,
             uint32_t *__restrict__ dkey, unsigned long long *__restrict__ zbits,
             uint32_t *__restrict__ order,
-            uint32_t *__restrict__ tcount, uint32_t *__restrict__ tmask) {
+            uint32_t *__restrict__ tcount, uint32_t *__restrict__ tmask,
+            uint32_t *__restrict__ ctr_words, uint32_t *__restrict__ ranges, int64_t n_range_words) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // the pass's device counters and tile ranges start at zero (saves two memsets)
+    if (i < (int64_t)(sizeof(sm_render_counters) / 4)) ctr_words[i] = 0u;
+    if (i < n_range_words) ranges[i] = 0u;
     if (i >= n) return;
     const int64_t slot = slots ? (int64_t)slots[i] : i;
     const float4 A = params[slot * 4 + 0];   // px py pz qw
@@ -234,12 +238,6 @@ gather_by_rank(const uint32_t *__restrict__ order, int64_t n, const ProjRec *__r
     }
 }
 
-__global__ void check_instances(sm_render_counters *ctr, int64_t max_instances) {
-    const uint32_t n = ctr->n_instances;
-    const bool of = (int64_t)n > max_instances;
-    ctr->overflow = of ? 1u : 0u;
-    ctr->reserved[0] = of ? 0u : n;   // count the sort / ranges see
-}
 
 // Instance emission.  Splat footprints are heavy-tailed and the biggest
 // (nearest) ones sit together at the lowest depth ranks, so emission is split:
@@ -474,8 +472,8 @@ static void bin_tiles(const RenderBufs &b, const RenderLayout &L, const sm_rende
     prof_begin(ST_BIN, st);
     gather_by_rank<<<gb, 256, 0, st>>>(b.order0, n, b.rec, b.tcount, b.tmask, b.rec_sorted, b.tcount_r,
                                        b.tmask_r);
-    exclusive_scan(b.tcount_r, b.toff, n, b.scan, &b.ctr->n_instances, st);
-    check_instances<<<1, 1, 0, st>>>(b.ctr, dims.max_instances);
+    exclusive_scan(b.tcount_r, b.toff, n, b.scan, &b.ctr->n_instances, st, dims.max_instances,
+                   &b.ctr->overflow, &b.ctr->reserved[0]);   // + the instance-capacity check
     // b.tcount (per visible index) is dead after gather_by_rank: reuse it as the big-splat queue
     emit_instances<KeyT><<<gb, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.tmask_r, b.toff, n, b.ctr, b.tcount,
                                              L.rank_bits, L.tiles_x, k0);
@@ -523,15 +521,18 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
     }
     RenderBufs b = render_bufs(ws, L);
     CamDev cd = make_cam(cam, L);
-    cudaMemsetAsync(b.ctr, 0, sizeof(sm_render_counters), st);
-    cudaMemsetAsync(b.ranges, 0, L.n_tiles * 8, st);
-    if (n > 0) {
+    if (n == 0) {
+        cudaMemsetAsync(b.ctr, 0, sizeof(sm_render_counters), st);
+        cudaMemsetAsync(b.ranges, 0, L.n_tiles * 8, st);
+    } else {
         const unsigned gb = (unsigned)ceil_div(n, 256);
+        const unsigned gp = (unsigned)ceil_div(n > 2 * L.n_tiles + 16 ? n : 2 * L.n_tiles + 16, 256);
         // 32-bit depth keys, ping-pong halves of the dkey0 region; fp64 z bits in dkey1
         uint32_t *dk = reinterpret_cast<uint32_t *>(b.dkey0);
         prof_begin(ST_PROJECT, st);
-        project_fwd<<<gb, 256, 0, st>>>(reinterpret_cast<const float4 *>(params), slots, n, cd,
-                                        g_ellipse_cull, b.rec, b.p64, dk, b.dkey1, b.order0, b.tcount, b.tmask);
+        project_fwd<<<gp, 256, 0, st>>>(reinterpret_cast<const float4 *>(params), slots, n, cd,
+                                        g_ellipse_cull, b.rec, b.p64, dk, b.dkey1, b.order0, b.tcount, b.tmask,
+                                        reinterpret_cast<uint32_t *>(b.ctr), b.ranges, 2 * L.n_tiles);
         prof_end(ST_PROJECT, st);
         const SortScratch ss = sort_scratch(b.sort_hist, dims.max_gaussians > dims.max_instances
                                                              ? dims.max_gaussians : dims.max_instances);
@@ -546,7 +547,7 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
             bin_tiles<unsigned long long>(b, L, dims, n, gb, ss, st);
         else
             bin_tiles<uint32_t>(b, L, dims, n, gb, ss, st);
-        count_launches(1 + (1 + L.depth_passes) + 1 + 7 + (1 + L.tile_passes) + 1);
+        count_launches(1 + (1 + L.depth_passes) + 1 + 6 + (1 + L.tile_passes) + 1);
     }
     prof_begin(ST_COMPOSITE_FWD, st);
     if (L.key_bytes == 8)

@@ -225,15 +225,17 @@ inline int64_t sort_scratch_bytes(int64_t max_n) {
            align_up(kMaxPasses * 4, 256);
 }
 
+// Layout: tile counters | histograms | look-back status, contiguous so one
+// memset clears what a sort uses.
 inline SortScratch sort_scratch(void *base, int64_t max_n) {
     char *b = static_cast<char *>(base);
     SortScratch s;
     s.max_tiles = sort_tiles(max_n);
+    s.tile_ctr = reinterpret_cast<uint32_t *>(b);
+    b += align_up(kMaxPasses * 4, 256);
     s.hist = reinterpret_cast<uint32_t *>(b);
     b += align_up((int64_t)kMaxPasses * kRadix * 4, 256);
     s.status = reinterpret_cast<uint32_t *>(b);
-    b += align_up((int64_t)kMaxPasses * s.max_tiles * kRadix * 4, 256);
-    s.tile_ctr = reinterpret_cast<uint32_t *>(b);
     return s;
 }
 
@@ -249,9 +251,9 @@ int radix_sort(K *k0, uint32_t *v0, K *k1, uint32_t *v1, const uint32_t *n_dev, 
                int64_t max_n, int begin_bit, int end_bit, const SortScratch &s, cudaStream_t st) {
     const int npass = radix_passes(begin_bit, end_bit);
     const int64_t tiles = ceil_div(max_n > 0 ? max_n : 1, (int64_t)kSortThreads * ITEMS);
-    cudaMemsetAsync(s.hist, 0, (size_t)npass * kRadix * 4, st);
-    cudaMemsetAsync(s.status, 0, (size_t)npass * tiles * kRadix * 4, st);
-    cudaMemsetAsync(s.tile_ctr, 0, (size_t)npass * 4, st);
+    cudaMemsetAsync(s.tile_ctr, 0,   // tile counters + histograms + this sort's status rows
+                    (size_t)(reinterpret_cast<char *>(s.status + (int64_t)npass * tiles * kRadix) -
+                             reinterpret_cast<char *>(s.tile_ctr)), st);
     const unsigned hgrid = (unsigned)min64(tiles * 2, 148 * 8);
     onesweep_histogram<K><<<hgrid, kSortThreads, 0, st>>>(k0, n_dev, n_host, begin_bit, end_bit, s.hist);
     int cur = 0;
@@ -316,9 +318,12 @@ scan_reduce(const uint32_t *__restrict__ in, int64_t n, uint32_t *__restrict__ p
     if (threadIdx.x == 0) partial[blockIdx.x] = tot;
 }
 
-// single CTA: exclusive scan of partial[0:nb], writes total to *total
+// single CTA: exclusive scan of partial[0:nb], writes total to *total; with
+// cap >= 0 also *over = (total > cap) and *count = over ? 0 : total (the
+// render's instance-capacity check, folded in to save a launch)
 __global__ void __launch_bounds__(kScanThreads)
-scan_partials(uint32_t *__restrict__ partial, int64_t nb, uint32_t *__restrict__ total) {
+scan_partials(uint32_t *__restrict__ partial, int64_t nb, uint32_t *__restrict__ total, int64_t cap,
+              uint32_t *__restrict__ over, uint32_t *__restrict__ count) {
     __shared__ uint32_t ws[32];
     __shared__ uint32_t carry;
     if (threadIdx.x == 0) carry = 0;
@@ -334,7 +339,14 @@ scan_partials(uint32_t *__restrict__ partial, int64_t nb, uint32_t *__restrict__
         if (threadIdx.x == 0) carry = c + bt;
         __syncthreads();
     }
-    if (threadIdx.x == 0) *total = carry;
+    if (threadIdx.x == 0) {
+        *total = carry;
+        if (cap >= 0) {
+            const bool of = (int64_t)carry > cap;
+            *over = of ? 1u : 0u;
+            *count = of ? 0u : carry;
+        }
+    }
 }
 
 __global__ void __launch_bounds__(kScanThreads)
@@ -366,10 +378,11 @@ inline int64_t scan_scratch_bytes(int64_t max_n) {
 
 // out = exclusive_scan(in[0:n]); *total = sum.  n is host-known.
 inline void exclusive_scan(const uint32_t *in, uint32_t *out, int64_t n, uint32_t *partial,
-                           uint32_t *total, cudaStream_t st) {
+                           uint32_t *total, cudaStream_t st, int64_t cap = -1, uint32_t *over = nullptr,
+                           uint32_t *count = nullptr) {
     const int64_t nb = ceil_div(n > 0 ? n : 1, kScanTile);
     scan_reduce<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, partial);
-    scan_partials<<<1, kScanThreads, 0, st>>>(partial, nb, total);
+    scan_partials<<<1, kScanThreads, 0, st>>>(partial, nb, total, cap, over, count);
     scan_downsweep<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, partial, out);
 }
 
