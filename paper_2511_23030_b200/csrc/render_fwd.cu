@@ -84,18 +84,12 @@ struct CamDev {
     int width, height, tiles_x, tiles_y;
 };
 
-__global__ void __launch_bounds__(256)
-project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots, int64_t n,
-            CamDev cam, int cull, ProjRec *__restrict__ rec, Proj64 *__restrict__ p64,
-            uint32_t *__restrict__ dkey, unsigned long long *__restrict__ zbits,
-            uint32_t *__restrict__ order,
-            uint32_t *__restrict__ tcount, uint32_t *__restrict__ tmask,
-            uint32_t *__restrict__ ctr_words, uint32_t *__restrict__ ranges, int64_t n_range_words) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    // the pass's device counters and tile ranges start at zero (saves two memsets)
-    if (i < (int64_t)(sizeof(sm_render_counters) / 4)) ctr_words[i] = 0u;
-    if (i < n_range_words) ranges[i] = 0u;
-    if (i >= n) return;
+// One Gaussian of K2; returns its 32-bit depth key (for the sort histogram).
+__device__ __forceinline__ uint32_t project_one(
+    int64_t i, const float4 *__restrict__ params, const int32_t *__restrict__ slots, const CamDev &cam,
+    int cull, ProjRec *__restrict__ rec, Proj64 *__restrict__ p64, uint32_t *__restrict__ dkey,
+    unsigned long long *__restrict__ zbits, uint32_t *__restrict__ order, uint32_t *__restrict__ tcount,
+    uint32_t *__restrict__ tmask) {
     const int64_t slot = slots ? (int64_t)slots[i] : i;
     const float4 A = params[slot * 4 + 0];   // px py pz qw
     const float4 B = params[slot * 4 + 1];   // qx qy qz sx
@@ -109,11 +103,12 @@ project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots
     if (!(g.z >= cam.near_plane)) {   // renderloss.py:179 keep = z >= near
         dkey[i] = ~0u;                   // after every kept depth, index order
         tcount[i] = 0;
-        return;
+        return ~0u;
     }
     // depth order key: fp32 z (monotone rounding of z > 0, ordered as uint);
     // ties are resolved on the exact fp64 bits by depth_tie_fixup
-    dkey[i] = __float_as_uint((float)g.z);
+    const uint32_t key = __float_as_uint((float)g.z);
+    dkey[i] = key;
     zbits[i] = (unsigned long long)__double_as_longlong(g.z);
     // renderloss.py:110-135: conic and clamped 3-sigma bbox (fp64)
     const double a = g.a, b = g.b, c = g.c;
@@ -139,7 +134,7 @@ project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots
         r.beta = r.G = 0.f;
         r.K = -1.f;
         rec[i] = r;
-        return;
+        return key;
     }
     const double ia = c / det, ib = -b / det, ic = a / det;
     const double rx = 3.0 * sqrt(a), ry = 3.0 * sqrt(c);
@@ -174,7 +169,7 @@ project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots
     p64[i] = q;
     if (x1 < x0 || y1 < y0) {
         tcount[i] = 0;
-        return;
+        return key;
     }
     // tiles the q <= 9 ellipse reaches (RowSpan); small splats keep them as a mask
     const RowSpan sp(r);
@@ -187,6 +182,32 @@ project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots
         for (int ty = sp.ty0; ty <= sp.ty1; ty++) cnt += (uint32_t)sp.count(ty);
         tcount[i] = cnt;
     }
+    return key;
+}
+
+// K2 over the visible set; also zeroes the pass's device counters and tile
+// ranges and counts the depth keys' digits for the sort (saves two memsets
+// and the sort's histogram pass).
+__global__ void __launch_bounds__(256)
+project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots, int64_t n,
+            CamDev cam, int cull, ProjRec *__restrict__ rec, Proj64 *__restrict__ p64,
+            uint32_t *__restrict__ dkey, unsigned long long *__restrict__ zbits,
+            uint32_t *__restrict__ order,
+            uint32_t *__restrict__ tcount, uint32_t *__restrict__ tmask,
+            uint32_t *__restrict__ ctr_words, uint32_t *__restrict__ ranges, int64_t n_range_words,
+            uint32_t *__restrict__ depth_hist) {
+    __shared__ uint32_t h[4][256];
+    block_hist_zero(h, 4);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < (int64_t)(sizeof(sm_render_counters) / 4)) ctr_words[i] = 0u;
+    if (i < n_range_words) ranges[i] = 0u;
+    __syncthreads();
+    if (i < n) {
+        const uint32_t key = project_one(i, params, slots, cam, cull, rec, p64, dkey, zbits, order, tcount, tmask);
+        block_hist_add(h, key, 0, 32);
+    }
+    __syncthreads();
+    block_hist_flush(h, 4, depth_hist);
 }
 
 // The 32-bit depth sort is stable, so within a run of equal fp32 keys the
@@ -481,6 +502,8 @@ static void bin_tiles(const RenderBufs &b, const RenderLayout &L, const sm_rende
                                             L.tiles_x, k0);
     prof_end(ST_BIN, st);
     prof_begin(ST_TILE_SORT, st);
+    // (counting the tile digits inside the emission was measured slower than
+    // the sort's own histogram pass: shared-atomic contention on 2 x 256 bins)
     const int cur = radix_sort<KeyT, false, kSortItemsWide>(k0, nullptr, k1, nullptr, &b.ctr->reserved[0], 0,
                                             dims.max_instances, L.rank_bits, L.rank_bits + L.tile_bits, ss, st);
     tile_ranges<KeyT><<<148 * 8, 256, 0, st>>>(cur ? k1 : k0, b.ctr, L.rank_bits, b.ranges);
@@ -529,17 +552,18 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
         const unsigned gp = (unsigned)ceil_div(n > 2 * L.n_tiles + 16 ? n : 2 * L.n_tiles + 16, 256);
         // 32-bit depth keys, ping-pong halves of the dkey0 region; fp64 z bits in dkey1
         uint32_t *dk = reinterpret_cast<uint32_t *>(b.dkey0);
-        prof_begin(ST_PROJECT, st);
-        project_fwd<<<gp, 256, 0, st>>>(reinterpret_cast<const float4 *>(params), slots, n, cd,
-                                        g_ellipse_cull, b.rec, b.p64, dk, b.dkey1, b.order0, b.tcount, b.tmask,
-                                        reinterpret_cast<uint32_t *>(b.ctr), b.ranges, 2 * L.n_tiles);
-        prof_end(ST_PROJECT, st);
         const SortScratch ss = sort_scratch(b.sort_hist, dims.max_gaussians > dims.max_instances
                                                              ? dims.max_gaussians : dims.max_instances);
+        prof_begin(ST_PROJECT, st);
+        sort_reset(ss, n, 0, 32, st);   // the projection fills the depth sort's histograms
+        project_fwd<<<gp, 256, 0, st>>>(reinterpret_cast<const float4 *>(params), slots, n, cd,
+                                        g_ellipse_cull, b.rec, b.p64, dk, b.dkey1, b.order0, b.tcount, b.tmask,
+                                        reinterpret_cast<uint32_t *>(b.ctr), b.ranges, 2 * L.n_tiles, ss.hist);
+        prof_end(ST_PROJECT, st);
         // global stable depth order: 4 passes over the fp32 key + fp64 tie fixup
         prof_begin(ST_DEPTH_SORT, st);
         const int dcur = radix_sort<uint32_t, true>(dk, b.order0, dk + dims.max_gaussians, b.order1,
-                                                    nullptr, n, n, 0, 32, ss, st);
+                                                    nullptr, n, n, 0, 32, ss, st, /*hist_ready=*/true);
         (void)dcur;   // 4 passes: keys and order end in buffer 0
         depth_tie_fixup<<<gb, 256, 0, st>>>(dk, b.order0, n, b.dkey1);
         prof_end(ST_DEPTH_SORT, st);
@@ -547,7 +571,7 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
             bin_tiles<unsigned long long>(b, L, dims, n, gb, ss, st);
         else
             bin_tiles<uint32_t>(b, L, dims, n, gb, ss, st);
-        count_launches(1 + (1 + L.depth_passes) + 1 + 6 + (1 + L.tile_passes) + 1);
+        count_launches(1 + L.depth_passes + 1 + 6 + (1 + L.tile_passes) + 1);
     }
     prof_begin(ST_COMPOSITE_FWD, st);
     if (L.key_bytes == 8)

@@ -37,6 +37,29 @@ __device__ __forceinline__ int64_t load_count(const uint32_t *n_dev, int64_t n_h
     return n_dev ? (int64_t)(*n_dev) : n_host;
 }
 
+// Producer-side histograms: a kernel that writes keys can count their digits
+// in shared bins (block_hist_add) and flush them once per block
+// (block_hist_flush), which saves onesweep_histogram's extra pass over the
+// keys; the sort is then run with hist_ready = true after sort_reset.
+__device__ __forceinline__ void block_hist_zero(uint32_t (*h)[256], int npass) {
+    for (int i = threadIdx.x; i < npass * 256; i += blockDim.x) (&h[0][0])[i] = 0u;
+}
+
+template <typename K>
+__device__ __forceinline__ void block_hist_add(uint32_t (*h)[256], K key, int begin_bit, int end_bit) {
+    for (int p = 0, shift = begin_bit; shift < end_bit; p++, shift += 8) {
+        const int nb = min(8, end_bit - shift);
+        atomicAdd(&h[p][(uint32_t)(key >> shift) & ((1u << nb) - 1u)], 1u);
+    }
+}
+
+__device__ __forceinline__ void block_hist_flush(uint32_t (*h)[256], int npass, uint32_t *hist) {
+    for (int i = threadIdx.x; i < npass * 256; i += blockDim.x) {
+        const uint32_t v = (&h[0][0])[i];
+        if (v) atomicAdd(&hist[i], v);
+    }
+}
+
 // Global digit histograms of all passes: hist[p][d], p = 0..npasses-1.
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads)
@@ -239,23 +262,42 @@ inline SortScratch sort_scratch(void *base, int64_t max_n) {
     return s;
 }
 
-inline int radix_passes(int begin_bit, int end_bit) {
-    return (int)ceil_div(end_bit - begin_bit, kRadixBits);
-}
 
 // Stable sort of keys (+ optional u32 values) over bits [begin_bit, end_bit).
 // Ping-pongs (k0,v0) <-> (k1,v1); returns 0 if the result is in buffer 0.
 // `max_n` bounds the count (grids, status rows); the live count is n_dev or n_host.
-template <typename K, bool HAS_VAL, int ITEMS = kSortItems>
-int radix_sort(K *k0, uint32_t *v0, K *k1, uint32_t *v1, const uint32_t *n_dev, int64_t n_host,
-               int64_t max_n, int begin_bit, int end_bit, const SortScratch &s, cudaStream_t st) {
+inline int radix_passes(int begin_bit, int end_bit) {
+    return (int)ceil_div(end_bit - begin_bit, kRadixBits);
+}
+
+template <int ITEMS = kSortItems>
+inline int64_t sort_tile_count(int64_t max_n) {
+    return ceil_div(max_n > 0 ? max_n : 1, (int64_t)kSortThreads * ITEMS);
+}
+
+// Clears what one sort over bits [begin_bit, end_bit) uses: tile counters,
+// histograms, its look-back status rows.
+template <int ITEMS = kSortItems>
+inline void sort_reset(const SortScratch &s, int64_t max_n, int begin_bit, int end_bit, cudaStream_t st) {
     const int npass = radix_passes(begin_bit, end_bit);
-    const int64_t tiles = ceil_div(max_n > 0 ? max_n : 1, (int64_t)kSortThreads * ITEMS);
-    cudaMemsetAsync(s.tile_ctr, 0,   // tile counters + histograms + this sort's status rows
+    const int64_t tiles = sort_tile_count<ITEMS>(max_n);
+    cudaMemsetAsync(s.tile_ctr, 0,
                     (size_t)(reinterpret_cast<char *>(s.status + (int64_t)npass * tiles * kRadix) -
                              reinterpret_cast<char *>(s.tile_ctr)), st);
-    const unsigned hgrid = (unsigned)min64(tiles * 2, 148 * 8);
-    onesweep_histogram<K><<<hgrid, kSortThreads, 0, st>>>(k0, n_dev, n_host, begin_bit, end_bit, s.hist);
+}
+
+// hist_ready: the producer already filled the histograms after sort_reset.
+template <typename K, bool HAS_VAL, int ITEMS = kSortItems>
+int radix_sort(K *k0, uint32_t *v0, K *k1, uint32_t *v1, const uint32_t *n_dev, int64_t n_host,
+               int64_t max_n, int begin_bit, int end_bit, const SortScratch &s, cudaStream_t st,
+               bool hist_ready = false) {
+    const int npass = radix_passes(begin_bit, end_bit);
+    const int64_t tiles = sort_tile_count<ITEMS>(max_n);
+    if (!hist_ready) {
+        sort_reset<ITEMS>(s, max_n, begin_bit, end_bit, st);
+        const unsigned hgrid = (unsigned)min64(tiles * 2, 148 * 8);
+        onesweep_histogram<K><<<hgrid, kSortThreads, 0, st>>>(k0, n_dev, n_host, begin_bit, end_bit, s.hist);
+    }
     int cur = 0;
     for (int p = 0; p < npass; p++) {
         const int shift = begin_bit + p * kRadixBits;
