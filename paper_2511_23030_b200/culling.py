@@ -173,6 +173,7 @@ class _CacheEntry:
     chunk_size: float
     generation: int
     result: frozenset
+    t3: tuple = ()   # translation as Python floats (the query's prefilter)
 
 
 @dataclass
@@ -193,18 +194,22 @@ class VisibilityCache:
         # Most recent matching entry, as the reference scan (culling.py:213-229).
         # A vectorised distance prefilter (with a relative margin) limits the
         # exact per-entry test to plausible entries; the verdict is the exact one.
-        if self._entries:
-            tr = np.array([e.translation for e in self._entries])
-            d = np.sqrt(((tr - pose.translation) ** 2).sum(axis=1))
-            near = np.flatnonzero(d < self.cfg.pose_quantum_m * (1 + 1e-9) + 1e-300)
-            for i in near[::-1]:
-                e = self._entries[int(i)]
-                if self._match(e, pose, intr, generation, s):
-                    self._entries.append(self._entries.pop(int(i)))
+        if self._entries:   # newest first; plain-float prefilter (with margin), exact match after
+            px, py, pz = (float(v) for v in pose.translation)
+            lim = self.cfg.pose_quantum_m * (1 + 1e-9) + 1e-300
+            for i in range(len(self._entries) - 1, -1, -1):
+                e = self._entries[i]
+                ex, ey, ez = e.t3
+                dx, dy, dz = ex - px, ey - py, ez - pz
+                if math.sqrt((dx * dx + dy * dy) + dz * dz) < lim and self._match(e, pose, intr, generation, s):
+                    self._entries.append(self._entries.pop(i))
                     return set(e.result), True
+        if callable(candidates):   # built only on a miss
+            candidates = candidates()
         result = visible_chunks(pose, intr, extent, existing, self.cfg, s, candidates)
         self._entries.append(_CacheEntry(pose.translation.copy(), pose.rotation.copy(), intr, s,
-                                         generation, frozenset(result)))
+                                         generation, frozenset(result),
+                                         tuple(float(v) for v in pose.translation)))
         if len(self._entries) > self.cfg.cache_capacity:
             del self._entries[: len(self._entries) - self.cfg.cache_capacity]
         return set(result), False

@@ -265,7 +265,7 @@ class MappingEngine:
             return set(), False
         return self.cache.query(pose, self.intr, ChunkExtent(*ext), self.store.has_chunk,
                                 self.store.generation, self.store.chunk_size,
-                                candidates=self.store.known_chunk_ids())
+                                candidates=self.store.known_chunk_ids)
 
     # ------------------------------------------------------------ device
     def _device_pass(self, kf: Keyframe, slots, n: int, backward: bool = True):

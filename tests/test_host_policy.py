@@ -170,3 +170,75 @@ def test_synthetic_workloads_are_canonical():
     ids = grid.encode_positions(s.positions, 1.0)
     assert len(np.unique(ids)) == 128        # the 8x8x2 chunk grid
     assert len(room_poses(16)) == 16
+
+
+def test_select_keyframe_fast_path_equals_generator_path():
+    """select_keyframe with the precomputed uniform (plain-Python pairwise sum,
+    cumsum, searchsorted) picks what NumPy's Generator.choice picks, for
+    candidate lists below and above NumPy's 8-element pairwise block."""
+    rng = np.random.default_rng(11)
+    for trial in range(400):
+        k = int(rng.integers(1, 40))
+        pos = rng.uniform(-1, 1, (k, 3))
+        ia = select.KeyframeIndex(config=select.SelectConfig(grid_resolution_m=1e6))
+        ib = select.KeyframeIndex(config=select.SelectConfig(grid_resolution_m=1e6))
+        for i in range(k):
+            ia.add(i, pos[i])
+            ib.add(i, pos[i])
+        for i in range(k):
+            loss = float(rng.uniform(0, 3) * (rng.random() > 0.2))
+            select.record_loss(i, loss, ia)
+            select.record_loss(i, loss, ib)
+        seed = int(rng.integers(0, 2**63))
+        a = select.select_keyframe(list(range(k)), ia, seed)
+        b = select.select_keyframe(list(range(k)), ib, seed, uniform=select.draw_uniform(seed))
+        assert a == b, trial
+
+
+def test_visibility_cache_fast_scan_equals_vectorised_scan():
+    """VisibilityCache.query's plain-float newest-first scan returns the same
+    entry (result, hit flag, LRU order) as the vectorised prefilter it replaced
+    (the reference's most-recent-match scan, culling.py:213-229)."""
+    from paper_2511_23030_b200.core import CameraIntrinsics, Pose, quat_normalize
+    from paper_2511_23030_b200.culling import ChunkExtent, CullConfig, VisibilityCache, _CacheEntry
+    from paper_2511_23030_b200.grid import ChunkCoord
+
+    class Old(VisibilityCache):   # the replaced implementation
+        def query(self, pose, intr, extent, existing, generation, s, candidates=None):
+            if self._entries:
+                tr = np.array([e.translation for e in self._entries])
+                d = np.sqrt(((tr - pose.translation) ** 2).sum(axis=1))
+                for i in np.flatnonzero(d < self.cfg.pose_quantum_m * (1 + 1e-9) + 1e-300)[::-1]:
+                    e = self._entries[int(i)]
+                    if self._match(e, pose, intr, generation, s):
+                        self._entries.append(self._entries.pop(int(i)))
+                        return set(e.result), True
+            res = frozenset({len(self._entries)})   # a marker per miss
+            self._entries.append(_CacheEntry(pose.translation.copy(), pose.rotation.copy(), intr, s,
+                                             generation, res, tuple(float(v) for v in pose.translation)))
+            if len(self._entries) > self.cfg.cache_capacity:
+                del self._entries[: len(self._entries) - self.cfg.cache_capacity]
+            return set(res), False
+
+    import paper_2511_23030_b200.culling as C
+    rng = np.random.default_rng(3)
+    intr = CameraIntrinsics(fx=100.0, fy=100.0, cx=50.0, cy=40.0, width=100, height=80, near=0.05)
+    ext = ChunkExtent(ChunkCoord(0, 0, 0), ChunkCoord(1, 1, 1))
+    cfg = CullConfig()
+    new, old = VisibilityCache(cfg), Old(cfg)
+    base = [rng.uniform(-1, 1, 3) for _ in range(20)]
+    real = C.visible_chunks
+    try:   # the same marker results on both sides
+        for t in range(3000):
+            b = base[int(rng.integers(0, len(base)))]
+            tr = b + rng.normal(scale=cfg.pose_quantum_m * rng.choice([0.2, 0.7, 1.0, 3.0]), size=3)
+            q = quat_normalize(np.array([1.0, 0, 0, 0]) + rng.normal(scale=1e-3, size=4))
+            pose = Pose(rotation=q, translation=tr)
+            gen = int(rng.integers(0, 2))
+            C.visible_chunks = lambda *a, **k: {len(new._entries)}
+            ra = new.query(pose, intr, ext, lambda c: True, gen, 10.0, candidates=lambda: [])
+            rb = old.query(pose, intr, ext, lambda c: True, gen, 10.0)
+            assert ra == rb, t
+            assert [e.t3 for e in new._entries] == [e.t3 for e in old._entries]
+    finally:
+        C.visible_chunks = real
