@@ -384,6 +384,7 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
               float *__restrict__ st_tlast, int32_t *__restrict__ st_last, uint32_t *__restrict__ tile_work) {
     constexpr int NT = kTilePx;
     __shared__ ProjRec s_rec[NT];
+    __shared__ int4 s_box[NT];
     __shared__ uint32_t s_rank[NT];
     __shared__ int s_maxlast;
     const int tile = blockIdx.x;
@@ -401,20 +402,25 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
         if (idx < end) {
             const uint32_t rk = (uint32_t)(ikeys[idx] & rank_mask);
             s_rank[threadIdx.x] = rk;
-            s_rec[threadIdx.x] = recs[rk];
+            const ProjRec r = recs[rk];
+            s_rec[threadIdx.x] = r;
+            s_box[threadIdx.x] = make_int4(rec_x0(r), rec_x1(r) - rec_x0(r), rec_y0(r), rec_y1(r) - rec_y0(r));
         }
         __syncthreads();
         const int cnt = (int)min((uint32_t)NT, end - base);
         if (!all_done) {
             for (int j = 0; j < cnt; j++) {
+                const int4 bx = s_box[j];   // x0, x1 - x0, y0, y1 - y0 (decoded once at staging)
+                if (bx.z + bx.w < wy0 || bx.z > wy0 + 1) continue;   // warp-uniform row cull
+                if ((unsigned)(px - bx.x) > (unsigned)bx.y || (unsigned)(py - bx.z) > (unsigned)bx.w) continue;
                 const ProjRec &g = s_rec[j];
-                const int y0 = rec_y0(g), y1 = rec_y1(g);
-                if (y1 < wy0 || y0 > wy0 + 1) continue;   // warp-uniform row cull
-                const int x0 = rec_x0(g);
-                if ((unsigned)(px - x0) > (unsigned)(rec_x1(g) - x0)) continue;
-                const float dx = (float)(px - x0) + g.ox;
-                float dy, pw;
-                if (row_eval(g, dx, px, py, y0, y1, p64, order, s_rank[j], dy, pw)) {
+                // row_eval's expression and decision order
+                const float dx = (float)(px - bx.x) + g.ox;
+                const float dy = (float)(py - bx.z) + g.oy;
+                const float pw = dx * (g.ia * dx + 2.f * g.ib * dy) + g.ic * dy * dy;
+                const float d = pw - kPowCut;
+                const bool hit = fabsf(d) <= g.eps ? !(quad_q64(p64[order[s_rank[j]]], px, py) > 9.0) : d >= 0.f;
+                if (hit) {
                     s.add(g, pw, (int32_t)(base + j));
                     if (s.done) {
                         all_done = true;
