@@ -172,40 +172,18 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-// Shared by forward and backward so both take identical decisions.
-// Returns true when pixel (px,py) receives a contribution (in box, q <= 9).
-__device__ __forceinline__ bool pair_eval(const ProjRec &g, int px, int py, const Proj64 *p64,
-                                          const uint32_t *order, uint32_t rank, float &dx,
-                                          float &dy, float &pw) {
-    const int x0 = g.x0y0 & 0xffff, y0 = g.x0y0 >> 16;
-    const int x1 = (int)(short)(g.x1y1 & 0xffff), y1 = g.x1y1 >> 16;
-    if ((unsigned)(px - x0) > (unsigned)(x1 - x0) || (unsigned)(py - y0) > (unsigned)(y1 - y0))
-        return false;
-    dx = (float)(px - x0) + g.ox;
-    dy = (float)(py - y0) + g.oy;
-    pw = dx * (g.ia * dx + 2.f * g.ib * dy) + g.ic * dy * dy;
+// The q <= 9 decision (renderloss.py:141) both compositing kernels take for
+// pixel (px, py) inside a splat's box: pw = dx (ia dx + 2 ib dy) + ic dy^2 in
+// fp32 (dx = (px - x0) + ox, dy = (py - y0) + oy); when |pw - kPowCut| lies
+// within the splat's error band eps the exact fp64 quad_q64 decides.  The
+// forward and the backward evaluate pw in different (fp32 / packed fp32x2)
+// orders; outside the band both equal the exact verdict, inside it both use
+// quad_q64, so they always agree.
+__device__ __forceinline__ bool q_within_cutoff(float pw, float eps, const Proj64 *p64,
+                                                const uint32_t *order, uint32_t rank, int px, int py) {
     const float d = pw - kPowCut;
-    if (fabsf(d) <= g.eps) return !(quad_q64(p64[order[rank]], px, py) > 9.0);
-    return d >= 0.f;
+    return fabsf(d) <= eps ? !(quad_q64(p64[order[rank]], px, py) > 9.0) : d >= 0.f;
 }
-
-// Two-pixel variant used by the compositing kernels: the column test and dx
-// are shared by the thread's pixel pair (same px, rows py and py + 1).
-// Same expression and decision order as pair_eval, so results are identical.
-__device__ __forceinline__ bool row_eval(const ProjRec &g, float dx, int px, int py, int y0, int y1,
-                                         const Proj64 *p64, const uint32_t *order, uint32_t rank,
-                                         float &dy, float &pw) {
-    if ((unsigned)(py - y0) > (unsigned)(y1 - y0)) return false;
-    dy = (float)(py - y0) + g.oy;
-    pw = dx * (g.ia * dx + 2.f * g.ib * dy) + g.ic * dy * dy;
-    const float d = pw - kPowCut;
-    if (fabsf(d) <= g.eps) return !(quad_q64(p64[order[rank]], px, py) > 9.0);
-    return d >= 0.f;
-}
-
-// Compositing CTA: one 16x16 tile, 128 threads, each thread owns the pixel
-// pair (px, py), (px, py + 1); warp w covers tile rows 4w .. 4w + 3.
-constexpr int kCompThreads = 128;
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }

@@ -243,8 +243,8 @@ composite_bwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
             if (y1 < wy0 || y0 > wy0 + 3) continue;   // warp-uniform row cull
             const int k = bstart + j;
             const int x0 = rec_x0(g);
-            // both rows at once; the same q <= 9 decisions as the forward's
-            // row_eval (an fp32 q outside the error band decides alike)
+            // both rows at once; the same q <= 9 decisions as the forward
+            // (q_within_cutoff: an fp32 q outside the error band decides alike)
             const float dx = (float)(px - x0) + g.ox;
             const float2 dy = make_float2((float)(py - y0) + g.oy, (float)(py + 1 - y0) + g.oy);
             const float2 pw = fma2(dy, fma2(f2s(g.ic), dy, f2s(2.f * g.ib * dx)), f2s(g.ia * dx * dx));
@@ -252,12 +252,9 @@ composite_bwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
             const bool col = (unsigned)(px - x0) <= (unsigned)(rec_x1(g) - x0);
             bool h0 = col && (unsigned)(py - y0) <= (unsigned)(y1 - y0) && k <= pp.last0;
             bool h1 = col && (unsigned)(py + 1 - y0) <= (unsigned)(y1 - y0) && k <= pp.last1;
-            if ((h0 && fabsf(d.x) <= g.eps) || (h1 && fabsf(d.y) <= g.eps)) {   // rare: fp64
-                const Proj64 q = p64[order[s_rank[j]]];
-                if (h0 && fabsf(d.x) <= g.eps) h0 = !(quad_q64(q, px, py) > 9.0);
-                else h0 = h0 && d.x >= 0.f;
-                if (h1 && fabsf(d.y) <= g.eps) h1 = !(quad_q64(q, px, py + 1) > 9.0);
-                else h1 = h1 && d.y >= 0.f;
+            if ((h0 && fabsf(d.x) <= g.eps) || (h1 && fabsf(d.y) <= g.eps)) {   // rare: fp64 band
+                h0 = h0 && q_within_cutoff(pw.x, g.eps, p64, order, s_rank[j], px, py);
+                h1 = h1 && q_within_cutoff(pw.y, g.eps, p64, order, s_rank[j], px, py + 1);
             } else {
                 h0 = h0 && d.x >= 0.f;
                 h1 = h1 && d.y >= 0.f;
@@ -322,8 +319,8 @@ __device__ __forceinline__ void sum_slots(const ProjRec &g, uint32_t mask, int64
 // block each, fixed-assignment partial sums + fixed-order tree -> g2d[rank].  Smaller splats
 // are summed inline by project_bwd.  Both orders are fixed: deterministic.
 __global__ void __launch_bounds__(256)
-grad_gather_big(const ProjRec *__restrict__ recs, const uint32_t *__restrict__ tcount_r,
-                const uint32_t *__restrict__ toff, const sm_render_counters *ctr,
+grad_gather_big(const ProjRec *__restrict__ recs, const uint32_t *__restrict__ toff,
+                const sm_render_counters *ctr,
                 const uint32_t *__restrict__ big, const float *__restrict__ gbuf,
                 const int32_t *__restrict__ tile_hor, int tiles_x, float *__restrict__ g2d) {
     __shared__ BigRowTable tab;
@@ -562,7 +559,7 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
         launch_composite_bwd<uint32_t>(b, L, dims, d_rgb, d_depth, d_alpha, st);
     prof_end(ST_COMPOSITE_BWD, st);
     prof_begin(ST_GRAD_GATHER, st);
-    grad_gather_big<<<148 * 4, 256, 0, st>>>(b.rec_sorted, b.tcount_r, b.toff, b.ctr, b.tcount, b.gbuf,
+    grad_gather_big<<<148 * 4, 256, 0, st>>>(b.rec_sorted, b.toff, b.ctr, b.tcount, b.gbuf,
                                               b.tile_hor, L.tiles_x, b.g2d);
     prof_end(ST_GRAD_GATHER, st);
     count_launches(3);

@@ -414,13 +414,10 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
                 if (bx.z + bx.w < wy0 || bx.z > wy0 + 1) continue;   // warp-uniform row cull
                 if ((unsigned)(px - bx.x) > (unsigned)bx.y || (unsigned)(py - bx.z) > (unsigned)bx.w) continue;
                 const ProjRec &g = s_rec[j];
-                // row_eval's expression and decision order
                 const float dx = (float)(px - bx.x) + g.ox;
                 const float dy = (float)(py - bx.z) + g.oy;
                 const float pw = dx * (g.ia * dx + 2.f * g.ib * dy) + g.ic * dy * dy;
-                const float d = pw - kPowCut;
-                const bool hit = fabsf(d) <= g.eps ? !(quad_q64(p64[order[s_rank[j]]], px, py) > 9.0) : d >= 0.f;
-                if (hit) {
+                if (q_within_cutoff(pw, g.eps, p64, order, s_rank[j], px, py)) {
                     s.add(g, pw, (int32_t)(base + j));
                     if (s.done) {
                         all_done = true;

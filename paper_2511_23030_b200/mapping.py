@@ -344,7 +344,10 @@ class MappingEngine:
         g = torch.cuda.CUDAGraph()
         gid = lib.sm_profile_capture_begin()
         try:
-            with torch.cuda.graph(g, stream=self._cap_stream):
+            # thread-local capture: the streamer's reader / writer threads keep
+            # synchronising events and page-locking buffers while a graph is
+            # captured, which would invalidate a global-mode capture
+            with torch.cuda.graph(g, stream=self._cap_stream, capture_error_mode="thread_local"):
                 self._device_pass(kf, slots, n)
                 self._adam(slots, n)
                 self._queue_readback()
