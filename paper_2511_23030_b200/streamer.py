@@ -104,7 +104,7 @@ class ChunkStreamer:
         self._prefetched: dict[Path, object] = {}
         self.stats = {"prefetch_hits": 0, "pending_hits": 0, "victim_hits": 0, "async_writes": 0, "alloc_pinned": 0,
                       "alloc_device": 0, "alloc_s": 0.0, "read_s": 0.0, "stage_wait_s": 0.0,
-                      "validate_wait_s": 0.0}
+                      "validate_wait_s": 0.0, "read_file_s": 0.0, "unpack_s": 0.0, "write_async_s": 0.0}
 
     # ---------------------------------------------------------------- staging
     def _staging(self, nbytes: int):
@@ -188,6 +188,13 @@ class ChunkStreamer:
                 self._free_pins.append(src.pin)
 
     def read_file(self, path: Path):
+        t0 = time.perf_counter()
+        try:
+            return self._read_file(path)
+        finally:
+            self.stats["read_file_s"] += time.perf_counter() - t0
+
+    def _read_file(self, path: Path):
         """PinnedFile of `path` from the prefetch tier or the disk, or a
         DeviceRecords if its eviction write is still pending."""
         path = Path(path)
@@ -246,6 +253,13 @@ class ChunkStreamer:
         return slot
 
     def unpack_into(self, src, records: np.ndarray | None, n: int, stride: int, offset: int) -> None:
+        t0 = time.perf_counter()
+        try:
+            self._unpack_into(src, records, n, stride, offset)
+        finally:
+            self.stats["unpack_s"] += time.perf_counter() - t0
+
+    def _unpack_into(self, src, records: np.ndarray | None, n: int, stride: int, offset: int) -> None:
         """Chunk records -> slab rows [offset, offset + n) (K8)."""
         if n == 0:
             self.release(src)
@@ -315,6 +329,13 @@ class ChunkStreamer:
         return pin[:nbytes].numpy().copy()
 
     def write_async(self, path: Path, header: bytes, offset: int, n: int, stride: int) -> None:
+        t0 = time.perf_counter()
+        try:
+            self._write_async(path, header, offset, n, stride)
+        finally:
+            self.stats["write_async_s"] += time.perf_counter() - t0
+
+    def _write_async(self, path: Path, header: bytes, offset: int, n: int, stride: int) -> None:
         """Write-behind eviction of slab rows [offset, offset+n) to `path`."""
         torch = self.torch
         nbytes = n * stride
