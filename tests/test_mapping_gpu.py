@@ -160,3 +160,25 @@ def test_device_keyframe_tier_follows_store_lru(cuda, tmp_path):
     assert a.store.stats.keyframe_writes > 0 and a.store.stats.keyframe_loads > 0
     hw = a.store.slab.high_water()
     assert torch.equal(a.store.slab.params[:hw], b.store.slab.params[:hw])
+
+
+def test_instance_overflow_recovers_identically(cuda, tmp_path):
+    """A render workspace too small for the step's tile instances flags
+    overflow (device counter, no partial image), the step skips Adam, grows
+    the workspace and retries: results equal a run that never overflowed."""
+    import torch
+    a = _c1_engine(tmp_path / "a", budget=100_000)
+    b = _c1_engine(tmp_path / "b", budget=100_000)
+    assert a.optimization_step(0, 0).loss == b.optimization_step(0, 0).loss
+    d = a.render.dims
+    a.render.dims = type(d)(d.max_gaussians, 4096, d.width, d.height)   # far below the need
+    a.render.ws = torch.empty(a.render.lib.sm_render_workspace_size(a.render.dims), dtype=torch.uint8,
+                              device="cuda")
+    a.drop_graphs()
+    for s in range(1, 5):
+        ra = a.optimization_step(0, s)
+        rb = b.optimization_step(0, s)
+        assert ra.selected_kf == rb.selected_kf and ra.loss == rb.loss
+    assert a.render.dims.max_instances > 4096
+    hw = a.store.slab.high_water()
+    assert torch.equal(a.store.slab.params[:hw], b.store.slab.params[:hw])
