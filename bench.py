@@ -325,6 +325,7 @@ def main():
                 else "fallback 6.65 TB/s",
                 # the compositing kernels are issue / FP32-pipe bound, not HBM bound
                 "issue_active_pct": nk.get("issue_pct") if nk else None,
+                "fma_pipe_active_pct": nk.get("fma_pipe_pct") if nk else None,
                 "sm_throughput_pct": nk.get("sm_pct") if nk else None}
         for k, v in stages.items():
             f = STAGE_BYTES.get(k)

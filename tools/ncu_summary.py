@@ -28,6 +28,8 @@ METRICS = {
     "launch__block_size": "block",
     "sm__cycles_active.avg": "cyc_avg",
     "sm__cycles_active.max": "cyc_max",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_pipe_pct",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
 }
 
 
@@ -65,8 +67,8 @@ def main():
     for rec in recs:
         by_kernel.setdefault(rec["kernel"], rec)
     out.with_suffix(".json").write_text(json.dumps({"report": rep.name, "kernels": by_kernel}, indent=1))
-    cols = ["kernel", "us", "traffic_bytes", "dram_gbs", "sm_pct", "issue_pct", "warps_pct", "regs", "grid",
-            "block", "inst", "cyc_avg", "cyc_max"]
+    cols = ["kernel", "us", "traffic_bytes", "dram_gbs", "sm_pct", "issue_pct", "fma_pipe_pct", "warps_pct",
+            "regs", "grid", "block", "inst", "cyc_avg", "cyc_max"]
     lines = [f"# ncu --set full summary ({rep.name})", "",
              "Times are ncu's (serialised launch, cache flushed, its own clock control); "
              "use them for shares and counters, not as bench numbers.", "",
