@@ -215,6 +215,7 @@ class MappingEngine:
         self._pinned_kf: dict[int, tuple] = {}
         self._uniforms: dict[int, float] = {}
         self._eager_seen: dict = {}
+        self._layout_cache: dict = {}   # visible ids -> (store.layout_version, (slots, n))
 
     # -------------------------------------------------------------- inputs
     def add_keyframe(self, kf: Keyframe, index_usage: int | None = None) -> None:
@@ -440,11 +441,20 @@ class MappingEngine:
                                    uniform=pre)
         kf = store.keyframe_get(selected)
         visible, _ = self._visible_for_pose(kf.pose)
-        overlap_val = overlap(visible, store.resident_chunk_ids()) if visible else None
+        # overlap(visible, resident) (select.py), counted without building the sets
+        overlap_val = store.resident_count_of(visible) / len(visible) if visible else None
         ids = sorted(visible)
         if ids:
             store.ensure_resident(ids)
-        slots, n = self.active.build(store.segments(ids))
+        ids_t = tuple(ids)
+        ent = self._layout_cache.get(ids_t)
+        if ent is not None and ent[0] == store.layout_version:   # same chunks at the same rows
+            slots, n = ent[1]
+        else:
+            slots, n = self.active.build(store.segments(ids))
+            if len(self._layout_cache) >= 64:
+                self._layout_cache.clear()
+            self._layout_cache[ids_t] = (store.layout_version, (slots, n))
         loss = self.train_view(kf, slots, n)
         record_loss(selected, loss, self.index)
         kf.last_loss = loss
