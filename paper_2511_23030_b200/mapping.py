@@ -324,10 +324,10 @@ class MappingEngine:
         if nxt not in self._uniforms:
             self._uniforms = {nxt: draw_uniform(derive_seed(self.seed, 2, nxt))}
 
-    def _graph_key(self, kf: Keyframe, slots, n: int):
+    def _graph_key(self, kf: Keyframe, slots, n: int, dp: bool = False):
         s = self.store.slab
         return (kf.id, slots.data_ptr(), n, s.params.data_ptr(), s.grads.data_ptr(),
-                self.render.ws.data_ptr(), self.upload_keyframes_each_step)
+                self.render.ws.data_ptr(), self.upload_keyframes_each_step, dp)
 
     def drop_graphs(self) -> None:
         lib = _lib.load()
@@ -335,8 +335,9 @@ class MappingEngine:
             lib.sm_profile_graph_free(gid)
         self._graphs = {}
 
-    def _capture(self, kf: Keyframe, slots, n: int):
-        """Capture fwd -> loss -> bwd -> Adam -> readback as one CUDA graph."""
+    def _capture(self, kf: Keyframe, slots, n: int, dp: bool = False):
+        """Capture fwd -> loss -> bwd -> Adam -> readback as one CUDA graph
+        (dp: fwd -> loss -> bwd only; the all-reduce and Adam follow eagerly)."""
         torch, lib = self.torch, _lib.load()
         if not hasattr(self, "_cap_stream"):
             self._cap_stream = torch.cuda.Stream(device=self.device)
@@ -350,11 +351,33 @@ class MappingEngine:
             # captured, which would invalidate a global-mode capture
             with torch.cuda.graph(g, stream=self._cap_stream, capture_error_mode="thread_local"):
                 self._device_pass(kf, slots, n)
-                self._adam(slots, n)
-                self._queue_readback()
+                if not dp:
+                    self._adam(slots, n)
+                    self._queue_readback()
         finally:
             lib.sm_profile_capture_end()
-        self._graphs[self._graph_key(kf, slots, n)] = (g, gid)
+        self._graphs[self._graph_key(kf, slots, n, dp)] = (g, gid)
+
+    def _dp_device_pass(self, kf: Keyframe, slots, n: int) -> None:
+        """fwd -> loss -> bwd of this rank's keyframe: graph replay when captured,
+        else eager (captured on the second visit, like train_view)."""
+        self.render.ensure(n, kf.intrinsics.width, kf.intrinsics.height)
+        key = self._graph_key(kf, slots, n, True)
+        entry = getattr(self, "_graphs", {}).get(key) if self.use_graphs else None
+        if entry is not None:
+            g, gid = entry
+            g.replay()
+            self.counter_replays += 1
+            _lib.load().sm_profile_graph_replayed(gid)
+            return
+        self.counter_eager += 1
+        self._device_pass(kf, slots, n)
+        if self.use_graphs and n:
+            seen = self._eager_seen.get(key, 0) + 1
+            self._eager_seen[key] = seen
+            if seen >= self.capture_after:
+                self._capture(kf, slots, n, dp=True)
+                self._eager_seen.pop(key, None)
 
     def train_view(self, kf: Keyframe, slots, n: int) -> float:
         """One device iteration with overflow recovery; returns the loss.
@@ -503,7 +526,7 @@ class MappingEngine:
         slots_u, n_u = self._union_set.build(store.segments(union))
         slab = store.slab
         for _ in range(6):
-            self._device_pass(kfs[rank], slots_m, n_m)
+            self._dp_device_pass(kfs[rank], slots_m, n_m)
             buf = self._lossbuf
             buf.zero_()
             buf[rank:rank + 1].copy_(self.loss.out[:1])
@@ -515,6 +538,7 @@ class MappingEngine:
                 break
             slab.grads.zero_()
             self.render.grow_instances(self.render.counters()["n_instances"] * 2)
+            self.drop_graphs()
         else:
             raise DeviceFailure("tile-instance buffer kept overflowing")
         self._adam_noskip(slots_u, n_u)
