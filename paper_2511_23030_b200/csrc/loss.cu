@@ -26,6 +26,11 @@ namespace sm {
 constexpr int kLW = 32, kLH = 16;   // output tile (columns x rows)
 constexpr int kHW = kLW + 10, kHH = kLH + 10;   // + 5-px halo each side
 __constant__ float c_gw[11];
+__constant__ float c_gwp[18];   // c_gwp[j + 3] = c_gw[j] for j in [0, 11), zero elsewhere (j in [-3, 15))
+
+// tap weights of two neighbouring outputs (packed fp32x2 filters): output o
+// at input offset k uses c_gw[k - o]
+__device__ __forceinline__ float2 wpair(int k, int o) { return make_float2(c_gwp[k - o + 3], c_gwp[k - o + 2]); }
 
 struct LossAcc {
     double l1, ssim, dsum, dcount;
@@ -64,45 +69,45 @@ loss_fwd_kernel(const float *__restrict__ rgb, const float *__restrict__ depth,
     // horizontal: 26 rows x 32 centres, 4 consecutive centres per thread
     for (int it = threadIdx.x; it < kHH * (kLW / 4); it += 256) {
         const int r = it / (kLW / 4), c0 = 4 * (it % (kLW / 4));
-        float a[5][4];
+        float2 a[5][2];   // [stat][outputs (0,1) | (2,3)], packed fp32x2
 #pragma unroll
-        for (int t = 0; t < 5; t++)
-#pragma unroll
-            for (int o = 0; o < 4; o++) a[t][o] = 0.f;
+        for (int t = 0; t < 5; t++) a[t][0] = a[t][1] = f2s(0.f);
 #pragma unroll
         for (int k = 0; k < 14; k++) {
             const float xv = sx[r][c0 + k], yv = sy[r][c0 + k];
             const float v[5] = {xv, yv, xv * xv, yv * yv, xv * yv};
+            const float2 w01 = wpair(k, 0), w23 = wpair(k, 2);   // zero taps outside the window
 #pragma unroll
-            for (int o = 0; o < 4; o++) {
-                if (k - o >= 0 && k - o < 11) {
-                    const float w = c_gw[k - o];
-#pragma unroll
-                    for (int t = 0; t < 5; t++) a[t][o] += w * v[t];
-                }
+            for (int t = 0; t < 5; t++) {
+                a[t][0] = fma2(w01, f2s(v[t]), a[t][0]);
+                a[t][1] = fma2(w23, f2s(v[t]), a[t][1]);
             }
         }
 #pragma unroll
-        for (int t = 0; t < 5; t++)
-#pragma unroll
-            for (int o = 0; o < 4; o++) hs[t][r][c0 + o] = a[t][o];
+        for (int t = 0; t < 5; t++) {
+            hs[t][r][c0 + 0] = a[t][0].x;
+            hs[t][r][c0 + 1] = a[t][0].y;
+            hs[t][r][c0 + 2] = a[t][1].x;
+            hs[t][r][c0 + 3] = a[t][1].y;
+        }
     }
     __syncthreads();
     // vertical: 16 x 32 outputs, 2 rows per thread
     const int lx = threadIdx.x % kLW, ly0 = 2 * (threadIdx.x / kLW);
-    float m[2][5];
+    float2 m2[5];   // (row ly0, row ly0 + 1) per statistic
 #pragma unroll
-    for (int o = 0; o < 2; o++)
-#pragma unroll
-        for (int t = 0; t < 5; t++) m[o][t] = 0.f;
+    for (int t = 0; t < 5; t++) m2[t] = f2s(0.f);
 #pragma unroll
     for (int k = 0; k < 12; k++) {
+        const float2 w = wpair(k, 0);
 #pragma unroll
-        for (int t = 0; t < 5; t++) {
-            const float h = hs[t][ly0 + k][lx];
-            if (k < 11) m[0][t] += c_gw[k] * h;
-            if (k >= 1) m[1][t] += c_gw[k - 1] * h;
-        }
+        for (int t = 0; t < 5; t++) m2[t] = fma2(w, f2s(hs[t][ly0 + k][lx]), m2[t]);
+    }
+    float m[2][5];
+#pragma unroll
+    for (int t = 0; t < 5; t++) {
+        m[0][t] = m2[t].x;
+        m[1][t] = m2[t].y;
     }
     float s_val = 0.f, l1 = 0.f, dsum = 0.f, dcnt = 0.f;
 #pragma unroll
@@ -209,45 +214,43 @@ loss_bwd_kernel(const float *__restrict__ rgb, const float *__restrict__ depth,
     __syncthreads();
     for (int it = threadIdx.x; it < kHH * (kLW / 4); it += 256) {   // adjoint, horizontal
         const int r = it / (kLW / 4), c0 = 4 * (it % (kLW / 4));
-        float a[3][4];
+        float2 a[3][2];   // symmetric kernel: adjoint = same taps
 #pragma unroll
-        for (int t = 0; t < 3; t++)
-#pragma unroll
-            for (int o = 0; o < 4; o++) a[t][o] = 0.f;
+        for (int t = 0; t < 3; t++) a[t][0] = a[t][1] = f2s(0.f);
 #pragma unroll
         for (int k = 0; k < 14; k++) {
-            float v[3];
+            const float2 w01 = wpair(k, 0), w23 = wpair(k, 2);
 #pragma unroll
-            for (int t = 0; t < 3; t++) v[t] = sm3[t][r][c0 + k];
-#pragma unroll
-            for (int o = 0; o < 4; o++) {
-                if (k - o >= 0 && k - o < 11) {
-                    const float w = c_gw[k - o];   // symmetric kernel: adjoint = same taps
-#pragma unroll
-                    for (int t = 0; t < 3; t++) a[t][o] += w * v[t];
-                }
+            for (int t = 0; t < 3; t++) {
+                const float v = sm3[t][r][c0 + k];
+                a[t][0] = fma2(w01, f2s(v), a[t][0]);
+                a[t][1] = fma2(w23, f2s(v), a[t][1]);
             }
         }
 #pragma unroll
-        for (int t = 0; t < 3; t++)
-#pragma unroll
-            for (int o = 0; o < 4; o++) ha[t][r][c0 + o] = a[t][o];
+        for (int t = 0; t < 3; t++) {
+            ha[t][r][c0 + 0] = a[t][0].x;
+            ha[t][r][c0 + 1] = a[t][0].y;
+            ha[t][r][c0 + 2] = a[t][1].x;
+            ha[t][r][c0 + 3] = a[t][1].y;
+        }
     }
     __syncthreads();
     const int lx = threadIdx.x % kLW, ly0 = 2 * (threadIdx.x / kLW);
-    float a[2][3];
+    float2 a2[3];
 #pragma unroll
-    for (int o = 0; o < 2; o++)
-#pragma unroll
-        for (int t = 0; t < 3; t++) a[o][t] = 0.f;
+    for (int t = 0; t < 3; t++) a2[t] = f2s(0.f);
 #pragma unroll
     for (int k = 0; k < 12; k++) {
+        const float2 w = wpair(k, 0);
 #pragma unroll
-        for (int t = 0; t < 3; t++) {
-            const float h = ha[t][ly0 + k][lx];
-            if (k < 11) a[0][t] += c_gw[k] * h;
-            if (k >= 1) a[1][t] += c_gw[k - 1] * h;
-        }
+        for (int t = 0; t < 3; t++) a2[t] = fma2(w, f2s(ha[t][ly0 + k][lx]), a2[t]);
+    }
+    float a[2][3];
+#pragma unroll
+    for (int t = 0; t < 3; t++) {
+        a[0][t] = a2[t].x;
+        a[1][t] = a2[t].y;
     }
     const float Nf = (float)((double)W * H);
     const float Nc = (float)((double)(W - 10) * (H - 10));
@@ -308,6 +311,10 @@ int loss_forward_backward(const float *rgb, const float *depth, const uint8_t *g
         float wf[11];
         for (int i = 0; i < 11; i++) wf[i] = (float)(w[i] / s);
         cudaError_t e = cudaMemcpyToSymbol(c_gw, wf, sizeof(wf));
+        if (e != cudaSuccess) return cuda_status(e, "loss weights");
+        float wp[18] = {0};
+        for (int i = 0; i < 11; i++) wp[i + 3] = wf[i];
+        e = cudaMemcpyToSymbol(c_gwp, wp, sizeof(wp));
         if (e != cudaSuccess) return cuda_status(e, "loss weights");
         g_weights_set = true;
     }
