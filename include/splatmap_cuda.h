@@ -95,6 +95,20 @@ int sm_render_forward(const float *params, const int32_t *slots, int64_t n,
                       void *workspace, int64_t workspace_bytes,
                       float *out_rgb, float *out_depth, float *out_alpha, void *stream);
 
+/* sm_render_forward with a caller-kept tile schedule for one view (no
+ * reference counterpart; renderloss.py:170 render_arrays is the computation).
+ * tile_order: device uint32 [tiles_x * tiles_y], a permutation of the tile
+ * indices (identity for a view's first render).  The compositing CTAs take
+ * their tiles in this order, and on return it holds this render's
+ * longest-first order (tiles ranked by the instances the backward revisits),
+ * so re-rendering the same view (a mapping keyframe) starts its heaviest
+ * tiles first.  Outputs are identical to sm_render_forward for any
+ * permutation: tiles are independent. */
+int sm_render_forward_ordered(const float *params, const int32_t *slots, int64_t n,
+                              const sm_camera *cam, const sm_render_dims *dims,
+                              void *workspace, int64_t workspace_bytes, uint32_t *tile_order,
+                              float *out_rgb, float *out_depth, float *out_alpha, void *stream);
+
 /* Reverse-order backward of the last sm_render_forward on this workspace
  * (no reference counterpart: the reference is forward-only, README.md:125).
  * Upstream grads d_* are (H,W,3)/(H,W)/(H,W) fp32, each nullable (= zero).

@@ -77,6 +77,8 @@ def load():
     _sig(lib.sm_render_workspace_size, i64, POINTER(RenderDims))
     _sig(lib.sm_render_forward, c_int, vp, vp, i64, POINTER(Camera), POINTER(RenderDims), vp, i64,
          vp, vp, vp, vp)
+    _sig(lib.sm_render_forward_ordered, c_int, vp, vp, i64, POINTER(Camera), POINTER(RenderDims), vp,
+         i64, vp, vp, vp, vp, vp)
     _sig(lib.sm_render_backward, c_int, vp, vp, i64, POINTER(Camera), POINTER(RenderDims), vp, i64,
          vp, vp, vp, vp, vp)
     _sig(lib.sm_set_ellipse_cull, None, c_int)

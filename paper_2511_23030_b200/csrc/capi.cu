@@ -70,7 +70,20 @@ int sm_render_forward(const float *params, const int32_t *slots, int64_t n, cons
         return SM_ERR_INVALID;
     }
     return render_forward(params, slots, n, *cam, *dims, workspace, workspace_bytes, out_rgb,
-                          out_depth, out_alpha, SM_STREAM(stream));
+                          out_depth, out_alpha, nullptr, SM_STREAM(stream));
+}
+
+int sm_render_forward_ordered(const float *params, const int32_t *slots, int64_t n, const sm_camera *cam,
+                              const sm_render_dims *dims, void *workspace, int64_t workspace_bytes,
+                              uint32_t *tile_order, float *out_rgb, float *out_depth, float *out_alpha,
+                              void *stream) {
+    if (!cam || !dims || !workspace || !tile_order || !out_rgb || !out_depth || !out_alpha ||
+        (n > 0 && !params)) {
+        set_error("sm_render_forward_ordered: null argument");
+        return SM_ERR_INVALID;
+    }
+    return render_forward(params, slots, n, *cam, *dims, workspace, workspace_bytes, out_rgb,
+                          out_depth, out_alpha, tile_order, SM_STREAM(stream));
 }
 
 int sm_render_backward(const float *params, const int32_t *slots, int64_t n, const sm_camera *cam,

@@ -219,7 +219,7 @@ __device__ __forceinline__ void project_geometry(double px, double py, double pz
 
 int render_forward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,
                    const sm_render_dims &dims, void *ws, int64_t ws_bytes, float *out_rgb,
-                   float *out_depth, float *out_alpha, cudaStream_t st);
+                   float *out_depth, float *out_alpha, uint32_t *view_order, cudaStream_t st);
 int render_backward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,
                     const sm_render_dims &dims, void *ws, int64_t ws_bytes, const float *d_rgb,
                     const float *d_depth, const float *d_alpha, float *grads, cudaStream_t st);

@@ -381,13 +381,15 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
               const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
               int height, int tiles_x, float *__restrict__ out_rgb, float *__restrict__ out_depth,
               float *__restrict__ out_alpha, float4 *__restrict__ st_cd, float *__restrict__ st_t,
-              float *__restrict__ st_tlast, int32_t *__restrict__ st_last, uint32_t *__restrict__ tile_work) {
+              float *__restrict__ st_tlast, int32_t *__restrict__ st_last, uint32_t *__restrict__ tile_work,
+              const uint32_t *__restrict__ launch_order) {
     constexpr int NT = kTilePx;
     __shared__ ProjRec s_rec[NT];
     __shared__ int4 s_box[NT];
     __shared__ uint32_t s_rank[NT];
     __shared__ int s_maxlast;
-    const int tile = blockIdx.x;
+    // longest-first when the caller keeps the previous render's order of this view
+    const int tile = launch_order ? (int)launch_order[blockIdx.x] : (int)blockIdx.x;
     const int ty0 = (tile / tiles_x) * kTile;
     const int px = (tile % tiles_x) * kTile + (threadIdx.x & (kTile - 1));
     const int py = ty0 + threadIdx.x / kTile;
@@ -443,10 +445,12 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
 // of the tiles into 64 work buckets, heaviest bucket first (one block).  The
 // backward's CTAs then start heavy tiles first and light ones fill in behind
 // them (LPT), shortening the tail.  Order inside a bucket is arbitrary: tiles
-// are independent, so results do not depend on it.
+// are independent, so results do not depend on it.  `keep` (nullable) gets
+// a copy: the next forward of the same view launches in this order.
 constexpr int kWorkBuckets = 64;
 __global__ void __launch_bounds__(1024)
-order_tiles(const uint32_t *__restrict__ work, int n_tiles, uint32_t *__restrict__ order) {
+order_tiles(const uint32_t *__restrict__ work, int n_tiles, uint32_t *__restrict__ order,
+            uint32_t *__restrict__ keep) {
     __shared__ uint32_t hist[kWorkBuckets], base[kWorkBuckets];
     __shared__ uint32_t wmax;
     if (threadIdx.x < kWorkBuckets) hist[threadIdx.x] = 0;
@@ -466,8 +470,11 @@ order_tiles(const uint32_t *__restrict__ work, int n_tiles, uint32_t *__restrict
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < n_tiles; i += blockDim.x)
-        order[atomicAdd(&base[kWorkBuckets - 1 - min(work[i] / div, (uint32_t)kWorkBuckets - 1)], 1u)] = (uint32_t)i;
+    for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) {
+        const uint32_t o = atomicAdd(&base[kWorkBuckets - 1 - min(work[i] / div, (uint32_t)kWorkBuckets - 1)], 1u);
+        order[o] = (uint32_t)i;
+        if (keep) keep[o] = (uint32_t)i;
+    }
 }
 
 int g_ellipse_cull = 1;   // sm_set_ellipse_cull (tests: culled == unculled, bit for bit)
@@ -515,18 +522,19 @@ static void bin_tiles(const RenderBufs &b, const RenderLayout &L, const sm_rende
 
 template <typename KeyT>
 static void launch_composite_fwd(const RenderBufs &b, const RenderLayout &L, const sm_render_dims &dims,
-                                 float *out_rgb, float *out_depth, float *out_alpha, cudaStream_t st) {
+                                 float *out_rgb, float *out_depth, float *out_alpha, uint32_t *view_order,
+                                 cudaStream_t st) {
     const KeyT rank_mask = (KeyT)((1ull << L.rank_bits) - 1ull);
     const KeyT *ik = static_cast<const KeyT *>(L.tile_passes & 1 ? b.ikey1 : b.ikey0);
     composite_fwd<KeyT><<<(unsigned)L.n_tiles, kTilePx, 0, st>>>(
         b.ranges, ik, rank_mask, b.rec_sorted, b.p64, b.order0, dims.width, dims.height, L.tiles_x,
-        out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, b.tile_work);
-    order_tiles<<<1, 1024, 0, st>>>(b.tile_work, (int)L.n_tiles, b.tile_order);
+        out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, b.tile_work, view_order);
+    order_tiles<<<1, 1024, 0, st>>>(b.tile_work, (int)L.n_tiles, b.tile_order, view_order);
 }
 
 int render_forward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,
                    const sm_render_dims &dims, void *ws, int64_t ws_bytes, float *out_rgb,
-                   float *out_depth, float *out_alpha, cudaStream_t st) {
+                   float *out_depth, float *out_alpha, uint32_t *view_order, cudaStream_t st) {
     const RenderLayout L = render_layout(dims);
     if (ws_bytes < L.total) {
         set_error("render workspace too small: %lld < %lld", (long long)ws_bytes, (long long)L.total);
@@ -578,9 +586,9 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
     }
     prof_begin(ST_COMPOSITE_FWD, st);
     if (L.key_bytes == 8)
-        launch_composite_fwd<unsigned long long>(b, L, dims, out_rgb, out_depth, out_alpha, st);
+        launch_composite_fwd<unsigned long long>(b, L, dims, out_rgb, out_depth, out_alpha, view_order, st);
     else
-        launch_composite_fwd<uint32_t>(b, L, dims, out_rgb, out_depth, out_alpha, st);
+        launch_composite_fwd<uint32_t>(b, L, dims, out_rgb, out_depth, out_alpha, view_order, st);
     prof_end(ST_COMPOSITE_FWD, st);
     count_launches(2);
     SM_CHECK_LAUNCH("render_forward");

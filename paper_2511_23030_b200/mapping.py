@@ -216,6 +216,7 @@ class MappingEngine:
         self._uniforms: dict[int, float] = {}
         self._eager_seen: dict = {}
         self._layout_cache: dict = {}   # visible ids -> (store.layout_version, (slots, n))
+        self._tile_orders: dict[int, object] = {}   # keyframe id -> its longest-first tile schedule
 
     # -------------------------------------------------------------- inputs
     def add_keyframe(self, kf: Keyframe, index_usage: int | None = None) -> None:
@@ -227,6 +228,24 @@ class MappingEngine:
 
     def _drop_device_keyframe(self, kid: int) -> None:
         self._kf_dev.pop(kid, None)
+        self._tile_orders.pop(kid, None)
+        # captured graphs of this keyframe read the dropped buffers
+        graphs = getattr(self, "_graphs", {})
+        stale = [k for k in graphs if k[0] == kid]
+        if stale:
+            lib = _lib.load()
+            for k in stale:
+                lib.sm_profile_graph_free(graphs.pop(k)[1])
+
+    view_tile_order = True   # keep each keyframe's longest-first tile schedule
+
+    def _tile_order(self, kf: Keyframe):
+        if not self.view_tile_order:
+            return None
+        o = self._tile_orders.get(kf.id)
+        if o is None:
+            o = self._tile_orders[kf.id] = self.render.new_tile_order(kf.intrinsics.width, kf.intrinsics.height)
+        return o
 
     def device_keyframe_ids(self) -> set[int]:
         return {k for k in self._kf_dev if k >= 0}
@@ -274,7 +293,8 @@ class MappingEngine:
         slab = self.store.slab
         cam = camera_for(kf.pose, kf.intrinsics)
         dk = self._device_keyframe(kf)
-        self.render.forward(slab.params, slots, n, cam, self.rgb, self.depth, self.alpha)
+        self.render.forward(slab.params, slots, n, cam, self.rgb, self.depth, self.alpha,
+                            tile_order=self._tile_order(kf))
         if getattr(dk, "pending", None) is not None:   # join the side-stream upload
             self.torch.cuda.current_stream(self.device).wait_stream(dk.pending)
             dk.pending = None

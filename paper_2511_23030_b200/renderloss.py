@@ -129,13 +129,33 @@ class RenderEngine:
     def ws_bytes(self) -> int:
         return int(self.ws.numel())
 
-    def forward(self, params, slots, n: int, cam: _lib.Camera, rgb, depth, alpha, stream=None):
+    def forward(self, params, slots, n: int, cam: _lib.Camera, rgb, depth, alpha, stream=None,
+                tile_order=None):
+        """tile_order: optional per-view int32 device tensor (``new_tile_order``)
+        carrying the view's longest-first tile schedule from render to render."""
         self.ensure(n, cam.width, cam.height)
-        rc = self.lib.sm_render_forward(_lib.ptr(params), _lib.ptr(slots), int(n), ctypes.byref(cam),
-                                        ctypes.byref(self.dims), _lib.ptr(self.ws), self.ws_bytes,
-                                        _lib.ptr(rgb), _lib.ptr(depth), _lib.ptr(alpha),
-                                        _lib.stream_handle(stream))
+        if tile_order is None:
+            rc = self.lib.sm_render_forward(_lib.ptr(params), _lib.ptr(slots), int(n), ctypes.byref(cam),
+                                            ctypes.byref(self.dims), _lib.ptr(self.ws), self.ws_bytes,
+                                            _lib.ptr(rgb), _lib.ptr(depth), _lib.ptr(alpha),
+                                            _lib.stream_handle(stream))
+        else:
+            if tile_order.numel() != self.n_tiles(cam.width, cam.height):
+                raise ValueError("tile_order does not match the camera's tile count")
+            rc = self.lib.sm_render_forward_ordered(_lib.ptr(params), _lib.ptr(slots), int(n),
+                                                    ctypes.byref(cam), ctypes.byref(self.dims),
+                                                    _lib.ptr(self.ws), self.ws_bytes, _lib.ptr(tile_order),
+                                                    _lib.ptr(rgb), _lib.ptr(depth), _lib.ptr(alpha),
+                                                    _lib.stream_handle(stream))
         _lib.check(rc, "render_forward")
+
+    @staticmethod
+    def n_tiles(width: int, height: int) -> int:
+        return ((width + 15) // 16) * ((height + 15) // 16)
+
+    def new_tile_order(self, width: int, height: int):
+        """Identity schedule for a view's first render (device int32)."""
+        return self.torch.arange(self.n_tiles(width, height), dtype=self.torch.int32, device=self.device)
 
     def backward(self, params, slots, n: int, cam: _lib.Camera, d_rgb, d_depth, d_alpha, grads,
                  stream=None):

@@ -147,6 +147,8 @@ def test_device_keyframe_tier_follows_store_lru(cuda, tmp_path):
         assert ra.selected_kf == rb.selected_kf and ra.loss == rb.loss
         assert a.device_keyframe_ids() <= a.store.resident_keyframe_ids()
         assert len(a.store.resident_keyframe_ids()) <= 3
+        # graphs captured for an evicted keyframe read its dropped buffers: gone too
+        assert {k[0] for k in getattr(a, "_graphs", {})} <= a.store.resident_keyframe_ids()
     for kid in (0, 1, 2):   # evicted keyframes come back from their .dkf files
         losses = []
         for e in (a, b):

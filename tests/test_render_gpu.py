@@ -285,6 +285,59 @@ def test_wide_instance_keys_bit_identical(cuda):
         assert torch.equal(a, b), name
 
 
+def test_view_tile_order_bit_identical(cuda):
+    """sm_render_forward_ordered (a view's longest-first tile schedule carried
+    from render to render): images and gradients equal the plain forward's
+    for the identity, the learned and a random schedule; the returned order is
+    a permutation with non-increasing revisit work (64 buckets)."""
+    import torch
+
+    from paper_2511_23030_b200 import renderloss as rl
+    scene, pose, intr, rng = _grad_case(9, n=4000, w=200, h=136)
+    sa = rl.SceneArrays(**scene)
+    params = torch.from_numpy(rl.pack_params(sa)).cuda()
+    cam = rl.camera_for(pose, intr)
+    h, w = intr.height, intr.width
+    d_rgb = torch.as_tensor(rng.normal(size=(h, w, 3)), dtype=torch.float32).cuda()
+    d_depth = torch.as_tensor(rng.normal(size=(h, w)) * 0.1, dtype=torch.float32).cuda()
+    eng = rl.RenderEngine()
+    nt = eng.n_tiles(w, h)
+
+    def run(order):
+        out = [torch.empty((h, w, 3), device="cuda"), torch.empty((h, w), device="cuda"),
+               torch.empty((h, w), device="cuda")]
+        eng.forward(params, None, len(sa), cam, *out, tile_order=order)
+        grads = torch.zeros_like(params)
+        eng.backward(params, None, len(sa), cam, d_rgb, d_depth, None, grads)
+        torch.cuda.synchronize()
+        return out + [grads]
+
+    ref = run(None)
+    order = eng.new_tile_order(w, h)
+    shuffled = torch.as_tensor(rng.permutation(nt).astype(np.int32)).cuda()
+    for o in (order, order, shuffled):
+        got = run(o)
+        for name, a, b in zip(("rgb", "depth", "alpha", "grads"), ref, got):
+            assert torch.equal(a, b), name
+        assert torch.equal(torch.sort(o).values, torch.arange(nt, dtype=torch.int32, device="cuda"))
+    lay = eng.dims
+    r = eng.ws[eng.lib.sm_render_ws_offset(lay, 0):][: 8 * nt].view(torch.int32).view(nt, 2).cpu().numpy()
+    last = eng.ws[eng.lib.sm_render_ws_offset(lay, 1):][: 4 * h * w].view(torch.int32).cpu().numpy()
+    last = last.reshape(h, w)
+    work = np.zeros(nt, np.int64)
+    tx = (w + 15) // 16
+    for t in range(nt):
+        blk = last[(t // tx) * 16:(t // tx) * 16 + 16, (t % tx) * 16:(t % tx) * 16 + 16]
+        m = int(blk.max())
+        work[t] = m - r[t, 0] + 1 if m >= r[t, 0] else 0
+    wo = work[shuffled.cpu().numpy()]
+    div = max(1, (int(work.max()) + 63) // 64)
+    bucket = np.minimum(wo // div, 63)
+    assert np.all(np.diff(bucket) <= 0), bucket[:20]
+    with pytest.raises(ValueError):
+        eng.forward(params, None, len(sa), cam, *ref[:3], tile_order=order[:-1])
+
+
 def _gpu_depth_order(scene, pose, intr):
     import torch
 

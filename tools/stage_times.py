@@ -19,6 +19,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--no-view-order", action="store_true", help="plain forward tile order (A/B)")
     args = ap.parse_args()
     import torch
 
@@ -26,6 +27,7 @@ def main():
     from paper_2511_23030_b200.workloads import build_c2
     lib = _lib.load()
     eng = build_c2(args.n, 16, store_dir=tempfile.mkdtemp())
+    eng.view_tile_order = not args.no_view_order
     eng.warm_graphs()
     for s in range(10):
         eng.optimization_step(0, s)
