@@ -5,8 +5,11 @@
 writes paper_2511_23030_b200/libsplatmap_cuda.<name>.so (git-ignored; it
 travels to the GPU box with the snapshot).  Select it at run time with
 SM_LIB_VARIANT=<name>, e.g. to time two kernel versions in one gpurun call.
+SM_NVCC_EXTRA adds nvcc flags (e.g. -DSM_BWD_MINB=4); `git stash create`
+gives a revision of the uncommitted working tree.
 """
 
+import os
 import subprocess
 import sys
 import tempfile
@@ -28,7 +31,8 @@ def main():
         for src in B.SOURCES:
             obj = Path(td) / (Path(src).stem + ".o")
             subprocess.run([B.nvcc(), *B.ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                            "--expt-relaxed-constexpr", "-I", str(Path(td) / "include"), "-c",
+                            "--expt-relaxed-constexpr", "-I", str(Path(td) / "include"),
+                            *os.environ.get("SM_NVCC_EXTRA", "").split(), "-c",
                             str(csrc / src), "-o", str(obj)], check=True)
             objs.append(str(obj))
         out = ROOT / "paper_2511_23030_b200" / f"libsplatmap_cuda.{name}.so"
