@@ -217,6 +217,24 @@ __device__ __forceinline__ void project_geometry(double px, double py, double pz
     (void)b01;
 }
 
+// A second branch of the caller's stream (one per host thread and device)
+// for launches that can overlap the main chain: begin() forks it off the
+// caller's stream, end() joins it back, so every entry point keeps the
+// caller-stream semantics and CUDA-graph capture records the two branches.
+struct StreamFork {
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    void begin(cudaStream_t st) {
+        cudaEventRecord(fork, st);
+        cudaStreamWaitEvent(side, fork, 0);
+    }
+    void end(cudaStream_t st) {
+        cudaEventRecord(join, side);
+        cudaStreamWaitEvent(st, join, 0);
+    }
+};
+StreamFork &stream_fork();
+
 int render_forward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,
                    const sm_render_dims &dims, void *ws, int64_t ws_bytes, float *out_rgb,
                    float *out_depth, float *out_alpha, uint32_t *view_order, cudaStream_t st);

@@ -378,30 +378,53 @@ struct CamBwd {
 
 // K6: per depth rank, chain the 2D grads through the fp64 projection and
 // accumulate the 14 parameter grads into the slot-indexed grad records.
+// Two launches on two branches of the stream: small splats (their instance
+// slots summed inline) run while grad_gather_big sums the big ones, which a
+// second, small launch over the big-splat queue then finishes.  Each splat's
+// grads are written by exactly one of them: identical results.
 #ifndef SM_PBWD_MINB
 #define SM_PBWD_MINB 3   // 3 x 256 threads per SM (<= 85 registers): measured best of 1-3
 #endif
+__device__ __forceinline__ void project_bwd_rank(int64_t r, const float (&gk)[10], const float4 *params,
+                                                 const int32_t *slots, const CamBwd &cam,
+                                                 const uint32_t *order, float *grads);
+
 __global__ void __launch_bounds__(256, SM_PBWD_MINB)
-project_bwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots, int64_t n,
-            CamBwd cam, const uint32_t *__restrict__ order, const uint32_t *__restrict__ tcount_r,
-            const uint32_t *__restrict__ tmask_r,
-            const ProjRec *__restrict__ recs, const uint32_t *__restrict__ toff,
-            const float *__restrict__ gbuf, const int32_t *__restrict__ tile_hor, int tiles_x,
-            const float *__restrict__ g2d, float *__restrict__ grads) {
+project_bwd_small(const float4 *__restrict__ params, const int32_t *__restrict__ slots, int64_t n,
+                  CamBwd cam, const uint32_t *__restrict__ order, const uint32_t *__restrict__ tcount_r,
+                  const uint32_t *__restrict__ tmask_r, const ProjRec *__restrict__ recs,
+                  const uint32_t *__restrict__ toff, const float *__restrict__ gbuf,
+                  const int32_t *__restrict__ tile_hor, int tiles_x, float *__restrict__ grads) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     const uint32_t cnt = tcount_r[r];
     if (cnt == 0) return;
-    float gk[10];
     const ProjRec rec = recs[r];
-    if (bbox_tiles(rec) > kEmitSmall) {   // summed by grad_gather_big
+    if (bbox_tiles(rec) > kEmitSmall) return;   // project_bwd_big
+    float gk[10];
+#pragma unroll
+    for (int k = 0; k < 10; k++) gk[k] = 0.f;
+    sum_slots(rec, tmask_r[r], r, toff[r], gbuf, tile_hor, tiles_x, gk);
+    project_bwd_rank(r, gk, params, slots, cam, order, grads);
+}
+
+__global__ void __launch_bounds__(64)
+project_bwd_big(const float4 *__restrict__ params, const int32_t *__restrict__ slots, CamBwd cam,
+                const uint32_t *__restrict__ order, const sm_render_counters *ctr,
+                const uint32_t *__restrict__ big, const float *__restrict__ g2d, float *__restrict__ grads) {
+    const uint32_t nbig = ctr->overflow ? 0u : ctr->reserved[1];
+    for (uint32_t bi = blockIdx.x * blockDim.x + threadIdx.x; bi < nbig; bi += gridDim.x * blockDim.x) {
+        const int64_t r = big[bi];
+        float gk[10];
 #pragma unroll
         for (int k = 0; k < 10; k++) gk[k] = g2d[r * kG2dStride + k];
-    } else {
-#pragma unroll
-        for (int k = 0; k < 10; k++) gk[k] = 0.f;
-        sum_slots(rec, tmask_r[r], r, toff[r], gbuf, tile_hor, tiles_x, gk);
+        project_bwd_rank(r, gk, params, slots, cam, order, grads);
     }
+}
+
+__device__ __forceinline__ void project_bwd_rank(int64_t r, const float (&gk)[10], const float4 *params,
+                                                 const int32_t *slots, const CamBwd &cam,
+                                                 const uint32_t *order, float *grads) {
     const uint32_t i = order[r];
     const int64_t slot = slots ? (int64_t)slots[i] : (int64_t)i;
     const float4 A = params[slot * 4 + 0];
@@ -558,11 +581,6 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
     else
         launch_composite_bwd<uint32_t>(b, L, dims, d_rgb, d_depth, d_alpha, st);
     prof_end(ST_COMPOSITE_BWD, st);
-    prof_begin(ST_GRAD_GATHER, st);
-    grad_gather_big<<<148 * 4, 256, 0, st>>>(b.rec_sorted, b.toff, b.ctr, b.tcount, b.gbuf,
-                                              b.tile_hor, L.tiles_x, b.g2d);
-    prof_end(ST_GRAD_GATHER, st);
-    count_launches(3);
     CamBwd cb;
     for (int k = 0; k < 9; k++) cb.r[k] = cam.r_wc[k];
     for (int k = 0; k < 3; k++) cb.t[k] = cam.t[k];
@@ -570,11 +588,22 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
     cb.fy = cam.fy;
     cb.cx = cam.cx;
     cb.cy = cam.cy;
+    // big splats on a forked branch (b.tcount holds the big-splat queue)
+    StreamFork &fk = stream_fork();
+    fk.begin(st);
+    prof_begin(ST_GRAD_GATHER, fk.side);
+    grad_gather_big<<<148 * 4, 256, 0, fk.side>>>(b.rec_sorted, b.toff, b.ctr, b.tcount, b.gbuf,
+                                                   b.tile_hor, L.tiles_x, b.g2d);
+    project_bwd_big<<<148, 64, 0, fk.side>>>(reinterpret_cast<const float4 *>(params), slots, cb, b.order0,
+                                             b.ctr, b.tcount, b.g2d, grads);
+    prof_end(ST_GRAD_GATHER, fk.side);
     prof_begin(ST_PROJECT_BWD, st);
-    project_bwd<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+    project_bwd_small<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
         reinterpret_cast<const float4 *>(params), slots, n, cb, b.order0, b.tcount_r, b.tmask_r, b.rec_sorted,
-        b.toff, b.gbuf, b.tile_hor, L.tiles_x, b.g2d, grads);
+        b.toff, b.gbuf, b.tile_hor, L.tiles_x, grads);
     prof_end(ST_PROJECT_BWD, st);
+    fk.end(st);
+    count_launches(4);
     SM_CHECK_LAUNCH("render_backward");
     return SM_OK;
 }

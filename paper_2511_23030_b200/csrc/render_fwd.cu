@@ -477,6 +477,19 @@ order_tiles(const uint32_t *__restrict__ work, int n_tiles, uint32_t *__restrict
     }
 }
 
+StreamFork &stream_fork() {
+    static thread_local StreamFork forks[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    StreamFork &f = forks[dev & 63];
+    if (!f.side) {
+        cudaStreamCreateWithFlags(&f.side, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming);
+    }
+    return f;
+}
+
 int g_ellipse_cull = 1;   // sm_set_ellipse_cull (tests: culled == unculled, bit for bit)
 
 CamDev make_cam(const sm_camera &c, const RenderLayout &L) {
