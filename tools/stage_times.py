@@ -19,6 +19,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--blocks", type=int, default=5)
     ap.add_argument("--no-view-order", action="store_true", help="plain forward tile order (A/B)")
     args = ap.parse_args()
     import torch
@@ -32,13 +33,16 @@ def main():
     for s in range(10):
         eng.optimization_step(0, s)
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for s in range(args.steps):
-        eng.optimization_step(1, s)
-    b.record()
-    torch.cuda.synchronize()
-    plain = a.elapsed_time(b) / args.steps
+    blocks = []
+    for blk in range(args.blocks):   # plain step time: several blocks, median (box noise)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for s in range(args.steps):
+            eng.optimization_step(1, blk * args.steps + s)
+        b.record()
+        torch.cuda.synchronize()
+        blocks.append(a.elapsed_time(b) / args.steps)
+    plain = sorted(blocks)[len(blocks) // 2]
     lib.sm_profile_enable(1)
     eng.drop_graphs()
     eng.warm_graphs()
@@ -51,8 +55,11 @@ def main():
     out = {k: round(v[0] / args.steps, 4) for k, v in prof.items() if v[1]}
     out["_sum"] = round(sum(out.values()), 4)
     out["_step_ms"] = round(plain, 4)
+    out["_step_ms_min"] = round(min(blocks), 4)
     out["_visible"] = eng.counter_gaussians / max(eng.counter_steps, 1)
     out["_instances"] = eng.counter_instances / max(eng.counter_steps, 1)
+    ctr = eng.render.ws[:64].view(torch.int32).cpu().numpy()
+    out["_big_splats_last"] = int(ctr[5])   # sm_render_counters.reserved[1]: big-splat queue length
     print(json.dumps(out))
 
 
