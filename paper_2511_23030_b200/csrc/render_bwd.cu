@@ -589,20 +589,24 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
     cb.cx = cam.cx;
     cb.cy = cam.cy;
     // big splats on a forked branch (b.tcount holds the big-splat queue)
+#ifndef SM_FORK
+#define SM_FORK 1   // 0: one branch (A/B timing of the two launches)
+#endif
     StreamFork &fk = stream_fork();
-    fk.begin(st);
-    prof_begin(ST_GRAD_GATHER, fk.side);
-    grad_gather_big<<<148 * 4, 256, 0, fk.side>>>(b.rec_sorted, b.toff, b.ctr, b.tcount, b.gbuf,
+    if (SM_FORK) fk.begin(st);
+    cudaStream_t side = SM_FORK ? fk.side : st;
+    prof_begin(ST_GRAD_GATHER, side);
+    grad_gather_big<<<148 * 4, 256, 0, side>>>(b.rec_sorted, b.toff, b.ctr, b.tcount, b.gbuf,
                                                    b.tile_hor, L.tiles_x, b.g2d);
-    project_bwd_big<<<148, 64, 0, fk.side>>>(reinterpret_cast<const float4 *>(params), slots, cb, b.order0,
+    project_bwd_big<<<148, 64, 0, side>>>(reinterpret_cast<const float4 *>(params), slots, cb, b.order0,
                                              b.ctr, b.tcount, b.g2d, grads);
-    prof_end(ST_GRAD_GATHER, fk.side);
+    prof_end(ST_GRAD_GATHER, side);
     prof_begin(ST_PROJECT_BWD, st);
     project_bwd_small<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
         reinterpret_cast<const float4 *>(params), slots, n, cb, b.order0, b.tcount_r, b.tmask_r, b.rec_sorted,
         b.toff, b.gbuf, b.tile_hor, L.tiles_x, grads);
     prof_end(ST_PROJECT_BWD, st);
-    fk.end(st);
+    if (SM_FORK) fk.end(st);
     count_launches(4);
     SM_CHECK_LAUNCH("render_backward");
     return SM_OK;
