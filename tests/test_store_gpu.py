@@ -244,3 +244,84 @@ def test_streamer_device_reload_paths_bit_exact(cuda, tmp_path):
     s = st.streamer.stats
     assert s["victim_hits"] + s["pending_hits"] >= 2 and s["prefetch_hits"] >= 1, s
     st.flush()
+
+
+def test_hbm_cap_compaction_bit_exact(cuda, tmp_path):
+    """A slab under a hard HBM cap (C5's 8 GB, scaled down) never grows:
+    when no free extent fits a chunk it packs the resident segments to the
+    front (compaction).  Against an uncapped store driven by the same
+    operations (inserts in slices with flush + evict, paging, training-like
+    updates with Adam state): identical policy stats, identical resident rows
+    after every step and byte-identical files; the cap holds and a working
+    set that cannot fit raises HbmCapExceeded."""
+    import torch
+
+    from paper_2511_23030_b200.errors import HbmCapExceeded
+    from paper_2511_23030_b200.slab import GaussianSlab
+    from paper_2511_23030_b200.store import ChunkStore, StoreConfig
+    from paper_2511_23030_b200.workloads import c1_scene
+    from paper_2511_23030_b200.grid import encode_positions
+    scene = c1_scene(20_000)
+    # the map is built slice by slice like C5: whole chunks per slice (<= 2500 rows)
+    cid = encode_positions(scene.positions, 5.0)
+    order = np.argsort(cid, kind="stable")
+    starts = np.r_[0, np.flatnonzero(np.diff(cid[order])) + 1, len(order)]
+    slices, a = [], 0
+    for b0, b1 in zip(starts[:-1], starts[1:]):
+        if b1 - a > 2_500:
+            slices.append(order[a:b0])
+            a = b0
+    slices.append(order[a:])
+    # the reference policy loads a working set before it evicts down to the
+    # budget: the cap must hold budget + working set (+ segment slack)
+    cap_rows = 5_200
+    stores = []
+    for name, cap in (("free", None), ("capped", cap_rows * GaussianSlab.bytes_per_gaussian())):
+        st = ChunkStore(StoreConfig(disk_root=tmp_path / name, chunk_size_m=5.0, gaussian_budget=2_500,
+                                    io_ns_per_byte=1.0, hbm_cap_bytes=cap))
+        for idx in slices:
+            st.insert_arrays(scene.positions[idx], scene.rotations[idx], scene.scales[idx],
+                             scene.opacities[idx], scene.sh[idx])
+            st.flush()
+            st.evict_lru(st.stats.active_gaussians, protected=set())
+        stores.append(st)
+    free, capped = stores
+    assert capped.slab.capacity == cap_rows
+    ids = sorted(free.known_chunk_ids())
+    rng = np.random.default_rng(8)
+    for step in range(120):
+        want = []
+        for c in rng.permutation(ids):   # a random working set that fits the budget
+            if sum(free.chunk_gaussian_count(x) for x in want) + free.chunk_gaussian_count(c) <= 2_000:
+                want.append(int(c))
+            if len(want) >= rng.integers(2, 7):
+                break
+        reps = [st.ensure_resident(want) for st in stores]
+        assert reps[0] == reps[1]
+        for st in stores:   # "training": rows and Adam state change, chunks go dirty
+            for c in want:
+                ch = st.chunk(c)
+                rows = slice(ch.offset, ch.offset + ch.count)
+                st.slab.params[rows, 0:3] += 1e-3 * (step + 1)
+                st.slab.adam_m[rows, 0:14] += 1.0
+                st.slab.adam_m[rows, 14] += 1.0
+                st.slab.adam_v[rows, 0:14] += 0.5
+            st.mark_trained(want)
+        assert _stats(free) == _stats(capped)
+        assert free.resident_chunk_ids() == capped.resident_chunk_ids()
+        for c in want:
+            a, b = free.chunk(c), capped.chunk(c)
+            for name in ("params", "adam_m", "adam_v", "sh_rest"):
+                ta, tb = getattr(free.slab, name), getattr(capped.slab, name)
+                assert torch.equal(ta[a.offset:a.offset + a.count], tb[b.offset:b.offset + b.count]), (step, c)
+        assert capped.slab.capacity == cap_rows   # never grew
+    assert capped.slab.compactions > 0
+    for st in stores:
+        st.flush()
+        st.streamer.drain()
+    for c in ids:
+        name = f"{c:016x}.dcg"
+        assert (tmp_path / "free" / "chunks" / name).read_bytes() == \
+               (tmp_path / "capped" / "chunks" / name).read_bytes()
+    with pytest.raises(HbmCapExceeded):   # a working set larger than the cap
+        capped.ensure_resident(ids)
