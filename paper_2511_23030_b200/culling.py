@@ -174,6 +174,7 @@ class _CacheEntry:
     generation: int
     result: frozenset
     t3: tuple = ()   # translation as Python floats (the query's prefilter)
+    r4: tuple = ()   # rotation as Python floats
 
 
 @dataclass
@@ -188,6 +189,24 @@ class VisibilityCache:
                 and float(np.linalg.norm(e.translation - pose.translation)) < self.cfg.pose_quantum_m
                 and _rotation_angle(e.rotation, pose.rotation) < self.cfg.pose_quantum_rad)
 
+    def _match_fast(self, e: _CacheEntry, d: float, qa: tuple, pose: Pose, intr, generation: int,
+                    s: float) -> bool:
+        """_match's verdict from plain floats when both quantities are clear of
+        their thresholds (NumPy's norm / dot differ from these by a few ulp,
+        which moves the angle by < 1e-7 rad: far inside the margins), else
+        _match itself."""
+        if e.generation != generation or e.chunk_size != s or not (e.intr is intr or e.intr == intr):
+            return False
+        if e.r4 and d < self.cfg.pose_quantum_m * (1 - 1e-9):
+            r = e.r4
+            dot = abs(((r[0] * qa[0] + r[1] * qa[1]) + r[2] * qa[2]) + r[3] * qa[3])
+            ang = 2.0 * math.acos(min(1.0, dot))
+            if ang < self.cfg.pose_quantum_rad - 1e-6:
+                return True
+            if ang > self.cfg.pose_quantum_rad + 1e-6:
+                return False
+        return self._match(e, pose, intr, generation, s)
+
     def query(self, pose: Pose, intr: CameraIntrinsics, extent: ChunkExtent,
               existing: Callable[[int], bool], generation: int, s: float,
               candidates: Iterable[int] | None = None) -> tuple[set[int], bool]:
@@ -196,12 +215,16 @@ class VisibilityCache:
         # exact per-entry test to plausible entries; the verdict is the exact one.
         if self._entries:   # newest first; plain-float prefilter (with margin), exact match after
             px, py, pz = (float(v) for v in pose.translation)
+            qa = tuple(float(v) for v in pose.rotation)
             lim = self.cfg.pose_quantum_m * (1 + 1e-9) + 1e-300
             for i in range(len(self._entries) - 1, -1, -1):
                 e = self._entries[i]
                 ex, ey, ez = e.t3
                 dx, dy, dz = ex - px, ey - py, ez - pz
-                if math.sqrt((dx * dx + dy * dy) + dz * dz) < lim and self._match(e, pose, intr, generation, s):
+                d = math.sqrt((dx * dx + dy * dy) + dz * dz)
+                if d >= lim:
+                    continue
+                if self._match_fast(e, d, qa, pose, intr, generation, s):
                     self._entries.append(self._entries.pop(i))
                     return set(e.result), True
         if callable(candidates):   # built only on a miss
@@ -209,7 +232,8 @@ class VisibilityCache:
         result = visible_chunks(pose, intr, extent, existing, self.cfg, s, candidates)
         self._entries.append(_CacheEntry(pose.translation.copy(), pose.rotation.copy(), intr, s,
                                          generation, frozenset(result),
-                                         tuple(float(v) for v in pose.translation)))
+                                         tuple(float(v) for v in pose.translation),
+                                         tuple(float(v) for v in pose.rotation)))
         if len(self._entries) > self.cfg.cache_capacity:
             del self._entries[: len(self._entries) - self.cfg.cache_capacity]
         return set(result), False

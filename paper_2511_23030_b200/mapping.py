@@ -337,6 +337,15 @@ class MappingEngine:
     use_graphs = True
     capture_after = 2   # eager visits of a (keyframe, active set) before its graph is captured
 
+    _while_gpu = None
+
+    def _run_while_gpu(self) -> None:
+        """Host bookkeeping of the current step that does not need its loss
+        (store flags), run once while the device pass is in flight."""
+        f, self._while_gpu = self._while_gpu, None
+        if f is not None:
+            f()
+
     def _precompute_next_draw(self) -> None:
         """The next single-GPU step's uniform draw depends only on its derived
         seed (not on this step's loss): compute it while the GPU works."""
@@ -417,6 +426,7 @@ class MappingEngine:
             g.replay()
             self.counter_replays += 1
             self._precompute_next_draw()   # host work overlapped with the GPU pass
+            self._run_while_gpu()
             loss, overflow = self._finish_readback()
             _lib.load().sm_profile_graph_replayed(gid)
             if not overflow:
@@ -431,6 +441,7 @@ class MappingEngine:
             self._device_pass(kf, slots, n)
             self._adam(slots, n)
             self._queue_readback()
+            self._run_while_gpu()
             loss, overflow = self._finish_readback()
             if not overflow:
                 self.counter_steps += 1
@@ -480,8 +491,8 @@ class MappingEngine:
         except EmptyCandidates:
             candidates = [self.latest_kf]
         pre = self._uniforms.pop(self.step_counter, None)
-        selected = select_keyframe(candidates, self.index, derive_seed(self.seed, 2, self.step_counter),
-                                   uniform=pre)
+        seed = derive_seed(self.seed, 2, self.step_counter) if pre is None else None   # else unused
+        selected = select_keyframe(candidates, self.index, seed, uniform=pre)
         kf = store.keyframe_get(selected)
         visible, _ = self._visible_for_pose(kf.pose)
         # overlap(visible, resident) (select.py), counted without building the sets
@@ -498,13 +509,16 @@ class MappingEngine:
             if len(self._layout_cache) >= 64:
                 self._layout_cache.clear()
             self._layout_cache[ids_t] = (store.layout_version, (slots, n))
+        def bookkeeping():   # needs no loss: runs while the GPU works (train_view)
+            store.mark_keyframe_dirty(selected)
+            if ids:
+                store.mark_trained(ids)
+        self._while_gpu = bookkeeping
         loss = self.train_view(kf, slots, n)
+        self._run_while_gpu()   # (if train_view did not)
         record_loss(selected, loss, self.index)
         kf.last_loss = loss
         kf.usage_remaining = self.index.usage_of(selected)
-        store.mark_keyframe_dirty(selected)
-        if ids:
-            store.mark_trained(ids)
         self.step_counter += 1
         io = stats.io_nanos - io0
         step_ns = (io + NS_PER_RENDERED_GAUSSIAN * n + NS_PER_PIXEL * self.intr.width * self.intr.height

@@ -43,6 +43,18 @@ def main():
         torch.cuda.synchronize()
         blocks.append(a.elapsed_time(b) / args.steps)
     plain = sorted(blocks)[len(blocks) // 2]
+    # one captured step graph replayed back to back: the device time of a
+    # step without the host policy between steps
+    g = next(iter(eng._graphs.values()))[0]
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(10):
+        g.replay()
+    a.record()
+    for _ in range(args.steps):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    graph_only = a.elapsed_time(b) / args.steps
     lib.sm_profile_enable(1)
     eng.drop_graphs()
     eng.warm_graphs()
@@ -56,6 +68,7 @@ def main():
     out["_sum"] = round(sum(out.values()), 4)
     out["_step_ms"] = round(plain, 4)
     out["_step_ms_min"] = round(min(blocks), 4)
+    out["_graph_replay_ms"] = round(graph_only, 4)
     out["_visible"] = eng.counter_gaussians / max(eng.counter_steps, 1)
     out["_instances"] = eng.counter_instances / max(eng.counter_steps, 1)
     ctr = eng.render.ws[:64].view(torch.int32).cpu().numpy()
