@@ -183,6 +183,7 @@ class VisibilityCache:
 
     cfg: CullConfig = field(default_factory=CullConfig)
     _entries: list = field(default_factory=list)
+    version: int = 0   # bumped by every query (hits reorder the LRU)
 
     def _match(self, e: _CacheEntry, pose: Pose, intr, generation: int, s: float) -> bool:
         return (e.generation == generation and e.chunk_size == s and e.intr == intr
@@ -207,12 +208,28 @@ class VisibilityCache:
                 return False
         return self._match(e, pose, intr, generation, s)
 
+    def peek(self, pose: Pose, intr: CameraIntrinsics, generation: int, s: float) -> frozenset | None:
+        """The result a query would return from the cache now (None on a
+        miss), without touching the LRU order."""
+        px, py, pz = (float(v) for v in pose.translation)
+        qa = tuple(float(v) for v in pose.rotation)
+        lim = self.cfg.pose_quantum_m * (1 + 1e-9) + 1e-300
+        for i in range(len(self._entries) - 1, -1, -1):
+            e = self._entries[i]
+            ex, ey, ez = e.t3
+            dx, dy, dz = ex - px, ey - py, ez - pz
+            d = math.sqrt((dx * dx + dy * dy) + dz * dz)
+            if d < lim and self._match_fast(e, d, qa, pose, intr, generation, s):
+                return e.result
+        return None
+
     def query(self, pose: Pose, intr: CameraIntrinsics, extent: ChunkExtent,
               existing: Callable[[int], bool], generation: int, s: float,
               candidates: Iterable[int] | None = None) -> tuple[set[int], bool]:
         # Most recent matching entry, as the reference scan (culling.py:213-229).
         # A vectorised distance prefilter (with a relative margin) limits the
         # exact per-entry test to plausible entries; the verdict is the exact one.
+        self.version += 1
         if self._entries:   # newest first; plain-float prefilter (with margin), exact match after
             px, py, pz = (float(v) for v in pose.translation)
             qa = tuple(float(v) for v in pose.rotation)

@@ -326,7 +326,10 @@ class MappingEngine:
         self.counter_visited += int(ctr[6])   # instances the backward revisited
         return float(v[0]), bool(ctr[1])
 
+    counter_speculative = 0   # steps whose graph was launched before their host policy
+
     def reset_counters(self) -> None:
+        self.counter_speculative = 0
         self.counter_steps = 0
         self.counter_gaussians = 0
         self.counter_instances = 0
@@ -408,7 +411,61 @@ class MappingEngine:
                 self._capture(kf, slots, n, dp=True)
                 self._eager_seen.pop(key, None)
 
-    def train_view(self, kf: Keyframe, slots, n: int) -> float:
+    def _speculate(self) -> None:
+        """While the device pass runs: for every keyframe the next draw can
+        pick, what the next step's policy would hand the device if nothing
+        had to be paged -- its visible set as the visibility cache would
+        answer (peek: no LRU change), the active-set slots from the layout
+        cache and the captured graph.  The next step validates the entry of
+        the keyframe it draws (same latest keyframe, store generation, layout
+        and cache state, every visible chunk resident) and launches that graph
+        before running the policy, which then only has to agree with it; the
+        host policy time leaves the gap between device passes."""
+        self._spec = None
+        store = self.store
+        graphs = getattr(self, "_graphs", None)
+        if not self.use_graphs or not graphs or self.latest_kf is None or store.coord_extent() is None:
+            return
+        try:
+            cands = candidate_set(self.index.position_of(self.latest_kf), self.index)
+        except EmptyCandidates:
+            cands = [self.latest_kf]
+        gen, lv = store.generation, store.layout_version
+        out = {}
+        for c in cands:
+            kf = store._keyframes.get(c)   # resident keyframes only (no load, no LRU tick)
+            if kf is None:
+                continue
+            res = self.cache.peek(kf.pose, self.intr, gen, store.chunk_size)
+            if not res:
+                continue
+            ids_t = tuple(sorted(res))
+            ent = self._layout_cache.get(ids_t)
+            if ent is None or ent[0] != lv:
+                continue
+            slots, n = ent[1]
+            entry = graphs.get(self._graph_key(kf, slots, n))
+            if entry is not None:
+                out[c] = (ids_t, slots, n, kf, entry)
+        self._spec = (self.latest_kf, gen, lv, self.cache.version, out)
+
+    _spec = None
+
+    def _take_speculation(self, selected: int):
+        sp, self._spec = self._spec, None
+        if sp is None:
+            return None
+        latest, gen, lv, cv, out = sp
+        st = self.store
+        if (latest != self.latest_kf or gen != st.generation or lv != st.layout_version
+                or cv != self.cache.version):
+            return None
+        e = out.get(selected)
+        if e is None or st._keyframes.get(selected) is not e[3] or st.resident_count_of(e[0]) != len(e[0]):
+            return None
+        return e
+
+    def train_view(self, kf: Keyframe, slots, n: int, launched: bool = False) -> float:
         """One device iteration with overflow recovery; returns the loss.
 
         The first visit of a (keyframe, active set) runs eagerly and then
@@ -421,12 +478,16 @@ class MappingEngine:
         self.last_n = n
         graphs = getattr(self, "_graphs", {})
         entry = graphs.get(self._graph_key(kf, slots, n)) if self.use_graphs else None
+        if launched and entry is None:
+            raise RuntimeError("speculatively launched graph not found")
         if entry is not None:
             g, gid = entry
-            g.replay()
+            if not launched:   # (optimization_step launched it speculatively)
+                g.replay()
             self.counter_replays += 1
             self._precompute_next_draw()   # host work overlapped with the GPU pass
             self._run_while_gpu()
+            self._speculate()
             loss, overflow = self._finish_readback()
             _lib.load().sm_profile_graph_replayed(gid)
             if not overflow:
@@ -493,6 +554,10 @@ class MappingEngine:
         pre = self._uniforms.pop(self.step_counter, None)
         seed = derive_seed(self.seed, 2, self.step_counter) if pre is None else None   # else unused
         selected = select_keyframe(candidates, self.index, seed, uniform=pre)
+        spec = self._take_speculation(selected)
+        if spec is not None:   # launch first; the policy below then only confirms it
+            spec[4][0].replay()
+            self.counter_speculative += 1
         kf = store.keyframe_get(selected)
         visible, _ = self._visible_for_pose(kf.pose)
         # overlap(visible, resident) (select.py), counted without building the sets
@@ -509,12 +574,15 @@ class MappingEngine:
             if len(self._layout_cache) >= 64:
                 self._layout_cache.clear()
             self._layout_cache[ids_t] = (store.layout_version, (slots, n))
+        if spec is not None and (ids_t != spec[0] or slots.data_ptr() != spec[1].data_ptr() or n != spec[2]):
+            raise RuntimeError("speculative launch diverged from the step's policy")
+
         def bookkeeping():   # needs no loss: runs while the GPU works (train_view)
             store.mark_keyframe_dirty(selected)
             if ids:
                 store.mark_trained(ids)
         self._while_gpu = bookkeeping
-        loss = self.train_view(kf, slots, n)
+        loss = self.train_view(kf, slots, n, launched=spec is not None)
         self._run_while_gpu()   # (if train_view did not)
         record_loss(selected, loss, self.index)
         kf.last_loss = loss

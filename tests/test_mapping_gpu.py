@@ -69,6 +69,8 @@ def test_training_reduces_loss(cuda, tmp_path):
 
 
 def test_graph_replay_equals_eager(cuda, tmp_path):
+    """Graph replay (incl. speculative launches: the drawn keyframe's graph
+    starts before its policy runs) = eager execution, bit for bit."""
     import torch
     a = _c1_engine(tmp_path / "a", budget=100_000, use_graphs=True)
     b = _c1_engine(tmp_path / "b", budget=100_000, use_graphs=False)
@@ -80,6 +82,7 @@ def test_graph_replay_equals_eager(cuda, tmp_path):
     hw = sa.high_water()
     assert torch.equal(sa.params[:hw], sb.params[:hw])
     assert torch.equal(sa.adam_m[:hw], sb.adam_m[:hw])
+    assert a.counter_speculative > 0   # steps launched before their host policy ran
 
 
 def test_dp_step_world1_equals_single_step(cuda, tmp_path):
