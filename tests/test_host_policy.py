@@ -242,3 +242,47 @@ def test_visibility_cache_fast_scan_equals_vectorised_scan():
             assert [e.t3 for e in new._entries] == [e.t3 for e in old._entries]
     finally:
         C.visible_chunks = real
+
+
+def test_slab_allocator_cap_and_compaction_cpu():
+    """GaussianSlab's allocator on CPU tensors: first fit with coalescing;
+    under a row cap (C5's HBM cap) it never grows, packs live segments to the
+    front when no extent fits (rows and Adam state move with them, spare rows
+    get zero gradients) and raises HbmCapExceeded past the cap."""
+    import torch
+
+    from paper_2511_23030_b200.errors import HbmCapExceeded
+    from paper_2511_23030_b200.slab import GaussianSlab
+    slab = GaussianSlab(0, device="cpu", max_rows=1000)
+    assert slab.capacity == 1000 and slab.hbm_bytes() == 1000 * GaussianSlab.bytes_per_gaussian()
+    segs = {}
+
+    def pack_hook():
+        keys = sorted(segs)
+        new = slab.pack([segs[k] for k in keys])
+        for k, off in zip(keys, new):
+            segs[k] = (off, segs[k][1], segs[k][2])
+    slab.compact_hook = pack_hook
+    for k, size in enumerate([300, 200, 300, 150]):
+        off = slab.alloc(size)
+        segs[k] = (off, size, size - 10)
+        slab.params[off:off + size - 10, 0] = float(k)
+        slab.adam_m[off:off + size - 10, 14] = float(10 + k)
+    slab.free(segs[0][0], 300)   # holes: [0, 300) and [950, 1000)
+    slab.free(segs[2][0], 300)   # [500, 800) coalesces nothing with [0, 300)
+    del segs[0], segs[2]
+    assert slab.used() == 350
+    off = slab.alloc(500)   # no 500-row extent: compaction, then fits
+    assert slab.compactions == 1 and slab.capacity == 1000
+    assert sorted(v[0] for v in segs.values()) == [0, 200]   # packed in offset order
+    for k, (o, size, used) in segs.items():
+        assert torch.all(slab.params[o:o + used, 0] == float(k))
+        assert torch.all(slab.adam_m[o:o + used, 14] == float(10 + k))
+        assert torch.all(slab.grads[o + used:o + size] == 0)
+    assert off == 350
+    with pytest.raises(HbmCapExceeded):
+        slab.alloc(200)   # 150 rows free: past the cap
+    uncapped = GaussianSlab(1024, device="cpu")
+    a = uncapped.alloc(1000)
+    b = uncapped.alloc(1000)   # grows
+    assert uncapped.capacity >= 2000 and b == a + 1000
