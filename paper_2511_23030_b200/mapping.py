@@ -444,9 +444,10 @@ class MappingEngine:
             if ent is None or ent[0] != lv:
                 continue
             slots, n = ent[1]
-            entry = graphs.get(self._graph_key(kf, slots, n))
+            key = self._graph_key(kf, slots, n)
+            entry = graphs.get(key)
             if entry is not None:
-                out[c] = (ids_t, slots, n, kf, entry)
+                out[c] = (ids_t, slots, n, kf, entry, key)
         self._spec = (self.latest_kf, gen, lv, self.cache.version, out)
 
     _spec = None
@@ -463,6 +464,8 @@ class MappingEngine:
         e = out.get(selected)
         if e is None or st._keyframes.get(selected) is not e[3] or st.resident_count_of(e[0]) != len(e[0]):
             return None
+        if self._graph_key(e[3], e[1], e[2]) != e[5] or self._graphs.get(e[5]) is not e[4]:
+            return None   # mode / workspace changed, or the graph was dropped
         return e
 
     def train_view(self, kf: Keyframe, slots, n: int, launched: bool = False) -> float:
