@@ -171,6 +171,10 @@ def pack_keyframe(kf: Keyframe) -> bytes:
     return head + kf.rgb_u8().tobytes() + kf.depth.astype("<f4").tobytes()
 
 
+def keyframe_file_size(kf: Keyframe) -> int:
+    return _KF.size + kf.intrinsics.width * kf.intrinsics.height * 7
+
+
 def unpack_keyframe(data: bytes) -> Keyframe:
     _header(data, KEYFRAME_MAGIC, _KF.size, "keyframe")
     f = _KF.unpack_from(data, 0)

@@ -38,11 +38,12 @@ from .errors import CorruptChunk, IoFailure
 
 
 class _PendingWrite:
-    __slots__ = ("path", "header", "pin", "nbytes", "event", "done", "dev", "stride")
+    __slots__ = ("path", "header", "pin", "nbytes", "event", "done", "dev", "stride", "make")
 
-    def __init__(self, path, header, pin, nbytes, event, dev, stride):
+    def __init__(self, path, header, pin, nbytes, event, dev, stride, make=None):
         self.path, self.header, self.pin, self.nbytes = path, header, pin, nbytes
         self.event, self.dev, self.stride = event, dev, stride
+        self.make = make   # host-built file (keyframes): bytes produced on the writer thread
         self.done = threading.Event()
 
 
@@ -361,17 +362,35 @@ class ChunkStreamer:
         self.stats["async_writes"] += 1
         self._queue.put(pw)
 
+    def write_bytes_async(self, path: Path, make) -> None:
+        """Write-behind of a host-built file: `make()` runs on a writer thread
+        and returns the file's bytes (same newest-write-wins and wait_path
+        rules as the chunk write-behind)."""
+        pw = _PendingWrite(Path(path), b"", None, 0, None, None, 0, make)
+        with self._lock:
+            self._pending[pw.path] = pw
+            self._drop_victim(pw.path)
+            fut = self._prefetched.pop(pw.path, None)
+        if fut is not None:
+            fut.add_done_callback(lambda f: f.exception() is None and self.release(f.result()))
+        self.stats["async_writes"] += 1
+        self._queue.put(pw)
+
     def _write_loop(self) -> None:
         while True:
             pw = self._queue.get()
             if pw is None:
                 return
             try:
-                pw.event.synchronize()   # the D2H copy of the packed records
+                if pw.event is not None:
+                    pw.event.synchronize()   # the D2H copy of the packed records
                 tmp = pw.path.with_name(f"{pw.path.name}.{threading.get_ident()}.tmp")
                 with open(tmp, "wb") as f:   # straight from pinned memory, no bytes copy
-                    f.write(pw.header)
-                    f.write(memoryview(pw.pin.numpy())[:pw.nbytes])
+                    if pw.make is not None:
+                        f.write(pw.make())
+                    else:
+                        f.write(pw.header)
+                        f.write(memoryview(pw.pin.numpy())[:pw.nbytes])
                 with self._lock:   # several writers: only the newest write of a path lands
                     current = self._pending.get(pw.path) is pw
                     if current:
@@ -385,8 +404,11 @@ class ChunkStreamer:
                     landed = self._pending.get(pw.path) is pw and self._writer_error is None
                     if self._pending.get(pw.path) is pw:
                         del self._pending[pw.path]
-                    self._free_pins.append(pw.pin)
-                    if landed and self.victim_limit > 0:   # keep the packed bytes in HBM
+                    if pw.pin is not None:
+                        self._free_pins.append(pw.pin)
+                    if pw.dev is None:
+                        pass
+                    elif landed and self.victim_limit > 0:   # keep the packed bytes in HBM
                         self._drop_victim(pw.path)
                         self._victims[pw.path] = DeviceRecords(pw.header, pw.dev, pw.nbytes, pw.stride)
                         self._victim_bytes += pw.dev.numel()
