@@ -103,7 +103,8 @@ class ChunkStreamer:
             t.start()
         self._pool = ThreadPoolExecutor(max_workers=reader_threads)
         self._prefetched: dict[Path, object] = {}
-        self.stats = {"prefetch_hits": 0, "pending_hits": 0, "victim_hits": 0, "async_writes": 0, "alloc_pinned": 0,
+        self.stats = {"prefetch_hits": 0, "pending_hits": 0, "victim_hits": 0, "async_writes": 0,
+                      "superseded_writes": 0, "alloc_pinned": 0,
                       "alloc_device": 0, "alloc_s": 0.0, "read_s": 0.0, "stage_wait_s": 0.0,
                       "validate_wait_s": 0.0, "read_file_s": 0.0, "unpack_s": 0.0, "write_async_s": 0.0}
 
@@ -382,6 +383,11 @@ class ChunkStreamer:
             if pw is None:
                 return
             try:
+                with self._lock:   # superseded by a newer write of the path: skip the disk work
+                    stale = self._pending.get(pw.path) is not pw
+                if stale:
+                    self.stats["superseded_writes"] += 1
+                    continue
                 if pw.event is not None:
                     pw.event.synchronize()   # the D2H copy of the packed records
                 tmp = pw.path.with_name(f"{pw.path.name}.{threading.get_ident()}.tmp")
