@@ -87,6 +87,7 @@ class ChunkStreamer:
         self.write_behind = write_behind
         self._pending: dict[Path, _PendingWrite] = {}
         self._lock = threading.Lock()
+        self._freed = threading.Condition(self._lock)   # a pooled buffer came back
         self._queue: queue.Queue = queue.Queue()
         self._writer_error: BaseException | None = None
         self._free_pins: list = []
@@ -104,7 +105,7 @@ class ChunkStreamer:
         self._pool = ThreadPoolExecutor(max_workers=reader_threads)
         self._prefetched: dict[Path, object] = {}
         self.stats = {"prefetch_hits": 0, "pending_hits": 0, "victim_hits": 0, "async_writes": 0,
-                      "superseded_writes": 0, "alloc_pinned": 0,
+                      "superseded_writes": 0, "pool_wait_s": 0.0, "alloc_pinned": 0,
                       "alloc_device": 0, "alloc_s": 0.0, "read_s": 0.0, "stage_wait_s": 0.0,
                       "validate_wait_s": 0.0, "read_file_s": 0.0, "unpack_s": 0.0, "write_async_s": 0.0}
 
@@ -150,13 +151,36 @@ class ChunkStreamer:
             return len(self._free_pins)
 
     def _take(self, pool: list, nbytes: int, pinned: bool):
+        """A pooled buffer of >= nbytes.  When the pool is empty: a device
+        buffer is taken back from the oldest victim-cache entry, a pinned one
+        is waited for while write-behinds are in flight (they free one per
+        landed file, far sooner than page-locking a new buffer takes); only
+        then is a buffer allocated."""
         torch = self.torch
         self._ensure_arena()
-        with self._lock:
+
+        def fit():
             best = None
             for i, t in enumerate(pool):   # smallest buffer that fits
                 if t.numel() >= nbytes and (best is None or t.numel() < pool[best].numel()):
                     best = i
+            return best
+
+        with self._lock:
+            best = fit()
+            if best is None and not pinned:
+                for path in list(self._victims):   # oldest first
+                    old = self._victims.pop(path)
+                    self._victim_bytes -= old.dev.numel()
+                    pool.append(old.dev)
+                    best = fit()
+                    if best is not None:
+                        break
+            if best is None and pinned and self._pending:
+                t0 = time.perf_counter()
+                self._freed.wait_for(lambda: fit() is not None or not self._pending, timeout=2.0)
+                self.stats["pool_wait_s"] += time.perf_counter() - t0
+                best = fit()
             if best is not None:
                 return pool.pop(best)
         size = -(-(nbytes + 4096) // self._QUANTUM) * self._QUANTUM
@@ -188,6 +212,7 @@ class ChunkStreamer:
         if isinstance(src, PinnedFile):
             with self._lock:
                 self._free_pins.append(src.pin)
+                self._freed.notify_all()
 
     def read_file(self, path: Path):
         t0 = time.perf_counter()
@@ -412,6 +437,7 @@ class ChunkStreamer:
                         del self._pending[pw.path]
                     if pw.pin is not None:
                         self._free_pins.append(pw.pin)
+                        self._freed.notify_all()
                     if pw.dev is None:
                         pass
                     elif landed and self.victim_limit > 0:   # keep the packed bytes in HBM
