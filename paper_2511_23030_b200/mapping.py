@@ -430,6 +430,7 @@ class MappingEngine:
             cands = candidate_set(self.index.position_of(self.latest_kf), self.index)
         except EmptyCandidates:
             cands = [self.latest_kf]
+        self._spec_cands = (self.latest_kf, self.index.version, cands)
         gen, lv = store.generation, store.layout_version
         out = {}
         for c in cands:
@@ -451,6 +452,7 @@ class MappingEngine:
         self._spec = (self.latest_kf, gen, lv, self.cache.version, out)
 
     _spec = None
+    _spec_cands = None
 
     def _take_speculation(self, selected: int):
         sp, self._spec = self._spec, None
@@ -550,10 +552,14 @@ class MappingEngine:
         io0, loads0, ev0 = stats.io_nanos, stats.chunk_loads, stats.chunk_evictions
         if self.latest_kf is None:
             raise RuntimeError("no keyframe ingested yet")
-        try:
-            candidates = candidate_set(self.index.position_of(self.latest_kf), self.index)
-        except EmptyCandidates:
-            candidates = [self.latest_kf]
+        sc = self._spec_cands   # (prepared while the previous pass ran)
+        if sc is not None and sc[0] == self.latest_kf and sc[1] == self.index.version:
+            candidates = sc[2]
+        else:
+            try:
+                candidates = candidate_set(self.index.position_of(self.latest_kf), self.index)
+            except EmptyCandidates:
+                candidates = [self.latest_kf]
         pre = self._uniforms.pop(self.step_counter, None)
         seed = derive_seed(self.seed, 2, self.step_counter) if pre is None else None   # else unused
         selected = select_keyframe(candidates, self.index, seed, uniform=pre)
