@@ -374,8 +374,11 @@ struct FwdPix {
 // memory; a warp skips a splat whose 3-sigma box misses its 2 rows
 // (warp-uniform), a thread skips it when its column is outside the box, and
 // the block stops once every pixel's transmittance is below 1e-10.
+#ifndef SM_FWD_MINB
+#define SM_FWD_MINB 1
+#endif
 template <typename KeyT>
-__global__ void __launch_bounds__(kTilePx)
+__global__ void __launch_bounds__(kTilePx, SM_FWD_MINB)
 composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikeys,
               KeyT rank_mask, const ProjRec *__restrict__ recs,
               const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
