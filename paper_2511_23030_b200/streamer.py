@@ -167,22 +167,25 @@ class ChunkStreamer:
             return best
 
         with self._lock:
-            best = fit()
-            if best is None and not pinned:
-                for path in list(self._victims):   # oldest first
-                    old = self._victims.pop(path)
-                    self._victim_bytes -= old.dev.numel()
-                    pool.append(old.dev)
-                    best = fit()
-                    if best is not None:
-                        break
-            if best is None and pinned and self._pending:
-                t0 = time.perf_counter()
-                self._freed.wait_for(lambda: fit() is not None or not self._pending, timeout=2.0)
-                self.stats["pool_wait_s"] += time.perf_counter() - t0
+            deadline = time.perf_counter() + 2.0
+            while True:
                 best = fit()
-            if best is not None:
-                return pool.pop(best)
+                if best is None and not pinned:
+                    for path in list(self._victims):   # oldest first
+                        old = self._victims.pop(path)
+                        self._victim_bytes -= old.dev.numel()
+                        pool.append(old.dev)
+                        best = fit()
+                        if best is not None:
+                            break
+                if best is not None:
+                    return pool.pop(best)
+                left = deadline - time.perf_counter()
+                if not self._pending or left <= 0:
+                    break
+                t0 = time.perf_counter()
+                self._freed.wait(timeout=left)   # a write landing returns its buffers
+                self.stats["pool_wait_s"] += time.perf_counter() - t0
         size = -(-(nbytes + 4096) // self._QUANTUM) * self._QUANTUM
         t0 = time.perf_counter()
         if pinned:
@@ -437,7 +440,7 @@ class ChunkStreamer:
                         del self._pending[pw.path]
                     if pw.pin is not None:
                         self._free_pins.append(pw.pin)
-                        self._freed.notify_all()
+                    self._freed.notify_all()   # (waiters run once this block releases the lock)
                     if pw.dev is None:
                         pass
                     elif landed and self.victim_limit > 0:   # keep the packed bytes in HBM

@@ -325,3 +325,53 @@ def test_hbm_cap_compaction_bit_exact(cuda, tmp_path):
                (tmp_path / "capped" / "chunks" / name).read_bytes()
     with pytest.raises(HbmCapExceeded):   # a working set larger than the cap
         capped.ensure_resident(ids)
+
+
+def test_streamer_under_pool_pressure_matches_sync(cuda, tmp_path):
+    """Staging pools of two buffers each: evictions wait for landed writes
+    (pinned) or take victim-cache buffers back (device) instead of
+    allocating; the paging sequence still ends in byte-identical files and
+    identical resident rows compared with synchronous I/O."""
+    import torch
+
+    from paper_2511_23030_b200.core import Gaussian, quat_normalize
+    from paper_2511_23030_b200.store import ChunkStore, StoreConfig
+    rng = np.random.default_rng(21)
+    gs = []
+    for cx in range(8):   # eight chunks of 300
+        for _ in range(300):
+            gs.append(Gaussian(position=[cx * 10.0 + rng.uniform(-4, 4), rng.uniform(-4, 4), rng.uniform(-4, 4)],
+                               rotation=quat_normalize(rng.normal(size=4)), scale=rng.uniform(0.01, 0.2, 3),
+                               opacity=float(rng.uniform(0, 1)), sh=rng.normal(size=48)))
+    stores = []
+    for name, wb in (("sync", False), ("tight", True)):
+        st = ChunkStore(StoreConfig(disk_root=tmp_path / name, chunk_size_m=10.0, gaussian_budget=900,
+                                    io_ns_per_byte=1.0, write_behind=wb))
+        if wb:
+            st.streamer.PINNED_SLOTS = 2
+            st.streamer.DEVICE_SLOTS = 2
+            st.streamer.victim_limit = 1 << 20
+        st.insert_gaussians(gs)
+        stores.append(st)
+    ids = sorted(stores[0].known_chunk_ids())
+    order = np.random.default_rng(3).integers(0, len(ids), size=(40, 3))
+    for step, pick in enumerate(order):
+        want = sorted({ids[int(k)] for k in pick})
+        for st in stores:
+            st.ensure_resident(want)
+            for c in want:   # training-like edit, chunk goes dirty
+                ch = st.chunk(c)
+                st.slab.params[ch.offset:ch.offset + ch.count, 0] += 1e-3 * (step + 1)
+            st.mark_trained(want)
+        assert _stats(stores[0]) == _stats(stores[1])
+        for c in want:
+            a, b = stores[0].chunk(c), stores[1].chunk(c)
+            assert torch.equal(stores[0].slab.params[a.offset:a.offset + a.count],
+                               stores[1].slab.params[b.offset:b.offset + b.count])
+    for st in stores:
+        st.flush()
+    tight = stores[1].streamer.stats
+    assert tight["async_writes"] > 0 and tight["alloc_pinned"] == 0 and tight["alloc_device"] == 0
+    for c in ids:
+        name = f"{c:016x}.dcg"
+        assert (tmp_path / "sync" / "chunks" / name).read_bytes() == (tmp_path / "tight" / "chunks" / name).read_bytes()
