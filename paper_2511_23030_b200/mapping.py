@@ -212,6 +212,7 @@ class MappingEngine:
         self.h2d_bytes = 0
         self.d2h_bytes = 0
         self.upload_keyframes_each_step = False   # e2e mode: GT from pinned host every step
+        self.upload_side_stream = True   # the e2e upload overlaps the forward on its own stream
         self._pinned_kf: dict[int, tuple] = {}
         self._uniforms: dict[int, float] = {}
         self._eager_seen: dict = {}
@@ -264,6 +265,10 @@ class MappingEngine:
             # H2D on a side stream, overlapped with the forward render (which
             # does not read the ground truth); the loss waits for it
             cur = torch.cuda.current_stream(self.device)
+            if not self.upload_side_stream:   # (A/B: the copy in line with the forward)
+                d.rgb_u8.copy_(pin[0], non_blocking=True)
+                d.depth.copy_(pin[1], non_blocking=True)
+                return d
             if not hasattr(self, "_up_stream"):
                 self._up_stream = torch.cuda.Stream(device=self.device)
             self._up_stream.wait_stream(cur)   # the previous step's loss is done with d

@@ -16,11 +16,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--blocks", type=int, default=4)
+    ap.add_argument("--serial-upload", action="store_true", help="upload on the compute stream (A/B)")
     args = ap.parse_args()
     import torch
 
     from paper_2511_23030_b200.workloads import build_c2
     eng = build_c2(1_000_000, 16, store_dir=tempfile.mkdtemp())
+    eng.upload_side_stream = not args.serial_upload
     out = {False: [], True: []}
     for up in (False, True):
         eng.upload_keyframes_each_step = up
