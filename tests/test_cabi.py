@@ -3,6 +3,9 @@ declares (no device needed: nothing here launches a kernel)."""
 import ctypes
 import re
 
+import numpy as np
+import pytest
+
 from tests.conftest import ROOT
 
 HEADER = ROOT / "include" / "splatmap_cuda.h"
@@ -55,3 +58,20 @@ def test_invalid_arguments_map_to_errors():
 def test_oracle_library_builds_and_loads():
     from oracle import oracle
     assert oracle.lib().or_render_fwd is not None
+
+
+def test_no_cpu_fallback_without_a_device():
+    """Without a CUDA device the product path raises DeviceFailure: nothing
+    silently falls back to a CPU (or oracle) implementation."""
+    import torch
+
+    from paper_2511_23030_b200 import renderloss as rl
+    from paper_2511_23030_b200.core import CameraIntrinsics, Pose
+    from paper_2511_23030_b200.errors import DeviceFailure
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    sa = rl.SceneArrays(np.array([[0.0, 0.0, 2.0]]), np.array([[1.0, 0, 0, 0]]), np.full((1, 3), 0.1),
+                        np.array([0.5]), np.zeros((1, 3)))
+    with pytest.raises(DeviceFailure):
+        rl.render_arrays(sa, Pose(), CameraIntrinsics(fx=40.0, fy=40.0, cx=16, cy=16, width=32, height=32,
+                                                      near=0.1))
