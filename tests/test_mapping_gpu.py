@@ -187,3 +187,29 @@ def test_instance_overflow_recovers_identically(cuda, tmp_path):
     assert a.render.dims.max_instances > 4096
     hw = a.store.slab.high_water()
     assert torch.equal(a.store.slab.params[:hw], b.store.slab.params[:hw])
+
+
+def test_keyframes_arriving_mid_run_graphs_equal_eager(cuda, tmp_path):
+    """Keyframes joining between steps (a moving camera): the speculative
+    launch and the graph cache must notice the new latest keyframe and the
+    changed candidate set -- graph replay stays bit-identical to eager runs."""
+    import torch
+
+    from paper_2511_23030_b200.core import Keyframe
+    from paper_2511_23030_b200.synthetic import C1_INTR, perturbed
+    from paper_2511_23030_b200.workloads import _gt_frames, c1_poses, c1_scene
+    engines = [_c1_engine(tmp_path / "a", budget=100_000, use_graphs=True),
+               _c1_engine(tmp_path / "b", budget=100_000, use_graphs=False)]
+    poses = c1_poses(14)[10:]   # four more keyframes further along the trajectory
+    frames = _gt_frames(perturbed(c1_scene(20_000), 49), poses, C1_INTR, torch.device("cuda"))
+    step = 0
+    for k, (pose, (rgb, depth)) in enumerate(zip(poses, frames)):
+        for e in engines:
+            e.add_keyframe(Keyframe(id=100 + k, pose=pose, intrinsics=C1_INTR, rgb=rgb, depth=depth))
+        for _ in range(4):
+            ra, rb = (e.optimization_step(k, step) for e in engines)
+            assert ra.selected_kf == rb.selected_kf and ra.loss == rb.loss, step
+            step += 1
+    sa, sb = engines[0].store.slab, engines[1].store.slab
+    hw = sa.high_water()
+    assert torch.equal(sa.params[:hw], sb.params[:hw])
