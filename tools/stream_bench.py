@@ -41,7 +41,7 @@ def run(mode: str, scene, poses, frames, args):
     budget = len(scene) + 1 if mode == "resident" else args.budget
     store = ChunkStore(StoreConfig(disk_root=root, chunk_size_m=10.0, gaussian_budget=budget,
                                    keyframe_budget=400, io_ns_per_byte=1.0,
-                                   write_behind=(mode == "streamed")))
+                                   write_behind=(mode == "streamed"), writer_threads=args.writers))
     store.insert_arrays(scene.positions, scene.rotations, scene.scales, scene.opacities, scene.sh)
     store.flush()
     if mode != "resident":   # cold start: the map is on disk, HBM empty
@@ -105,6 +105,7 @@ def main():
     ap.add_argument("--budget", type=int, default=1_500_000)
     ap.add_argument("--max-distance", type=float, default=50.0)
     ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--writers", type=int, default=4, help="write-behind threads")
     ap.add_argument("--modes", default="resident,sync,streamed")
     ap.add_argument("--profile", action="store_true", help="cProfile each run (host hot spots to stderr)")
     args = ap.parse_args()
