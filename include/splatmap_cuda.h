@@ -136,7 +136,12 @@ void sm_set_ellipse_cull(int on);
 #define SM_WS_PIX_LAST 1
 #define SM_WS_DEPTH_ORDER 2   /* uint32 [n]: depth rank -> visible index */
 #define SM_WS_RANK_TILES 3    /* uint32 [n]: kept tiles per depth rank   */
+#define SM_WS_TILE_KEYS 4     /* [counters.n_instances] sorted instance keys
+                               * (tile << rank_bits) | depth rank, uint32 or
+                               * uint64 (sm_render_key_layout)            */
 int64_t sm_render_ws_offset(const sm_render_dims *dims, int which);
+/* Bit layout of the SM_WS_TILE_KEYS keys of a workspace (host-only). */
+int sm_render_key_layout(const sm_render_dims *dims, int32_t *rank_bits, int32_t *key_bytes);
 
 /* ------------------------------------------------------------------ loss
  * renderloss.total_loss / image_loss / ssim / depth_loss (renderloss.py:226-274):
@@ -164,6 +169,17 @@ int sm_loss_forward_backward(const float *rgb, const float *depth, const uint8_t
 int sm_adam_step(float *params, float *m, float *v, float *grads, const int32_t *slots,
                  int64_t n, const sm_adam_config *cfg /* host */, const uint32_t *skip_flag,
                  void *stream);
+
+/* Data-parallel exchange (no reference counterpart -- the
+ * reference is single-process).  sm_pack_grads gathers the gradient records
+ * of the active set into packed[i] = grads[slots[i]] ([n][16] floats, the
+ * buffer the ranks sum with one NCCL all-reduce) and zeroes those slab rows;
+ * sm_adam_step_packed is sm_adam_step reading gradient i from packed[i]
+ * (bit-identical to sm_adam_step on the same sums). */
+int sm_pack_grads(float *grads, const int32_t *slots, int64_t n, float *packed, void *stream);
+int sm_adam_step_packed(float *params, float *m, float *v, const float *packed_grads,
+                        const int32_t *slots, int64_t n, const sm_adam_config *cfg /* host */,
+                        const uint32_t *skip_flag, void *stream);
 
 /* --------------------------------------------------------------- culling
  * Per-chunk frustum + distance test, brute force over a chunk table; equal

@@ -11,6 +11,9 @@ arrays:
   (tests/golden/render_fd.npz).
 * ``total_loss``     -> renderloss.py:226-274, optional dL/d(rgb, depth)
 * ``adam``           -> torch.optim.Adam formula (the reference has no Adam)
+* ``bin_tiles``      -> the device's K2/K3 arithmetic (oracle/bin_oracle.c):
+  depth order (renderloss.py:202), 3-sigma boxes (renderloss.py:122-135),
+  tile-sorted (tile, rank) instance keys and per-tile ranges, bit-exact.
 """
 
 from __future__ import annotations
@@ -56,6 +59,11 @@ def lib():
         _lib.or_train_step.argtypes = (
             [ctypes.c_int64] + [_dp] * 7 + [ctypes.c_double] * 5 + [ctypes.c_int] * 2 + [_dp] * 2
             + [ctypes.c_double] * 2 + [_dp] + [ctypes.c_double] * 4 + [_dp] * 2 + [_i64p, ctypes.c_int])
+        _lib.ob_bin_tiles.restype = ctypes.c_int64
+        _lib.ob_bin_tiles.argtypes = (
+            [ctypes.c_int64, ctypes.POINTER(ctypes.c_float), _dp, _dp] + [ctypes.c_double] * 5
+            + [ctypes.c_int] * 4 + [_i64p, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int64,
+                                     ctypes.POINTER(ctypes.c_uint32)])
         _lib.or_adam.restype = None
         _lib.or_adam.argtypes = ([ctypes.c_int64] + [_dp] * 4 + [ctypes.c_double] * 4
                                  + [ctypes.c_int64])
@@ -265,3 +273,35 @@ def adam(param, m, v, grad, lr, beta1, beta2, eps, step):
         assert a.dtype == np.float64 and a.flags.c_contiguous
     g = _c(grad)
     lib().or_adam(param.size, _p(param), _p(m), _p(v), _p(g), lr, beta1, beta2, eps, int(step))
+
+
+def bin_tiles(params, pose_rotation, pose_translation, fx, fy, cx, cy, near, width, height,
+              ellipse_cull=True, rank_bits=None):
+    """K2/K3 restatement on float32 param records (n, 16).
+
+    Returns (order, keys, ranges): order[rank] = index (np.argsort(z,
+    kind="stable") over the kept set, culled after); keys = sorted uint64
+    (tile << rank_bits) | rank; ranges = uint32 (tiles, 2) [start, end).
+    """
+    p = np.ascontiguousarray(np.asarray(params, dtype=np.float32).reshape(-1, 16))
+    n = p.shape[0]
+    if rank_bits is None:
+        rank_bits = max(1, int(np.ceil(np.log2(max(n, 2)))))
+    r_wc = _c(quat_to_matrix(pose_rotation))
+    t = _c(pose_translation, (3,))
+    tiles = ((width + 15) // 16) * ((height + 15) // 16)
+    order = np.zeros(max(n, 1), dtype=np.int64)
+    ranges = np.zeros((tiles, 2), dtype=np.uint32)
+    cap = max(16 * n, 1024)
+    while True:
+        keys = np.zeros(cap, dtype=np.uint64)
+        cnt = lib().ob_bin_tiles(n, p.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), _p(r_wc), _p(t),
+                                 fx, fy, cx, cy, near, int(width), int(height), int(bool(ellipse_cull)),
+                                 int(rank_bits), order.ctypes.data_as(_i64p),
+                                 keys.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), cap,
+                                 ranges.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)))
+        if cnt < 0:
+            raise MemoryError("oracle binning failed")
+        if cnt <= cap:
+            return order[:n], keys[:cnt], ranges
+        cap = int(cnt)

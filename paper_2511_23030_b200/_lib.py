@@ -83,10 +83,13 @@ def load():
          vp, vp, vp, vp, vp)
     _sig(lib.sm_set_ellipse_cull, None, c_int)
     _sig(lib.sm_render_ws_offset, i64, POINTER(RenderDims), c_int)
+    _sig(lib.sm_render_key_layout, c_int, POINTER(RenderDims), POINTER(i32), POINTER(i32))
     _sig(lib.sm_loss_workspace_size, i64, i32, i32)
     _sig(lib.sm_loss_forward_backward, c_int, vp, vp, vp, vp, vp, i32, i32, i32, c_float, c_float,
          vp, i64, vp, vp, vp, vp)
     _sig(lib.sm_adam_step, c_int, vp, vp, vp, vp, vp, i64, POINTER(AdamConfig), vp, vp)
+    _sig(lib.sm_pack_grads, c_int, vp, vp, i64, vp, vp)
+    _sig(lib.sm_adam_step_packed, c_int, vp, vp, vp, vp, vp, i64, POINTER(AdamConfig), vp, vp)
     _sig(lib.sm_cull_chunks, c_int, vp, i64, POINTER(c_double), POINTER(c_double), c_double,
          c_double, vp, vp)
     _sig(lib.sm_encode_positions, c_int, vp, i64, c_double, vp, vp, vp)

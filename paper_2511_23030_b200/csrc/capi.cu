@@ -27,7 +27,8 @@ int loss_forward_backward(const float *, const float *, const uint8_t *, const f
                           int, int, int, float, float, void *, int64_t, float *, float *, float *,
                           cudaStream_t);
 int adam_step(float *, float *, float *, float *, const int32_t *, int64_t, const sm_adam_config &,
-              const uint32_t *, cudaStream_t);
+              const uint32_t *, const float *, cudaStream_t);
+int pack_grads(float *, const int32_t *, int64_t, float *, cudaStream_t);
 int cull_chunks(const int32_t *, int64_t, const double *, const double *, double, double, uint8_t *,
                 cudaStream_t);
 int encode_positions(const float *, int64_t, double, uint64_t *, int64_t *, cudaStream_t);
@@ -108,8 +109,20 @@ int64_t sm_render_ws_offset(const sm_render_dims *dims, int which) {
         case SM_WS_PIX_LAST: return L.o_pix_last;
         case SM_WS_DEPTH_ORDER: return L.o_order0;
         case SM_WS_RANK_TILES: return L.o_tcount_r;
+        case SM_WS_TILE_KEYS: return L.tile_passes & 1 ? L.o_ikey1 : L.o_ikey0;
         default: return -1;
     }
+}
+
+int sm_render_key_layout(const sm_render_dims *dims, int32_t *rank_bits, int32_t *key_bytes) {
+    if (!dims || !rank_bits || !key_bytes) {
+        set_error("sm_render_key_layout: null argument");
+        return SM_ERR_INVALID;
+    }
+    const RenderLayout L = render_layout(*dims);
+    *rank_bits = L.rank_bits;
+    *key_bytes = L.key_bytes;
+    return SM_OK;
 }
 
 int64_t sm_loss_workspace_size(int32_t width, int32_t height) { return loss_workspace_size(width, height); }
@@ -134,7 +147,24 @@ int sm_adam_step(float *params, float *m, float *v, float *grads, const int32_t 
         set_error("sm_adam_step: null argument");
         return SM_ERR_INVALID;
     }
-    return adam_step(params, m, v, grads, slots, n, *cfg, skip_flag, SM_STREAM(stream));
+    return adam_step(params, m, v, grads, slots, n, *cfg, skip_flag, nullptr, SM_STREAM(stream));
+}
+
+int sm_pack_grads(float *grads, const int32_t *slots, int64_t n, float *packed, void *stream) {
+    if (n > 0 && (!grads || !packed)) {
+        set_error("sm_pack_grads: null argument");
+        return SM_ERR_INVALID;
+    }
+    return pack_grads(grads, slots, n, packed, SM_STREAM(stream));
+}
+
+int sm_adam_step_packed(float *params, float *m, float *v, const float *packed_grads, const int32_t *slots,
+                        int64_t n, const sm_adam_config *cfg, const uint32_t *skip_flag, void *stream) {
+    if (!cfg || (n > 0 && (!params || !m || !v || !packed_grads))) {
+        set_error("sm_adam_step_packed: null argument");
+        return SM_ERR_INVALID;
+    }
+    return adam_step(params, m, v, nullptr, slots, n, *cfg, skip_flag, packed_grads, SM_STREAM(stream));
 }
 
 int sm_cull_chunks(const int32_t *coords, int64_t n, const double *planes, const double *cam_center,

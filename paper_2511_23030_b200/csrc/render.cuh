@@ -138,7 +138,15 @@ inline RenderBufs render_bufs(void *ws, const RenderLayout &L) {
 }
 
 // fp64 projection of one Gaussian (renderloss.py:176-199).  Keeps the
-// intermediates the backward needs.
+// intermediates the backward needs.  Every operation is an explicit
+// round-to-nearest op (no FMA contraction) in a fixed order, so the host
+// restatement (oracle/bin_oracle.c, gcc -ffp-contract=off) reproduces the
+// projected records -- and through them the tile keys and ranges -- bit for
+// bit; on an HBM-bound kernel the unfused fp64 ops cost nothing measurable.
+#define DM __dmul_rn
+#define DA __dadd_rn
+#define DS __dsub_rn
+#define DD __ddiv_rn
 struct ProjGeom {
     double x, y, z;        // camera-frame centre
     double u, v;           // pixel mean
@@ -153,45 +161,44 @@ __device__ __forceinline__ void project_geometry(double px, double py, double pz
                                                  double sy, double sz, const double *rwc,
                                                  const double *t, double fx, double fy,
                                                  double cx, double cy, ProjGeom &g) {
-    const double d0 = px - t[0], d1 = py - t[1], d2 = pz - t[2];
-    // cam = (p - t) @ r_wc
-    g.x = d0 * rwc[0] + d1 * rwc[3] + d2 * rwc[6];
-    g.y = d0 * rwc[1] + d1 * rwc[4] + d2 * rwc[7];
-    // z without FMA contraction: (d0 r02 + d1 r12) + d2 r22, the depth-order
-    // key, reproducible on the host (tests compare the order bit for bit)
-    g.z = __dadd_rn(__dadd_rn(__dmul_rn(d0, rwc[2]), __dmul_rn(d1, rwc[5])), __dmul_rn(d2, rwc[8]));
+    const double d0 = DS(px, t[0]), d1 = DS(py, t[1]), d2 = DS(pz, t[2]);
+    // cam = (p - t) @ r_wc, each component (d0 r0j + d1 r1j) + d2 r2j
+    g.x = DA(DA(DM(d0, rwc[0]), DM(d1, rwc[3])), DM(d2, rwc[6]));
+    g.y = DA(DA(DM(d0, rwc[1]), DM(d1, rwc[4])), DM(d2, rwc[7]));
+    g.z = DA(DA(DM(d0, rwc[2]), DM(d1, rwc[5])), DM(d2, rwc[8]));   // the depth-order key
     const double x = g.x, y = g.y, z = g.z;
-    g.u = fx * x / z + cx;
-    g.v = fy * y / z + cy;
+    g.u = DA(DD(DM(fx, x), z), cx);
+    g.v = DA(DD(DM(fy, y), z), cy);
     // renderloss.py:155-167
     double *R = g.R;
-    R[0] = 1 - 2 * (qy * qy + qz * qz);
-    R[1] = 2 * (qx * qy - qw * qz);
-    R[2] = 2 * (qx * qz + qw * qy);
-    R[3] = 2 * (qx * qy + qw * qz);
-    R[4] = 1 - 2 * (qx * qx + qz * qz);
-    R[5] = 2 * (qy * qz - qw * qx);
-    R[6] = 2 * (qx * qz - qw * qy);
-    R[7] = 2 * (qy * qz + qw * qx);
-    R[8] = 1 - 2 * (qx * qx + qy * qy);
-    g.s2[0] = sx * sx;
-    g.s2[1] = sy * sy;
-    g.s2[2] = sz * sz;
+    R[0] = DS(1.0, DM(2.0, DA(DM(qy, qy), DM(qz, qz))));
+    R[1] = DM(2.0, DS(DM(qx, qy), DM(qw, qz)));
+    R[2] = DM(2.0, DA(DM(qx, qz), DM(qw, qy)));
+    R[3] = DM(2.0, DA(DM(qx, qy), DM(qw, qz)));
+    R[4] = DS(1.0, DM(2.0, DA(DM(qx, qx), DM(qz, qz))));
+    R[5] = DM(2.0, DS(DM(qy, qz), DM(qw, qx)));
+    R[6] = DM(2.0, DS(DM(qx, qz), DM(qw, qy)));
+    R[7] = DM(2.0, DA(DM(qy, qz), DM(qw, qx)));
+    R[8] = DS(1.0, DM(2.0, DA(DM(qx, qx), DM(qy, qy))));
+    g.s2[0] = DM(sx, sx);
+    g.s2[1] = DM(sy, sy);
+    g.s2[2] = DM(sz, sz);
     // M = W R where W = r_wc^T  (W_ij = rwc[j*3+i]);  Sc = M diag(s2) M^T
     double M[9];
 #pragma unroll
     for (int i = 0; i < 3; i++)
 #pragma unroll
         for (int k = 0; k < 3; k++)
-            M[i * 3 + k] = rwc[0 * 3 + i] * R[0 * 3 + k] + rwc[1 * 3 + i] * R[1 * 3 + k] +
-                           rwc[2 * 3 + i] * R[2 * 3 + k];
+            M[i * 3 + k] = DA(DA(DM(rwc[0 * 3 + i], R[0 * 3 + k]), DM(rwc[1 * 3 + i], R[1 * 3 + k])),
+                              DM(rwc[2 * 3 + i], R[2 * 3 + k]));
     double S[3][3];
 #pragma unroll
     for (int i = 0; i < 3; i++)
 #pragma unroll
         for (int j = i; j < 3; j++) {
-            double s = M[i * 3 + 0] * g.s2[0] * M[j * 3 + 0] + M[i * 3 + 1] * g.s2[1] * M[j * 3 + 1] +
-                       M[i * 3 + 2] * g.s2[2] * M[j * 3 + 2];
+            const double s = DA(DA(DM(DM(M[i * 3 + 0], g.s2[0]), M[j * 3 + 0]),
+                                   DM(DM(M[i * 3 + 1], g.s2[1]), M[j * 3 + 1])),
+                                DM(DM(M[i * 3 + 2], g.s2[2]), M[j * 3 + 2]));
             S[i][j] = s;
             S[j][i] = s;
         }
@@ -202,19 +209,18 @@ __device__ __forceinline__ void project_geometry(double px, double py, double pz
     g.Sc[4] = S[1][2];
     g.Sc[5] = S[2][2];
     // J = [[fx/z, 0, -fx x/z^2], [0, fy/z, -fy y/z^2]]
-    const double j00 = fx / z, j02 = -fx * x / (z * z);
-    const double j11 = fy / z, j12 = -fy * y / (z * z);
+    const double zz = DM(z, z);
+    const double j00 = DD(fx, z), j02 = -DD(DM(fx, x), zz);
+    const double j11 = DD(fy, z), j12 = -DD(DM(fy, y), zz);
     // cov2 = J Sc J^T
-    const double a00 = j00 * S[0][0] + j02 * S[2][0];
-    const double a01 = j00 * S[0][1] + j02 * S[2][1];
-    const double a02 = j00 * S[0][2] + j02 * S[2][2];
-    const double b01 = j11 * S[1][0] + j12 * S[2][0];
-    const double b11 = j11 * S[1][1] + j12 * S[2][1];
-    const double b12 = j11 * S[1][2] + j12 * S[2][2];
-    g.a = a00 * j00 + a02 * j02 + 0.3;
-    g.b = a01 * j11 + a02 * j12;
-    g.c = b11 * j11 + b12 * j12 + 0.3;
-    (void)b01;
+    const double a00 = DA(DM(j00, S[0][0]), DM(j02, S[2][0]));
+    const double a01 = DA(DM(j00, S[0][1]), DM(j02, S[2][1]));
+    const double a02 = DA(DM(j00, S[0][2]), DM(j02, S[2][2]));
+    const double b11 = DA(DM(j11, S[1][1]), DM(j12, S[2][1]));
+    const double b12 = DA(DM(j11, S[1][2]), DM(j12, S[2][2]));
+    g.a = DA(DA(DM(a00, j00), DM(a02, j02)), 0.3);
+    g.b = DA(DM(a01, j11), DM(a02, j12));
+    g.c = DA(DA(DM(b11, j11), DM(b12, j12)), 0.3);
 }
 
 // A second branch of the caller's stream (one per host thread and device)

@@ -112,7 +112,7 @@ __device__ __forceinline__ uint32_t project_one(
     zbits[i] = (unsigned long long)__double_as_longlong(g.z);
     // renderloss.py:110-135: conic and clamped 3-sigma bbox (fp64)
     const double a = g.a, b = g.b, c = g.c;
-    const double det = a * c - b * b;
+    const double det = DS(DM(a, c), DM(b, b));
     ProjRec r;
     r.op = C.z;
     r.z = (float)g.z;
@@ -120,7 +120,7 @@ __device__ __forceinline__ uint32_t project_one(
     float col[3];
 #pragma unroll
     for (int k = 0; k < 3; k++) {
-        double v = SM_SH_C0 * sh[k] + 0.5;
+        const double v = DA(DM(SM_SH_C0, sh[k]), 0.5);
         col[k] = (float)(v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v));
     }
     r.r = col[0];
@@ -136,29 +136,29 @@ __device__ __forceinline__ uint32_t project_one(
         rec[i] = r;
         return key;
     }
-    const double ia = c / det, ib = -b / det, ic = a / det;
-    const double rx = 3.0 * sqrt(a), ry = 3.0 * sqrt(c);
-    double fx0 = ceil(g.u - rx), fx1 = floor(g.u + rx);
-    double fy0 = ceil(g.v - ry), fy1 = floor(g.v + ry);
+    const double ia = DD(c, det), ib = DD(-b, det), ic = DD(a, det);
+    const double rx = DM(3.0, __dsqrt_rn(a)), ry = DM(3.0, __dsqrt_rn(c));
+    double fx0 = ceil(DS(g.u, rx)), fx1 = floor(DA(g.u, rx));
+    double fy0 = ceil(DS(g.v, ry)), fy1 = floor(DA(g.v, ry));
     fx0 = fmin(fmax(fx0, 0.0), (double)cam.width);
     fy0 = fmin(fmax(fy0, 0.0), (double)cam.height);
     fx1 = fmax(fmin(fx1, (double)(cam.width - 1)), -1.0);
     fy1 = fmax(fmin(fy1, (double)(cam.height - 1)), -1.0);
     const int x0 = (int)fx0, x1 = (int)fx1, y0 = (int)fy0, y1 = (int)fy1;
-    r.ox = (float)((double)x0 - g.u);
-    r.oy = (float)((double)y0 - g.v);
-    r.ia = (float)(kPowScale * ia);
-    r.ib = (float)(kPowScale * ib);
-    r.ic = (float)(kPowScale * ic);
+    r.ox = (float)DS((double)x0, g.u);
+    r.oy = (float)DS((double)y0, g.v);
+    r.ia = (float)DM(kPowScale, ia);
+    r.ib = (float)DM(kPowScale, ib);
+    r.ic = (float)DM(kPowScale, ic);
     // fp32 error bound of the quadratic form near q = 9 scales with the
     // anisotropy K = ac/det (sum of |terms| <= 36 K); generous margin.
-    const double K = a * c / det;
-    r.eps = (float)(1e-4 * (1.0 + K) * -kPowScale);
+    const double K = DD(DM(a, c), det);
+    r.eps = (float)DM(DM(1e-4, DA(1.0, K)), -kPowScale);
     r.x0y0 = (int32_t)(((uint32_t)y0 << 16) | ((uint32_t)x0 & 0xffffu));
     r.x1y1 = (int32_t)(((uint32_t)(y1 & 0xffff) << 16) | ((uint32_t)x1 & 0xffffu));
-    r.beta = (float)(b / c);
-    r.G = (float)(9.0 * det / c);
-    r.K = cull ? (float)(det / (c * c)) : -1.f;
+    r.beta = (float)DD(b, c);
+    r.G = (float)DD(DM(9.0, det), c);
+    r.K = cull ? (float)DD(det, DM(c, c)) : -1.f;
     rec[i] = r;
     Proj64 q;
     q.u = g.u;

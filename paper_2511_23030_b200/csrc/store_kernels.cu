@@ -22,7 +22,7 @@ struct AdamDev {
 __global__ void __launch_bounds__(256)
 adam_quarter_kernel(float4 *__restrict__ params, float4 *__restrict__ m, float4 *__restrict__ v,
                     float4 *__restrict__ grads, const int32_t *__restrict__ slots, int64_t n,
-                    AdamDev c, const uint32_t *__restrict__ skip) {
+                    AdamDev c, const uint32_t *__restrict__ skip, const float4 *__restrict__ packed) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int q = threadIdx.x & 3;
     const int64_t i = t >> 2;
@@ -31,7 +31,7 @@ adam_quarter_kernel(float4 *__restrict__ params, float4 *__restrict__ m, float4 
     float4 p = make_float4(0.f, 0.f, 0.f, 0.f), g = p, mm = p, vv = p;
     if (ok) {
         p = params[s * 4 + q];
-        g = grads[s * 4 + q];
+        g = packed ? packed[i * 4 + q] : grads[s * 4 + q];   // packed: the DP exchange buffer
         mm = m[s * 4 + q];
         vv = v[s * 4 + q];
     }
@@ -74,11 +74,39 @@ adam_quarter_kernel(float4 *__restrict__ params, float4 *__restrict__ m, float4 
     params[s * 4 + q] = make_float4(pv[0], pv[1], pv[2], pv[3]);
     m[s * 4 + q] = make_float4(mv[0], mv[1], mv[2], mv[3]);
     v[s * 4 + q] = make_float4(vvv[0], vvv[1], vvv[2], vvv[3]);
+    if (!packed) grads[s * 4 + q] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// The data-parallel exchange buffer: the active rows' gradient records packed
+// in active-set order (packed[i] = grads[slots[i]]), the slab rows zeroed for
+// the next accumulation.  One 16-byte quarter per thread.
+__global__ void __launch_bounds__(256)
+pack_grads_kernel(float4 *__restrict__ grads, const int32_t *__restrict__ slots, int64_t n,
+                  float4 *__restrict__ packed) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = t >> 2;
+    if (i >= n) return;
+    const int q = (int)(t & 3);
+    const int64_t s = slots ? (int64_t)slots[i] : i;
+    packed[t] = grads[s * 4 + q];
     grads[s * 4 + q] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
+int pack_grads(float *grads, const int32_t *slots, int64_t n, float *packed, cudaStream_t st) {
+    if (n < 0) {
+        set_error("negative n");
+        return SM_ERR_INVALID;
+    }
+    if (n == 0) return SM_OK;
+    count_launches(1);
+    pack_grads_kernel<<<(unsigned)ceil_div(n * 4, 256), 256, 0, st>>>(
+        reinterpret_cast<float4 *>(grads), slots, n, reinterpret_cast<float4 *>(packed));
+    SM_CHECK_LAUNCH("pack_grads");
+    return SM_OK;
+}
+
 int adam_step(float *params, float *m, float *v, float *grads, const int32_t *slots, int64_t n,
-              const sm_adam_config &cfg, const uint32_t *skip, cudaStream_t st) {
+              const sm_adam_config &cfg, const uint32_t *skip, const float *packed, cudaStream_t st) {
     if (n < 0) {
         set_error("negative n");
         return SM_ERR_INVALID;
@@ -94,7 +122,8 @@ int adam_step(float *params, float *m, float *v, float *grads, const int32_t *sl
     count_launches(1);
     adam_quarter_kernel<<<(unsigned)ceil_div(n * 4, 256), 256, 0, st>>>(
         reinterpret_cast<float4 *>(params), reinterpret_cast<float4 *>(m),
-        reinterpret_cast<float4 *>(v), reinterpret_cast<float4 *>(grads), slots, n, d, skip);
+        reinterpret_cast<float4 *>(v), reinterpret_cast<float4 *>(grads), slots, n, d, skip,
+        reinterpret_cast<const float4 *>(packed));
     prof_end(ST_ADAM, st);
     SM_CHECK_LAUNCH("adam_step");
     return SM_OK;

@@ -362,8 +362,14 @@ class MappingEngine:
             self._uniforms = {nxt: draw_uniform(derive_seed(self.seed, 2, nxt))}
 
     def _graph_key(self, kf: Keyframe, slots, n: int, dp: bool = False):
+        """A captured graph bakes in the camera (sm_camera is copied by value
+        into the kernel arguments), so the key carries the pose bytes and the
+        intrinsics: a pose correction (store.update_keyframe_pose, the
+        reference's loopclose.py:183) re-captures instead of replaying the old
+        camera."""
         s = self.store.slab
-        return (kf.id, slots.data_ptr(), n, s.params.data_ptr(), s.grads.data_ptr(),
+        cam = (kf.pose.rotation.tobytes(), kf.pose.translation.tobytes(), kf.intrinsics)
+        return (kf.id, cam, slots.data_ptr(), n, s.params.data_ptr(), s.grads.data_ptr(),
                 self.render.ws.data_ptr(), self.upload_keyframes_each_step, dp)
 
     def drop_graphs(self) -> None:
@@ -393,7 +399,11 @@ class MappingEngine:
                     self._queue_readback()
         finally:
             lib.sm_profile_capture_end()
-        self._graphs[self._graph_key(kf, slots, n, dp)] = (g, gid)
+        key = self._graph_key(kf, slots, n, dp)
+        # graphs of this keyframe under an older camera can never replay again
+        for k in [k for k in self._graphs if k[0] == kf.id and k[1] != key[1]]:
+            lib.sm_profile_graph_free(self._graphs.pop(k)[1])
+        self._graphs[key] = (g, gid)
 
     def _dp_device_pass(self, kf: Keyframe, slots, n: int) -> None:
         """fwd -> loss -> bwd of this rank's keyframe: graph replay when captured,

@@ -90,6 +90,7 @@ class ChunkStreamer:
         self._freed = threading.Condition(self._lock)   # a pooled buffer came back
         self._queue: queue.Queue = queue.Queue()
         self._writer_error: BaseException | None = None
+        self._failed: list[_PendingWrite] = []   # write-behinds that raised (kept pending)
         self._free_pins: list = []
         self._arena_ready = False
         # device victim cache: packed records of chunks whose write-behind
@@ -218,6 +219,7 @@ class ChunkStreamer:
                 self._freed.notify_all()
 
     def read_file(self, path: Path):
+        self.check()   # a failed write-behind surfaces at the next paging operation
         t0 = time.perf_counter()
         try:
             return self._read_file(path)
@@ -359,6 +361,7 @@ class ChunkStreamer:
         return pin[:nbytes].numpy().copy()
 
     def write_async(self, path: Path, header: bytes, offset: int, n: int, stride: int) -> None:
+        self.check()
         t0 = time.perf_counter()
         try:
             self._write_async(path, header, offset, n, stride)
@@ -382,6 +385,7 @@ class ChunkStreamer:
             ev.record(self.d2h_stream)
         pw = _PendingWrite(Path(path), header, pin, nbytes, ev, dev, stride)
         with self._lock:
+            self._release_superseded(self._pending.get(pw.path))
             self._pending[pw.path] = pw
             self._drop_victim(pw.path)
             fut = self._prefetched.pop(pw.path, None)
@@ -397,6 +401,7 @@ class ChunkStreamer:
         rules as the chunk write-behind)."""
         pw = _PendingWrite(Path(path), b"", None, 0, None, None, 0, make)
         with self._lock:
+            self._release_superseded(self._pending.get(pw.path))
             self._pending[pw.path] = pw
             self._drop_victim(pw.path)
             fut = self._prefetched.pop(pw.path, None)
@@ -410,51 +415,72 @@ class ChunkStreamer:
             pw = self._queue.get()
             if pw is None:
                 return
+            failed = False
             try:
-                with self._lock:   # superseded by a newer write of the path: skip the disk work
-                    stale = self._pending.get(pw.path) is not pw
-                if stale:
-                    self.stats["superseded_writes"] += 1
-                    continue
-                if pw.event is not None:
-                    pw.event.synchronize()   # the D2H copy of the packed records
-                tmp = pw.path.with_name(f"{pw.path.name}.{threading.get_ident()}.tmp")
-                with open(tmp, "wb") as f:   # straight from pinned memory, no bytes copy
-                    if pw.make is not None:
-                        f.write(pw.make())
-                    else:
-                        f.write(pw.header)
-                        f.write(memoryview(pw.pin.numpy())[:pw.nbytes])
-                with self._lock:   # several writers: only the newest write of a path lands
-                    current = self._pending.get(pw.path) is pw
-                    if current:
-                        tmp.replace(pw.path)
-                if not current:
-                    tmp.unlink(missing_ok=True)
-            except BaseException as exc:   # surfaced at the next check()/drain()
+                self._write_one(pw)
+            except BaseException as exc:   # surfaced at the next paging call / drain()
                 self._writer_error = exc
-            finally:
-                with self._lock:
-                    landed = self._pending.get(pw.path) is pw and self._writer_error is None
-                    if self._pending.get(pw.path) is pw:
-                        del self._pending[pw.path]
-                    if pw.pin is not None:
-                        self._free_pins.append(pw.pin)
-                    self._freed.notify_all()   # (waiters run once this block releases the lock)
-                    if pw.dev is None:
-                        pass
-                    elif landed and self.victim_limit > 0:   # keep the packed bytes in HBM
-                        self._drop_victim(pw.path)
-                        self._victims[pw.path] = DeviceRecords(pw.header, pw.dev, pw.nbytes, pw.stride)
-                        self._victim_bytes += pw.dev.numel()
-                        while self._victim_bytes > self.victim_limit and self._victims:
-                            _, old = self._victims.popitem(last=False)
-                            self._victim_bytes -= old.dev.numel()
-                            self._free_devs.append(old.dev)
-                    else:
-                        self._free_devs.append(pw.dev)
-                pw.done.set()
-                self._queue.task_done()
+                failed = True
+            if pw.event is not None:
+                # a superseded write skipped its wait: the D2H may still be
+                # reading `dev` / filling `pin`, so neither goes back to a pool
+                # before it completes
+                pw.event.synchronize()
+            self._settle(pw, failed)
+            pw.done.set()
+            self._queue.task_done()
+
+    def _write_one(self, pw: _PendingWrite) -> None:
+        with self._lock:   # superseded by a newer write of the path: skip the disk work
+            stale = self._pending.get(pw.path) is not pw
+        if stale:
+            self.stats["superseded_writes"] += 1
+            return
+        if pw.event is not None:
+            pw.event.synchronize()   # the D2H copy of the packed records
+        tmp = pw.path.with_name(f"{pw.path.name}.{threading.get_ident()}.tmp")
+        with open(tmp, "wb") as f:   # straight from pinned memory, no bytes copy
+            if pw.make is not None:
+                f.write(pw.make())
+            else:
+                f.write(pw.header)
+                f.write(memoryview(pw.pin.numpy())[:pw.nbytes])
+        with self._lock:   # several writers: only the newest write of a path lands
+            current = self._pending.get(pw.path) is pw
+            if current:
+                tmp.replace(pw.path)
+        if not current:
+            tmp.unlink(missing_ok=True)
+
+    def _settle(self, pw: _PendingWrite, failed: bool) -> None:
+        """Return a finished write's buffers (or keep them, see below)."""
+        with self._lock:
+            current = self._pending.get(pw.path) is pw
+            if failed and current:
+                # keep the entry and its packed device bytes: a reload is still
+                # served from them (no silent stale read of the old file) and
+                # the next drain() re-queues the write
+                self._failed.append(pw)
+                self._freed.notify_all()
+                return
+            landed = current and not failed
+            if current:
+                del self._pending[pw.path]
+            if pw.pin is not None:
+                self._free_pins.append(pw.pin)
+            self._freed.notify_all()   # (waiters run once this block releases the lock)
+            if pw.dev is None:
+                pass
+            elif landed and self.victim_limit > 0:   # keep the packed bytes in HBM
+                self._drop_victim(pw.path)
+                self._victims[pw.path] = DeviceRecords(pw.header, pw.dev, pw.nbytes, pw.stride)
+                self._victim_bytes += pw.dev.numel()
+                while self._victim_bytes > self.victim_limit and self._victims:
+                    _, old = self._victims.popitem(last=False)
+                    self._victim_bytes -= old.dev.numel()
+                    self._free_devs.append(old.dev)
+            else:
+                self._free_devs.append(pw.dev)
 
     def _drop_victim(self, path: Path) -> None:   # caller holds the lock
         old = self._victims.pop(path, None)
@@ -478,8 +504,30 @@ class ChunkStreamer:
             exc, self._writer_error = self._writer_error, None
             raise IoFailure(f"write-behind failed: {exc}") from exc
 
+    def _retry_failed(self) -> None:
+        """Re-queue the write-behinds that failed and are still the newest
+        write of their path (their packed bytes were kept)."""
+        with self._lock:
+            retry = [pw for pw in self._failed if self._pending.get(pw.path) is pw]
+            self._failed = []
+        for pw in retry:
+            pw.done = threading.Event()
+            self._queue.put(pw)
+
+    def _release_superseded(self, old) -> None:   # caller holds the lock
+        """A new write replaces a failed one of the same path: its buffers
+        return to the pools (its D2H completed before it was attempted)."""
+        if old is not None and old in self._failed:
+            self._failed.remove(old)
+            if old.pin is not None:
+                self._free_pins.append(old.pin)
+            if old.dev is not None:
+                self._free_devs.append(old.dev)
+
     def drain(self) -> None:
-        """Block until every pending write reached the disk (flush point)."""
+        """Block until every pending write reached the disk (flush point).
+        A write that failed before is retried once per drain."""
+        self._retry_failed()
         self._queue.join()
         self.check()
 

@@ -18,6 +18,7 @@ Fixtures:
   grid.npz          encode_positions, chunk coords, frustum planes, visible sets
   diskformat.npz    pack_chunk / pack_keyframe bytes
   store_trace.json  ChunkStore policy trace (loads, evictions, stats)
+  view_edits.json   in-place edits through chunk.gaussians / gather_visible + flushed file hashes
 """
 
 from __future__ import annotations
@@ -352,6 +353,83 @@ def make_store_trace():
     (HERE / "store_trace.json").write_text(json.dumps(trace))
 
 
+def make_view_edits():
+    """Write-through view contract (store.py:361-379): the reference store
+    edited in place through chunk.gaussians / gather_visible -- the
+    refine_reset loop (loopclose.py:236-242: opacity + opt_state = b"" then
+    mark_chunk_mutated), nudge-style sh0/opacity edits (sim.py:309-317) and
+    scale edits through GaussianRefs -- interleaved with paging.  Records the
+    declarative op list and the sha256 of every flushed chunk file."""
+    import hashlib
+    rng = np.random.default_rng(23)
+    out = {"inserts": [], "ops": []}
+    with tempfile.TemporaryDirectory() as d:
+        st = store.ChunkStore(store.StoreConfig(disk_root=d, chunk_size_m=10.0, gaussian_budget=70,
+                                                keyframe_budget=4, io_ns_per_byte=1.0))
+        cells = [(x, y, 0) for x in range(-2, 2) for y in range(-1, 2)]
+        gs = []
+        for k in range(150):
+            cx, cy, cz = cells[k % len(cells)]
+            p = [cx * 10 + rng.uniform(-4.9, 4.9), cy * 10 + rng.uniform(-4.9, 4.9), rng.uniform(-4.9, 4.9)]
+            opt = b"" if k % 5 else bytes(rng.integers(0, 256, int(rng.integers(1, 9))).astype(np.uint8))
+            gs.append(core.Gaussian(position=p, opacity=float(rng.uniform(0, 1)),
+                                    scale=rng.uniform(0.01, 1, size=3),
+                                    rotation=core.quat_normalize(rng.normal(size=4)), sh=rng.normal(size=48),
+                                    opt_state=opt))
+        for a in range(0, 150, 50):
+            batch = gs[a:a + 50]
+            st.insert_gaussians(batch)
+            out["inserts"].append([{"position": g.position.tolist(), "opacity": g.opacity,
+                                    "scale": g.scale.tolist(), "rotation": g.rotation.tolist(),
+                                    "sh": g.sh.tolist(), "opt": g.opt_state.hex()} for g in batch])
+        all_ids = sorted(st.known_chunk_ids())
+        f32 = lambda v: float(np.float32(v))  # noqa: E731
+        for step in range(40):
+            kind = rng.choice(["reset", "nudge", "scale", "ensure"], p=[0.2, 0.35, 0.2, 0.25])
+            if kind == "ensure" or not st.resident_chunk_ids():
+                ids = sorted({all_ids[int(rng.integers(len(all_ids)))] for _ in range(int(rng.integers(1, 4)))})
+                st.ensure_resident(ids)
+                out["ops"].append({"op": "ensure", "ids": [str(i) for i in ids]})
+                continue
+            res = sorted(st.resident_chunk_ids())
+            cid = res[int(rng.integers(len(res)))]
+            if kind == "reset":   # refine_reset's inner loop (loopclose.py:236-242)
+                op = f32(rng.uniform(0.05, 0.2))
+                for g in st.chunk(cid).gaussians:
+                    g.opacity = op
+                    g.opt_state = b""
+                st.mark_chunk_mutated(cid)
+                out["ops"].append({"op": "reset", "id": str(cid), "opacity": op})
+            elif kind == "nudge":   # sim.py:309-317 style in-place edits
+                n = len(st.chunk(cid))
+                if not n:
+                    continue
+                edits = []
+                for _ in range(int(rng.integers(1, 4))):
+                    i = int(rng.integers(n))
+                    g = st.chunk(cid).gaussians[i]
+                    sh0 = np.float32(g.sh[[0, 16, 32]] + rng.normal(size=3) * 0.1).astype(np.float64)
+                    g.sh[[0, 16, 32]] = sh0
+                    newop = None
+                    if rng.random() < 0.5:
+                        newop = f32(min(1.0, g.opacity + 0.02))
+                        g.opacity = newop
+                    edits.append({"index": i, "sh0": sh0.tolist(), "opacity": newop})
+                st.mark_chunk_mutated(cid)
+                out["ops"].append({"op": "nudge", "id": str(cid), "edits": edits})
+            else:   # in-place scale edits through gather_visible refs
+                refs = st.gather_visible([cid])
+                picks = sorted({int(rng.integers(len(refs))) for _ in range(3)}) if refs else []
+                for k in picks:
+                    g = refs[k].gaussian
+                    g.scale[:] = np.float32(g.scale * 1.25).astype(np.float64)
+                out["ops"].append({"op": "scale", "id": str(cid), "picks": picks})
+        st.flush()
+        out["files"] = {p.name: hashlib.sha256(p.read_bytes()).hexdigest()
+                        for p in sorted((Path(d) / "chunks").glob("*.dcg"))}
+    (HERE / "view_edits.json").write_text(json.dumps(out))
+
+
 def make_select_trace():
     """KeyframeIndex / select_keyframe / record_loss policy trace (select.py)."""
     from splatmap import select, sim
@@ -385,6 +463,7 @@ if __name__ == "__main__":
     make_grid()
     make_diskformat()
     make_store_trace()
+    make_view_edits()
     make_render_fd()
     for p in sorted(HERE.glob("*.npz")) + sorted(HERE.glob("*.json")):
         print(f"{p.name:24s} {p.stat().st_size:>9d} bytes")

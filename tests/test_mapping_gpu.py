@@ -213,3 +213,103 @@ def test_keyframes_arriving_mid_run_graphs_equal_eager(cuda, tmp_path):
     sa, sb = engines[0].store.slab, engines[1].store.slab
     hw = sa.high_water()
     assert torch.equal(sa.params[:hw], sb.params[:hw])
+
+
+def test_pose_update_recaptures_graph(cuda, tmp_path):
+    """store.update_keyframe_pose (the reference's loopclose.py:183 call) by
+    less than the visibility cache's pose quantum keeps the visible set, the
+    slots and the layout; the captured graph must not replay the old camera.
+    Graph replay after the correction equals eager execution bit for bit."""
+    import torch
+
+    from paper_2511_23030_b200.core import Pose
+    a = _c1_engine(tmp_path / "a", budget=100_000, use_graphs=True)
+    b = _c1_engine(tmp_path / "b", budget=100_000, use_graphs=False)
+    for s in range(10):   # every keyframe's graph captured
+        assert a.optimization_step(0, s).loss == b.optimization_step(0, s).loss
+    assert getattr(a, "_graphs", {})
+    for e in (a, b):
+        for kid in sorted(e.store.resident_keyframe_ids()):
+            kf = e.store.keyframe_get(kid)
+            e.store.update_keyframe_pose(kid, Pose(rotation=kf.pose.rotation,
+                                                   translation=kf.pose.translation + np.array([2e-3, -1e-3, 0.0])))
+    for s in range(10, 20):
+        ra, rb = a.optimization_step(0, s), b.optimization_step(0, s)
+        assert ra.selected_kf == rb.selected_kf and ra.loss == rb.loss, s
+    hw = a.store.slab.high_water()
+    assert torch.equal(a.store.slab.params[:hw], b.store.slab.params[:hw])
+    # at most one camera per keyframe among the live graphs
+    cams = {}
+    for k in a._graphs:
+        assert cams.setdefault(k[0], k[1]) == k[1]
+
+
+def _oracle_state(eng):
+    """fp64 oracle TrainState holding the slab rows [0, high water) exactly."""
+    from oracle import oracle as O
+    s = eng.store.slab
+    hw = s.high_water()
+    p = s.params[:hw].cpu().numpy().astype(np.float64)
+    st = O.TrainState(p[:, 0:3], p[:, 3:7], p[:, 7:10], p[:, 10], p[:, 11:14])
+    st.m = s.adam_m[:hw, :14].cpu().numpy().astype(np.float64).copy()
+    st.v = s.adam_v[:hw, :14].cpu().numpy().astype(np.float64).copy()
+    st.steps = s.adam_m[:hw, 14].cpu().numpy().astype(np.int64).copy()
+    return st, p
+
+
+STEP_GROUPS = {"positions": slice(0, 3), "rotations": slice(3, 7), "scales": slice(7, 10),
+               "opacities": slice(10, 11), "sh0": slice(11, 14)}
+
+
+def test_optimization_step_matches_oracle(cuda, tmp_path):
+    """a15: MappingEngine.optimization_step (the drop-in for sim.py:319-370:
+    policy + fwd -> loss -> bwd -> Adam, graph-replayed) against the oracle's
+    fused CPU step (oracle/render_oracle.c or_train_step, fp64) on the same
+    keyframe and active set (sorted-chunk-id order), step by step from the
+    same state.  Tolerances (written here): loss relative 1e-5; Adam moments
+    per parameter group ||dm|| <= 1e-3 ||m|| (the gradient tolerance, m is a
+    gradient average) and ||dv|| <= 2e-3 ||v||; the parameter update of every
+    Gaussian within 1e-6 (1 + |p|) + 1e-3 |update|, except Gaussians whose
+    gradient is below the fp32 resolution of the compositing sums (Adam's
+    eps = 1e-15 turns a gradient of ~1e-9 into a full-size signed step, and
+    its sign is noise in either precision): at most 0.5 % of the active set,
+    and their steps stay bounded by 2 lr."""
+    from paper_2511_23030_b200.mapping import AdamSettings
+    eng = _c1_engine(tmp_path, budget=100_000)
+    a = AdamSettings()
+    lr = np.array([a.lr_position] * 3 + [a.lr_rotation] * 4 + [a.lr_scale] * 3 + [a.lr_opacity] + [a.lr_sh0] * 3)
+    worst = []
+    for s in range(8):
+        st, before = _oracle_state(eng)
+        row = eng.optimization_step(0, s)
+        kf = eng.store.keyframe_get(row.selected_kf)
+        ids = sorted(eng._visible_for_pose(kf.pose)[0])
+        sub = np.concatenate([np.arange(o, o + c) for o, c in eng.store.segments(ids)])
+        loss = st.step(kf.pose.rotation, kf.pose.translation, kf.intrinsics, kf.rgb.astype(np.float64),
+                       kf.depth.astype(np.float64), eng.weights.lambda_s, eng.weights.lambda_depth, lr,
+                       a.beta1, a.beta2, a.eps, a.min_scale, subset=sub)
+        assert abs(row.loss - loss) <= 1e-5 * max(1.0, abs(loss)), (s, row.loss, loss)
+        slab = eng.store.slab
+        hw = slab.high_water()
+        got = slab.params[:hw].cpu().numpy().astype(np.float64)[sub][:, :14]
+        gm = slab.adam_m[:hw].cpu().numpy().astype(np.float64)[sub]
+        gv = slab.adam_v[:hw].cpu().numpy().astype(np.float64)[sub]
+        want = np.concatenate([st.pos, st.rot, st.scale, st.opac[:, None], st.sh0], 1)[sub]
+        assert np.array_equal(gm[:, 14], st.steps[sub].astype(np.float64)), s
+        for name, sl in STEP_GROUPS.items():
+            dm = np.linalg.norm(gm[:, sl] - st.m[sub][:, sl])
+            dv = np.linalg.norm(gv[:, sl] - st.v[sub][:, sl])
+            assert dm <= 1e-3 * np.linalg.norm(st.m[sub][:, sl]) + 1e-30, (s, name, "m", dm)
+            assert dv <= 2e-3 * np.linalg.norm(st.v[sub][:, sl]) + 1e-30, (s, name, "v", dv)
+        upd_g = got - before[sub][:, :14]
+        upd_o = want - before[sub][:, :14]
+        bad = np.abs(upd_g - upd_o) > 1e-6 * (1 + np.abs(want)) + 1e-3 * np.abs(upd_o)
+        bad_rows = bad.any(axis=1)
+        worst.append(bad_rows.mean())
+        assert bad_rows.mean() <= 5e-3, (s, bad_rows.sum(), len(sub))
+        assert np.all(np.abs(upd_g[bad]) <= 2.0 * np.broadcast_to(lr, bad.shape)[bad] + 1e-7), s
+        # the outliers are the near-zero-gradient Gaussians
+        g_o = np.abs(st.m[sub] / (1 - a.beta1 ** st.steps[sub][:, None]))
+        scale = np.abs(g_o).max(axis=0)
+        assert np.all(g_o[bad] <= 1e-4 * np.broadcast_to(scale, g_o.shape)[bad]), s
+    print("fraction of rows outside the elementwise bound per step:", worst)

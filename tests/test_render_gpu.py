@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from tests.golden_cases import f32, oracle_args, render_case
+from tests.golden_cases import edge_scene, f32, oracle_args, render_case
 
 pytestmark = pytest.mark.gpu
 
@@ -211,38 +211,7 @@ def test_edge_cases_match_oracle(cuda):
     with boxes reaching in, needle-thin and near-point (0.3-px dilation only)
     splats, and a stack of opaque splats that saturates T below 1e-10 (early
     termination in the forward, T recovery in the backward)."""
-    from paper_2511_23030_b200.core import CameraIntrinsics, Pose, quat_normalize
-    rng = np.random.default_rng(17)
-    intr = CameraIntrinsics(fx=60.0, fy=60.0, cx=48.3, cy=30.1, width=97, height=61, near=0.2)
-    pose = Pose(rotation=quat_normalize([1.0, 0.01, -0.02, 0.005]), translation=[0.0, 0.0, 0.0])
-    parts = []
-
-    def add(pos, scales, op, quats=None):
-        m = len(pos)
-        q = quats if quats is not None else rng.normal(size=(m, 4))
-        q = q / np.linalg.norm(q, axis=1, keepdims=True)
-        parts.append((np.asarray(pos, float), q, np.asarray(scales, float), np.asarray(op, float),
-                      (rng.uniform(0.05, 0.95, (m, 3)) - 0.5) / 0.28209479177))
-
-    m = 300   # background
-    add(np.stack([rng.uniform(-3, 3, m), rng.uniform(-2, 2, m), rng.uniform(1, 8, m)], 1),
-        rng.uniform(0.03, 0.4, (m, 3)), rng.uniform(0.2, 0.95, m))
-    m = 40    # straddling / behind the near plane
-    add(np.stack([rng.uniform(-0.3, 0.3, m), rng.uniform(-0.2, 0.2, m), rng.uniform(-0.1, 0.5, m)], 1),
-        rng.uniform(0.02, 0.2, (m, 3)), rng.uniform(0.2, 0.9, m))
-    m = 40    # far off screen, large: boxes clipped to the image
-    add(np.stack([rng.choice([-1, 1], m) * rng.uniform(4, 9, m), rng.uniform(-2, 2, m), rng.uniform(2, 6, m)], 1),
-        rng.uniform(0.5, 2.5, (m, 3)), rng.uniform(0.3, 0.9, m))
-    m = 60    # needles and near-points
-    sc = np.exp(rng.uniform(np.log(1e-4), np.log(0.5), (m, 3)))
-    sc[: m // 2, 1:] = 1e-4
-    add(np.stack([rng.uniform(-1.5, 1.5, m), rng.uniform(-1, 1, m), rng.uniform(1, 4, m)], 1), sc,
-        rng.uniform(0.3, 0.95, m))
-    m = 30    # opaque stack in front of the centre: saturates T
-    add(np.stack([rng.normal(0, 0.05, m), rng.normal(0, 0.05, m), np.linspace(1.0, 1.6, m)], 1),
-        np.full((m, 3), 0.25), np.full(m, 0.999), np.tile([1.0, 0, 0, 0], (m, 1)))
-    pos, q, sc, op, sh0 = (np.concatenate(x) for x in zip(*parts))
-    scene = f32(dict(positions=pos, rotations=q, scales=sc, opacities=op, sh0=sh0))
+    scene, pose, intr, rng = edge_scene()
     ref = O.render_arrays(*oracle_args(scene, pose, intr))
     _assert_close(_render(scene, pose, intr), ref, "edge")
     h, w = intr.height, intr.width
@@ -459,3 +428,51 @@ def test_full_size_c2_view_matches_oracle(cuda):
         a, b = gpu[k], gref[k]
         nb = np.linalg.norm(b)
         assert np.linalg.norm(a - b) <= 1e-3 * nb + 1e-9, (k, np.linalg.norm(a - b) / max(nb, 1e-30))
+
+
+def _rigid_case(rng, n, span=2.0, pose_sigma=0.3, t_sigma=5.0):
+    from paper_2511_23030_b200.core import Gaussian, Pose, RigidTransform, quat_multiply, quat_normalize
+    scene = []
+    for _ in range(n):
+        sh = np.zeros(48)
+        sh[[0, 16, 32]] = (rng.uniform(0.05, 0.95, 3) - 0.5) / 0.28209479177
+        scene.append(Gaussian(position=[rng.uniform(-span, span), rng.uniform(-span, span), rng.uniform(2, 8)],
+                              rotation=quat_normalize(rng.normal(size=4)), scale=rng.uniform(0.05, 0.3, size=3),
+                              opacity=float(rng.uniform(0.3, 0.95)), sh=sh))
+    pose = Pose(translation=rng.normal(size=3) * pose_sigma)
+    t = RigidTransform(rotation=quat_normalize(rng.normal(size=4)), translation=rng.normal(size=3) * t_sigma)
+    moved_pose = Pose(rotation=quat_normalize(quat_multiply(t.rotation, pose.rotation)),
+                      translation=t.apply_point(pose.translation))
+    return scene, pose, t, moved_pose
+
+
+def test_rigid_co_transform_invariance(cuda):
+    """test_renderloss.py:113-129 on the GPU path: moving scene and camera by
+    the same rigid transform leaves the image unchanged (rgb < 1e-5, depth
+    < 1e-4)."""
+    from paper_2511_23030_b200.core import CameraIntrinsics, transform_gaussian
+    from paper_2511_23030_b200.renderloss import render
+    rng = np.random.default_rng(61)
+    intr = CameraIntrinsics(fx=30.0, fy=30.0, cx=16.0, cy=16.0, width=64, height=64)
+    for _ in range(3):
+        scene, pose, t, moved_pose = _rigid_case(rng, 120, pose_sigma=0.2, t_sigma=4.0)
+        base = render(scene, pose, intr)
+        out = render([transform_gaussian(g, t) for g in scene], moved_pose, intr)
+        assert np.abs(base.rgb - out.rgb).max() < 1e-5
+        assert np.abs(base.depth - out.depth).max() < 1e-4
+
+
+def test_criterion_6_rigid_render_invariance(cuda):
+    """Acceptance criterion 6 (test_acceptance.py:235-261) on the GPU path:
+    20 random 150-splat scenes, rgb invariant to a rigid co-transform < 1e-5."""
+    from paper_2511_23030_b200.core import CameraIntrinsics, transform_gaussian
+    from paper_2511_23030_b200.renderloss import render
+    rng = np.random.default_rng(106)
+    intr = CameraIntrinsics(fx=50.0, fy=50.0, cx=32.0, cy=32.0, width=64, height=64, near=0.2, far=100.0)
+    worst = 0.0
+    for _ in range(20):
+        scene, pose, t, moved_pose = _rigid_case(rng, 150)
+        base = render(scene, pose, intr)
+        out = render([transform_gaussian(g, t) for g in scene], moved_pose, intr)
+        worst = max(worst, float(np.abs(out.rgb - base.rgb).max()))
+    assert worst < 1e-5, worst

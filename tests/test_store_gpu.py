@@ -375,3 +375,79 @@ def test_streamer_under_pool_pressure_matches_sync(cuda, tmp_path):
     for c in ids:
         name = f"{c:016x}.dcg"
         assert (tmp_path / "sync" / "chunks" / name).read_bytes() == (tmp_path / "tight" / "chunks" / name).read_bytes()
+
+
+def test_write_through_views_match_reference_bytes(cuda, tmp_path):
+    """chunk.gaussians / gather_visible are live views (store.py:361-379): the
+    reference's refine_reset loop (loopclose.py:236-242), nudge-style in-place
+    sh0 / opacity edits (sim.py:309-317) and scale edits through GaussianRefs,
+    interleaved with paging, flush byte-identical files
+    (tests/golden/view_edits.json was recorded on the reference store)."""
+    import hashlib
+
+    from paper_2511_23030_b200.core import Gaussian
+    from paper_2511_23030_b200.store import ChunkStore, StoreConfig
+    rec = json.loads((GOLDEN / "view_edits.json").read_text())
+    st = ChunkStore(StoreConfig(disk_root=tmp_path, chunk_size_m=10.0, gaussian_budget=70,
+                                keyframe_budget=4, io_ns_per_byte=1.0))
+    for batch in rec["inserts"]:
+        st.insert_gaussians([Gaussian(position=g["position"], opacity=g["opacity"], scale=g["scale"],
+                                      rotation=g["rotation"], sh=g["sh"], opt_state=bytes.fromhex(g["opt"]))
+                             for g in batch])
+    for op in rec["ops"]:
+        if op["op"] == "ensure":
+            st.ensure_resident([int(i) for i in op["ids"]])
+            continue
+        cid = int(op["id"])
+        if op["op"] == "reset":
+            for g in st.chunk(cid).gaussians:
+                g.opacity = op["opacity"]
+                g.opt_state = b""
+            st.mark_chunk_mutated(cid)
+        elif op["op"] == "nudge":
+            for e in op["edits"]:
+                g = st.chunk(cid).gaussians[e["index"]]
+                g.sh[[0, 16, 32]] = e["sh0"]
+                if e["opacity"] is not None:
+                    g.opacity = e["opacity"]
+            st.mark_chunk_mutated(cid)
+        else:
+            refs = st.gather_visible([cid])
+            for k in op["picks"]:
+                g = refs[k].gaussian
+                g.scale[:] = np.float32(g.scale * 1.25).astype(np.float64)
+    st.flush()
+    got = {p.name: hashlib.sha256(p.read_bytes()).hexdigest()
+           for p in sorted((tmp_path / "chunks").glob("*.dcg"))}
+    assert got == rec["files"]
+
+
+def test_opt_state_reset_gives_fresh_adam(cuda, tmp_path):
+    """opt_state = b"" through a view resets the row's Adam state (the
+    loopclose.py:241 contract): a trained chunk's reset rows get zero moments
+    and step 0 and are written with opt_len 0, untouched rows keep their
+    Adam tail; a view whose rows moved on (training) fails loudly."""
+    from paper_2511_23030_b200 import diskformat
+    from paper_2511_23030_b200.errors import NotResident
+    from paper_2511_23030_b200.workloads import build_c1
+    eng = build_c1(n=4000, keyframes=3, budget=100_000, store_dir=tmp_path)
+    for s in range(4):
+        eng.optimization_step(0, s)
+    st = eng.store
+    cid = max((c for c in st.resident_chunk_ids() if st.chunk(c).trained), key=lambda c: len(st.chunk(c)))
+    ch = st.chunk(cid)
+    views = ch.gaussians
+    assert all(len(g.opt_state) == diskformat.ADAM_TAIL for g in views)
+    reset = set(range(0, len(views), 2))
+    for i in reset:
+        views[i].opt_state = b""
+    st.mark_chunk_mutated(cid)
+    lo = ch.offset
+    m = st.slab.adam_m[lo:lo + len(ch)].cpu().numpy()
+    assert np.all(m[sorted(reset)] == 0.0) and np.all(m[1::2, 14] > 0)
+    st.flush()
+    _, gs = diskformat.unpack_chunk((tmp_path / "chunks" / f"{cid:016x}.dcg").read_bytes())
+    assert [len(g.opt_state) for g in gs] == [0 if i in reset else diskformat.ADAM_TAIL for i in range(len(gs))]
+    st.mark_trained([cid])   # the device rows moved on (what a training step does)
+    with pytest.raises(NotResident):
+        views[1].opacity = 0.5
