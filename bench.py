@@ -39,6 +39,9 @@ sys.path.insert(0, str(ROOT))
 METRIC = "mapping iters/sec (render fwd+bwd+Adam)"
 UNIT = "it/s"
 WORKLOAD = "C2: 1M-Gaussian Replica-shaped room, 640x480, 8x8x2 chunks (s=1 m), 16 keyframes"
+WORKLOAD_C3 = ("C3: C2's 1M room at 640x480, K keyframes per mapping step (default 8), data-parallel over the "
+               "GPUs (keyframe j on rank j mod G), packed union gradients summed with one NCCL all-reduce, "
+               "replicated Adam; value = keyframe iterations/s over all ranks")
 
 
 def _peaks():
@@ -119,6 +122,30 @@ def _ncu_kernel(name: str):
         return None
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _ensure_ranks(args) -> None:
+    """`bench.py --gpus N` outside torchrun re-executes itself under
+    torch.distributed.run with N ranks (one per GPU, 127.0.0.1); under a
+    launcher whose world size is not N it refuses to run."""
+    env = os.environ.get("WORLD_SIZE")
+    if env is None:
+        if args.gpus > 1:
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                   f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+                   f"--master-port={_free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+            sys.exit(subprocess.call(cmd))
+        return
+    if int(env) != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env}; refusing to report\n")
+        sys.exit(2)
+
+
 def _dist():
     import torch
     import torch.distributed as dist
@@ -160,55 +187,74 @@ def cpu_baseline_step(eng, kf_id: int, seconds: float = 20.0, threads: int | Non
                       f"Gaussians at 640x480, {per:.2f} s each, {threads} threads"}
 
 
+def workload_config(args) -> dict:
+    """The benchmarked configuration -- identical in both arms' lines."""
+    c3 = args.gpus > 1 or args.keyframes_per_step > 1
+    return {"workload": WORKLOAD_C3 if c3 else WORKLOAD, "keyframes_per_step": args.keyframes_per_step,
+            "gaussians_total": args.n, "keyframes": args.keyframes, "resolution": [640, 480],
+            "parallelism": f"dp{args.gpus}",
+            "l2": "inputs larger than L2 (slab params+Adam+grads 256 MB/1M Gaussians)"}
+
+
 def run_reference(args, world, rank):
-    """--impl reference: the reference algorithm's CPU path (oracle port) on the C2 config."""
+    """--impl reference: the reference algorithm's CPU path on this host.
+
+    The like-for-like arm (oracle/ref_arm.py OracleMappingLoop): the
+    reference's own policy code (baseline/_ref/splatmap select / culling,
+    unmodified) draws the same keyframe sequence as the GPU arm -- one
+    iteration per keyframe (the GPU arm's graph warm-up), W warm-up steps,
+    then exactly K timed steps of K keyframes each -- and each keyframe
+    iteration (render, loss + gradient, backward, Adam on the active set)
+    runs in the fp64 oracle on all host threads.  Two more measurements
+    travel in the line: the same iteration on 1 thread (BASELINE.md 3's
+    primary denominator) and, for context, the unmodified reference
+    sim._Replay.optimization_step (forward + nudge only) on the same scene.
+    """
     if rank != 0:
         return
-    from oracle import oracle as O
+    from oracle.ref_arm import OracleMappingLoop, reference_replay_leg
     from paper_2511_23030_b200.synthetic import C2_INTR, perturbed, room_poses, room_scene
-    scene = room_scene(1_000_000, seed=42)
-    poses = room_poses(16, seed=42)
-    target = perturbed(scene, 49)
     threads = os.cpu_count() or 1
-    st = O.TrainState(scene.positions, scene.rotations, scene.scales, scene.opacities, scene.sh0)
-    intr = C2_INTR
-    gts = {}
-    lr = [1e-4] * 3 + [1e-3] * 4 + [5e-5] * 3 + [1e-2] + [2.5e-3] * 3
-    budget = 150.0
-    t_all = time.perf_counter()
-    steps, times, n_active = 0, [], []
-    for k in range(max(0, min(args.warmup, 1)) + max(1, args.steps)):
-        kf = k % 2
-        if kf not in gts:
-            rgb, depth, _ = O.render_arrays(target.positions, target.rotations, target.scales,
-                                            target.opacities, target.sh0, poses[kf].rotation,
-                                            poses[kf].translation, intr.fx, intr.fy, intr.cx, intr.cy,
-                                            intr.near, intr.width, intr.height, threads=threads)
-            gts[kf] = (np.round(np.clip(rgb, 0, 1) * 255) / 255, depth)
-        t0 = time.perf_counter()
-        # the reference step: chunk culling -> active-set gather -> render/loss -> update
-        idx = O.active_set(st.pos, poses[kf].rotation, poses[kf].translation, intr, 200.0, 1.0)
-        st.step(poses[kf].rotation, poses[kf].translation, intr, gts[kf][0], gts[kf][1], 0.2, 0.5, lr,
-                0.9, 0.999, 1e-15, 1e-5, threads=threads, subset=idx)
-        dt = time.perf_counter() - t0
-        n_active.append(len(idx))
-        if k >= min(args.warmup, 1):
-            times.append(dt)
-            steps += 1
-        if time.perf_counter() - t_all > budget and steps >= 1:
-            break
-    per = sum(times) / len(times)
-    value = 1.0 / per
+    kps = args.keyframes_per_step
+    scene = room_scene(args.n, seed=42)
+    poses = room_poses(args.keyframes, seed=42)
+    target = perturbed(scene, 49)
+    loop = OracleMappingLoop(scene, target, poses, C2_INTR, threads=threads)
+    loop.warm()
+    for _ in range(args.warmup * kps):
+        loop.step()
+    n0 = len(loop.n_active)
+    t0 = time.perf_counter()
+    for _ in range(args.steps * kps):   # C3: K keyframe iterations per step, in sequence
+        loop.step()
+    dt = time.perf_counter() - t0
+    seq = loop.selected[-args.steps * kps:]
+    n_act = float(np.mean(loop.n_active[n0:]))
+    value = args.steps * kps / dt
+    t1 = time.perf_counter()
+    loop.train(seq[-1], threads=1)
+    one = 1.0 / (time.perf_counter() - t1)
+    ctx = None
+    if not args.no_context:
+        try:
+            ctx = reference_replay_leg(scene, target, poses, C2_INTR, steps=2, warmup=1, gts=loop.gt)
+        except Exception as exc:   # report, never fake
+            ctx = {"value": None, "sample": f"failed: {type(exc).__name__}: {exc}"}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": per * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": WORKLOAD, "parallelism": "cpu"},
+        "data": "synthetic", "config": workload_config(args),
+        "kf_sequence": seq,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{steps} oracle mapping iterations (chunk cull + active-set gather "
-                                   f"+ fp64 fwd+loss+bwd+Adam, ~{int(np.mean(n_active))} active of 1M "
-                                   f"Gaussians, 640x480, oracle/render_oracle.c; the reference itself is "
-                                   f"forward-only) with {threads} threads"},
+                         "sample": f"{args.steps} steps x {kps} keyframe iteration(s) after {len(poses)} "
+                                   f"warm-up iterations + {args.warmup} warm-up steps: reference policy "
+                                   f"(baseline/_ref/splatmap select/culling) + fp64 oracle fwd+loss+bwd+Adam "
+                                   f"(oracle/render_oracle.c) on ~{int(n_act)} active of {args.n} Gaussians, "
+                                   f"640x480, {threads} threads",
+                         "single_thread": {"value": one, "unit": UNIT, "cores": 1,
+                                           "sample": "1 keyframe iteration of the same loop, 1 thread"}},
+        "reference_replay": ctx,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -224,9 +270,16 @@ def main():
     ap.add_argument("--keyframes", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-context", action="store_true", help="reference arm: skip the _Replay context leg")
+    ap.add_argument("--keyframes-per-step", type=int, default=None,
+                    help="K keyframes per mapping step (default 1 on one GPU = C2, 8 on N > 1 = C3)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = (1, 0, 0)
+    if args.impl != "reference":
+        _ensure_ranks(args)
+    if args.keyframes_per_step is None:
+        args.keyframes_per_step = 1 if args.gpus == 1 else 8
     if args.impl == "reference":
         world = int(os.environ.get("WORLD_SIZE", "1"))
         rank = int(os.environ.get("RANK", "0"))
@@ -243,8 +296,10 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
-    step_fn = (lambda f, s: eng.optimization_step(f, s)) if world == 1 else \
-        (lambda f, s: eng.optimization_step_dp(f, s, world, rank))
+    kps = args.keyframes_per_step
+    c3 = world > 1 or kps > 1
+    step_fn = (lambda f, s: eng.optimization_step(f, s)) if not c3 else \
+        (lambda f, s: eng.optimization_step_dp(f, s, world, rank, keyframes=kps))
     def timed(frame: int, clocks_gpu=None):
         """barrier + sync, CUDA events around exactly args.steps steps, max over ranks."""
         if dist is not None:
@@ -276,13 +331,32 @@ def main():
     launches0 = lib.sm_launch_count()
     ms, clk = timed(1, clocks_gpu=local)
     launches = lib.sm_launch_count() - launches0
+    kf_seq = [r.selected_kf for r in eng.rows[-args.steps * (kps if c3 else 1):]]
     ms_step = ms / args.steps
-    units = args.steps * world
+    units = args.steps * (kps if c3 else 1)   # keyframe iterations, all ranks
     value = units / (ms / 1e3)
     n_vis = eng.counter_gaussians / max(eng.counter_steps, 1)
     n_inst = eng.counter_instances / max(eng.counter_steps, 1)
     n_visit = eng.counter_visited / max(eng.counter_steps, 1)
     gauss_s = eng.counter_gaussians * world / (ms / 1e3)
+    c3_g1 = None
+    if rank == 0 and world == 1 and not c3:
+        # C3 at G = 1 (K = 8 keyframes per step on this GPU): the T_1(K) of the
+        # scaling runs, where N > 1 lines report the same K split over N ranks
+        dp = lambda f, s: eng.optimization_step_dp(f, s, 1, 0, keyframes=8)  # noqa: E731
+        for s in range(3):
+            dp(5, s)
+        n3 = max(args.steps // 8, 20)
+        torch.cuda.synchronize()
+        a3, b3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a3.record()
+        for s in range(n3):
+            dp(6, s)
+        b3.record()
+        torch.cuda.synchronize()
+        t3 = a3.elapsed_time(b3)
+        c3_g1 = {"workload": WORKLOAD_C3, "keyframes_per_step": 8, "n_gpus": 1, "steps": n3,
+                 "ms_per_step": t3 / n3, "value": 8 * n3 / (t3 / 1e3), "unit": UNIT}
     # ------------------------------------------------------------ e2e through the public API
     eng.upload_keyframes_each_step = True
     eng.warm_graphs()
@@ -342,15 +416,14 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "gaussians_total": args.n,
-                   "visible_gaussians_per_step": n_vis, "tile_instances_per_step": n_inst,
-                   "revisited_instances_per_step": n_visit,
-                   "resolution": [eng.intr.width, eng.intr.height], "keyframes_per_step_per_gpu": 1,
-                   "parallelism": f"dp{world}",
-                   "l2": "inputs larger than L2 (slab params+Adam+grads 256 MB/1M Gaussians)"},
+        "config": workload_config(args),
+        "measured": {"visible_gaussians_per_step": n_vis, "tile_instances_per_step": n_inst,
+                     "revisited_instances_per_step": n_visit},
+        "kf_sequence": kf_seq,
         "gaussians_per_s": gauss_s,
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clk, "roofline": roof,
         "stages": stages, "stages_pass_ms_per_step": pms / args.steps, "cpu_baseline": cpu,
+        "c3_g1": c3_g1,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -10,9 +10,9 @@ fused Adam over the active set, with a single 32-byte device->host read
 (loss + overflow flag) per step.
 
 Data-parallel mode (``optimization_step_dp``): K keyframes per step, rank r
-renders keyframes r, r+G, ...; gradients are summed with one NCCL
-all-reduce over the slab's used rows, then every rank applies the identical
-Adam update to its replica of the active tier.
+renders keyframes r, r+G, ...; the union active set's gradient records are
+packed and summed with one NCCL all-reduce, then every rank applies the
+identical Adam update to its replica of the active tier.
 """
 
 from __future__ import annotations
@@ -48,25 +48,33 @@ def derive_seed(master: int, purpose: int, counter: int) -> int:
 
 
 def dp_select(index: KeyframeIndex, latest_kf: int, seed: int, step_counter: int,
-              world: int) -> list[int]:
-    """Keyframes of one data-parallel step, identical on every rank: `world`
-    sequential loss-weighted draws (select.py policy) with derived seeds
-    (seed, 2, step*world + r); rank r trains keyframe r."""
+              k: int) -> list[int]:
+    """The K keyframes of one data-parallel mapping step, identical on every
+    rank: K loss-weighted draws (select.py policy) from the same candidate
+    set with derived seeds (seed, 2, step * K + j).  Keyframe j is rendered
+    by rank j mod G (C3: K = 8 over G = 1, 2, 4, 8).  K = 1 is exactly the
+    single-GPU step's draw (sim.py:331)."""
     try:
         candidates = candidate_set(index.position_of(latest_kf), index)
     except EmptyCandidates:
         candidates = [latest_kf]
-    return [select_keyframe(candidates, index, derive_seed(seed, 2, step_counter * world + r))
-            for r in range(world)]
+    return [select_keyframe(candidates, index, derive_seed(seed, 2, step_counter * k + j))
+            for j in range(k)]
 
 
-def allreduce_step(grads, lossbuf, group=None) -> None:
-    """The DP exchange: sum the gradient slab (NCCL on GPUs, gloo in tests) and
-    the per-rank [loss..., overflow] vector."""
+def owned_keyframes(k: int, world: int, rank: int) -> list[int]:
+    """Positions j of the step's K keyframes that rank `rank` renders."""
+    return list(range(rank, k, world))
+
+
+def allreduce_step(packed, lossbuf, group=None) -> None:
+    """The DP exchange: sum the packed gradient records of the union active
+    set and the [loss_0 .. loss_{K-1}, overflow] vector over the ranks (NCCL
+    on GPUs, gloo in the CPU tests)."""
     import torch.distributed as dist
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return
-    dist.all_reduce(grads, group=group)
+    dist.all_reduce(packed, group=group)
     dist.all_reduce(lossbuf, group=group)
 
 
@@ -408,6 +416,8 @@ class MappingEngine:
     def _dp_device_pass(self, kf: Keyframe, slots, n: int) -> None:
         """fwd -> loss -> bwd of this rank's keyframe: graph replay when captured,
         else eager (captured on the second visit, like train_view)."""
+        if self.upload_keyframes_each_step:
+            self.h2d_bytes += kf.intrinsics.width * kf.intrinsics.height * 7
         self.render.ensure(n, kf.intrinsics.width, kf.intrinsics.height)
         key = self._graph_key(kf, slots, n, True)
         entry = getattr(self, "_graphs", {}).get(key) if self.use_graphs else None
@@ -622,57 +632,85 @@ class MappingEngine:
         return row
 
     # ------------------------------------------------------ data parallel
-    def optimization_step_dp(self, frame_idx: int, step_idx: int, world: int, rank: int,
-                             group=None, inserted: int = 0) -> list[FrameMetrics]:
-        """One data-parallel mapping step: `world` keyframes, one per rank.
+    def _packed_buffer(self, n: int):
+        buf = getattr(self, "_packed", None)
+        if buf is None or buf.shape[0] < n:
+            buf = self._packed = self.torch.empty((max(int(n * 1.25), 1024), 16), dtype=self.torch.float32,
+                                                  device=self.device)
+        return buf
 
-        Every rank runs the same host policy (same derived seeds), so the
-        keyframe draws, visible sets and residency of the replicated active
-        tier are identical everywhere.  Rank r renders and backpropagates
-        keyframe r; the slab gradients are summed with one NCCL all-reduce,
-        the per-keyframe losses travel in a second tiny all-reduce, and each
-        rank applies the same Adam update over the union active set.
+    def optimization_step_dp(self, frame_idx: int, step_idx: int, world: int, rank: int,
+                             group=None, inserted: int = 0, keyframes: int | None = None) -> list[FrameMetrics]:
+        """One data-parallel mapping step over K keyframes.
+
+        Every rank runs the same host policy (same derived seeds), so the K
+        keyframe draws, their visible sets and the residency of the
+        replicated active tier are identical everywhere.  Rank r renders and
+        backpropagates keyframes r, r + G, ... into its slab gradients; the
+        union active set's gradient records are packed (K6 output rows ->
+        [n_union, 16]) and summed with one all-reduce, together with the
+        per-keyframe losses and an overflow count; every rank then applies
+        the same Adam update over the union from the summed buffer.  The
+        host reads the losses while Adam runs (the next draw needs them).
+        K = 1, G = 1 is bit-identical to ``optimization_step``.
         """
-        import torch.distributed as dist
         torch = self.torch
+        k = int(keyframes or world)
         store, stats = self.store, self.store.stats
         io0, loads0, ev0 = stats.io_nanos, stats.chunk_loads, stats.chunk_evictions
-        selected = dp_select(self.index, self.latest_kf, self.seed, self.step_counter, world)
+        selected = dp_select(self.index, self.latest_kf, self.seed, self.step_counter, k)
         kfs = [store.keyframe_get(s) for s in selected]
         vis = [self._visible_for_pose(kf.pose)[0] for kf in kfs]
         union = sorted(set().union(*vis))
         overlap_val = overlap(set(union), store.resident_chunk_ids()) if union else None
         if union:
             store.ensure_resident(union)
-        if not hasattr(self, "_union_set"):
+        if getattr(self, "_union_set", None) is None:
             self._union_set = _ActiveSet(self.device)
-            self._lossbuf = torch.zeros(world + 1, dtype=torch.float32, device=self.device)
-        mine = sorted(vis[rank])
-        slots_m, n_m = self.active.build(store.segments(mine))
+        if getattr(self, "_lossbuf", None) is None or self._lossbuf.numel() != k + 1:
+            self._lossbuf = torch.zeros(k + 1, dtype=torch.float32, device=self.device)
+            self._loss_host = torch.zeros(k + 1, dtype=torch.float32, pin_memory=True)
+        mine = owned_keyframes(k, world, rank)
         slots_u, n_u = self._union_set.build(store.segments(union))
-        slab = store.slab
+        packed = self._packed_buffer(n_u)
+        lib, stream = _lib.load(), _lib.stream_handle()
+        buf, host = self._lossbuf, self._loss_host
+        n_mine = 0
         for _ in range(6):
-            self._dp_device_pass(kfs[rank], slots_m, n_m)
-            buf = self._lossbuf
             buf.zero_()
-            buf[rank:rank + 1].copy_(self.loss.out[:1])
-            buf[world:world + 1].copy_(self.render.overflow_flag().float())
-            allreduce_step(slab.grads[:slab.high_water()], buf, group)
-            host = buf.cpu().numpy()
-            self.d2h_bytes += 4 * (world + 1)
-            if host[world] == 0:
+            n_mine = 0
+            for j in mine:
+                slots_j, n_j = self.active.build(store.segments(sorted(vis[j])))
+                self._dp_device_pass(kfs[j], slots_j, n_j)
+                buf[j:j + 1].copy_(self.loss.out[:1])
+                buf[k:k + 1].add_(self.render.overflow_flag().float())
+                n_mine += n_j
+            _lib.check(lib.sm_pack_grads(_lib.ptr(store.slab.grads), _lib.ptr(slots_u), n_u,
+                                         _lib.ptr(packed), stream), "pack_grads")
+            allreduce_step(packed[:n_u], buf, group)
+            host.copy_(buf, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            # Adam over the union from the summed records; skipped on the device
+            # when any rank overflowed (the overflow sum's float bits are non-zero)
+            _lib.check(lib.sm_adam_step_packed(_lib.ptr(store.slab.params), _lib.ptr(store.slab.adam_m),
+                                               _lib.ptr(store.slab.adam_v), _lib.ptr(packed), _lib.ptr(slots_u),
+                                               n_u, self._adam_c, _lib.ptr(buf[k:k + 1]), stream),
+                       "adam_step_packed")
+            ev.synchronize()
+            self.d2h_bytes += 4 * (k + 1)
+            if host[k] == 0:
                 break
-            slab.grads.zero_()
             self.render.grow_instances(self.render.counters()["n_instances"] * 2)
             self.drop_graphs()
         else:
             raise DeviceFailure("tile-instance buffer kept overflowing")
-        self._adam_noskip(slots_u, n_u)
         self.counter_steps += 1
-        self.counter_gaussians += n_m
+        self.counter_gaussians += n_mine
+        losses = host.numpy().astype(np.float64)
         rows = []
-        for r, (sel, kf) in enumerate(zip(selected, kfs)):
-            loss = float(host[r])
+        for j, (sel, kf) in enumerate(zip(selected, kfs)):
+            loss = float(losses[j])
             record_loss(sel, loss, self.index)
             kf.last_loss = loss
             kf.usage_remaining = self.index.usage_of(sel)
@@ -680,7 +718,7 @@ class MappingEngine:
                 store.mark_keyframe_dirty(sel)
             io = stats.io_nanos - io0
             step_ns = (io + NS_PER_RENDERED_GAUSSIAN * n_u + NS_PER_PIXEL * self.intr.width *
-                       self.intr.height * world + NS_PER_INSERTED_GAUSSIAN * inserted + NS_STEP_BASE)
+                       self.intr.height * k + NS_PER_INSERTED_GAUSSIAN * inserted + NS_STEP_BASE)
             rows.append(FrameMetrics(frame_idx, step_idx, stats.active_gaussians, stats.active_chunks,
                                      stats.active_keyframes, stats.chunk_loads - loads0,
                                      stats.chunk_evictions - ev0, io, step_ns, sel, overlap_val, loss))
@@ -689,10 +727,3 @@ class MappingEngine:
         self.step_counter += 1
         self.rows.extend(rows)
         return rows
-
-    def _adam_noskip(self, slots, n: int) -> None:
-        s = self.store.slab
-        rc = _lib.load().sm_adam_step(_lib.ptr(s.params), _lib.ptr(s.adam_m), _lib.ptr(s.adam_v),
-                                      _lib.ptr(s.grads), _lib.ptr(slots), int(n), self._adam_c, None,
-                                      _lib.stream_handle())
-        _lib.check(rc, "adam_step")
