@@ -119,6 +119,20 @@ int sm_render_backward(const float *params, const int32_t *slots, int64_t n,
                        const float *d_rgb, const float *d_depth, const float *d_alpha,
                        float *grads, void *stream);
 
+/* sm_render_backward + the K7 Adam step fused into its last stage (the
+ * single-keyframe mapping step, sim.py:319-370 with the nudge replaced by
+ * training): each active splat's gradient goes straight from the chain rule
+ * into its Adam update (params / adam_m / adam_v updated in place, the
+ * same arithmetic as sm_adam_step, bit for bit), splats the view does not
+ * reach get their zero-gradient step; no gradient buffer.  skip_flag as in
+ * sm_adam_step. */
+int sm_render_backward_adam(float *params, const int32_t *slots, int64_t n,
+                            const sm_camera *cam, const sm_render_dims *dims,
+                            void *workspace, int64_t workspace_bytes,
+                            const float *d_rgb, const float *d_depth, const float *d_alpha,
+                            float *adam_m, float *adam_v, const sm_adam_config *cfg /* host */,
+                            const uint32_t *skip_flag, void *stream);
+
 /* Tile binning keeps only the tiles a splat's q <= 9 ellipse reaches (on, the
  * default) or every tile of its 3-sigma box (off).  Images and gradients are
  * bit-identical either way (the dropped tiles are ones the compositor skips

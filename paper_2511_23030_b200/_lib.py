@@ -81,6 +81,8 @@ def load():
          i64, vp, vp, vp, vp, vp)
     _sig(lib.sm_render_backward, c_int, vp, vp, i64, POINTER(Camera), POINTER(RenderDims), vp, i64,
          vp, vp, vp, vp, vp)
+    _sig(lib.sm_render_backward_adam, c_int, vp, vp, i64, POINTER(Camera), POINTER(RenderDims), vp, i64,
+         vp, vp, vp, vp, vp, POINTER(AdamConfig), vp, vp)
     _sig(lib.sm_set_ellipse_cull, None, c_int)
     _sig(lib.sm_render_ws_offset, i64, POINTER(RenderDims), c_int)
     _sig(lib.sm_render_key_layout, c_int, POINTER(RenderDims), POINTER(i32), POINTER(i32))

@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <cstring>
 
+#include "adam.cuh"
 #include "render.cuh"
 
 namespace sm {
@@ -96,7 +97,24 @@ int sm_render_backward(const float *params, const int32_t *slots, int64_t n, con
         return SM_ERR_INVALID;
     }
     return render_backward(params, slots, n, *cam, *dims, workspace, workspace_bytes, d_rgb, d_depth,
-                           d_alpha, grads, SM_STREAM(stream));
+                           d_alpha, grads, nullptr, SM_STREAM(stream));
+}
+
+int sm_render_backward_adam(float *params, const int32_t *slots, int64_t n, const sm_camera *cam,
+                            const sm_render_dims *dims, void *workspace, int64_t workspace_bytes,
+                            const float *d_rgb, const float *d_depth, const float *d_alpha, float *adam_m,
+                            float *adam_v, const sm_adam_config *cfg, const uint32_t *skip_flag, void *stream) {
+    if (!cam || !dims || !workspace || !cfg || (n > 0 && (!params || !adam_m || !adam_v))) {
+        set_error("sm_render_backward_adam: null argument");
+        return SM_ERR_INVALID;
+    }
+    AdamFuse af;
+    af.m = reinterpret_cast<float4 *>(adam_m);
+    af.v = reinterpret_cast<float4 *>(adam_v);
+    af.skip = skip_flag;
+    af.c = adam_dev(*cfg);
+    return render_backward(params, slots, n, *cam, *dims, workspace, workspace_bytes, d_rgb, d_depth,
+                           d_alpha, nullptr, &af, SM_STREAM(stream));
 }
 
 void sm_set_ellipse_cull(int on) { g_ellipse_cull = on ? 1 : 0; }

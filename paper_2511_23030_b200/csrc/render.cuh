@@ -244,8 +244,10 @@ StreamFork &stream_fork();
 int render_forward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,
                    const sm_render_dims &dims, void *ws, int64_t ws_bytes, float *out_rgb,
                    float *out_depth, float *out_alpha, uint32_t *view_order, cudaStream_t st);
+struct AdamFuse;
 int render_backward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,
                     const sm_render_dims &dims, void *ws, int64_t ws_bytes, const float *d_rgb,
-                    const float *d_depth, const float *d_alpha, float *grads, cudaStream_t st);
+                    const float *d_depth, const float *d_alpha, float *grads, const AdamFuse *fuse,
+                    cudaStream_t st);
 
 }  // namespace sm

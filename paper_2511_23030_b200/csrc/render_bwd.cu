@@ -17,6 +17,7 @@
 // transposed warp butterfly (14 shuffles), per-warp shared slots added in warp
 // order, one gradient slot per (splat, tile) instance, and a fixed-order sum
 // over a splat's instances (inline in project_bwd, or a block per big splat).
+#include "adam.cuh"
 #include "prof.cuh"
 #include "render.cuh"
 
@@ -385,46 +386,67 @@ struct CamBwd {
 #ifndef SM_PBWD_MINB
 #define SM_PBWD_MINB 3   // 3 x 256 threads per SM (<= 85 registers): measured best of 1-3
 #endif
-__device__ __forceinline__ void project_bwd_rank(int64_t r, const float (&gk)[10], const float4 *params,
+__device__ __forceinline__ void project_bwd_rank(int64_t r, const float (&gk)[10], float4 *params,
                                                  const int32_t *slots, const CamBwd &cam,
-                                                 const uint32_t *order, float *grads);
+                                                 const uint32_t *order, float *grads, const AdamFuse &af);
+
+// Adam of a splat the view does not reach (zero gradient: its moments still
+// decay and move it, exactly as the standalone K7 over the active set does).
+__device__ __forceinline__ void adam_zero_grad(int64_t slot, float4 *params, const AdamFuse &af) {
+    float4 p[4], m[4], v[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) p[q] = params[slot * 4 + q], m[q] = af.m[slot * 4 + q], v[q] = af.v[slot * 4 + q];
+    const float g[14] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    adam_record(p, m, v, g, af.c);
+#pragma unroll
+    for (int q = 0; q < 4; q++) params[slot * 4 + q] = p[q], af.m[slot * 4 + q] = m[q], af.v[slot * 4 + q] = v[q];
+}
 
 __global__ void __launch_bounds__(256, SM_PBWD_MINB)
-project_bwd_small(const float4 *__restrict__ params, const int32_t *__restrict__ slots, int64_t n,
+project_bwd_small(float4 *__restrict__ params, const int32_t *__restrict__ slots, int64_t n,
                   CamBwd cam, const uint32_t *__restrict__ order, const uint32_t *__restrict__ tcount_r,
                   const uint32_t *__restrict__ tmask_r, const ProjRec *__restrict__ recs,
                   const uint32_t *__restrict__ toff, const float *__restrict__ gbuf,
-                  const int32_t *__restrict__ tile_hor, int tiles_x, float *__restrict__ grads) {
+                  const int32_t *__restrict__ tile_hor, int tiles_x, float *__restrict__ grads, AdamFuse af) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
+    if (af.m && af.skip && *af.skip) return;   // overflowed forward: no update
     const uint32_t cnt = tcount_r[r];
-    if (cnt == 0) return;
+    if (cnt == 0) {   // culled by the near plane or reaching no tile
+        if (af.m) {
+            const uint32_t i = order[r];
+            adam_zero_grad(slots ? (int64_t)slots[i] : (int64_t)i, params, af);
+        }
+        return;
+    }
     const ProjRec rec = recs[r];
     if (bbox_tiles(rec) > kEmitSmall) return;   // project_bwd_big
     float gk[10];
 #pragma unroll
     for (int k = 0; k < 10; k++) gk[k] = 0.f;
     sum_slots(rec, tmask_r[r], r, toff[r], gbuf, tile_hor, tiles_x, gk);
-    project_bwd_rank(r, gk, params, slots, cam, order, grads);
+    project_bwd_rank(r, gk, params, slots, cam, order, grads, af);
 }
 
 __global__ void __launch_bounds__(64)
-project_bwd_big(const float4 *__restrict__ params, const int32_t *__restrict__ slots, CamBwd cam,
+project_bwd_big(float4 *__restrict__ params, const int32_t *__restrict__ slots, CamBwd cam,
                 const uint32_t *__restrict__ order, const sm_render_counters *ctr,
-                const uint32_t *__restrict__ big, const float *__restrict__ g2d, float *__restrict__ grads) {
+                const uint32_t *__restrict__ big, const float *__restrict__ g2d, float *__restrict__ grads,
+                AdamFuse af) {
     const uint32_t nbig = ctr->overflow ? 0u : ctr->reserved[1];
+    if (af.m && af.skip && *af.skip) return;
     for (uint32_t bi = blockIdx.x * blockDim.x + threadIdx.x; bi < nbig; bi += gridDim.x * blockDim.x) {
         const int64_t r = big[bi];
         float gk[10];
 #pragma unroll
         for (int k = 0; k < 10; k++) gk[k] = g2d[r * kG2dStride + k];
-        project_bwd_rank(r, gk, params, slots, cam, order, grads);
+        project_bwd_rank(r, gk, params, slots, cam, order, grads, af);
     }
 }
 
-__device__ __forceinline__ void project_bwd_rank(int64_t r, const float (&gk)[10], const float4 *params,
+__device__ __forceinline__ void project_bwd_rank(int64_t r, const float (&gk)[10], float4 *params,
                                                  const int32_t *slots, const CamBwd &cam,
-                                                 const uint32_t *order, float *grads) {
+                                                 const uint32_t *order, float *grads, const AdamFuse &af) {
     const uint32_t i = order[r];
     const int64_t slot = slots ? (int64_t)slots[i] : (int64_t)i;
     const float4 A = params[slot * 4 + 0];
@@ -523,6 +545,18 @@ __device__ __forceinline__ void project_bwd_rank(int64_t r, const float (&gk)[10
                               qw * gR[6] + qz * gR[7] - 2.0 * qy * gR[8]);
     const double gqz = 2.0 * (-2.0 * qz * gR[0] - qw * gR[1] + qx * gR[2] + qw * gR[3] -
                               2.0 * qz * gR[4] + qy * gR[5] + qx * gR[6] + qy * gR[7]);
+    if (af.m) {   // fused Adam (single-keyframe step): the gradient never leaves registers
+        const float g[14] = {(float)gpos[0], (float)gpos[1], (float)gpos[2], (float)gw, (float)gqx, (float)gqy,
+                             (float)gqz, (float)gsc[0], (float)gsc[1], (float)gsc[2], (float)gop,
+                             (float)gsh[0], (float)gsh[1], (float)gsh[2]};
+        float4 p[4] = {A, B, C, D}, m[4], v[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) m[q] = af.m[slot * 4 + q], v[q] = af.v[slot * 4 + q];
+        adam_record(p, m, v, g, af.c);
+#pragma unroll
+        for (int q = 0; q < 4; q++) params[slot * 4 + q] = p[q], af.m[slot * 4 + q] = m[q], af.v[slot * 4 + q] = v[q];
+        return;
+    }
     float4 *dst = reinterpret_cast<float4 *>(grads) + slot * 4;
     float4 o0 = dst[0], o1 = dst[1], o2 = dst[2], o3 = dst[3];
     o0.x += (float)gpos[0];
@@ -559,7 +593,8 @@ static void launch_composite_bwd(const RenderBufs &b, const RenderLayout &L, con
 
 int render_backward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,
                     const sm_render_dims &dims, void *ws, int64_t ws_bytes, const float *d_rgb,
-                    const float *d_depth, const float *d_alpha, float *grads, cudaStream_t st) {
+                    const float *d_depth, const float *d_alpha, float *grads, const AdamFuse *fuse,
+                    cudaStream_t st) {
     const RenderLayout L = render_layout(dims);
     if (ws_bytes < L.total) {
         set_error("render workspace too small: %lld < %lld", (long long)ws_bytes, (long long)L.total);
@@ -575,6 +610,9 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
     }
     if (n == 0) return SM_OK;
     RenderBufs b = render_bufs(ws, L);
+    AdamFuse af{};
+    if (fuse) af = *fuse;
+    float4 *pw = reinterpret_cast<float4 *>(const_cast<float *>(params));   // written only when fused
     prof_begin(ST_COMPOSITE_BWD, st);
     if (L.key_bytes == 8)
         launch_composite_bwd<unsigned long long>(b, L, dims, d_rgb, d_depth, d_alpha, st);
@@ -598,13 +636,12 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
     prof_begin(ST_GRAD_GATHER, side);
     grad_gather_big<<<148 * 4, 256, 0, side>>>(b.rec_sorted, b.toff, b.ctr, b.tcount, b.gbuf,
                                                    b.tile_hor, L.tiles_x, b.g2d);
-    project_bwd_big<<<148, 64, 0, side>>>(reinterpret_cast<const float4 *>(params), slots, cb, b.order0,
-                                             b.ctr, b.tcount, b.g2d, grads);
+    project_bwd_big<<<148, 64, 0, side>>>(pw, slots, cb, b.order0, b.ctr, b.tcount, b.g2d, grads, af);
     prof_end(ST_GRAD_GATHER, side);
     prof_begin(ST_PROJECT_BWD, st);
     project_bwd_small<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
-        reinterpret_cast<const float4 *>(params), slots, n, cb, b.order0, b.tcount_r, b.tmask_r, b.rec_sorted,
-        b.toff, b.gbuf, b.tile_hor, L.tiles_x, grads);
+        pw, slots, n, cb, b.order0, b.tcount_r, b.tmask_r, b.rec_sorted, b.toff, b.gbuf, b.tile_hor, L.tiles_x,
+        grads, af);
     prof_end(ST_PROJECT_BWD, st);
     if (SM_FORK) fk.end(st);
     count_launches(4);

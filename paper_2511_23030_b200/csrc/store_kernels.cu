@@ -2,23 +2,20 @@
 // and the bit-exact chunk-id encoder.
 #include <cmath>
 
+#include "adam.cuh"
 #include "common.cuh"
 #include "prof.cuh"
 
 namespace sm {
 
 // ------------------------------------------------------------------ K7
-struct AdamDev {
-    float lr[14];
-    float b1, b2, eps, min_scale;
-};
-
 // Four threads per Gaussian, one float4 quarter of each record each (so a
 // warp streams 8 full 64-byte records per array with 16-byte accesses and a
 // thread keeps ~30 registers instead of ~90).  Quarter q holds record scalars
 // 4q..4q+3: q0 = px py pz qw, q1 = qx qy qz sx, q2 = sy sz op sh0r,
 // q3 = sh0g sh0b - - (m.q3.z = per-Gaussian step count).  The quaternion
-// spans q0.w and q1.xyz: its norm is exchanged with one shuffle.
+// spans q0.w and q1.xyz: its norm is exchanged with one shuffle.  The
+// arithmetic is adam.cuh's (bit-identical to the backward-fused form).
 __global__ void __launch_bounds__(256)
 adam_quarter_kernel(float4 *__restrict__ params, float4 *__restrict__ m, float4 *__restrict__ v,
                     float4 *__restrict__ grads, const int32_t *__restrict__ slots, int64_t n,
@@ -37,32 +34,24 @@ adam_quarter_kernel(float4 *__restrict__ params, float4 *__restrict__ m, float4 
     }
     // per-Gaussian step count lives in m quarter 3, component z
     const float step = __shfl_sync(0xffffffffu, mm.z, (threadIdx.x & 31) | 3) + 1.f;
-    // bias corrections with IEEE powf (1 - 0.999^t cancels: keep them exact),
-    // once per splat; per element one approximate sqrt and reciprocal instead
-    // of IEEE div / sqrt (the kernel was issue-bound), relative error ~3e-7 of
-    // the update (oracle tolerance 1e-6 (1 + |p|))
-    const float ibc1 = 1.f / (1.f - powf(c.b1, step));
-    const float ibc2s = 1.f / sqrtf(1.f - powf(c.b2, step));   // 1 / sqrt(bc2)
+    float ibc1, ibc2s;
+    adam_bias(c, step, ibc1, ibc2s);
     float pv[4] = {p.x, p.y, p.z, p.w}, gv[4] = {g.x, g.y, g.z, g.w};
     float mv[4] = {mm.x, mm.y, mm.z, mm.w}, vvv[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
     for (int k = 0; k < 4; k++) {
         const int idx = 4 * q + k;
-        if (idx < 14) {
-            mv[k] = c.b1 * mv[k] + (1.f - c.b1) * gv[k];
-            vvv[k] = c.b2 * vvv[k] + (1.f - c.b2) * gv[k] * gv[k];
-            pv[k] -= (c.lr[idx] * ibc1) * mv[k] * rcp_approx(sqrt_approx(vvv[k]) * ibc2s + c.eps);
-        }
+        if (idx < 14) pv[k] = adam_elem(pv[k], mv[k], vvv[k], gv[k], c.lr[idx], ibc1, ibc2s, c);
     }
     if (q == 3) mv[2] = step;
     // quaternion renormalisation (core.py:186 unit-norm invariant)
-    const float part = q == 0 ? pv[3] * pv[3] : (q == 1 ? pv[0] * pv[0] + pv[1] * pv[1] + pv[2] * pv[2] : 0.f);
+    const float part = q == 0 ? __fmul_rn(pv[3], pv[3]) : (q == 1 ? quat_xyz2(pv[0], pv[1], pv[2]) : 0.f);
     const float other = __shfl_xor_sync(0xffffffffu, part, 1);
-    const float qn = sqrtf(part + other);
-    if (q == 0) pv[3] = qn > 0.f ? pv[3] * (1.f / qn) : 1.f;
+    const float qn = __fsqrt_rn(q == 0 ? __fadd_rn(part, other) : __fadd_rn(other, part));
+    if (q == 0) pv[3] = qn > 0.f ? __fmul_rn(pv[3], 1.f / qn) : 1.f;
     if (q == 1) {
         const float inv = qn > 0.f ? 1.f / qn : 0.f;
-        pv[0] *= inv, pv[1] *= inv, pv[2] *= inv;
+        pv[0] = __fmul_rn(pv[0], inv), pv[1] = __fmul_rn(pv[1], inv), pv[2] = __fmul_rn(pv[2], inv);
         pv[3] = fmaxf(pv[3], c.min_scale);   // sx
     }
     if (q == 2) {
@@ -112,12 +101,7 @@ int adam_step(float *params, float *m, float *v, float *grads, const int32_t *sl
         return SM_ERR_INVALID;
     }
     if (n == 0) return SM_OK;
-    AdamDev d;
-    for (int k = 0; k < 14; k++) d.lr[k] = cfg.lr[k];
-    d.b1 = cfg.beta1;
-    d.b2 = cfg.beta2;
-    d.eps = cfg.eps;
-    d.min_scale = cfg.min_scale;
+    const AdamDev d = adam_dev(cfg);
     prof_begin(ST_ADAM, st);
     count_launches(1);
     adam_quarter_kernel<<<(unsigned)ceil_div(n * 4, 256), 256, 0, st>>>(

@@ -301,8 +301,12 @@ class MappingEngine:
                                 candidates=self.store.known_chunk_ids)
 
     # ------------------------------------------------------------ device
-    def _device_pass(self, kf: Keyframe, slots, n: int, backward: bool = True):
-        """fwd -> loss(+grad) -> bwd for one keyframe; grads accumulate in the slab."""
+    fused_adam = True   # single-keyframe steps: Adam fused into the backward (sm_render_backward_adam)
+
+    def _device_pass(self, kf: Keyframe, slots, n: int, backward: bool = True, adam: bool = False):
+        """fwd -> loss(+grad) -> bwd for one keyframe; grads accumulate in the
+        slab, or with adam=True the Adam step is applied by the backward
+        itself (no gradient buffer) or by K7 right after it."""
         slab = self.store.slab
         cam = camera_for(kf.pose, kf.intrinsics)
         dk = self._device_keyframe(kf)
@@ -313,8 +317,13 @@ class MappingEngine:
             dk.pending = None
         self.loss.run(self.rgb, self.depth, dk.rgb_u8, None, dk.depth, 3, self.weights,
                       self.d_rgb if backward else None, self.d_depth if backward else None)
-        if backward and n:
+        if backward and n and adam and self.fused_adam:
+            self.render.backward_adam(slab.params, slots, n, cam, self.d_rgb, self.d_depth, None, slab.adam_m,
+                                      slab.adam_v, self._adam_c, self.render.overflow_flag())
+        elif backward and n:
             self.render.backward(slab.params, slots, n, cam, self.d_rgb, self.d_depth, None, slab.grads)
+            if adam:
+                self._adam(slots, n)
 
     def _adam(self, slots, n: int) -> None:
         s = self.store.slab
@@ -377,8 +386,8 @@ class MappingEngine:
         camera."""
         s = self.store.slab
         cam = (kf.pose.rotation.tobytes(), kf.pose.translation.tobytes(), kf.intrinsics)
-        return (kf.id, cam, slots.data_ptr(), n, s.params.data_ptr(), s.grads.data_ptr(),
-                self.render.ws.data_ptr(), self.upload_keyframes_each_step, dp)
+        return (kf.id, cam, slots.data_ptr(), n, s.params.data_ptr(), s.grads.data_ptr(), s.adam_m.data_ptr(),
+                self.render.ws.data_ptr(), self.upload_keyframes_each_step, dp, self.fused_adam)
 
     def drop_graphs(self) -> None:
         lib = _lib.load()
@@ -401,9 +410,8 @@ class MappingEngine:
             # synchronising events and page-locking buffers while a graph is
             # captured, which would invalidate a global-mode capture
             with torch.cuda.graph(g, stream=self._cap_stream, capture_error_mode="thread_local"):
-                self._device_pass(kf, slots, n)
+                self._device_pass(kf, slots, n, adam=not dp)
                 if not dp:
-                    self._adam(slots, n)
                     self._queue_readback()
         finally:
             lib.sm_profile_capture_end()
@@ -529,8 +537,7 @@ class MappingEngine:
             self.drop_graphs()
         for _ in range(6):
             self.counter_eager += 1
-            self._device_pass(kf, slots, n)
-            self._adam(slots, n)
+            self._device_pass(kf, slots, n, adam=True)
             self._queue_readback()
             self._run_while_gpu()
             loss, overflow = self._finish_readback()

@@ -165,6 +165,17 @@ class RenderEngine:
                                          _lib.ptr(grads), _lib.stream_handle(stream))
         _lib.check(rc, "render_backward")
 
+    def backward_adam(self, params, slots, n: int, cam: _lib.Camera, d_rgb, d_depth, d_alpha, adam_m, adam_v,
+                      cfg: _lib.AdamConfig, skip_flag=None, stream=None):
+        """Backward with the Adam step fused in (sm_render_backward_adam):
+        params / adam_m / adam_v of the active slots are updated in place."""
+        rc = self.lib.sm_render_backward_adam(_lib.ptr(params), _lib.ptr(slots), int(n), ctypes.byref(cam),
+                                              ctypes.byref(self.dims), _lib.ptr(self.ws), self.ws_bytes,
+                                              _lib.ptr(d_rgb), _lib.ptr(d_depth), _lib.ptr(d_alpha),
+                                              _lib.ptr(adam_m), _lib.ptr(adam_v), ctypes.byref(cfg),
+                                              _lib.ptr(skip_flag), _lib.stream_handle(stream))
+        _lib.check(rc, "render_backward_adam")
+
     def counters_async(self, stream=None):
         """Queue a D2H copy of the workspace counters into pinned memory."""
         src = self.ws[:64].view(self.torch.int32)

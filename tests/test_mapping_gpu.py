@@ -323,3 +323,21 @@ def test_optimization_step_matches_oracle(cuda, tmp_path):
         assert bad.any(1).mean() <= 0.02, (s, int(bad.any(1).sum()), len(sub))
         assert np.all(np.abs(upd_g[bad]) <= 2.0 * np.broadcast_to(lr, bad.shape)[bad] + 1e-7), s
     print("per step: rows outside the elementwise bound, unexplained elements, max |m|/colmax:", worst)
+
+
+def test_fused_adam_backward_bit_identical(cuda, tmp_path):
+    """sm_render_backward_adam (Adam applied by the backward's last stage, no
+    gradient buffer) = sm_render_backward + sm_adam_step, bit for bit, over
+    steps that include splats the view does not reach (zero-gradient steps)."""
+    import torch
+    a = _c1_engine(tmp_path / "a", budget=100_000)
+    b = _c1_engine(tmp_path / "b", budget=100_000)
+    b.fused_adam = False
+    for s in range(8):
+        ra, rb = a.optimization_step(0, s), b.optimization_step(0, s)
+        assert ra.selected_kf == rb.selected_kf and ra.loss == rb.loss, s
+    sa, sb = a.store.slab, b.store.slab
+    hw = sa.high_water()
+    for name in ("params", "adam_m", "adam_v"):
+        assert torch.equal(getattr(sa, name)[:hw], getattr(sb, name)[:hw]), name
+    assert float(sb.grads[:hw].abs().max()) == 0.0
