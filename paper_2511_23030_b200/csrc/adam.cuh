@@ -48,35 +48,61 @@ __device__ __forceinline__ float quat_xyz2(float qx, float qy, float qz) {
     return __fadd_rn(__fadd_rn(__fmul_rn(qx, qx), __fmul_rn(qy, qy)), __fmul_rn(qz, qz));
 }
 
-// Adam on a whole 16-float record (one thread): p / m / v are the record's
-// four float4 quarters; m[3].z carries the per-Gaussian step count.
-__device__ __forceinline__ void adam_record(float4 (&p)[4], float4 (&m)[4], float4 (&v)[4], const float (&g)[14],
-                                            const AdamDev &c) {
-    float pv[16], mv[16], vv[16];
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-        pv[4 * q] = p[q].x, pv[4 * q + 1] = p[q].y, pv[4 * q + 2] = p[q].z, pv[4 * q + 3] = p[q].w;
-        mv[4 * q] = m[q].x, mv[4 * q + 1] = m[q].y, mv[4 * q + 2] = m[q].z, mv[4 * q + 3] = m[q].w;
-        vv[4 * q] = v[q].x, vv[4 * q + 1] = v[q].y, vv[4 * q + 2] = v[q].z, vv[4 * q + 3] = v[q].w;
-    }
-    const float step = mv[14] + 1.f;
-    float ibc1, ibc2s;
-    adam_bias(c, step, ibc1, ibc2s);
-#pragma unroll
-    for (int k = 0; k < 14; k++) pv[k] = adam_elem(pv[k], mv[k], vv[k], g[k], c.lr[k], ibc1, ibc2s, c);
-    mv[14] = step;
-    const float qn = __fsqrt_rn(__fadd_rn(__fmul_rn(pv[3], pv[3]), quat_xyz2(pv[4], pv[5], pv[6])));
-    pv[3] = qn > 0.f ? __fmul_rn(pv[3], 1.f / qn) : 1.f;
+// Adam on a whole 16-float record by one thread, streamed quarter by
+// quarter (only one m / v quarter live at a time: the fused backward has
+// little register room left): p holds the record (updated in place), the
+// moments are read and written at m_rec / v_rec; m quarter 3 .z carries the
+// per-Gaussian step count.  Same operations, same order as the quarter kernel.
+// `m3` = m_rec[3] and the bias corrections of step m3.z + 1, prepared by the
+// caller (the fused backward does it before its chain rule, so powf's
+// registers are free again at its peak).
+struct AdamPre {
+    float4 m3;
+    float step, ibc1, ibc2s;
+};
+
+__device__ __forceinline__ AdamPre adam_pre(const float4 *m_rec, const AdamDev &c) {
+    AdamPre a;
+    a.m3 = m_rec[3];
+    a.step = a.m3.z + 1.f;
+    adam_bias(c, a.step, a.ibc1, a.ibc2s);
+    return a;
+}
+
+__device__ __forceinline__ void adam_record(float4 (&p)[4], float4 *m_rec, float4 *v_rec, const float (&g)[14],
+                                            const AdamDev &c, const AdamPre &pre) {
+    float4 m3 = pre.m3;
+    const float step = pre.step, ibc1 = pre.ibc1, ibc2s = pre.ibc2s;
+    float4 m = m_rec[0], v = v_rec[0];
+    p[0].x = adam_elem(p[0].x, m.x, v.x, g[0], c.lr[0], ibc1, ibc2s, c);
+    p[0].y = adam_elem(p[0].y, m.y, v.y, g[1], c.lr[1], ibc1, ibc2s, c);
+    p[0].z = adam_elem(p[0].z, m.z, v.z, g[2], c.lr[2], ibc1, ibc2s, c);
+    p[0].w = adam_elem(p[0].w, m.w, v.w, g[3], c.lr[3], ibc1, ibc2s, c);
+    m_rec[0] = m, v_rec[0] = v;
+    m = m_rec[1], v = v_rec[1];
+    p[1].x = adam_elem(p[1].x, m.x, v.x, g[4], c.lr[4], ibc1, ibc2s, c);
+    p[1].y = adam_elem(p[1].y, m.y, v.y, g[5], c.lr[5], ibc1, ibc2s, c);
+    p[1].z = adam_elem(p[1].z, m.z, v.z, g[6], c.lr[6], ibc1, ibc2s, c);
+    p[1].w = adam_elem(p[1].w, m.w, v.w, g[7], c.lr[7], ibc1, ibc2s, c);
+    m_rec[1] = m, v_rec[1] = v;
+    m = m_rec[2], v = v_rec[2];
+    p[2].x = adam_elem(p[2].x, m.x, v.x, g[8], c.lr[8], ibc1, ibc2s, c);
+    p[2].y = adam_elem(p[2].y, m.y, v.y, g[9], c.lr[9], ibc1, ibc2s, c);
+    p[2].z = adam_elem(p[2].z, m.z, v.z, g[10], c.lr[10], ibc1, ibc2s, c);
+    p[2].w = adam_elem(p[2].w, m.w, v.w, g[11], c.lr[11], ibc1, ibc2s, c);
+    m_rec[2] = m, v_rec[2] = v;
+    v = v_rec[3];
+    p[3].x = adam_elem(p[3].x, m3.x, v.x, g[12], c.lr[12], ibc1, ibc2s, c);
+    p[3].y = adam_elem(p[3].y, m3.y, v.y, g[13], c.lr[13], ibc1, ibc2s, c);
+    m3.z = step;
+    m_rec[3] = m3, v_rec[3] = v;
+    // quaternion renormalisation, scale floor, opacity clamp (core.py:186-190)
+    const float qn = __fsqrt_rn(__fadd_rn(__fmul_rn(p[0].w, p[0].w), quat_xyz2(p[1].x, p[1].y, p[1].z)));
+    p[0].w = qn > 0.f ? __fmul_rn(p[0].w, 1.f / qn) : 1.f;
     const float inv = qn > 0.f ? 1.f / qn : 0.f;
-    pv[4] = __fmul_rn(pv[4], inv), pv[5] = __fmul_rn(pv[5], inv), pv[6] = __fmul_rn(pv[6], inv);
-    pv[7] = fmaxf(pv[7], c.min_scale), pv[8] = fmaxf(pv[8], c.min_scale), pv[9] = fmaxf(pv[9], c.min_scale);
-    pv[10] = fminf(fmaxf(pv[10], 0.f), 1.f);
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-        p[q] = make_float4(pv[4 * q], pv[4 * q + 1], pv[4 * q + 2], pv[4 * q + 3]);
-        m[q] = make_float4(mv[4 * q], mv[4 * q + 1], mv[4 * q + 2], mv[4 * q + 3]);
-        v[q] = make_float4(vv[4 * q], vv[4 * q + 1], vv[4 * q + 2], vv[4 * q + 3]);
-    }
+    p[1].x = __fmul_rn(p[1].x, inv), p[1].y = __fmul_rn(p[1].y, inv), p[1].z = __fmul_rn(p[1].z, inv);
+    p[1].w = fmaxf(p[1].w, c.min_scale), p[2].x = fmaxf(p[2].x, c.min_scale), p[2].y = fmaxf(p[2].y, c.min_scale);
+    p[2].z = fminf(fmaxf(p[2].z, 0.f), 1.f);
 }
 
 // The backward-fused Adam (single-keyframe mapping step): project_bwd applies

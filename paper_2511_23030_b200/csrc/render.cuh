@@ -143,10 +143,14 @@ inline RenderBufs render_bufs(void *ws, const RenderLayout &L) {
 // restatement (oracle/bin_oracle.c, gcc -ffp-contract=off) reproduces the
 // projected records -- and through them the tile keys and ranges -- bit for
 // bit; on an HBM-bound kernel the unfused fp64 ops cost nothing measurable.
-#define DM __dmul_rn
-#define DA __dadd_rn
-#define DS __dsub_rn
-#define DD __ddiv_rn
+// Exact = true: every operation an explicit round-to-nearest op (the
+// forward, whose records must match oracle/bin_oracle.c bit for bit);
+// false: the compiler may contract to FMA (the backward's chain rule, which
+// is only held to the gradient tolerance and is register-bound).
+#define DM(a, b) (Exact ? __dmul_rn((a), (b)) : (a) * (b))
+#define DA(a, b) (Exact ? __dadd_rn((a), (b)) : (a) + (b))
+#define DS(a, b) (Exact ? __dsub_rn((a), (b)) : (a) - (b))
+#define DD(a, b) (Exact ? __ddiv_rn((a), (b)) : (a) / (b))
 struct ProjGeom {
     double x, y, z;        // camera-frame centre
     double u, v;           // pixel mean
@@ -156,6 +160,7 @@ struct ProjGeom {
     double Sc[6];          // camera covariance, symmetric: xx xy xz yy yz zz
 };
 
+template <bool Exact = true>
 __device__ __forceinline__ void project_geometry(double px, double py, double pz, double qw,
                                                  double qx, double qy, double qz, double sx,
                                                  double sy, double sz, const double *rwc,

@@ -386,6 +386,7 @@ struct CamBwd {
 #ifndef SM_PBWD_MINB
 #define SM_PBWD_MINB 3   // 3 x 256 threads per SM (<= 85 registers): measured best of 1-3
 #endif
+template <bool FUSED>
 __device__ __forceinline__ void project_bwd_rank(int64_t r, const float (&gk)[10], float4 *params,
                                                  const int32_t *slots, const CamBwd &cam,
                                                  const uint32_t *order, float *grads, const AdamFuse &af);
@@ -393,15 +394,16 @@ __device__ __forceinline__ void project_bwd_rank(int64_t r, const float (&gk)[10
 // Adam of a splat the view does not reach (zero gradient: its moments still
 // decay and move it, exactly as the standalone K7 over the active set does).
 __device__ __forceinline__ void adam_zero_grad(int64_t slot, float4 *params, const AdamFuse &af) {
-    float4 p[4], m[4], v[4];
+    float4 p[4];
 #pragma unroll
-    for (int q = 0; q < 4; q++) p[q] = params[slot * 4 + q], m[q] = af.m[slot * 4 + q], v[q] = af.v[slot * 4 + q];
+    for (int q = 0; q < 4; q++) p[q] = params[slot * 4 + q];
     const float g[14] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    adam_record(p, m, v, g, af.c);
+    adam_record(p, af.m + slot * 4, af.v + slot * 4, g, af.c, adam_pre(af.m + slot * 4, af.c));
 #pragma unroll
-    for (int q = 0; q < 4; q++) params[slot * 4 + q] = p[q], af.m[slot * 4 + q] = m[q], af.v[slot * 4 + q] = v[q];
+    for (int q = 0; q < 4; q++) params[slot * 4 + q] = p[q];
 }
 
+template <bool FUSED>
 __global__ void __launch_bounds__(256, SM_PBWD_MINB)
 project_bwd_small(float4 *__restrict__ params, const int32_t *__restrict__ slots, int64_t n,
                   CamBwd cam, const uint32_t *__restrict__ order, const uint32_t *__restrict__ tcount_r,
@@ -410,10 +412,10 @@ project_bwd_small(float4 *__restrict__ params, const int32_t *__restrict__ slots
                   const int32_t *__restrict__ tile_hor, int tiles_x, float *__restrict__ grads, AdamFuse af) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
-    if (af.m && af.skip && *af.skip) return;   // overflowed forward: no update
+    if (FUSED && af.skip && *af.skip) return;   // overflowed forward: no update
     const uint32_t cnt = tcount_r[r];
     if (cnt == 0) {   // culled by the near plane or reaching no tile
-        if (af.m) {
+        if (FUSED) {
             const uint32_t i = order[r];
             adam_zero_grad(slots ? (int64_t)slots[i] : (int64_t)i, params, af);
         }
@@ -425,30 +427,34 @@ project_bwd_small(float4 *__restrict__ params, const int32_t *__restrict__ slots
 #pragma unroll
     for (int k = 0; k < 10; k++) gk[k] = 0.f;
     sum_slots(rec, tmask_r[r], r, toff[r], gbuf, tile_hor, tiles_x, gk);
-    project_bwd_rank(r, gk, params, slots, cam, order, grads, af);
+    project_bwd_rank<FUSED>(r, gk, params, slots, cam, order, grads, af);
 }
 
+template <bool FUSED>
 __global__ void __launch_bounds__(64)
 project_bwd_big(float4 *__restrict__ params, const int32_t *__restrict__ slots, CamBwd cam,
                 const uint32_t *__restrict__ order, const sm_render_counters *ctr,
                 const uint32_t *__restrict__ big, const float *__restrict__ g2d, float *__restrict__ grads,
                 AdamFuse af) {
     const uint32_t nbig = ctr->overflow ? 0u : ctr->reserved[1];
-    if (af.m && af.skip && *af.skip) return;
+    if (FUSED && af.skip && *af.skip) return;
     for (uint32_t bi = blockIdx.x * blockDim.x + threadIdx.x; bi < nbig; bi += gridDim.x * blockDim.x) {
         const int64_t r = big[bi];
         float gk[10];
 #pragma unroll
         for (int k = 0; k < 10; k++) gk[k] = g2d[r * kG2dStride + k];
-        project_bwd_rank(r, gk, params, slots, cam, order, grads, af);
+        project_bwd_rank<FUSED>(r, gk, params, slots, cam, order, grads, af);
     }
 }
 
+template <bool FUSED>
 __device__ __forceinline__ void project_bwd_rank(int64_t r, const float (&gk)[10], float4 *params,
                                                  const int32_t *slots, const CamBwd &cam,
                                                  const uint32_t *order, float *grads, const AdamFuse &af) {
     const uint32_t i = order[r];
     const int64_t slot = slots ? (int64_t)slots[i] : (int64_t)i;
+    AdamPre pre;
+    if (FUSED) pre = adam_pre(af.m + slot * 4, af.c);   // before the chain rule's register peak
     const float4 A = params[slot * 4 + 0];
     const float4 B = params[slot * 4 + 1];
     const float4 C = params[slot * 4 + 2];
@@ -459,7 +465,7 @@ __device__ __forceinline__ void project_bwd_rank(int64_t r, const float (&gk)[10
     ProjGeom g;
     const double qw = A.w, qx = B.x, qy = B.y, qz = B.z;
     const double s[3] = {B.w, C.x, C.y};
-    project_geometry(A.x, A.y, A.z, qw, qx, qy, qz, s[0], s[1], s[2], cam.r, cam.t, cam.fx, cam.fy,
+    project_geometry<false>(A.x, A.y, A.z, qw, qx, qy, qz, s[0], s[1], s[2], cam.r, cam.t, cam.fx, cam.fy,
                      cam.cx, cam.cy, g);
     const double fx = cam.fx, fy = cam.fy;
     const double x = g.x, y = g.y, z = g.z;
@@ -545,16 +551,16 @@ __device__ __forceinline__ void project_bwd_rank(int64_t r, const float (&gk)[10
                               qw * gR[6] + qz * gR[7] - 2.0 * qy * gR[8]);
     const double gqz = 2.0 * (-2.0 * qz * gR[0] - qw * gR[1] + qx * gR[2] + qw * gR[3] -
                               2.0 * qz * gR[4] + qy * gR[5] + qx * gR[6] + qy * gR[7]);
-    if (af.m) {   // fused Adam (single-keyframe step): the gradient never leaves registers
+    if (FUSED) {   // fused Adam (single-keyframe step): the gradient never leaves registers
         const float g[14] = {(float)gpos[0], (float)gpos[1], (float)gpos[2], (float)gw, (float)gqx, (float)gqy,
                              (float)gqz, (float)gsc[0], (float)gsc[1], (float)gsc[2], (float)gop,
                              (float)gsh[0], (float)gsh[1], (float)gsh[2]};
-        float4 p[4] = {A, B, C, D}, m[4], v[4];
+        // keep the moment loads below the chain rule (register pressure)
+        asm volatile("" ::: "memory");
+        float4 p[4] = {params[slot * 4 + 0], params[slot * 4 + 1], params[slot * 4 + 2], params[slot * 4 + 3]};
+        adam_record(p, af.m + slot * 4, af.v + slot * 4, g, af.c, pre);
 #pragma unroll
-        for (int q = 0; q < 4; q++) m[q] = af.m[slot * 4 + q], v[q] = af.v[slot * 4 + q];
-        adam_record(p, m, v, g, af.c);
-#pragma unroll
-        for (int q = 0; q < 4; q++) params[slot * 4 + q] = p[q], af.m[slot * 4 + q] = m[q], af.v[slot * 4 + q] = v[q];
+        for (int q = 0; q < 4; q++) params[slot * 4 + q] = p[q];
         return;
     }
     float4 *dst = reinterpret_cast<float4 *>(grads) + slot * 4;
@@ -636,12 +642,20 @@ int render_backward(const float *params, const int32_t *slots, int64_t n, const 
     prof_begin(ST_GRAD_GATHER, side);
     grad_gather_big<<<148 * 4, 256, 0, side>>>(b.rec_sorted, b.toff, b.ctr, b.tcount, b.gbuf,
                                                    b.tile_hor, L.tiles_x, b.g2d);
-    project_bwd_big<<<148, 64, 0, side>>>(pw, slots, cb, b.order0, b.ctr, b.tcount, b.g2d, grads, af);
+    if (fuse)
+        project_bwd_big<true><<<148, 64, 0, side>>>(pw, slots, cb, b.order0, b.ctr, b.tcount, b.g2d, grads, af);
+    else
+        project_bwd_big<false><<<148, 64, 0, side>>>(pw, slots, cb, b.order0, b.ctr, b.tcount, b.g2d, grads, af);
     prof_end(ST_GRAD_GATHER, side);
     prof_begin(ST_PROJECT_BWD, st);
-    project_bwd_small<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
-        pw, slots, n, cb, b.order0, b.tcount_r, b.tmask_r, b.rec_sorted, b.toff, b.gbuf, b.tile_hor, L.tiles_x,
-        grads, af);
+    if (fuse)
+        project_bwd_small<true><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+            pw, slots, n, cb, b.order0, b.tcount_r, b.tmask_r, b.rec_sorted, b.toff, b.gbuf, b.tile_hor,
+            L.tiles_x, grads, af);
+    else
+        project_bwd_small<false><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+            pw, slots, n, cb, b.order0, b.tcount_r, b.tmask_r, b.rec_sorted, b.toff, b.gbuf, b.tile_hor,
+            L.tiles_x, grads, af);
     prof_end(ST_PROJECT_BWD, st);
     if (SM_FORK) fk.end(st);
     count_launches(4);

@@ -18,6 +18,8 @@
 #include "render.cuh"
 #include "sort.cuh"
 
+constexpr bool Exact = true;   // render.cuh DM/DA/DS/DD: explicit rounding in K2
+
 namespace sm {
 
 // ---------------------------------------------------------------- layout

@@ -90,8 +90,9 @@ def test_dp_world2_k8_equals_one_rank_accumulation(cuda, tmp_path):
             for name, sl in GROUPS.items():                          # exchange = accumulation (fp32 order)
                 d = np.linalg.norm(a["packed"][:, sl] - r["packed"][:, sl])
                 assert d <= 1e-5 * np.linalg.norm(r["packed"][:, sl]) + 1e-30, (name, d)
-        else:
-            assert np.allclose(a["losses"], r["losses"], rtol=1e-5, atol=0), s
+        else:   # after one step: moments at the fp32 noise floor may have taken opposite full-size
+            # Adam steps in the two summation orders (see test_optimization_step_matches_oracle)
+            assert np.allclose(a["losses"], r["losses"], rtol=2e-4, atol=0), s
         upd_a = a["params"][:, :14] - a["before"][:, :14]
         upd_r = r["params"][:, :14] - r["before"][:, :14]
         bad = (np.abs(upd_a - upd_r) > 1e-6 * (1 + np.abs(r["params"][:, :14])) + 1e-3 * np.abs(upd_r)).any(1)
