@@ -271,7 +271,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-context", action="store_true", help="reference arm: skip the _Replay context leg")
-    ap.add_argument("--no-fused-adam", action="store_true", help="A/B: standalone K7 after the backward")
+    ap.add_argument("--fused-adam", action="store_true", help="A/B: Adam fused into the backward")
     ap.add_argument("--keyframes-per-step", type=int, default=None,
                     help="K keyframes per mapping step (default 1 on one GPU = C2, 8 on N > 1 = C3)")
     args = ap.parse_args()
@@ -294,7 +294,7 @@ def main():
     lib = _lib.load()
     eng = build_c2(args.n, args.keyframes, store_dir=tempfile.mkdtemp(prefix=f"bench_r{rank}_"),
                    device=f"cuda:{local}")
-    eng.fused_adam = not args.no_fused_adam
+    eng.fused_adam = args.fused_adam
     dist = None
     if world > 1:
         import torch.distributed as dist

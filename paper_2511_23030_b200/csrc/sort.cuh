@@ -93,19 +93,61 @@ __device__ __forceinline__ void st_status(uint32_t *p, uint32_t v) {
     *reinterpret_cast<volatile uint32_t *>(p) = v;
 }
 
-template <typename K, bool HAS_VAL, int ITEMS>
+// Shared-memory layout of one onesweep pass (dynamic: the 11-bit tile pass
+// needs ~96 KB).
+template <typename K, bool HAS_VAL, int ITEMS, int RB>
+struct PassSmem {
+    static constexpr int R = 1 << RB;
+    static constexpr size_t o_wcount = 0;                                    // [warps][R]
+    static constexpr size_t o_base = o_wcount + (size_t)kSortWarps * R * 4;  // [R]
+    static constexpr size_t o_excl = o_base + (size_t)R * 4;                  // [R]
+    static constexpr size_t o_wtot = o_excl + (size_t)R * 4;                  // [warps] + s_tile
+    static constexpr size_t o_keys = (o_wtot + (kSortWarps + 1) * 4 + 15) / 16 * 16;
+    static constexpr size_t o_vals = o_keys + (size_t)kSortThreads * ITEMS * sizeof(K);
+    static constexpr size_t bytes = o_vals + (HAS_VAL ? (size_t)kSortThreads * ITEMS * 4 : 0);
+};
+
+// Block exclusive scan of one value per thread (256 threads).
+__device__ __forceinline__ uint32_t sort_block_excl(uint32_t v, uint32_t *warp_tot) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    __syncthreads();   // warp_tot reuse
+    if (lane == 31) warp_tot[warp] = x;
+    __syncthreads();
+    uint32_t off = 0;
+    for (int w = 0; w < warp; w++) off += warp_tot[w];
+    return off + x - v;
+}
+
+// One stable pass over digit bits [shift, shift + nbits), RB-bit digits
+// (8: 256 bins, one per thread; 11: 2048 bins, eight per thread -- the tile
+// sort of a <= 2048-tile image in a single pass).  ranges_out (nullable,
+// RB = 11 tile sort): the block holding tile 0 writes each digit's
+// [start, end) of the sorted output (= the per-tile instance ranges), (0, 0)
+// for empty digits, for digits < n_ranges.
+template <typename K, bool HAS_VAL, int ITEMS, int RB = kRadixBits>
 __global__ void __launch_bounds__(kSortThreads)
 onesweep_pass(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
               K *__restrict__ keys_out, uint32_t *__restrict__ vals_out, const uint32_t *n_dev,
               int64_t n_host, int shift, int nbits, const uint32_t *__restrict__ hist_p,
-              uint32_t *__restrict__ status_p, uint32_t *__restrict__ tile_ctr_p) {
-    __shared__ uint32_t wcount[kSortWarps][kRadix];
-    __shared__ uint32_t digit_base[kRadix];
-    __shared__ uint32_t tile_excl[kRadix];
-    __shared__ uint32_t warp_tot[kSortWarps];
-    __shared__ uint32_t s_tile;
-    __shared__ K s_keys[(kSortThreads * ITEMS)];
-    __shared__ uint32_t s_vals[HAS_VAL ? (kSortThreads * ITEMS) : 1];
+              uint32_t *__restrict__ status_p, uint32_t *__restrict__ tile_ctr_p,
+              uint32_t *__restrict__ ranges_out = nullptr, int n_ranges = 0) {
+    using L = PassSmem<K, HAS_VAL, ITEMS, RB>;
+    constexpr int R = L::R;
+    constexpr int DPT = R / kSortThreads;   // digits per thread
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t(*wcount)[R] = reinterpret_cast<uint32_t(*)[R]>(smem + L::o_wcount);
+    uint32_t *digit_base = reinterpret_cast<uint32_t *>(smem + L::o_base);
+    uint32_t *tile_excl = reinterpret_cast<uint32_t *>(smem + L::o_excl);
+    uint32_t *warp_tot = reinterpret_cast<uint32_t *>(smem + L::o_wtot);
+    uint32_t &s_tile = warp_tot[kSortWarps];
+    K *s_keys = reinterpret_cast<K *>(smem + L::o_keys);
+    uint32_t *s_vals = reinterpret_cast<uint32_t *>(smem + L::o_vals);
     const int64_t n = load_count(n_dev, n_host);
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr_p, 1u);
     __syncthreads();
@@ -113,21 +155,23 @@ onesweep_pass(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals_i
     // grid is sized for the capacity) leave before doing any work
     if ((int64_t)s_tile * (kSortThreads * ITEMS) >= n) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&wcount[0][0])[i] = 0;
+    for (int i = threadIdx.x; i < kSortWarps * R; i += kSortThreads) (&wcount[0][0])[i] = 0;
+    const int d0 = threadIdx.x * DPT;   // this thread's digits d0 .. d0 + DPT - 1
     // global digit base = exclusive scan of this pass's histogram
     {
-        const uint32_t v = hist_p[threadIdx.x];
-        uint32_t x = v;
+        uint32_t h[DPT], sum = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+        for (int j = 0; j < DPT; j++) h[j] = hist_p[d0 + j], sum += h[j];
+        uint32_t run = sort_block_excl(sum, warp_tot);
+#pragma unroll
+        for (int j = 0; j < DPT; j++) {
+            digit_base[d0 + j] = run;
+            if (ranges_out && s_tile == 0 && d0 + j < n_ranges) {
+                ranges_out[2 * (d0 + j)] = h[j] ? run : 0u;
+                ranges_out[2 * (d0 + j) + 1] = h[j] ? run + h[j] : 0u;
+            }
+            run += h[j];
         }
-        if (lane == 31) warp_tot[warp] = x;
-        __syncthreads();
-        uint32_t off = 0;
-        for (int w = 0; w < warp; w++) off += warp_tot[w];
-        digit_base[threadIdx.x] = off + x - v;
     }
     __syncthreads();
     const uint32_t tile = s_tile;
@@ -146,8 +190,8 @@ onesweep_pass(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals_i
         if (HAS_VAL) val[j] = ok ? vals_in[i] : 0u;
         dig[j] = ok ? (uint32_t)((key[j] >> shift) & mask) : 0xffffffffu;
     }
-    // stable in-block ranking: warp w owns the contiguous segment w*256..,
-    // item j of lane l is element w*256 + j*32 + l, processed in (j, l) order
+    // stable in-block ranking: warp w owns the contiguous segment w*32*ITEMS..,
+    // item j of lane l is element w*32*ITEMS + j*32 + l, processed in (j, l) order
 #pragma unroll
     for (int j = 0; j < ITEMS; j++) {
         const uint32_t d = dig[j];
@@ -161,55 +205,82 @@ onesweep_pass(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals_i
         local[j] = cnt + __popc(lt);
     }
     __syncthreads();
-    // per digit (thread d): exclusive prefix across warps, tile aggregate,
-    // publish, decoupled look-back over predecessor tiles, publish prefix
-    {
-        const int d = threadIdx.x;
-        uint32_t run = 0;
+    // per digit: exclusive prefix across warps, tile aggregate, publish,
+    // decoupled look-back over predecessor tiles, publish prefix
+    uint32_t run[DPT];
+#pragma unroll
+    for (int j = 0; j < DPT; j++) {
+        const int d = d0 + j;
+        uint32_t r = 0;
 #pragma unroll
         for (int w = 0; w < kSortWarps; w++) {
             const uint32_t c = wcount[w][d];
-            wcount[w][d] = run;
-            run += c;
+            wcount[w][d] = r;
+            r += c;
         }
-        uint32_t *my = status_p + (int64_t)tile * kRadix + d;
-        if (tile == 0) {
-            st_status(my, kFlagPre | run);
-        } else {
-            st_status(my, kFlagAgg | run);
-            // look back 8 predecessors per round trip (independent loads)
-            uint32_t excl = 0;
+        run[j] = r;
+    }
+    uint32_t *my = status_p + (int64_t)tile * R + d0;
+    if (tile == 0) {
+#pragma unroll
+        for (int j = 0; j < DPT; j++) st_status(my + j, kFlagPre | run[j]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < DPT; j++) st_status(my + j, kFlagAgg | run[j]);
+        uint32_t excl[DPT];
+        if (DPT == 1) {   // look back 8 predecessors per round trip (independent loads)
+            uint32_t e = 0;
             bool found = false;
             for (int64_t t = (int64_t)tile - 1; t >= 0 && !found; t -= 8) {
-                uint32_t s[8];
+                uint32_t sv[8];
 #pragma unroll
-                for (int k = 0; k < 8; k++)
-                    s[k] = (t - k >= 0) ? ld_status(status_p + (t - k) * kRadix + d) : kFlagPre;
+                for (int k = 0; k < 8; k++) sv[k] = (t - k >= 0) ? ld_status(status_p + (t - k) * R + d0) : kFlagPre;
 #pragma unroll
                 for (int k = 0; k < 8; k++) {
                     if (found || t - k < 0) continue;
-                    uint32_t v = s[k];
-                    while ((v & (kFlagAgg | kFlagPre)) == 0) v = ld_status(status_p + (t - k) * kRadix + d);
-                    excl += v & kValMask;
+                    uint32_t v = sv[k];
+                    while ((v & (kFlagAgg | kFlagPre)) == 0) v = ld_status(status_p + (t - k) * R + d0);
+                    e += v & kValMask;
                     found = (v & kFlagPre) != 0;
                 }
             }
-            st_status(my, kFlagPre | (excl + run));
-            digit_base[d] += excl;
-        }
-        // tile-local exclusive prefix over digits (block scan of `run`)
-        uint32_t x = run;
+            excl[0] = e;
+        } else {   // DPT digits walk back together, one predecessor per round trip
+            unsigned todo = (1u << DPT) - 1u;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+            for (int j = 0; j < DPT; j++) excl[j] = 0;
+            for (int64_t t = (int64_t)tile - 1; t >= 0 && todo; t--) {
+                const uint32_t *row = status_p + t * R + d0;
+                uint32_t sv[DPT];
+#pragma unroll
+                for (int j = 0; j < DPT; j++) sv[j] = (todo >> j) & 1u ? ld_status(row + j) : 0u;
+#pragma unroll
+                for (int j = 0; j < DPT; j++) {
+                    if (!((todo >> j) & 1u)) continue;
+                    uint32_t v = sv[j];
+                    while ((v & (kFlagAgg | kFlagPre)) == 0) v = ld_status(row + j);
+                    excl[j] += v & kValMask;
+                    if (v & kFlagPre) todo &= ~(1u << j);
+                }
+            }
         }
-        __syncthreads();   // warp_tot reuse
-        if (lane == 31) warp_tot[warp] = x;
-        __syncthreads();
-        uint32_t off = 0;
-        for (int w = 0; w < warp; w++) off += warp_tot[w];
-        tile_excl[d] = off + x - run;
+#pragma unroll
+        for (int j = 0; j < DPT; j++) {
+            st_status(my + j, kFlagPre | (excl[j] + run[j]));
+            digit_base[d0 + j] += excl[j];
+        }
+    }
+    // tile-local exclusive prefix over digits (block scan of the runs)
+    {
+        uint32_t sum = 0;
+#pragma unroll
+        for (int j = 0; j < DPT; j++) sum += run[j];
+        uint32_t r = sort_block_excl(sum, warp_tot);
+#pragma unroll
+        for (int j = 0; j < DPT; j++) {
+            tile_excl[d0 + j] = r;
+            r += run[j];
+        }
     }
     __syncthreads();
     // stage the tile in shared memory in digit order, then write each digit's
@@ -230,6 +301,38 @@ onesweep_pass(const K *__restrict__ keys_in, const uint32_t *__restrict__ vals_i
         const uint32_t pos = digit_base[d] + (uint32_t)i - tile_excl[d];
         keys_out[pos] = k;
         if (HAS_VAL) vals_out[pos] = s_vals[i];
+    }
+}
+
+// Opt-in to > 48 KB of dynamic shared memory, once per instantiation.
+template <typename K, bool HAS_VAL, int ITEMS, int RB>
+inline size_t pass_smem() {
+    static bool done = false;
+    const size_t bytes = PassSmem<K, HAS_VAL, ITEMS, RB>::bytes;
+    if (!done) {
+        cudaFuncSetAttribute(onesweep_pass<K, HAS_VAL, ITEMS, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)bytes);
+        done = true;
+    }
+    return bytes;
+}
+
+// Global histogram of one 11-bit digit (the single-pass tile sort).
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads)
+digit_histogram11(const K *__restrict__ keys, const uint32_t *n_dev, int64_t n_host, int shift,
+                  uint32_t *__restrict__ hist) {
+    __shared__ uint32_t h[2048];
+    const int64_t n = load_count(n_dev, n_host);
+    for (int i = threadIdx.x; i < 2048; i += kSortThreads) h[i] = 0;
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * kSortThreads + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * kSortThreads)
+        atomicAdd(&h[(uint32_t)(keys[i] >> shift) & 2047u], 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2048; i += kSortThreads) {
+        const uint32_t v = h[i];
+        if (v) atomicAdd(&hist[i], v);
     }
 }
 
@@ -306,12 +409,30 @@ int radix_sort(K *k0, uint32_t *v0, K *k1, uint32_t *v1, const uint32_t *n_dev, 
         K *ko = cur ? k0 : k1;
         uint32_t *vi = cur ? v1 : v0;
         uint32_t *vo = cur ? v0 : v1;
-        onesweep_pass<K, HAS_VAL, ITEMS><<<(unsigned)tiles, kSortThreads, 0, st>>>(
-            ki, vi, ko, vo, n_dev, n_host, shift, nbits, s.hist + p * kRadix,
-            s.status + (int64_t)p * tiles * kRadix, s.tile_ctr + p);
+        onesweep_pass<K, HAS_VAL, ITEMS, kRadixBits>
+            <<<(unsigned)tiles, kSortThreads, pass_smem<K, HAS_VAL, ITEMS, kRadixBits>(), st>>>(
+                ki, vi, ko, vo, n_dev, n_host, shift, nbits, s.hist + p * kRadix,
+                s.status + (int64_t)p * tiles * kRadix, s.tile_ctr + p);
         cur ^= 1;
     }
     return cur;
+}
+
+// Stable sort of keys on bits [shift, shift + 11) in ONE pass (the tile bits
+// of the instance keys, <= 2048 tiles), writing the per-digit ranges as a
+// by-product.  Result in k1.  The scratch sized for kMaxPasses 8-bit passes
+// holds one 11-bit pass (same hist and status footprint).
+template <typename K, int ITEMS = kSortItemsWide>
+void radix_sort_11(const K *k0, K *k1, const uint32_t *n_dev, int64_t max_n, int shift, int n_ranges,
+                   uint32_t *ranges, const SortScratch &s, cudaStream_t st) {
+    const int64_t tiles = sort_tile_count<ITEMS>(max_n);
+    cudaMemsetAsync(s.tile_ctr, 0,
+                    (size_t)(reinterpret_cast<char *>(s.status + tiles * 2048) -
+                             reinterpret_cast<char *>(s.tile_ctr)), st);
+    const unsigned hgrid = (unsigned)min64(tiles * 2, 148 * 8);
+    digit_histogram11<K><<<hgrid, kSortThreads, 0, st>>>(k0, n_dev, 0, shift, s.hist);
+    onesweep_pass<K, false, ITEMS, 11><<<(unsigned)tiles, kSortThreads, pass_smem<K, false, ITEMS, 11>(), st>>>(
+        k0, nullptr, k1, nullptr, n_dev, 0, shift, 11, s.hist, s.status, s.tile_ctr, ranges, n_ranges);
 }
 
 // ------------------------------------------------------------ exclusive scan

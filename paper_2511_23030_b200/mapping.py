@@ -301,7 +301,10 @@ class MappingEngine:
                                 candidates=self.store.known_chunk_ids)
 
     # ------------------------------------------------------------ device
-    fused_adam = True   # single-keyframe steps: Adam fused into the backward (sm_render_backward_adam)
+    # single-keyframe steps: Adam fused into the backward (sm_render_backward_adam).  Measured
+    # slower at C2 (0.900 vs 0.880 ms/step: the fused projection backward spills and its
+    # one-thread-per-record Adam streams worse than K7's quarter threads), so off by default.
+    fused_adam = False
 
     def _device_pass(self, kf: Keyframe, slots, n: int, backward: bool = True, adam: bool = False):
         """fwd -> loss(+grad) -> bwd for one keyframe; grads accumulate in the
