@@ -332,7 +332,7 @@ def test_fused_adam_backward_bit_identical(cuda, tmp_path):
     import torch
     a = _c1_engine(tmp_path / "a", budget=100_000)
     b = _c1_engine(tmp_path / "b", budget=100_000)
-    b.fused_adam = False
+    a.fused_adam, b.fused_adam = True, False
     for s in range(8):
         ra, rb = a.optimization_step(0, s), b.optimization_step(0, s)
         assert ra.selected_kf == rb.selected_kf and ra.loss == rb.loss, s
