@@ -317,25 +317,6 @@ inline size_t pass_smem() {
     return bytes;
 }
 
-// Global histogram of one 11-bit digit (the single-pass tile sort).
-template <typename K>
-__global__ void __launch_bounds__(kSortThreads)
-digit_histogram11(const K *__restrict__ keys, const uint32_t *n_dev, int64_t n_host, int shift,
-                  uint32_t *__restrict__ hist) {
-    __shared__ uint32_t h[2048];
-    const int64_t n = load_count(n_dev, n_host);
-    for (int i = threadIdx.x; i < 2048; i += kSortThreads) h[i] = 0;
-    __syncthreads();
-    for (int64_t i = (int64_t)blockIdx.x * kSortThreads + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * kSortThreads)
-        atomicAdd(&h[(uint32_t)(keys[i] >> shift) & 2047u], 1u);
-    __syncthreads();
-    for (int i = threadIdx.x; i < 2048; i += kSortThreads) {
-        const uint32_t v = h[i];
-        if (v) atomicAdd(&hist[i], v);
-    }
-}
-
 struct SortScratch {
     uint32_t *hist;      // [kMaxPasses][kRadix]
     uint32_t *status;    // [kMaxPasses][max_tiles][kRadix]
@@ -416,23 +397,6 @@ int radix_sort(K *k0, uint32_t *v0, K *k1, uint32_t *v1, const uint32_t *n_dev, 
         cur ^= 1;
     }
     return cur;
-}
-
-// Stable sort of keys on bits [shift, shift + 11) in ONE pass (the tile bits
-// of the instance keys, <= 2048 tiles), writing the per-digit ranges as a
-// by-product.  Result in k1.  The scratch sized for kMaxPasses 8-bit passes
-// holds one 11-bit pass (same hist and status footprint).
-template <typename K, int ITEMS = kSortItemsWide>
-void radix_sort_11(const K *k0, K *k1, const uint32_t *n_dev, int64_t max_n, int shift, int n_ranges,
-                   uint32_t *ranges, const SortScratch &s, cudaStream_t st) {
-    const int64_t tiles = sort_tile_count<ITEMS>(max_n);
-    cudaMemsetAsync(s.tile_ctr, 0,
-                    (size_t)(reinterpret_cast<char *>(s.status + tiles * 2048) -
-                             reinterpret_cast<char *>(s.tile_ctr)), st);
-    const unsigned hgrid = (unsigned)min64(tiles * 2, 148 * 8);
-    digit_histogram11<K><<<hgrid, kSortThreads, 0, st>>>(k0, n_dev, 0, shift, s.hist);
-    onesweep_pass<K, false, ITEMS, 11><<<(unsigned)tiles, kSortThreads, pass_smem<K, false, ITEMS, 11>(), st>>>(
-        k0, nullptr, k1, nullptr, n_dev, 0, shift, 11, s.hist, s.status, s.tile_ctr, ranges, n_ranges);
 }
 
 // ------------------------------------------------------------ exclusive scan
