@@ -235,6 +235,36 @@ int sm_chunk_unpack(const uint8_t *records, int64_t n, int64_t stride, float *pa
 int sm_chunk_pack(const float *params, const float *sh_rest, const float *adam_m,
                   const float *adam_v, int64_t n, int64_t stride, uint8_t *records, void *stream);
 
+/* ---------------------------------------------------------------- ingest
+ * splatmap sample.py on the device (fp64, like the reference).
+ * sm_log_scores: |LoG * luma| of an (H,W,3) image (sample.py:63-75 log_norm
+ * before its max-normalisation; luma 0.299 r + 0.587 g + 0.114 b, zero
+ * padding, taps = host log_kernel(sigma, radius) (2r+1)^2 doubles, radius
+ * <= 3), written to scores_out [H*W] fp64, and the image's peak to *peak_out
+ * (device uint64, the fp64 bit pattern).  rgb_kind: SM_RGB_U8 (the
+ * keyframe's 8-bit colours, k/255 in float32 as core.py:262-267),
+ * SM_RGB_F32 or SM_RGB_F64.
+ * sm_sampling_probability: max(a / peak_a - b / peak_b, 0) (sample.py:78-84
+ * with log_norm's normalisation; a peak of 0 leaves its map unscaled);
+ * scores_rendered / peak_rendered NULL: the normalised input scores.
+ * sm_lift_pixels: sample.py:104-146 lift_to_gaussians for k (row, col)
+ * int32 pairs: float32-canonical param records [k][16] and valid_out[k] =
+ * depth > 0 (the caller keeps the valid ones in order).  r_wc / t host. */
+#define SM_RGB_U8 0
+#define SM_RGB_F32 1
+#define SM_RGB_F64 2
+int sm_log_scores(const void *rgb, int32_t rgb_kind, int32_t width, int32_t height,
+                  const double *taps /* host */, int32_t radius, double *scores_out, uint64_t *peak_out,
+                  void *stream);
+int sm_sampling_probability(const double *scores_input, const uint64_t *peak_input,
+                            const double *scores_rendered, const uint64_t *peak_rendered, int64_t n,
+                            double *ps_out, void *stream);
+int sm_lift_pixels(const int32_t *pixels, int64_t k, const float *depth, const void *rgb,
+                   int32_t rgb_kind, int32_t width, int32_t height, const double *r_wc /* host */,
+                   const double *t /* host */, double fx, double fy, double cx, double cy,
+                   double scale_factor, float opacity, float *params_out, int32_t *valid_out,
+                   void *stream);
+
 /* ------------------------------------------------------------ profiling
  * No reference counterpart (the reference bills a deterministic cost model,
  * sim.py:53-57).  When enabled, each stage (project_fwd, depth_sort,

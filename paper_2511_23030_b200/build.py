@@ -17,7 +17,7 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libsplatmap_cuda.so"
-SOURCES = ["capi.cu", "render_fwd.cu", "render_bwd.cu", "loss.cu", "store_kernels.cu", "prof.cu"]
+SOURCES = ["capi.cu", "render_fwd.cu", "render_bwd.cu", "loss.cu", "store_kernels.cu", "prof.cu", "ingest.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -30,6 +30,11 @@ int loss_forward_backward(const float *, const float *, const uint8_t *, const f
 int adam_step(float *, float *, float *, float *, const int32_t *, int64_t, const sm_adam_config &,
               const uint32_t *, const float *, cudaStream_t);
 int pack_grads(float *, const int32_t *, int64_t, float *, cudaStream_t);
+int log_scores(const void *, int, int, int, const double *, int, double *, unsigned long long *, cudaStream_t);
+int sampling_probability(const double *, const unsigned long long *, const double *, const unsigned long long *,
+                         int64_t, double *, cudaStream_t);
+int lift_pixels(const int32_t *, int64_t, const float *, const void *, int, int, int, const double *,
+                const double *, double, double, double, double, double, float, float *, int32_t *, cudaStream_t);
 int cull_chunks(const int32_t *, int64_t, const double *, const double *, double, double, uint8_t *,
                 cudaStream_t);
 int encode_positions(const float *, int64_t, double, uint64_t *, int64_t *, cudaStream_t);
@@ -228,6 +233,42 @@ int sm_chunk_pack(const float *params, const float *sh_rest, const float *adam_m
         return SM_ERR_INVALID;
     }
     return chunk_pack(params, sh_rest, adam_m, adam_v, n, stride, records, SM_STREAM(stream));
+}
+
+
+int sm_log_scores(const void *rgb, int32_t rgb_kind, int32_t width, int32_t height, const double *taps,
+                  int32_t radius, double *scores_out, uint64_t *peak_out, void *stream) {
+    if (!rgb || !taps || !scores_out || !peak_out || rgb_kind < SM_RGB_U8 || rgb_kind > SM_RGB_F64) {
+        set_error("sm_log_scores: null argument or bad rgb_kind");
+        return SM_ERR_INVALID;
+    }
+    return log_scores(rgb, rgb_kind, width, height, taps, radius, scores_out,
+                      reinterpret_cast<unsigned long long *>(peak_out), SM_STREAM(stream));
+}
+
+int sm_sampling_probability(const double *scores_input, const uint64_t *peak_input,
+                            const double *scores_rendered, const uint64_t *peak_rendered, int64_t n,
+                            double *ps_out, void *stream) {
+    if (n > 0 && (!scores_input || !peak_input || !ps_out || (!scores_rendered != !peak_rendered))) {
+        set_error("sm_sampling_probability: null argument");
+        return SM_ERR_INVALID;
+    }
+    return sampling_probability(scores_input, reinterpret_cast<const unsigned long long *>(peak_input),
+                                scores_rendered, reinterpret_cast<const unsigned long long *>(peak_rendered), n,
+                                ps_out, SM_STREAM(stream));
+}
+
+int sm_lift_pixels(const int32_t *pixels, int64_t k, const float *depth, const void *rgb, int32_t rgb_kind,
+                   int32_t width, int32_t height, const double *r_wc, const double *t, double fx, double fy,
+                   double cx, double cy, double scale_factor, float opacity, float *params_out,
+                   int32_t *valid_out, void *stream) {
+    if (k > 0 && (!pixels || !depth || !rgb || !r_wc || !t || !params_out || !valid_out || rgb_kind < SM_RGB_U8 ||
+                  rgb_kind > SM_RGB_F64)) {
+        set_error("sm_lift_pixels: null argument or bad rgb_kind");
+        return SM_ERR_INVALID;
+    }
+    return lift_pixels(pixels, k, depth, rgb, rgb_kind, width, height, r_wc, t, fx, fy, cx, cy, scale_factor,
+                       opacity, params_out, valid_out, SM_STREAM(stream));
 }
 
 }  // extern "C"

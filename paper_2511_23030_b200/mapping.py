@@ -182,7 +182,7 @@ class MappingEngine:
     def __init__(self, store: ChunkStore, intr: CameraIntrinsics, seed: int = 7,
                  cull: CullConfig | None = None, select: SelectConfig | None = None,
                  weights: LossWeights | None = None, adam: AdamSettings | None = None,
-                 comm=None):
+                 comm=None, sample=None):
         import torch
         self.torch = torch
         self.store = store
@@ -193,6 +193,10 @@ class MappingEngine:
         self.index = KeyframeIndex(config=select or SelectConfig())
         self.weights = weights or LossWeights()
         self.adam = adam or AdamSettings()
+        if sample is None:
+            from .sample import SampleConfig
+            sample = SampleConfig()
+        self.sample_cfg = sample
         self._adam_c = self.adam.to_c()
         self.comm = comm
         self.latest_kf: int | None = None
@@ -234,6 +238,58 @@ class MappingEngine:
         self.index.add(kf.id, kf.position,
                        usage_remaining=self.index.config.initial_usage if index_usage is None else index_usage)
         self.latest_kf = kf.id
+
+    def render_current(self, pose: Pose):
+        """sim._Replay._render_current (sim.py:255-262) on the device: the
+        visible chunks made resident and rendered into self.rgb / depth /
+        alpha (overflow retried); returns the active-set size."""
+        visible, _ = self._visible_for_pose(pose)
+        ids = sorted(visible)
+        if ids:
+            self.store.ensure_resident(ids)
+        slots, n = self.active.build(self.store.segments(ids))
+        cam = camera_for(pose, self.intr)
+        for _ in range(8):
+            self.render.forward(self.store.slab.params, slots, n, cam, self.rgb, self.depth, self.alpha)
+            c = self.render.counters()
+            if not c["overflow"]:
+                return n
+            self.render.grow_instances(c["n_instances"])
+            self.drop_graphs()
+        raise DeviceFailure("tile-instance buffer kept overflowing")
+
+    def ingest_keyframe(self, index: int, pose: Pose, rgb: np.ndarray, depth: np.ndarray) -> int:
+        """sim._Replay.ingest_keyframe (sim.py:264-278) with the per-pixel work
+        on the device: keyframe tier + index, the current view rendered in
+        HBM, |LoG| scores of the keyframe's 8-bit ground truth and of the
+        render (csrc/ingest.cu), the probability map down to the host for the
+        reference's own draw (Generator.choice, seed (seed, 1, index)), the
+        drawn pixels lifted on the device, inserted through the store's
+        policy.  Returns the number of Gaussians inserted."""
+        from .sample import DeviceSampler, sample_pixels
+        cfg = self.sample_cfg
+        kf = Keyframe(id=index, pose=pose, intrinsics=self.intr, rgb=rgb, depth=depth,
+                      usage_remaining=self.index.config.initial_usage)
+        self.add_keyframe(kf)
+        self.render_current(pose)
+        dk = self._device_keyframe(kf)
+        if getattr(dk, "pending", None) is not None:
+            self.torch.cuda.current_stream(self.device).wait_stream(dk.pending)
+            dk.pending = None
+        smp = getattr(self, "_sampler", None)
+        if smp is None:
+            smp = self._sampler = DeviceSampler(self.intr.width, self.intr.height, self.device)
+        smp.scores_of(dk.rgb_u8, 0, cfg.log_sigma, cfg.kernel_radius)
+        smp.scores_of(self.rgb, 1, cfg.log_sigma, cfg.kernel_radius)
+        ps = smp.probability().cpu().numpy()
+        self.d2h_bytes += ps.nbytes
+        pixels = sample_pixels(ps, cfg.samples_per_keyframe, derive_seed(self.seed, 1, index))
+        rec, _ = smp.lift(pixels, dk.depth, dk.rgb_u8, pose.rotation, pose.translation, self.intr, cfg)
+        if not len(rec):
+            return 0
+        sh = np.zeros((len(rec), 48), np.float64)
+        sh[:, [0, 16, 32]] = rec[:, 11:14]
+        return self.store.insert_arrays(rec[:, 0:3], rec[:, 3:7], rec[:, 7:10], rec[:, 10], sh)
 
     def _drop_device_keyframe(self, kid: int) -> None:
         self._kf_dev.pop(kid, None)

@@ -18,6 +18,7 @@ Fixtures:
   grid.npz          encode_positions, chunk coords, frustum planes, visible sets
   diskformat.npz    pack_chunk / pack_keyframe bytes
   store_trace.json  ChunkStore policy trace (loads, evictions, stats)
+  sample.npz        log_norm / sampling_probability / sample_pixels / lift / ingest_keyframe
   view_edits.json   in-place edits through chunk.gaussians / gather_visible + flushed file hashes
 """
 
@@ -430,6 +431,73 @@ def make_view_edits():
     (HERE / "view_edits.json").write_text(json.dumps(out))
 
 
+def make_sample():
+    """Ingest path (sample.py:49-146, sim.py:264-278): log_norm of images
+    (random, step edges, a rendered scene), sampling_probability,
+    sample_pixels draws, lift_to_gaussians (rotated poses, invalid depth),
+    and two reference _Replay.ingest_keyframe calls on a small scene."""
+    from splatmap import sample, sim
+    rng = np.random.default_rng(31)
+    out = {}
+    imgs = [rng.uniform(0, 1, (48, 64, 3)),
+            np.repeat(np.repeat((rng.uniform(0, 1, (6, 8, 3)) > 0.5).astype(np.float64), 8, 0), 8, 1),
+            np.zeros((20, 24, 3)), np.full((20, 24, 3), 0.6)]
+    scene = _scene(rng, 300)
+    intr = core.CameraIntrinsics(fx=50.0, fy=50.0, cx=31.5, cy=23.5, width=64, height=48, near=0.2, far=100.0)
+    pose = core.Pose()
+    imgs.append(renderloss.render_arrays(scene, pose, intr).rgb)
+    for k, im in enumerate(imgs):
+        out[f"img{k}"] = im
+        for sig, rad in ((1.0, 2), (1.5, 3)):
+            out[f"log{k}_{sig}_{rad}"] = sample.log_norm(im, sig, rad)
+    out["n_img"] = np.array(len(imgs))
+    a, b = out["log0_1.0_2"], out["log4_1.0_2"]
+    ps = sample.sampling_probability(a, b)
+    out["ps"] = ps
+    for n, seed in ((50, 3), (500, 4), (5000, 5)):
+        out[f"draw_{n}_{seed}"] = np.array(sample.sample_pixels(ps, n, seed), dtype=np.int64).reshape(-1, 2)
+    # lift: rotated pose, some invalid depth, quantised rgb
+    for k in range(3):
+        q = core.quat_normalize(rng.normal(size=4))
+        t = rng.normal(size=3) * 2
+        depth = rng.uniform(0.5, 6.0, (48, 64)).astype(np.float32)
+        depth[rng.random((48, 64)) < 0.2] = 0.0
+        kf = core.Keyframe(id=k, pose=core.Pose(rotation=q, translation=t), intrinsics=intr,
+                           rgb=rng.uniform(0, 1, (48, 64, 3)), depth=depth)
+        pix = [(int(r), int(c)) for r, c in zip(rng.integers(0, 48, 200), rng.integers(0, 64, 200))]
+        gs = sample.lift_to_gaussians(pix, kf, sample.SampleConfig(init_scale_factor=1.0 + 0.5 * k))
+        out[f"lift{k}_q"], out[f"lift{k}_t"] = q, t
+        out[f"lift{k}_rgb"], out[f"lift{k}_depth"] = kf.rgb, kf.depth
+        out[f"lift{k}_pix"] = np.array(pix, dtype=np.int64)
+        out[f"lift{k}_pos"] = np.array([g.position for g in gs])
+        out[f"lift{k}_scale"] = np.array([g.scale for g in gs])
+        out[f"lift{k}_sh0"] = np.array([g.sh[[0, 16, 32]] for g in gs])
+    # two ingests through the reference replay (first: empty map, second: the
+    # map the first inserted renders into the current view)
+    with tempfile.TemporaryDirectory() as d:
+        d = Path(d)
+        cfg = sim.ReplayConfig(trajectory=d / "t", images_dir=d / "i", depth_dir=d / "d", out=d / "o.csv",
+                               store_dir=d / "store", chunk_size=2.0, gaussian_budget=100_000, seed=7,
+                               samples_per_keyframe=800)
+        rep = sim._Replay(cfg, intr)
+        for k in range(2):
+            pose_k = core.Pose(translation=[0.1 * k, 0.0, 0.0])
+            tgt = renderloss.render_arrays(scene, pose_k, intr)
+            depth = np.where(tgt.alpha > 0.5, tgt.depth, 0.0).astype(np.float32)
+            n_ins = rep.ingest_keyframe(k, pose_k, tgt.rgb, depth)
+            out[f"ingest{k}_rgb"], out[f"ingest{k}_depth"] = tgt.rgb, depth
+            out[f"ingest{k}_t"] = np.asarray(pose_k.translation)
+            out[f"ingest{k}_n"] = np.array(n_ins)
+        rows, cids = [], []
+        for cid, gs in rep.store.iter_map():
+            for g in gs:
+                cids.append(cid)
+                rows.append(list(g.position) + list(g.scale) + [g.opacity] + list(g.sh[[0, 16, 32]]))
+        out["ingest_map"] = np.array(rows)
+        out["ingest_cids"] = np.array(cids, dtype=np.uint64)
+    np.savez_compressed(HERE / "sample.npz", **out)
+
+
 def make_select_trace():
     """KeyframeIndex / select_keyframe / record_loss policy trace (select.py)."""
     from splatmap import select, sim
@@ -464,6 +532,7 @@ if __name__ == "__main__":
     make_diskformat()
     make_store_trace()
     make_view_edits()
+    make_sample()
     make_render_fd()
     for p in sorted(HERE.glob("*.npz")) + sorted(HERE.glob("*.json")):
         print(f"{p.name:24s} {p.stat().st_size:>9d} bytes")

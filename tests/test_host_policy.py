@@ -286,3 +286,17 @@ def test_slab_allocator_cap_and_compaction_cpu():
     a = uncapped.alloc(1000)
     b = uncapped.alloc(1000)   # grows
     assert uncapped.capacity >= 2000 and b == a + 1000
+
+
+def test_sample_pixels_host_draw_matches_reference(golden):
+    """sample.py:87-101: the draw stays on the host (NumPy Generator.choice
+    without replacement); fed the reference's probability map it returns the
+    reference's pixels (tests/golden/sample.npz)."""
+    from paper_2511_23030_b200.sample import log_kernel, sample_pixels
+    g = golden("sample.npz")
+    for n, seed in ((50, 3), (500, 4), (5000, 5)):
+        draw = np.array(sample_pixels(g["ps"], n, seed), dtype=np.int64).reshape(-1, 2)
+        assert np.array_equal(draw, g[f"draw_{n}_{seed}"])
+    assert sample_pixels(np.zeros((4, 5)), 10, 1) == []
+    k = log_kernel(1.0, 2)
+    assert k.shape == (5, 5) and abs(k.sum()) < 1e-12 and k[2, 2] == k.min()
