@@ -265,6 +265,20 @@ int sm_lift_pixels(const int32_t *pixels, int64_t k, const float *depth, const v
                    double scale_factor, float opacity, float *params_out, int32_t *valid_out,
                    void *stream);
 
+/* ---------------------------------------------------------- loop closure
+ * loopclose.py on the device.
+ * sm_transform_rows: _transform_chunk (loopclose.py:146-150) on n param
+ * records in place -- p' = R p + t, q' = normalize(q_t * q) (core.py:76-87,
+ * 141-142, 309-314) in fp64 from the float32 values, stored float32
+ * (storage_canonical); scale, opacity, SH and Adam state untouched.
+ * rotation (row-major 3x3), translation, quaternion (w,x,y,z) are host.
+ * sm_reset_rows: refine_reset (loopclose.py:228-245) on n rows: opacity <-
+ * `opacity`, Adam moments and step count zeroed (opt_state = b""). */
+int sm_transform_rows(float *params, int64_t n, const double *rotation /* host */,
+                      const double *translation /* host */, const double *quaternion /* host */,
+                      void *stream);
+int sm_reset_rows(float *params, float *adam_m, float *adam_v, int64_t n, float opacity, void *stream);
+
 /* ------------------------------------------------------------ profiling
  * No reference counterpart (the reference bills a deterministic cost model,
  * sim.py:53-57).  When enabled, each stage (project_fwd, depth_sort,

@@ -30,6 +30,8 @@ int loss_forward_backward(const float *, const float *, const uint8_t *, const f
 int adam_step(float *, float *, float *, float *, const int32_t *, int64_t, const sm_adam_config &,
               const uint32_t *, const float *, cudaStream_t);
 int pack_grads(float *, const int32_t *, int64_t, float *, cudaStream_t);
+int transform_rows(float *, int64_t, const double *, const double *, const double *, cudaStream_t);
+int reset_rows(float *, float *, float *, int64_t, float, cudaStream_t);
 int log_scores(const void *, int, int, int, const double *, int, double *, unsigned long long *, cudaStream_t);
 int sampling_probability(const double *, const unsigned long long *, const double *, const unsigned long long *,
                          int64_t, double *, cudaStream_t);
@@ -269,6 +271,23 @@ int sm_lift_pixels(const int32_t *pixels, int64_t k, const float *depth, const v
     }
     return lift_pixels(pixels, k, depth, rgb, rgb_kind, width, height, r_wc, t, fx, fy, cx, cy, scale_factor,
                        opacity, params_out, valid_out, SM_STREAM(stream));
+}
+
+int sm_transform_rows(float *params, int64_t n, const double *rotation, const double *translation,
+                      const double *quaternion, void *stream) {
+    if (n > 0 && (!params || !rotation || !translation || !quaternion)) {
+        set_error("sm_transform_rows: null argument");
+        return SM_ERR_INVALID;
+    }
+    return transform_rows(params, n, rotation, translation, quaternion, SM_STREAM(stream));
+}
+
+int sm_reset_rows(float *params, float *adam_m, float *adam_v, int64_t n, float opacity, void *stream) {
+    if (n > 0 && (!params || !adam_m || !adam_v)) {
+        set_error("sm_reset_rows: null argument");
+        return SM_ERR_INVALID;
+    }
+    return reset_rows(params, adam_m, adam_v, n, opacity, SM_STREAM(stream));
 }
 
 }  // extern "C"

@@ -113,6 +113,82 @@ int adam_step(float *params, float *m, float *v, float *grads, const int32_t *sl
     return SM_OK;
 }
 
+// ------------------------------------------------------ loop closure
+// Rigid correction of a chunk's rows in place (loopclose.py:146-150 with
+// core.py transform_gaussian + storage_canonical): p' = R p + t and
+// q' = normalize(q_t * q) in fp64 from the stored float32 values, rounded
+// back to float32; everything else (scale, opacity, SH, Adam state) is kept.
+struct RigidDev {
+    double r[9];   // R of the transform, row-major
+    double t[3];
+    double q[4];   // its quaternion (w, x, y, z)
+};
+
+__global__ void __launch_bounds__(256)
+transform_rows_kernel(float4 *__restrict__ params, int64_t n, RigidDev c) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4 A = params[4 * i], B = params[4 * i + 1];   // px py pz qw | qx qy qz sx
+    const double p[3] = {A.x, A.y, A.z};
+    double w[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+        w[a] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(c.r[3 * a], p[0]), __dmul_rn(c.r[3 * a + 1], p[1])),
+                                   __dmul_rn(c.r[3 * a + 2], p[2])),
+                         c.t[a]);
+    // Hamilton product q_t * q (core.py:76-87), then normalize
+    const double aw = c.q[0], ax = c.q[1], ay = c.q[2], az = c.q[3];
+    const double bw = A.w, bx = B.x, by = B.y, bz = B.z;
+    double q[4];
+    q[0] = __dsub_rn(__dsub_rn(__dsub_rn(__dmul_rn(aw, bw), __dmul_rn(ax, bx)), __dmul_rn(ay, by)), __dmul_rn(az, bz));
+    q[1] = __dsub_rn(__dadd_rn(__dadd_rn(__dmul_rn(aw, bx), __dmul_rn(ax, bw)), __dmul_rn(ay, bz)), __dmul_rn(az, by));
+    q[2] = __dadd_rn(__dadd_rn(__dsub_rn(__dmul_rn(aw, by), __dmul_rn(ax, bz)), __dmul_rn(ay, bw)), __dmul_rn(az, bx));
+    q[3] = __dadd_rn(__dsub_rn(__dadd_rn(__dmul_rn(aw, bz), __dmul_rn(ax, by)), __dmul_rn(ay, bx)), __dmul_rn(az, bw));
+    const double nrm = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(q[0], q[0]), __dmul_rn(q[1], q[1])),
+                                                      __dmul_rn(q[2], q[2])),
+                                            __dmul_rn(q[3], q[3])));
+    A.x = (float)w[0], A.y = (float)w[1], A.z = (float)w[2];
+    A.w = (float)__ddiv_rn(q[0], nrm);
+    B.x = (float)__ddiv_rn(q[1], nrm), B.y = (float)__ddiv_rn(q[2], nrm), B.z = (float)__ddiv_rn(q[3], nrm);
+    params[4 * i] = A;
+    params[4 * i + 1] = B;
+}
+
+// refine_reset (loopclose.py:228-245): opacity <- value, optimizer state
+// fresh (opt_state = b"": zero moments and step count).
+__global__ void __launch_bounds__(256)
+reset_rows_kernel(float *__restrict__ params, float4 *__restrict__ m, float4 *__restrict__ v, int64_t n,
+                  float opacity) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = t >> 2;
+    if (i >= n) return;
+    const int q = (int)(t & 3);
+    m[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    v[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (q == 0) params[16 * i + 10] = opacity;
+}
+
+int transform_rows(float *params, int64_t n, const double *r, const double *t, const double *q, cudaStream_t st) {
+    if (n <= 0) return SM_OK;
+    RigidDev c;
+    for (int k = 0; k < 9; k++) c.r[k] = r[k];
+    for (int k = 0; k < 3; k++) c.t[k] = t[k];
+    for (int k = 0; k < 4; k++) c.q[k] = q[k];
+    count_launches(1);
+    transform_rows_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(reinterpret_cast<float4 *>(params), n, c);
+    SM_CHECK_LAUNCH("transform_rows");
+    return SM_OK;
+}
+
+int reset_rows(float *params, float *m, float *v, int64_t n, float opacity, cudaStream_t st) {
+    if (n <= 0) return SM_OK;
+    count_launches(1);
+    reset_rows_kernel<<<(unsigned)ceil_div(n * 4, 256), 256, 0, st>>>(params, reinterpret_cast<float4 *>(m),
+                                                                       reinterpret_cast<float4 *>(v), n, opacity);
+    SM_CHECK_LAUNCH("reset_rows");
+    return SM_OK;
+}
+
 // ------------------------------------------------------------------ K1
 struct CullDev {
     double planes[24];

@@ -19,6 +19,7 @@ Fixtures:
   diskformat.npz    pack_chunk / pack_keyframe bytes
   store_trace.json  ChunkStore policy trace (loads, evictions, stats)
   sample.npz        log_norm / sampling_probability / sample_pixels / lift / ingest_keyframe
+  loopclose.json    run_correction (batch / sequential): reports, stats, flushed map
   view_edits.json   in-place edits through chunk.gaussians / gather_visible + flushed file hashes
 """
 
@@ -498,6 +499,74 @@ def make_sample():
     np.savez_compressed(HERE / "sample.npz", **out)
 
 
+def make_loopclose():
+    """Loop-closure correction (loopclose.py:146-268) on the reference store:
+    two clusters, two keyframes, a rotation + translation and a translation
+    (each crossing chunk boundaries), keyframe 1 a junction, batch and
+    sequential modes (budget 150 forces paging in sequential).  Records the
+    outcome reports, stats and the flushed map."""
+    from splatmap import loopclose
+    out = {}
+    intr = core.CameraIntrinsics(fx=20.0, fy=20.0, cx=8.0, cy=8.0, width=16, height=16, near=0.1, far=60.0)
+
+    def cluster(rng, n, center, spread):
+        gs = []
+        for _ in range(n):
+            sh = np.zeros(48)
+            sh[[0, 16, 32]] = (rng.uniform(0.1, 0.9, 3) - 0.5) / 0.28209479177
+            gs.append(core.Gaussian(position=np.asarray(center) + rng.uniform(-spread, spread, 3),
+                                    rotation=core.quat_normalize(rng.normal(size=4)),
+                                    scale=rng.uniform(0.08, 0.25, size=3), opacity=float(rng.uniform(0.4, 0.9)),
+                                    sh=sh, opt_state=rng.bytes(4)))
+        return gs
+
+    def kf(kid, pose):
+        r = np.random.default_rng(kid + 100)
+        return core.Keyframe(id=kid, pose=pose, intrinsics=intr, rgb=r.integers(0, 256, size=(16, 16, 3)) / 255.0,
+                             depth=r.uniform(1, 10, size=(16, 16)).astype(np.float32))
+
+    cs = loopclose.CorrectionSet(entries=(
+        (0, core.RigidTransform(rotation=core.quat_normalize([0.98, 0.0, 0.0, 0.2]), translation=[12.0, 0.0, 0.0])),
+        (1, core.RigidTransform(translation=[0.0, 11.0, 0.0]))), junction_ids=frozenset({1}))
+    cull = culling.CullConfig(max_distance_m=100.0)
+    inserts = []
+    rng = np.random.default_rng(13)
+    for n_c, center in ((50, (0.0, 0.0, 4.0)), (50, (3.0, 0.0, 8.0)), (70, (60.0, 0.0, 4.0))):
+        gs = cluster(rng, n_c, center, 2.0)
+        inserts.append([[*g.position, *g.rotation, *g.scale, g.opacity, *g.sh[[0, 16, 32]]] for g in gs])
+        out.setdefault("opts", []).extend(g.opt_state.hex() for g in gs)
+    out["inserts"] = inserts
+    for mode in (loopclose.CorrectionMode.BATCH, loopclose.CorrectionMode.SEQUENTIAL):
+        with tempfile.TemporaryDirectory() as d:
+            st = store.ChunkStore(store.StoreConfig(disk_root=Path(d), gaussian_budget=150, keyframe_budget=8,
+                                                    io_ns_per_byte=1.0))
+            r2 = np.random.default_rng(13)
+            st.insert_gaussians(cluster(r2, 50, (0.0, 0.0, 4.0), 2.0))
+            st.insert_gaussians(cluster(r2, 50, (3.0, 0.0, 8.0), 2.0))
+            st.insert_gaussians(cluster(r2, 70, (60.0, 0.0, 4.0), 2.0))   # out of view: paging
+            st.keyframe_add(kf(0, core.Pose()))
+            st.keyframe_add(kf(1, core.Pose(translation=[2.0, 0.0, 0.0])))
+            o = loopclose.run_correction(cs, st, cull, force_mode=mode)
+            st.flush()
+            m = []
+            for cid, gs in st.iter_map():
+                for g in gs:
+                    m.append([str(cid), *g.position, *g.rotation, *g.scale, g.opacity, *g.sh[[0, 16, 32]],
+                              g.opt_state.hex()])
+            s_ = st.stats
+            out[mode.value] = {
+                "plan": [o.plan.mode.value, sorted(str(c) for c in o.plan.unique_chunks), o.plan.estimated_gaussians],
+                "report": [o.report.transformed, o.report.skipped_duplicates,
+                           sorted(str(c) for c in o.report.touched_chunks)],
+                "moves": [o.moves.moved, sorted(str(c) for c in o.moves.created_chunks),
+                          sorted(str(c) for c in o.moves.emptied_chunks)],
+                "resets": o.reset_gaussians,
+                "stats": [s_.chunk_loads, s_.chunk_evictions, s_.chunk_writes, s_.total_gaussians_ever],
+                "poses": [[*st.keyframe_get(k).pose.rotation, *st.keyframe_get(k).pose.translation] for k in (0, 1)],
+                "map": m}
+    (HERE / "loopclose.json").write_text(json.dumps(out))
+
+
 def make_select_trace():
     """KeyframeIndex / select_keyframe / record_loss policy trace (select.py)."""
     from splatmap import select, sim
@@ -533,6 +602,7 @@ if __name__ == "__main__":
     make_store_trace()
     make_view_edits()
     make_sample()
+    make_loopclose()
     make_render_fd()
     for p in sorted(HERE.glob("*.npz")) + sorted(HERE.glob("*.json")):
         print(f"{p.name:24s} {p.stat().st_size:>9d} bytes")
