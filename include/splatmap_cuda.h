@@ -279,6 +279,13 @@ int sm_transform_rows(float *params, int64_t n, const double *rotation /* host *
                       void *stream);
 int sm_reset_rows(float *params, float *adam_m, float *adam_v, int64_t n, float opacity, void *stream);
 
+/* .dkf keyframe file (diskformat.py:198-216 pack_keyframe) assembled on the
+ * device from the keyframe tier's HBM copy: header (host, 140 bytes, the
+ * <4sIQ7d6dIIdI layout) | rgb_u8 (H,W,3) | depth f32 (H,W); out receives
+ * 140 + 7 W H bytes (device).  Byte-identical to pack_keyframe. */
+int sm_keyframe_pack(const uint8_t *header /* host */, const uint8_t *rgb_u8, const float *depth,
+                     int32_t width, int32_t height, uint8_t *out, void *stream);
+
 /* ------------------------------------------------------------ profiling
  * No reference counterpart (the reference bills a deterministic cost model,
  * sim.py:53-57).  When enabled, each stage (project_fwd, depth_sort,

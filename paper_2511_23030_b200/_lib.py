@@ -93,6 +93,7 @@ def load():
     _sig(lib.sm_pack_grads, c_int, vp, vp, i64, vp, vp)
     _sig(lib.sm_transform_rows, c_int, vp, i64, POINTER(c_double), POINTER(c_double), POINTER(c_double), vp)
     _sig(lib.sm_reset_rows, c_int, vp, vp, vp, i64, c_float, vp)
+    _sig(lib.sm_keyframe_pack, c_int, vp, vp, vp, i32, i32, vp, vp)
     _dp = POINTER(c_double)
     _sig(lib.sm_log_scores, c_int, vp, i32, i32, i32, _dp, i32, vp, vp, vp)
     _sig(lib.sm_sampling_probability, c_int, vp, vp, vp, vp, i64, vp, vp)

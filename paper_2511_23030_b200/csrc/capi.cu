@@ -32,6 +32,7 @@ int adam_step(float *, float *, float *, float *, const int32_t *, int64_t, cons
 int pack_grads(float *, const int32_t *, int64_t, float *, cudaStream_t);
 int transform_rows(float *, int64_t, const double *, const double *, const double *, cudaStream_t);
 int reset_rows(float *, float *, float *, int64_t, float, cudaStream_t);
+int keyframe_pack(const uint8_t *, const uint8_t *, const float *, int64_t, uint8_t *, cudaStream_t);
 int log_scores(const void *, int, int, int, const double *, int, double *, unsigned long long *, cudaStream_t);
 int sampling_probability(const double *, const unsigned long long *, const double *, const unsigned long long *,
                          int64_t, double *, cudaStream_t);
@@ -288,6 +289,15 @@ int sm_reset_rows(float *params, float *adam_m, float *adam_v, int64_t n, float 
         return SM_ERR_INVALID;
     }
     return reset_rows(params, adam_m, adam_v, n, opacity, SM_STREAM(stream));
+}
+
+int sm_keyframe_pack(const uint8_t *header, const uint8_t *rgb_u8, const float *depth, int32_t width,
+                     int32_t height, uint8_t *out, void *stream) {
+    if (!header || !rgb_u8 || !depth || !out || width < 1 || height < 1) {
+        set_error("sm_keyframe_pack: null argument or empty image");
+        return SM_ERR_INVALID;
+    }
+    return keyframe_pack(header, rgb_u8, depth, (int64_t)width * height, out, SM_STREAM(stream));
 }
 
 }  // extern "C"

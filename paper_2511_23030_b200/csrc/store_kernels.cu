@@ -1,6 +1,7 @@
 // K1 chunk culling + active-set expansion, K7 fused Adam, K8/K9 chunk codec,
 // and the bit-exact chunk-id encoder.
 #include <cmath>
+#include <cstring>
 
 #include "adam.cuh"
 #include "common.cuh"
@@ -186,6 +187,42 @@ int reset_rows(float *params, float *m, float *v, int64_t n, float opacity, cuda
     reset_rows_kernel<<<(unsigned)ceil_div(n * 4, 256), 256, 0, st>>>(params, reinterpret_cast<float4 *>(m),
                                                                        reinterpret_cast<float4 *>(v), n, opacity);
     SM_CHECK_LAUNCH("reset_rows");
+    return SM_OK;
+}
+
+// ------------------------------------------------------ keyframe codec
+// .dkf file image (diskformat.py:198-216 pack_keyframe) from a keyframe's
+// HBM copy: 140-byte header (host-built) | RGB u8 (H,W,3) | depth f32
+// little-endian (H,W).  The keyframe's colours are already its 8-bit values
+// (k/255 re-quantises to k), so the file is a byte copy on the device; the
+// write-behind then moves it D2H and writes it (no host quantisation).
+struct KfHeader {
+    uint32_t w[35];   // 140 bytes
+};
+
+__global__ void __launch_bounds__(256)
+keyframe_pack_kernel(KfHeader h, const uint8_t *__restrict__ rgb, const uint8_t *__restrict__ depth, int64_t npx,
+                     uint8_t *__restrict__ out) {
+    const int64_t total = 140 + 7 * npx;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        uint8_t b;
+        if (i < 140)
+            b = (uint8_t)(h.w[i >> 2] >> (8 * (i & 3)));
+        else if (i < 140 + 3 * npx)
+            b = rgb[i - 140];
+        else
+            b = depth[i - 140 - 3 * npx];
+        out[i] = b;
+    }
+}
+
+int keyframe_pack(const uint8_t *header, const uint8_t *rgb, const float *depth, int64_t npx, uint8_t *out,
+                  cudaStream_t st) {
+    KfHeader h;
+    memcpy(h.w, header, 140);
+    count_launches(1);
+    keyframe_pack_kernel<<<148 * 4, 256, 0, st>>>(h, rgb, reinterpret_cast<const uint8_t *>(depth), npx, out);
+    SM_CHECK_LAUNCH("keyframe_pack");
     return SM_OK;
 }
 

@@ -163,12 +163,16 @@ def build_chunk_file(encoded_id: int, records: np.ndarray, count: int | None = N
     return _HDR.pack(CHUNK_MAGIC, FORMAT_VERSION, encoded_id, n, 0) + records.tobytes()
 
 
-def pack_keyframe(kf: Keyframe) -> bytes:
+def keyframe_header(kf: Keyframe) -> bytes:
+    """The 140-byte .dkf header (<4sIQ7d6dIIdI, diskformat.py:53,198-212)."""
     i = kf.intrinsics
-    head = _KF.pack(KEYFRAME_MAGIC, FORMAT_VERSION, kf.id, *kf.pose.translation, *kf.pose.rotation,
+    return _KF.pack(KEYFRAME_MAGIC, FORMAT_VERSION, kf.id, *kf.pose.translation, *kf.pose.rotation,
                     i.fx, i.fy, i.cx, i.cy, i.near, i.far, i.width, i.height, kf.last_loss,
                     kf.usage_remaining)
-    return head + kf.rgb_u8().tobytes() + kf.depth.astype("<f4").tobytes()
+
+
+def pack_keyframe(kf: Keyframe) -> bytes:
+    return keyframe_header(kf) + kf.rgb_u8().tobytes() + kf.depth.astype("<f4").tobytes()
 
 
 def keyframe_file_size(kf: Keyframe) -> int:

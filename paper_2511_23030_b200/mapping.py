@@ -218,6 +218,7 @@ class MappingEngine:
         # evicts the keyframe (its .dkf write-back is the store's)
         self._kf_dev: dict[int, _DeviceKeyframe] = {}
         store.keyframe_evict_hooks.append(self._drop_device_keyframe)
+        store.keyframe_device_packer = self._pack_device_keyframe
         self._readback = torch.zeros(12, dtype=torch.float32, pin_memory=True)
         self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
         self.cam = None
@@ -290,6 +291,25 @@ class MappingEngine:
         sh = np.zeros((len(rec), 48), np.float64)
         sh[:, [0, 16, 32]] = rec[:, 11:14]
         return self.store.insert_arrays(rec[:, 0:3], rec[:, 3:7], rec[:, 7:10], rec[:, 10], sh)
+
+    def _pack_device_keyframe(self, kid: int, kf: Keyframe, path) -> bool:
+        """The store evicts a dirty keyframe whose ground truth is in HBM:
+        assemble its .dkf on the device (sm_keyframe_pack, byte-identical to
+        diskformat.pack_keyframe) and hand it to the write-behind."""
+        d = self._kf_dev.get(kid)
+        if d is None:
+            return False
+        from .diskformat import keyframe_file_size, keyframe_header
+        head = np.frombuffer(keyframe_header(kf), dtype=np.uint8).copy()
+        w, h = kf.intrinsics.width, kf.intrinsics.height
+        lib = _lib.load()
+
+        def fill(dev):
+            _lib.check(lib.sm_keyframe_pack(head.ctypes.data_as(_lib.ctypes.c_void_p), _lib.ptr(d.rgb_u8),
+                                            _lib.ptr(d.depth), w, h, _lib.ptr(dev), _lib.stream_handle()),
+                       "keyframe_pack")
+        self.store.streamer.write_file_async(path, keyframe_file_size(kf), fill)
+        return True
 
     def _drop_device_keyframe(self, kid: int) -> None:
         self._kf_dev.pop(kid, None)

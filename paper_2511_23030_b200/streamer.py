@@ -38,12 +38,13 @@ from .errors import CorruptChunk, IoFailure
 
 
 class _PendingWrite:
-    __slots__ = ("path", "header", "pin", "nbytes", "event", "done", "dev", "stride", "make")
+    __slots__ = ("path", "header", "pin", "nbytes", "event", "done", "dev", "stride", "make", "cache")
 
-    def __init__(self, path, header, pin, nbytes, event, dev, stride, make=None):
+    def __init__(self, path, header, pin, nbytes, event, dev, stride, make=None, cache=True):
         self.path, self.header, self.pin, self.nbytes = path, header, pin, nbytes
         self.event, self.dev, self.stride = event, dev, stride
         self.make = make   # host-built file (keyframes): bytes produced on the writer thread
+        self.cache = cache   # keep the device bytes in the victim cache once written (chunks)
         self.done = threading.Event()
 
 
@@ -395,6 +396,31 @@ class ChunkStreamer:
         self.stats["async_writes"] += 1
         self._queue.put(pw)
 
+    def write_file_async(self, path: Path, nbytes: int, fill) -> None:
+        """Write-behind of a file assembled on the device: fill(dev) writes its
+        nbytes into a pooled device buffer on the current stream (e.g.
+        sm_keyframe_pack), the D2H runs on the copy stream, a writer thread
+        writes the file (no victim-cache entry: keyframes reload from disk)."""
+        self.check()
+        torch = self.torch
+        dev = self._take(self._free_devs, max(nbytes, 1), pinned=False)
+        pin = self._take(self._free_pins, max(nbytes, 1), pinned=True)
+        fill(dev)
+        cur = torch.cuda.current_stream(self.slab.device)
+        self.d2h_stream.wait_stream(cur)
+        ev = torch.cuda.Event()
+        with torch.cuda.stream(self.d2h_stream):
+            pin[:nbytes].copy_(dev[:nbytes], non_blocking=True)
+            ev.record(self.d2h_stream)
+        pw = _PendingWrite(Path(path), b"", pin, nbytes, ev, dev, 0, cache=False)
+        with self._lock:
+            self._release_superseded(self._pending.get(pw.path))
+            self._pending[pw.path] = pw
+            self._drop_victim(pw.path)
+        self.bytes_d2h += nbytes
+        self.stats["async_writes"] += 1
+        self._queue.put(pw)
+
     def write_bytes_async(self, path: Path, make) -> None:
         """Write-behind of a host-built file: `make()` runs on a writer thread
         and returns the file's bytes (same newest-write-wins and wait_path
@@ -471,7 +497,7 @@ class ChunkStreamer:
             self._freed.notify_all()   # (waiters run once this block releases the lock)
             if pw.dev is None:
                 pass
-            elif landed and self.victim_limit > 0:   # keep the packed bytes in HBM
+            elif landed and pw.cache and self.victim_limit > 0:   # keep the packed bytes in HBM
                 self._drop_victim(pw.path)
                 self._victims[pw.path] = DeviceRecords(pw.header, pw.dev, pw.nbytes, pw.stride)
                 self._victim_bytes += pw.dev.numel()

@@ -19,6 +19,7 @@ Fixtures:
   diskformat.npz    pack_chunk / pack_keyframe bytes
   store_trace.json  ChunkStore policy trace (loads, evictions, stats)
   sample.npz        log_norm / sampling_probability / sample_pixels / lift / ingest_keyframe
+  keyframe_trace.json keyframe-tier LRU / write-back trace + .dkf hashes
   loopclose.json    run_correction (batch / sequential): reports, stats, flushed map
   view_edits.json   in-place edits through chunk.gaussians / gather_visible + flushed file hashes
 """
@@ -567,6 +568,59 @@ def make_loopclose():
     (HERE / "loopclose.json").write_text(json.dumps(out))
 
 
+def make_keyframe_trace():
+    """Keyframe tier policy (store.py:427-489): seeded add / get / dirty /
+    update_keyframe_pose / flush operations under a budget of 3; after each
+    op the resident ids in LRU order and the keyframe stats; at the end the
+    sha256 of every .dkf file (diskformat.py:198-250)."""
+    import hashlib
+    rng = np.random.default_rng(29)
+    intr = core.CameraIntrinsics(fx=10.0, fy=10.0, cx=4.0, cy=3.0, width=8, height=6, near=0.1, far=50.0)
+    ops, added = [], []
+    with tempfile.TemporaryDirectory() as d:
+        st = store.ChunkStore(store.StoreConfig(disk_root=Path(d), keyframe_budget=3, io_ns_per_byte=1.0))
+        for step in range(90):
+            kind = rng.choice(["add", "get", "dirty", "pose", "flush"], p=[0.25, 0.45, 0.12, 0.12, 0.06])
+            if kind == "add" or not added:
+                kid = len(added)
+                pose = core.Pose(rotation=core.quat_normalize(rng.normal(size=4)), translation=rng.normal(size=3))
+                rgb = rng.uniform(0, 1, (6, 8, 3))
+                depth = rng.uniform(0.5, 5.0, (6, 8)).astype(np.float32)
+                kf = core.Keyframe(id=kid, pose=pose, intrinsics=intr, rgb=rgb, depth=depth,
+                                   last_loss=float(rng.uniform(0, 1)), usage_remaining=int(rng.integers(0, 9)))
+                st.keyframe_add(kf)
+                added.append(kid)
+                op = {"op": "add", "id": kid, "q": pose.rotation.tolist(), "t": pose.translation.tolist(),
+                      "rgb": rgb.tolist(), "depth": depth.tolist(), "loss": kf.last_loss,
+                      "usage": kf.usage_remaining}
+            elif kind == "get":
+                kid = int(added[int(rng.integers(len(added)))])
+                st.keyframe_get(kid)
+                op = {"op": "get", "id": kid}
+            elif kind == "dirty":
+                res = list(st._keyframes)
+                kid = int(res[int(rng.integers(len(res)))])
+                st.mark_keyframe_dirty(kid)
+                op = {"op": "dirty", "id": kid}
+            elif kind == "pose":
+                kid = int(added[int(rng.integers(len(added)))])
+                pose = core.Pose(rotation=core.quat_normalize(rng.normal(size=4)), translation=rng.normal(size=3))
+                st.update_keyframe_pose(kid, pose)
+                op = {"op": "pose", "id": kid, "q": pose.rotation.tolist(), "t": pose.translation.tolist()}
+            else:
+                st.flush()
+                op = {"op": "flush"}
+            s_ = st.stats
+            op["resident"] = [int(k) for k in st._keyframes]
+            op["stats"] = [s_.keyframe_loads, s_.keyframe_evictions, s_.keyframe_writes, s_.io_nanos,
+                           s_.bytes_read, s_.bytes_written, s_.active_keyframes]
+            ops.append(op)
+        st.flush()
+        files = {p.name: hashlib.sha256(p.read_bytes()).hexdigest()
+                 for p in sorted((Path(d) / "keyframes").glob("*.dkf"))}
+    (HERE / "keyframe_trace.json").write_text(json.dumps({"ops": ops, "files": files}))
+
+
 def make_select_trace():
     """KeyframeIndex / select_keyframe / record_loss policy trace (select.py)."""
     from splatmap import select, sim
@@ -603,6 +657,7 @@ if __name__ == "__main__":
     make_view_edits()
     make_sample()
     make_loopclose()
+    make_keyframe_trace()
     make_render_fd()
     for p in sorted(HERE.glob("*.npz")) + sorted(HERE.glob("*.json")):
         print(f"{p.name:24s} {p.stat().st_size:>9d} bytes")

@@ -451,3 +451,66 @@ def test_opt_state_reset_gives_fresh_adam(cuda, tmp_path):
     st.mark_trained([cid])   # the device rows moved on (what a training step does)
     with pytest.raises(NotResident):
         views[1].opacity = 0.5
+
+
+def test_keyframe_tier_trace_matches_reference(cuda, tmp_path):
+    """Keyframe tier (store.py:427-489) against the reference's own trace
+    (tests/golden/keyframe_trace.json): add / get / dirty / pose update /
+    flush under a budget of 3 -- LRU order, loads, evictions, write-backs,
+    io_ns and bytes after every op, and the flushed .dkf files byte for byte."""
+    import hashlib
+
+    from paper_2511_23030_b200.core import CameraIntrinsics, Keyframe, Pose
+    from paper_2511_23030_b200.store import ChunkStore, StoreConfig
+    rec = json.loads((GOLDEN / "keyframe_trace.json").read_text())
+    intr = CameraIntrinsics(fx=10.0, fy=10.0, cx=4.0, cy=3.0, width=8, height=6, near=0.1, far=50.0)
+    st = ChunkStore(StoreConfig(disk_root=tmp_path, keyframe_budget=3, io_ns_per_byte=1.0))
+    for k, op in enumerate(rec["ops"]):
+        if op["op"] == "add":
+            st.keyframe_add(Keyframe(id=op["id"], pose=Pose(rotation=op["q"], translation=op["t"]), intrinsics=intr,
+                                     rgb=np.array(op["rgb"]), depth=np.array(op["depth"], dtype=np.float32),
+                                     last_loss=op["loss"], usage_remaining=op["usage"]))
+        elif op["op"] == "get":
+            st.keyframe_get(op["id"])
+        elif op["op"] == "dirty":
+            st.mark_keyframe_dirty(op["id"])
+        elif op["op"] == "pose":
+            st.update_keyframe_pose(op["id"], Pose(rotation=op["q"], translation=op["t"]))
+        else:
+            st.flush()
+        s = st.stats
+        assert list(st._keyframes) == op["resident"], k
+        assert [s.keyframe_loads, s.keyframe_evictions, s.keyframe_writes, s.io_nanos, s.bytes_read,
+                s.bytes_written, s.active_keyframes] == op["stats"], (k, op["op"])
+    st.flush()
+    got = {p.name: hashlib.sha256(p.read_bytes()).hexdigest() for p in sorted((tmp_path / "keyframes").glob("*.dkf"))}
+    assert got == rec["files"]
+
+
+def test_keyframe_device_pack_byte_identical(cuda, tmp_path):
+    """The .dkf of an evicted keyframe assembled on the device from the HBM
+    keyframe tier (sm_keyframe_pack) equals diskformat.pack_keyframe, and
+    the write-behind path the store takes with it produces that file."""
+    from paper_2511_23030_b200 import diskformat
+    from paper_2511_23030_b200.workloads import build_c1
+    eng = build_c1(n=4000, keyframes=6, budget=100_000, store_dir=tmp_path / "s", keyframe_budget=3)
+    for s in range(6):
+        eng.optimization_step(0, s)
+    st = eng.store
+    kid = sorted(eng.device_keyframe_ids())[0]
+    kf = st.keyframe_get(kid)
+    kf.last_loss = 0.25
+    out = tmp_path / "probe.dkf"
+    assert eng._pack_device_keyframe(kid, kf, out)
+    st.streamer.drain()
+    assert out.read_bytes() == diskformat.pack_keyframe(kf)
+    writes0 = st.stats.keyframe_writes
+    for k in sorted(st.known_keyframe_ids()):   # cycle the tier: device-packed write-backs
+        st.keyframe_get(k)
+        st.mark_keyframe_dirty(k)
+        eng._device_keyframe(st.keyframe_get(k))
+    st.flush()
+    assert st.stats.keyframe_writes > writes0
+    for p in sorted((tmp_path / "s" / "keyframes").glob("*.dkf")):
+        k2 = diskformat.unpack_keyframe(p.read_bytes())
+        assert p.read_bytes() == diskformat.pack_keyframe(k2)
