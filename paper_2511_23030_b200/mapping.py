@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _lib
 from .core import CameraIntrinsics, Keyframe, Pose
-from .culling import ChunkExtent, CullConfig, VisibilityCache
+from .culling import ChunkExtent, CullConfig, VisibilityCache, visible_chunks
 from .errors import DeviceFailure, EmptyCandidates
 from .renderloss import LossEngine, LossWeights, RenderEngine, camera_for
 from .select import (KeyframeIndex, SelectConfig, candidate_set, draw_uniform, overlap, record_loss,
@@ -234,11 +234,13 @@ class MappingEngine:
 
     # -------------------------------------------------------------- inputs
     def add_keyframe(self, kf: Keyframe, index_usage: int | None = None) -> None:
-        """store.keyframe_add + index.add (sim.py:264-268), without ingestion."""
+        """store.keyframe_add + index.add (sim.py:264-268), without ingestion;
+        the new keyframe's on-disk chunks start streaming in right away."""
         self.store.keyframe_add(kf)
         self.index.add(kf.id, kf.position,
                        usage_remaining=self.index.config.initial_usage if index_usage is None else index_usage)
         self.latest_kf = kf.id
+        self._lookahead_prefetch()
 
     def render_current(self, pose: Pose):
         """sim._Replay._render_current (sim.py:255-262) on the device: the
@@ -445,10 +447,44 @@ class MappingEngine:
 
     def _run_while_gpu(self) -> None:
         """Host bookkeeping of the current step that does not need its loss
-        (store flags), run once while the device pass is in flight."""
+        (store flags, look-ahead prefetch), run once while the device pass is
+        in flight."""
         f, self._while_gpu = self._while_gpu, None
         if f is not None:
             f()
+            self._lookahead_prefetch()
+
+    prefetch_lookahead = True   # read the next draw's candidate views' chunks ahead of use
+
+    def _lookahead_prefetch(self) -> None:
+        """Speculative reads for the next step: every keyframe
+        the next draw can pick (the candidate set of the latest keyframe,
+        select.py:115-121) may need chunks that are on disk; their files are
+        read into pinned memory on the streamer's reader threads while the
+        device works.  No policy effect: the visibility sets come from the
+        cache without touching its LRU (or are computed without inserting)
+        and the store's residency is unchanged until ensure_resident."""
+        store = self.store
+        if not self.prefetch_lookahead or not store.has_disk_chunks() or self.latest_kf is None:
+            return
+        ext = store.coord_extent()
+        if ext is None:
+            return
+        try:
+            cands = candidate_set(self.index.position_of(self.latest_kf), self.index)
+        except EmptyCandidates:
+            cands = [self.latest_kf]
+        want: set[int] = set()
+        for c in cands:
+            kf = store._keyframes.get(c)
+            if kf is None:
+                continue
+            vis = self.cache.peek(kf.pose, self.intr, store.generation, store.chunk_size)
+            if vis is None:
+                vis = visible_chunks(kf.pose, self.intr, ChunkExtent(*ext), store.has_chunk, self.cull_cfg,
+                                     store.chunk_size, candidates=store.known_chunk_ids())
+            want |= set(vis)
+        store.prefetch(sorted(want))
 
     def _precompute_next_draw(self) -> None:
         """The next single-GPU step's uniform draw depends only on its derived

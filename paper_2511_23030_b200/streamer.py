@@ -69,13 +69,23 @@ class DeviceRecords:
 
 class ChunkStreamer:
     def __init__(self, slab, write_behind: bool = True, reader_threads: int = 4,
-                 writer_threads: int = 4, victim_bytes: int = 4 << 30):
+                 writer_threads: int = 4, victim_bytes: int = 4 << 30, device_pool_bytes: int | None = None):
+        """device_pool_bytes: a hard bound on the streamer's HBM (pack buffers
+        + victim cache + the load staging ring) for an HBM-capped store; the
+        pool is then never grown on demand -- a pack waits for a write-behind
+        to land instead.  None: the default 6 GB pool, grown if it runs dry."""
         import torch
         self.torch = torch
         self.slab = slab
+        self.device_pool_bytes = device_pool_bytes
+        if device_pool_bytes is not None:
+            # 4 load staging slots + the synchronous staging buffer stay inside the bound
+            self.DEVICE_SLOTS = max(2, int(device_pool_bytes) // self.PINNED_SLOT_BYTES - 5)
+            victim_bytes = min(victim_bytes, (self.DEVICE_SLOTS // 2) * self.PINNED_SLOT_BYTES)
         self.lib = _lib.load()
         self.copy_stream = torch.cuda.Stream(device=slab.device)   # H2D + validation of loads
         self.d2h_stream = torch.cuda.Stream(device=slab.device)    # write-behind D2H (own copy engine)
+        self.device_bytes = 0   # every device buffer this streamer allocated (pool, staging)
         self._dev = torch.empty(0, dtype=torch.uint8, device=slab.device)
         self._pin = torch.empty(0, dtype=torch.uint8, pin_memory=True)
         self._err = torch.empty(1, dtype=torch.int64, device=slab.device)
@@ -115,7 +125,9 @@ class ChunkStreamer:
     def _staging(self, nbytes: int):
         torch = self.torch
         if self._dev.numel() < nbytes:
+            self.device_bytes -= self._dev.numel()
             self._dev = torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, device=self.slab.device)
+            self.device_bytes += self._dev.numel()
         if self._pin.numel() < nbytes:
             self._pin = torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, pin_memory=True)
         return self._dev, self._pin
@@ -139,6 +151,7 @@ class ChunkStreamer:
                 for _ in range(self.PINNED_SLOTS)]
         devs = [torch.empty(self.PINNED_SLOT_BYTES, dtype=torch.uint8, device=self.slab.device)
                 for _ in range(self.DEVICE_SLOTS if self.write_behind else 0)]
+        self.device_bytes += sum(d.numel() for d in devs)
         with self._lock:
             self._free_pins.extend(bufs)
             self._free_devs.extend(devs)
@@ -183,17 +196,22 @@ class ChunkStreamer:
                 if best is not None:
                     return pool.pop(best)
                 left = deadline - time.perf_counter()
-                if not self._pending or left <= 0:
+                hard = not pinned and self.device_pool_bytes is not None
+                if not self._pending or (left <= 0 and not hard):
                     break
                 t0 = time.perf_counter()
-                self._freed.wait(timeout=left)   # a write landing returns its buffers
+                self._freed.wait(timeout=left if not hard else 1.0)   # a write landing returns its buffers
                 self.stats["pool_wait_s"] += time.perf_counter() - t0
+        if not pinned and self.device_pool_bytes is not None and nbytes <= self.PINNED_SLOT_BYTES:
+            from .errors import HbmCapExceeded
+            raise HbmCapExceeded("the streamer's device pool is exhausted under the HBM cap")
         size = -(-(nbytes + 4096) // self._QUANTUM) * self._QUANTUM
         t0 = time.perf_counter()
         if pinned:
             buf = torch.empty(size, dtype=torch.uint8, pin_memory=True)
         else:
             buf = torch.empty(size, dtype=torch.uint8, device=self.slab.device)
+            self.device_bytes += size
         with self._lock:
             self.stats["alloc_pinned" if pinned else "alloc_device"] += 1
             self.stats["alloc_s"] += time.perf_counter() - t0
@@ -282,7 +300,10 @@ class ChunkStreamer:
             slot["event"].synchronize()
             self.stats["stage_wait_s"] += time.perf_counter() - t0
         if slot["buf"] is None or slot["buf"].numel() < nbytes:
+            if slot["buf"] is not None:
+                self.device_bytes -= slot["buf"].numel()
             slot["buf"] = torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, device=self.slab.device)
+            self.device_bytes += slot["buf"].numel()
         return slot
 
     def unpack_into(self, src, records: np.ndarray | None, n: int, stride: int, offset: int) -> None:

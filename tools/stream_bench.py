@@ -12,7 +12,9 @@ Three runs of the identical trajectory:
 * resident  -- budget >= n: no paging at all (the compute-only reference),
 * sync      -- budget 1.5M, blocking reads and write-back,
 * streamed  -- budget 1.5M, write-behind eviction (copy stream + writer
-  thread) and prefetch of the newest keyframe's chunks on reader threads.
+  thread); the engine's own look-ahead prefetch (the newest keyframe's and
+  the next draw's candidate views' chunks, on reader threads) -- nothing is
+  prefetched by this harness.
 
 Prints one JSON line: steps/s of each run, paging volume, and
 overlap = t_resident / t_streamed (1.0 = streaming fully hidden).
@@ -59,6 +61,7 @@ def run(mode: str, scene, poses, frames, args):
     store.ensure_resident = timed_ensure
     store.streamer.warm()   # staging pools are allocated once, at startup
     eng = MappingEngine(store, C4_INTR, seed=7, cull=CullConfig(max_distance_m=args.max_distance))
+    eng.prefetch_lookahead = mode == "streamed"
     eng.use_graphs = not args.no_graphs
     st0 = store.stats
     loads0, ev0, wr0, rb0, wb0 = st0.chunk_loads, st0.chunk_evictions, st0.chunk_writes, st0.bytes_read, st0.bytes_written
@@ -70,10 +73,7 @@ def run(mode: str, scene, poses, frames, args):
     t0 = time.perf_counter()
     steps = 0
     for k, (pose, kf) in enumerate(zip(poses, kfs)):
-        eng.add_keyframe(kf)
-        if mode == "streamed":   # the newest keyframe's chunks are read while the current steps run
-            vis, _ = eng._visible_for_pose(pose)
-            store.prefetch(sorted(vis - store.resident_chunk_ids()))
+        eng.add_keyframe(kf)   # the engine itself prefetches (new keyframe, next draw's candidates)
         for s in range(args.steps):
             eng.optimization_step(k, s)
             steps += 1

@@ -73,6 +73,30 @@ def gt_frame(params, pose, intr, eng):
     return rgb.cpu().numpy(), depth.cpu().numpy()
 
 
+def disk_bandwidth(root: Path, nbytes: int = 2 << 30) -> dict:
+    """This box's disk, in the same job: sequential write with fsync, then a
+    read with the page cache dropped for the file (posix_fadvise DONTNEED)."""
+    import os
+    path = root / "_bw.bin"
+    buf = np.random.default_rng(0).integers(0, 255, 64 << 20, dtype=np.uint8).tobytes()
+    t0 = time.perf_counter()
+    with open(path, "wb", buffering=0) as f:
+        for _ in range(nbytes // len(buf)):
+            f.write(buf)
+        os.fsync(f.fileno())
+    w = time.perf_counter() - t0
+    fd = os.open(path, os.O_RDONLY)
+    os.posix_fadvise(fd, 0, 0, os.POSIX_FADV_DONTNEED)
+    os.close(fd)
+    t0 = time.perf_counter()
+    with open(path, "rb", buffering=0) as f:
+        while f.read(64 << 20):
+            pass
+    r = time.perf_counter() - t0
+    path.unlink()
+    return {"write_gbs": nbytes / w / 1e9, "read_gbs": nbytes / r / 1e9, "bytes": nbytes}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=100_000_000)
@@ -83,7 +107,7 @@ def main():
     ap.add_argument("--spacing", type=float, default=2.0)
     ap.add_argument("--keyframes", type=int, default=0, help="limit (default: the whole corridor)")
     ap.add_argument("--steps", type=int, default=8)
-    ap.add_argument("--resident-keyframes", type=int, default=100)
+    ap.add_argument("--resident-keyframes", type=int, default=0, help="limit (default: the same trajectory)")
     ap.add_argument("--max-distance", type=float, default=50.0)
     ap.add_argument("--out", default="")
     ap.add_argument("--profile", action="store_true", help="cProfile the streamed run (host hot spots)")
@@ -100,7 +124,8 @@ def main():
 
     device = torch.device("cuda")
     cap_bytes = int(args.cap_gb * (1 << 30))
-    cap_rows = cap_bytes // GaussianSlab.bytes_per_gaussian()
+    pool = min(6 << 30, cap_bytes // 8)   # the streamer's share of the cap (store.py)
+    cap_rows = (cap_bytes - pool) // GaussianSlab.bytes_per_gaussian()
     budget = args.budget or int(0.85 * cap_rows)
     n_kf = int(args.length / args.spacing)
     if args.keyframes:
@@ -113,8 +138,12 @@ def main():
     sl = Slices(args.n, args.length, args.slices, device)
     frames = [None] * n_kf
     eng_r = default_engine(device)
-    resident_scene = []   # slices covering the compute-only segment
-    seg_end = args.resident_keyframes * args.spacing + args.max_distance + 10.0
+    # the compute-only reference: the SAME scene and trajectory with every
+    # chunk resident (uncapped store, 100M x 436 B = 44 GB of HBM)
+    rroot = Path(tempfile.mkdtemp(prefix="c5_resident_"))
+    rstore = ChunkStore(StoreConfig(disk_root=rroot, chunk_size_m=10.0, gaussian_budget=args.n + 1,
+                                    keyframe_budget=400, io_ns_per_byte=1.0,
+                                    slab_capacity=int(args.n * 1.02) + 4096))
     next_pose = 0
     for i in range(args.slices):
         sc = sl.scene(i)
@@ -122,8 +151,7 @@ def main():
         store.flush()
         store.evict_lru(store.stats.active_gaussians, protected=set())
         store.flush()
-        if i * sl.len_s < seg_end:
-            resident_scene.append(sc)
+        rstore.insert_arrays(sc.positions, sc.rotations, sc.scales, sc.opacities, sc.sh)
         sl.add_target(i, sc)
         del sc
         # GT of every pose whose view window lies in the generated slices
@@ -143,18 +171,11 @@ def main():
     print(json.dumps({"built": True, "seconds": build_s, "chunks": len(store.known_chunk_ids()),
                       "disk_bytes": disk_bytes}), file=sys.stderr, flush=True)
 
-    # compute-only rate: the first keyframes with their chunks resident (uncapped store)
-    from paper_2511_23030_b200.synthetic import SceneData
-    rs = SceneData(*[np.concatenate([getattr(s, f) for s in resident_scene])
-                     for f in ("positions", "rotations", "scales", "opacities", "sh")])
-    del resident_scene
-    rroot = Path(tempfile.mkdtemp(prefix="c5_resident_"))
-    rstore = ChunkStore(StoreConfig(disk_root=rroot, chunk_size_m=10.0, gaussian_budget=len(rs) + 1,
-                                    keyframe_budget=400, io_ns_per_byte=1.0))
-    rstore.insert_arrays(rs.positions, rs.rotations, rs.scales, rs.opacities, rs.sh)
-    del rs
+    disk = disk_bandwidth(root)
+    print(json.dumps({"disk": disk}), file=sys.stderr, flush=True)
     res = {}
-    for mode, st, k in (("resident", rstore, min(args.resident_keyframes, n_kf)), ("streamed", store, n_kf)):
+    k_res = min(args.resident_keyframes, n_kf) if args.resident_keyframes else n_kf
+    for mode, st, k in (("resident", rstore, k_res), ("streamed", store, n_kf)):
         eng = MappingEngine(st, C4_INTR, seed=7, cull=CullConfig(max_distance_m=args.max_distance))
         blocked = [0.0]
         ensure = st.ensure_resident
@@ -184,10 +205,7 @@ def main():
         steps = 0
         for kf_i in range(k):
             pose = poses[kf_i]
-            eng.add_keyframe(kfs[kf_i])
-            if mode == "streamed":
-                vis, _ = eng._visible_for_pose(pose)
-                st.prefetch(sorted(vis - st.resident_chunk_ids()))
+            eng.add_keyframe(kfs[kf_i])   # the engine prefetches itself (look-ahead); no harness prefetch
             for s in range(args.steps):
                 eng.optimization_step(kf_i, s)
                 steps += 1
@@ -210,6 +228,7 @@ def main():
                      "keyframe_loads": d[6], "ensure_resident_s": blocked[0],
                      "mean_visible": eng.counter_gaussians / max(eng.counter_steps, 1),
                      "slab_bytes": st.slab.hbm_bytes(), "slab_compactions": st.slab.compactions,
+                     "hbm_bytes_store": st.slab.hbm_bytes() + st.streamer.device_bytes,
                      "graph_replays": eng.counter_replays, "eager_steps": eng.counter_eager}
         if st.streamer is not None:
             res[mode].update({f"streamer_{a}": b for a, b in st.streamer.stats.items()})
@@ -217,12 +236,16 @@ def main():
         st.flush()
         st.streamer.drain()
         del eng
-    line = {"workload": f"C5: {args.n} splats over {args.length:.0f} m (s = 10 m), 1241x376, HBM cap "
+    rs_, ss_ = res["resident"], res["streamed"]
+    floor_s = max(rs_["seconds"] * ss_["steps"] / max(rs_["steps"], 1),
+                  ss_["bytes_written"] / disk["write_gbs"] / 1e9)
+    line = {"disk": disk, "disk_floor_seconds": floor_s, "vs_disk_floor": floor_s / ss_["seconds"],
+            "workload": f"C5: {args.n} splats over {args.length:.0f} m (s = 10 m), 1241x376, HBM cap "
                         f"{args.cap_gb:g} GB ({cap_rows} slab rows), budget {budget}, {n_kf} keyframes x "
                         f"{args.steps} steps",
             "build_seconds": build_s, "disk_bytes": disk_bytes, "runs": res,
             "overlap": res["streamed"]["steps_per_s"] / res["resident"]["steps_per_s"],
-            "cap_held": res["streamed"]["slab_bytes"] <= cap_bytes}
+            "cap_held": res["streamed"]["hbm_bytes_store"] <= cap_bytes}
     print(json.dumps(line))
     if args.out:
         Path(args.out).write_text(json.dumps(line) + "\n")
