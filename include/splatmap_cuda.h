@@ -284,7 +284,9 @@ int sm_reset_rows(float *params, float *adam_m, float *adam_v, int64_t n, float 
 /* .dkf keyframe file (diskformat.py:198-216 pack_keyframe) assembled on the
  * device from the keyframe tier's HBM copy: header (host, 140 bytes, the
  * <4sIQ7d6dIIdI layout) | rgb_u8 (H,W,3) | depth f32 (H,W); out receives
- * 140 + 7 W H bytes (device).  Byte-identical to pack_keyframe. */
+ * 140 + 7 W H bytes (device memory, or pinned host memory: the write-behind
+ * has the kernel fill its pinned staging buffer directly).  Byte-identical
+ * to pack_keyframe. */
 int sm_keyframe_pack(const uint8_t *header /* host */, const uint8_t *rgb_u8, const float *depth,
                      int32_t width, int32_t height, uint8_t *out, void *stream);
 

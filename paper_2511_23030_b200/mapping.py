@@ -240,7 +240,7 @@ class MappingEngine:
         self.index.add(kf.id, kf.position,
                        usage_remaining=self.index.config.initial_usage if index_usage is None else index_usage)
         self.latest_kf = kf.id
-        self._lookahead_prefetch()
+        self._prefetch_view(kf.pose)
 
     def render_current(self, pose: Pose):
         """sim._Replay._render_current (sim.py:255-262) on the device: the
@@ -306,9 +306,9 @@ class MappingEngine:
         w, h = kf.intrinsics.width, kf.intrinsics.height
         lib = _lib.load()
 
-        def fill(dev):
+        def fill(pin):   # the kernel writes the file image straight into pinned host memory (UVA)
             _lib.check(lib.sm_keyframe_pack(head.ctypes.data_as(_lib.ctypes.c_void_p), _lib.ptr(d.rgb_u8),
-                                            _lib.ptr(d.depth), w, h, _lib.ptr(dev), _lib.stream_handle()),
+                                            _lib.ptr(d.depth), w, h, _lib.ptr(pin), _lib.stream_handle()),
                        "keyframe_pack")
         self.store.streamer.write_file_async(path, keyframe_file_size(kf), fill)
         return True
@@ -481,12 +481,24 @@ class MappingEngine:
             kf = store._keyframes.get(c)
             if kf is None:
                 continue
+            # only views the cache already knows (no cull on the step's host
+            # path); a new keyframe's view is computed once, in add_keyframe
             vis = self.cache.peek(kf.pose, self.intr, store.generation, store.chunk_size)
-            if vis is None:
-                vis = visible_chunks(kf.pose, self.intr, ChunkExtent(*ext), store.has_chunk, self.cull_cfg,
-                                     store.chunk_size, candidates=store.known_chunk_ids())
-            want |= set(vis)
-        store.prefetch(sorted(want))
+            if vis is not None:
+                want.update(vis)
+        if want:
+            store.prefetch(sorted(want))
+
+    def _prefetch_view(self, pose: Pose) -> None:
+        """A new keyframe's on-disk chunks start streaming in (one cull, no
+        visibility-cache insertion: no policy effect)."""
+        store = self.store
+        ext = store.coord_extent()
+        if not self.prefetch_lookahead or ext is None or not store.has_disk_chunks():
+            return
+        vis = visible_chunks(pose, self.intr, ChunkExtent(*ext), store.has_chunk, self.cull_cfg,
+                             store.chunk_size, candidates=store.known_chunk_ids())
+        store.prefetch(sorted(vis))
 
     def _precompute_next_draw(self) -> None:
         """The next single-GPU step's uniform draw depends only on its derived

@@ -418,22 +418,17 @@ class ChunkStreamer:
         self._queue.put(pw)
 
     def write_file_async(self, path: Path, nbytes: int, fill) -> None:
-        """Write-behind of a file assembled on the device: fill(dev) writes its
-        nbytes into a pooled device buffer on the current stream (e.g.
-        sm_keyframe_pack), the D2H runs on the copy stream, a writer thread
-        writes the file (no victim-cache entry: keyframes reload from disk)."""
+        """Write-behind of a file assembled by a kernel: fill(pin) writes its
+        nbytes into a pooled pinned buffer (device-addressable host memory)
+        on the current stream, e.g. sm_keyframe_pack; a writer thread writes
+        the file once that kernel completed.  Uses no device buffer."""
         self.check()
         torch = self.torch
-        dev = self._take(self._free_devs, max(nbytes, 1), pinned=False)
         pin = self._take(self._free_pins, max(nbytes, 1), pinned=True)
-        fill(dev)
-        cur = torch.cuda.current_stream(self.slab.device)
-        self.d2h_stream.wait_stream(cur)
+        fill(pin)
         ev = torch.cuda.Event()
-        with torch.cuda.stream(self.d2h_stream):
-            pin[:nbytes].copy_(dev[:nbytes], non_blocking=True)
-            ev.record(self.d2h_stream)
-        pw = _PendingWrite(Path(path), b"", pin, nbytes, ev, dev, 0, cache=False)
+        ev.record(torch.cuda.current_stream(self.slab.device))
+        pw = _PendingWrite(Path(path), b"", pin, nbytes, ev, None, 0, cache=False)
         with self._lock:
             self._release_superseded(self._pending.get(pw.path))
             self._pending[pw.path] = pw

@@ -275,8 +275,11 @@ def test_hbm_cap_compaction_bit_exact(cuda, tmp_path):
     # the reference policy loads a working set before it evicts down to the
     # budget: the cap must hold budget + working set (+ segment slack)
     cap_rows = 5_200
+    # the cap also covers the streamer's device buffers (1/8 of it, store.py)
+    cap_bytes = -(-cap_rows * GaussianSlab.bytes_per_gaussian() * 8 // 7)
+    cap_rows = (cap_bytes - cap_bytes // 8) // GaussianSlab.bytes_per_gaussian()
     stores = []
-    for name, cap in (("free", None), ("capped", cap_rows * GaussianSlab.bytes_per_gaussian())):
+    for name, cap in (("free", None), ("capped", cap_bytes)):
         st = ChunkStore(StoreConfig(disk_root=tmp_path / name, chunk_size_m=5.0, gaussian_budget=2_500,
                                     io_ns_per_byte=1.0, hbm_cap_bytes=cap))
         for idx in slices:
