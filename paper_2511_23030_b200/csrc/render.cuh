@@ -94,7 +94,7 @@ struct RenderLayout {
     int64_t o_counters, o_rec, o_rec_sorted, o_p64, o_dkey0, o_dkey1, o_order0, o_order1;
     int64_t o_tcount, o_tcount_r, o_tmask, o_tmask_r, o_toff, o_ikey0, o_ikey1, o_ranges;
     int64_t o_pix_cd, o_pix_t, o_pix_tlast, o_pix_last, o_g2d, o_sort_hist, o_scan;
-    int64_t o_gbuf, o_tile_hor, o_tile_work, o_tile_order, o_band_work, o_warp_last;
+    int64_t o_gbuf, o_tile_hor, o_tile_work, o_tile_order, o_band_work;
     int64_t total;
 };
 
@@ -117,7 +117,6 @@ struct RenderBufs {
     uint32_t *tile_work;    // per-tile instances the forward composited (the forward's view order)
     uint32_t *band_work;    // per-band instances the backward revisits [n_tiles][4]
     uint32_t *tile_order;   // bands by descending work: the backward's launch order [n_tiles * 4]
-    int32_t *warp_last;     // the forward warps' last contributors [n_tiles][8]
 };
 
 inline RenderBufs render_bufs(void *ws, const RenderLayout &L) {
@@ -151,7 +150,6 @@ inline RenderBufs render_bufs(void *ws, const RenderLayout &L) {
     r.tile_work = reinterpret_cast<uint32_t *>(b + L.o_tile_work);
     r.tile_order = reinterpret_cast<uint32_t *>(b + L.o_tile_order);
     r.band_work = reinterpret_cast<uint32_t *>(b + L.o_band_work);
-    r.warp_last = reinterpret_cast<int32_t *>(b + L.o_warp_last);
     return r;
 }
 

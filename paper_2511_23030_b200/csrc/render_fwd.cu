@@ -75,7 +75,6 @@ RenderLayout render_layout(const sm_render_dims &d) {
     L.o_tile_work = take(L.n_tiles * 4);
     L.o_tile_order = take(L.n_tiles * kBands * 4);
     L.o_band_work = take(L.n_tiles * kBands * 4);
-    L.o_warp_last = take(L.n_tiles * (kTile / 2) * 4);
     L.total = off;
     return L;
 }
@@ -460,93 +459,6 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
     }
 }
 
-// The same compositing with one independent 32-thread CTA per warp row pair
-// of a tile (8 per tile, lane l = column l % 16, row 2w + l / 16): each
-// warp stages its own 32-record chunks (from L2) and stops as soon as its
-// own 32 pixels are saturated -- no block barriers, no warp waiting for the
-// slowest pixel of its tile.  Writes each warp's last contributor to
-// warp_last[tile * 8 + w]; band_tile_work() turns those into the schedules.
-constexpr int kFwdWarps = kTile / 2;
-template <typename KeyT>
-__global__ void __launch_bounds__(32)
-composite_fwd_warps(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikeys,
-                    KeyT rank_mask, const ProjRec *__restrict__ recs,
-                    const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
-                    int height, int tiles_x, float *__restrict__ out_rgb, float *__restrict__ out_depth,
-                    float *__restrict__ out_alpha, float4 *__restrict__ st_cd, float *__restrict__ st_t,
-                    float *__restrict__ st_tlast, int32_t *__restrict__ st_last, int32_t *__restrict__ warp_last,
-                    const uint32_t *__restrict__ launch_order) {
-    __shared__ ProjRec s_rec[32];
-    __shared__ int4 s_box[32];
-    __shared__ uint32_t s_rank[32];
-    const int lane = threadIdx.x;
-    const int w = (int)(blockIdx.x % kFwdWarps);
-    // longest-first when the caller keeps the previous render's order of this view
-    const int tile = launch_order ? (int)launch_order[blockIdx.x / kFwdWarps] : (int)(blockIdx.x / kFwdWarps);
-    const int wy0 = (tile / tiles_x) * kTile + 2 * w;   // the warp's first row
-    const int px = (tile % tiles_x) * kTile + (lane & (kTile - 1));
-    const int py = wy0 + lane / kTile;
-    const uint32_t start = ranges[2 * tile], end = ranges[2 * tile + 1];
-    const bool in = px < width && py < height;
-    FwdPix s = FwdPix{1.f, 0.f, 0.f, 0.f, 0.f, 1.f, -1, !in};
-    for (uint32_t base = start; base < end; base += 32) {
-        if (__all_sync(0xffffffffu, s.done)) break;
-        const int cnt = (int)min(32u, end - base);
-        if (lane < cnt) {
-            const uint32_t rk = (uint32_t)(ikeys[base + lane] & rank_mask);
-            s_rank[lane] = rk;
-            const ProjRec r = recs[rk];
-            s_rec[lane] = r;
-            s_box[lane] = make_int4(rec_x0(r), rec_x1(r) - rec_x0(r), rec_y0(r), rec_y1(r) - rec_y0(r));
-        }
-        __syncwarp();
-        if (!s.done) {
-            for (int j = 0; j < cnt; j++) {
-                const int4 bx = s_box[j];   // x0, x1 - x0, y0, y1 - y0 (decoded once at staging)
-                if (bx.z + bx.w < wy0 || bx.z > wy0 + 1) continue;   // warp-uniform row cull
-                if ((unsigned)(px - bx.x) > (unsigned)bx.y || (unsigned)(py - bx.z) > (unsigned)bx.w) continue;
-                const ProjRec &g = s_rec[j];
-                const float dx = (float)(px - bx.x) + g.ox;
-                const float dy = (float)(py - bx.z) + g.oy;
-                const float pw = dx * (g.ia * dx + 2.f * g.ib * dy) + g.ic * dy * dy;
-                if (q_within_cutoff(pw, g.eps, p64, order, s_rank[j], px, py)) {
-                    s.add(g, pw, (int32_t)(base + j));
-                    if (s.done) break;
-                }
-            }
-        }
-        __syncwarp();
-    }
-    if (in)
-        s.store((int64_t)py * width + px, out_rgb, out_depth, out_alpha, st_cd, st_t, st_tlast, st_last);
-    const int wl = __reduce_max_sync(0xffffffffu, s.last);
-    if (lane == 0) warp_last[tile * kFwdWarps + w] = wl;
-}
-
-// Per band (backward schedule) and per tile (next forward of the view) work
-// from the warps' last contributors: band b = warps 2b, 2b + 1; work =
-// instances revisited, [start, max last].  Also sums the tile horizons.
-__global__ void __launch_bounds__(256)
-band_tile_work(const int32_t *__restrict__ warp_last, const uint32_t *__restrict__ ranges, int n_tiles,
-               uint32_t *__restrict__ band_work, uint32_t *__restrict__ tile_work, sm_render_counters *ctr) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t w = 0;
-    if (t < n_tiles) {
-        const int start = (int)ranges[2 * t];
-        int ml = -1;
-#pragma unroll
-        for (int b = 0; b < kBands; b++) {
-            const int bl = max(warp_last[t * kFwdWarps + 2 * b], warp_last[t * kFwdWarps + 2 * b + 1]);
-            band_work[t * kBands + b] = bl >= start ? (uint32_t)(bl - start + 1) : 0u;
-            ml = max(ml, bl);
-        }
-        w = ml >= start ? (uint32_t)(ml - start + 1) : 0u;
-        tile_work[t] = w;
-    }
-    const uint32_t sum = __reduce_add_sync(0xffffffffu, w);
-    if ((threadIdx.x & 31) == 0 && sum) atomicAdd(&ctr->reserved[3], sum);
-}
-
 // Longest-first launch order of the tiles for the backward: a counting sort
 // of the tiles into 64 work buckets, heaviest bucket first (one block).  The
 // backward's CTAs then start heavy tiles first and light ones fill in behind
@@ -648,22 +560,10 @@ static void launch_composite_fwd(const RenderBufs &b, const RenderLayout &L, con
                                  cudaStream_t st) {
     const KeyT rank_mask = (KeyT)((1ull << L.rank_bits) - 1ull);
     const KeyT *ik = static_cast<const KeyT *>(L.tile_passes & 1 ? b.ikey1 : b.ikey0);
-#ifndef SM_FWD_WARPS
-#define SM_FWD_WARPS 1   // 0: one 256-thread CTA per tile (A/B)
-#endif
-    if (SM_FWD_WARPS) {
-        int32_t *warp_last = b.warp_last;
-        composite_fwd_warps<KeyT><<<(unsigned)(L.n_tiles * kFwdWarps), 32, 0, st>>>(
-            b.ranges, ik, rank_mask, b.rec_sorted, b.p64, b.order0, dims.width, dims.height, L.tiles_x,
-            out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, warp_last, view_order);
-        band_tile_work<<<(unsigned)ceil_div(L.n_tiles, 256), 256, 0, st>>>(warp_last, b.ranges, (int)L.n_tiles,
-                                                                          b.band_work, b.tile_work, b.ctr);
-    } else {
-        composite_fwd<KeyT><<<(unsigned)L.n_tiles, kTilePx, 0, st>>>(
-            b.ranges, ik, rank_mask, b.rec_sorted, b.p64, b.order0, dims.width, dims.height, L.tiles_x,
-            out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, b.tile_work, b.band_work,
-            view_order, b.ctr);
-    }
+    composite_fwd<KeyT><<<(unsigned)L.n_tiles, kTilePx, 0, st>>>(
+        b.ranges, ik, rank_mask, b.rec_sorted, b.p64, b.order0, dims.width, dims.height, L.tiles_x,
+        out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, b.tile_work, b.band_work,
+        view_order, b.ctr);
     // the backward's band order; the next forward of this view gets the tile order
     order_tiles<<<1, 1024, 0, st>>>(b.band_work, (int)(L.n_tiles * kBands), b.tile_order, nullptr);
     if (view_order) order_tiles<<<1, 1024, 0, st>>>(b.tile_work, (int)L.n_tiles, nullptr, view_order);
@@ -727,7 +627,7 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
     else
         launch_composite_fwd<uint32_t>(b, L, dims, out_rgb, out_depth, out_alpha, view_order, st);
     prof_end(ST_COMPOSITE_FWD, st);
-    count_launches((view_order ? 3 : 2) + (SM_FWD_WARPS ? 1 : 0));
+    count_launches(view_order ? 3 : 2);
     SM_CHECK_LAUNCH("render_forward");
     return SM_OK;
 }
