@@ -98,20 +98,18 @@ class ClockSampler:
 # Algorithmic bytes per unit of each stage.
 #   n = visible Gaussians, i = tile instances, p = pixels
 # Algorithmic bytes per step and stage (n visible Gaussians, i tile instances,
-# p pixels, v instances the forward composites = the tile horizons' sum, vb
-# (instance, band) pairs the backward revisits):
+# p pixels, v instances the compositing revisits = the backward's horizon sum):
 STAGE_BYTES = {
-    "project_fwd": lambda n, i, p, v, vb: n * (4 + 64 + 64 + 40 + 8 + 4 + 4),
-    "depth_sort": lambda n, i, p, v, vb: n * 8 * 4 * 2 + n * 8,
-    "bin_emit": lambda n, i, p, v, vb: n * (4 + 4 + 64 + 64 + 4 * 4) + i * 4,
-    "tile_sort": lambda n, i, p, v, vb: i * 2 * 12 + i * 8,
-    "composite_fwd": lambda n, i, p, v, vb: v * (4 + 64) + p * (20 + 28),
-    "loss": lambda n, i, p, v, vb: p * (16 + 7 + 36 * 2 + 16),
-    # per (instance, band) revisit: key + record + emission slot + 40-B partial
-    "composite_bwd": lambda n, i, p, v, vb: vb * (4 + 64 + 4 + 40) + p * (28 + 16),
-    "project_bwd": lambda n, i, p, v, vb: n * (4 + 4 + 4 + 64 + 40 + 2 * 64),
-    "adam": lambda n, i, p, v, vb: n * (4 + 7 * 64),
-    "grad_gather": lambda n, i, p, v, vb: n * (4 + 4 + 64 + 48) + vb * (40 + 4),
+    "project_fwd": lambda n, i, p, v: n * (4 + 64 + 64 + 40 + 8 + 4 + 4),
+    "depth_sort": lambda n, i, p, v: n * 8 * 4 * 2 + n * 8,
+    "bin_emit": lambda n, i, p, v: n * (4 + 4 + 64 + 64 + 4 * 4) + i * 4,
+    "tile_sort": lambda n, i, p, v: i * 2 * 12 + i * 8,
+    "composite_fwd": lambda n, i, p, v: v * (4 + 64) + p * (20 + 28),
+    "loss": lambda n, i, p, v: p * (16 + 7 + 36 * 2 + 16),
+    "composite_bwd": lambda n, i, p, v: v * (4 + 64 + 48) + p * (28 + 16),
+    "project_bwd": lambda n, i, p, v: n * (4 + 4 + 4 + 64 + 40 + 2 * 64),
+    "adam": lambda n, i, p, v: n * (4 + 7 * 64),
+    "grad_gather": lambda n, i, p, v: n * (4 + 4 + 64 + 48) + v * (48 + 4),
 }
 NCU_SUMMARY = Path(__file__).resolve().parent / "profiles" / "r01_ncu_full.json"
 
@@ -342,7 +340,6 @@ def main():
     n_vis = eng.counter_gaussians / max(eng.counter_steps, 1)
     n_inst = eng.counter_instances / max(eng.counter_steps, 1)
     n_visit = eng.counter_visited / max(eng.counter_steps, 1)
-    n_band = eng.counter_band_visits / max(eng.counter_steps, 1)
     gauss_s = eng.counter_gaussians * world / (ms / 1e3)
     c3_g1 = None
     if rank == 0 and world == 1 and not c3:
@@ -392,7 +389,7 @@ def main():
     if dom:
         per_launch_ms = prof[dom][0] / prof[dom][1]
         launches_per_step = prof[dom][1] / args.steps
-        byt = STAGE_BYTES.get(dom, lambda *a: 0)(n_vis, n_inst, px, n_visit, n_band) / max(launches_per_step, 1)
+        byt = STAGE_BYTES.get(dom, lambda *a: 0)(n_vis, n_inst, px, n_visit) / max(launches_per_step, 1)
         achieved = byt / (per_launch_ms / 1e3) / 1e9
         nk = _ncu_kernel(dom)
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"],
@@ -409,7 +406,7 @@ def main():
         for k, v in stages.items():
             f = STAGE_BYTES.get(k)
             if f and v["calls"]:
-                b = f(n_vis, n_inst, px, n_visit, n_band) / (v["calls"] / args.steps)
+                b = f(n_vis, n_inst, px, n_visit) / (v["calls"] / args.steps)
                 v["gbs"] = b / (v["ms_per_step"] / (v["calls"] / args.steps) / 1e3) / 1e9
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -423,7 +420,7 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(args),
         "measured": {"visible_gaussians_per_step": n_vis, "tile_instances_per_step": n_inst,
-                     "revisited_instances_per_step": n_visit, "band_revisits_per_step": n_band},
+                     "revisited_instances_per_step": n_visit},
         "kf_sequence": kf_seq,
         "gaussians_per_s": gauss_s,
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clk, "roofline": roof,

@@ -69,9 +69,7 @@ typedef struct sm_render_counters {
     uint32_t n_visible;      /* Gaussians with >= 1 tile                     */
     uint32_t n_fallback;     /* not maintained (reserved)                    */
     uint32_t reserved[12];   /* [0] sort count, [1] big-splat queue length,
-                              * [2] (instance, band) pairs the last backward
-                              * revisited, [3] instances the last forward
-                              * composited (sum of the tile horizons)      */
+                              * [2] instances the last backward revisited    */
 } sm_render_counters;
 
 typedef struct sm_adam_config {

@@ -5,20 +5,6 @@
 namespace sm {
 
 constexpr int kG2dStride = 12;   // per-rank 2D grads: u v ia ib ic op r g b z - -
-// The backward works on bands of a tile: 4 bands of 4 pixel rows, one warp
-// each (an independent 32-thread CTA).  Every (instance, band) pair whose
-// box rows meet the band's rows gets its own 10-value partial gradient in the
-// instance's emission slot: gbuf[slot][band][10].
-constexpr int kBands = 4;
-constexpr int kBandRows = kTile / kBands;
-constexpr int kPartStride = kBands * 10;
-
-// The one predicate the backward (writer) and the gradient gathers (readers)
-// share: does a splat's clamped box [y0, y1] reach band b of tile row ty?
-__device__ __forceinline__ bool band_meets(int y0, int y1, int ty, int b) {
-    const int by0 = ty * kTile + b * kBandRows;
-    return y0 <= by0 + kBandRows - 1 && y1 >= by0;
-}
 constexpr uint32_t kEmitSmall = 32;   // splats with more box tiles are emitted / gathered per warp
 
 // Tiles of the 3-sigma box.  The small / big split is taken on this count, not
@@ -94,7 +80,7 @@ struct RenderLayout {
     int64_t o_counters, o_rec, o_rec_sorted, o_p64, o_dkey0, o_dkey1, o_order0, o_order1;
     int64_t o_tcount, o_tcount_r, o_tmask, o_tmask_r, o_toff, o_ikey0, o_ikey1, o_ranges;
     int64_t o_pix_cd, o_pix_t, o_pix_tlast, o_pix_last, o_g2d, o_sort_hist, o_scan;
-    int64_t o_gbuf, o_tile_hor, o_tile_work, o_tile_order, o_band_work;
+    int64_t o_gbuf, o_tile_hor, o_tile_work, o_tile_order;
     int64_t total;
 };
 
@@ -112,11 +98,10 @@ struct RenderBufs {
     int32_t *pix_last;
     float *g2d;
     uint32_t *sort_hist, *scan;
-    float *gbuf;         // per-instance, per-band partial gradients [max_instances][4][10] (backward)
-    int32_t *tile_hor;   // per-band horizon rank [n_tiles][4] (backward)
-    uint32_t *tile_work;    // per-tile instances the forward composited (the forward's view order)
-    uint32_t *band_work;    // per-band instances the backward revisits [n_tiles][4]
-    uint32_t *tile_order;   // bands by descending work: the backward's launch order [n_tiles * 4]
+    float *gbuf;         // per-instance gradient slots [max_instances][12] (backward)
+    int32_t *tile_hor;   // per-tile horizon rank (backward)
+    uint32_t *tile_work;    // per-tile instances the forward composited (backward's work)
+    uint32_t *tile_order;   // tiles by descending work: the backward's launch order
 };
 
 inline RenderBufs render_bufs(void *ws, const RenderLayout &L) {
@@ -149,7 +134,6 @@ inline RenderBufs render_bufs(void *ws, const RenderLayout &L) {
     r.tile_hor = reinterpret_cast<int32_t *>(b + L.o_tile_hor);
     r.tile_work = reinterpret_cast<uint32_t *>(b + L.o_tile_work);
     r.tile_order = reinterpret_cast<uint32_t *>(b + L.o_tile_order);
-    r.band_work = reinterpret_cast<uint32_t *>(b + L.o_band_work);
     return r;
 }
 

@@ -159,30 +159,26 @@ struct BwdPair {
     }
 };
 
-// One 32-thread CTA per (tile, band): band b of a 16x16 tile is its pixel
-// rows 4b .. 4b + 3, and lane l owns the pixel pair (column l % 16, rows
-// 4b + 2 (l / 16) and + 1), walked back in packed fp32x2 (BwdPair).  The band
-// revisits its tile's instances from its own last contributor back to the
-// tile start, 32 at a time: each lane stages one record (64 B, from L2) and
-// the instance's emission slot in the warp's shared memory, then the warp
-// steps through them back to front.  An instance whose box rows miss the
-// band is skipped (the gather applies the same band_meets predicate); one
-// that reaches the band gets the band's 10-value sum (a transposed warp
-// butterfly) in its partial slot gbuf[slot][band] -- zeros when no pixel of
-// the band passes the q <= 9 / T cutoffs.  No block barriers, no shared
-// partials to clear: bands advance independently and a light band of a
-// heavy tile finishes early (bands are launched longest-first).
+// Same tiling as composite_fwd: one CTA per 16x16 tile, 128 threads, each
+// owning a pixel pair (BwdPair); warp w covers tile rows 4w .. 4w + 3.
+// Instances are revisited from the block's last contributor back to the tile
+// start, one CTA-width batch at a time; a warp skips splats missing its rows,
+// lying past every one of its pixels' last contributor, or reaching none of
+// its pixels.
 //
-// Determinism: no floating-point atomics; a splat's gradient is the fixed-
-// order sum over its instances (emission order) and bands (0..3) in the
-// gather: reruns and CUDA-graph replays are bit-identical (the reference's
-// metrics determinism contract, test_acceptance.py criterion 10).
+// Determinism: no floating-point atomics.  Each warp's 10 sums for an
+// instance land in its own shared slot; after the batch the slots are added
+// in warp order and written to the instance's emission slot (toff[rank] + the
+// tile's index among the splat's kept tiles); grad_gather then sums a splat's
+// instances in a fixed order.  Reruns and CUDA-graph replays are bit-identical
+// (the reference's metrics determinism contract, test_acceptance.py crit. 10).
+constexpr int kBwdThreads = kTilePx / 2;
 #ifndef SM_BWD_MINB
-#define SM_BWD_MINB 20   // 20 warps per SM (<= 102 registers)
+#define SM_BWD_MINB 5   // 5 CTAs x 4 warps per SM: measured best (register cap 102)
 #endif
 
 template <typename KeyT>
-__global__ void __launch_bounds__(32, SM_BWD_MINB)
+__global__ void __launch_bounds__(kBwdThreads, SM_BWD_MINB)
 composite_bwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikeys,
               KeyT rank_mask, const ProjRec *__restrict__ recs,
               const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
@@ -191,61 +187,62 @@ composite_bwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
               const float4 *__restrict__ st_cd, const float *__restrict__ st_t,
               const float *__restrict__ st_tlast, const int32_t *__restrict__ st_last,
               const uint32_t *__restrict__ toff, const uint32_t *__restrict__ tmask_r,
-              float *__restrict__ gbuf, int32_t *__restrict__ band_hor, sm_render_counters *ctr,
-              const uint32_t *__restrict__ band_order) {
-    __shared__ ProjRec s_rec[32];
-    __shared__ uint32_t s_rank[32], s_slot[32];
-    __shared__ float s_out[32][10];
-    const int lane = threadIdx.x;
-    const int band_id = (int)band_order[blockIdx.x];   // heaviest bands first
-    const int tile = band_id / kBands, band = band_id % kBands;
-    const int tile_x = tile % tiles_x, tile_y = tile / tiles_x;
-    const int wy0 = tile_y * kTile + band * kBandRows;   // the band's first row
-    const int px = tile_x * kTile + (lane & (kTile - 1));
-    const int py = wy0 + 2 * (lane / kTile);
+              float *__restrict__ gbuf, int32_t *__restrict__ tile_hor, sm_render_counters *ctr,
+              const uint32_t *__restrict__ tile_order) {
+    constexpr int NT = kBwdThreads;
+    constexpr int NW = NT / 32;
+    __shared__ ProjRec s_rec[NT];
+    __shared__ uint32_t s_rank[NT];
+    __shared__ float s_part[NW][NT][10];
+    __shared__ int s_maxlast;
+    const int warp = threadIdx.x / 32;
+    const int tile = (int)tile_order[blockIdx.x];   // heaviest tiles first
+    const int lane = threadIdx.x & 31;
+    const int ty0 = (tile / tiles_x) * kTile;
+    const int px = (tile % tiles_x) * kTile + (threadIdx.x & (kTile - 1));
+    const int py = ty0 + 2 * (threadIdx.x / kTile);
+    const int wy0 = ty0 + 4 * (threadIdx.x / 32);
     const int start = (int)ranges[2 * tile];
     BwdPair pp;
     {
-        BwdPix a, c;
+        BwdPix a, b;
         a.init(px < width && py < height, (int64_t)py * width + px, d_rgb, d_depth, d_alpha, st_cd,
                st_t, st_tlast, st_last);
-        c.init(px < width && py + 1 < height, (int64_t)(py + 1) * width + px, d_rgb, d_depth, d_alpha,
+        b.init(px < width && py + 1 < height, (int64_t)(py + 1) * width + px, d_rgb, d_depth, d_alpha,
                st_cd, st_t, st_tlast, st_last);
-        pp.init(a, c);
+        pp.init(a, b);
     }
-    const int wmax = __reduce_max_sync(0xffffffffu, max(pp.last0, pp.last1));
-    if (lane == 0) {   // rank of the band's last visited instance (the gathers' horizon)
-        band_hor[band_id] = wmax >= start ? (int32_t)(uint32_t)(ikeys[wmax] & rank_mask) : -1;
-        if (wmax >= start) atomicAdd(&ctr->reserved[2], (uint32_t)(wmax - start + 1));
+    int wmax = max(pp.last0, pp.last1);
+    if (threadIdx.x == 0) s_maxlast = -1;
+    __syncthreads();
+#pragma unroll
+    for (int o = 16; o; o >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    if (lane == 0) atomicMax(&s_maxlast, wmax);
+    __syncthreads();
+    const int maxlast = s_maxlast;
+    if (threadIdx.x == 0) {   // rank of the tile's last visited instance (grad_gather's horizon)
+        tile_hor[tile] = maxlast >= start ? (int32_t)(uint32_t)(ikeys[maxlast] & rank_mask) : -1;
+        if (maxlast >= start) atomicAdd(&ctr->reserved[2], (uint32_t)(maxlast - start + 1));
     }
     const int via = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);   // 0..7
     const int vib = 8 + ((lane >> 4) & 1);                                                // 8..9
-    for (int cend = wmax + 1; cend > start; cend -= 32) {
-        const int cstart = max(start, cend - 32);
-        const int cnt = cend - cstart;
-        if (lane < cnt) {   // stage one record + its emission slot per lane
-            const uint32_t rk = (uint32_t)(ikeys[cstart + lane] & rank_mask);
-            const ProjRec g = recs[rk];
-            s_rec[lane] = g;
-            s_rank[lane] = rk;
-            uint32_t kept;   // the tile's index among the splat's kept tiles
-            if (bbox_tiles(g) <= kEmitSmall) {
-                const int tx0 = rec_x0(g) / kTile, ty0r = rec_y0(g) / kTile;
-                const int bit = (tile_y - ty0r) * (rec_x1(g) / kTile - tx0 + 1) + tile_x - tx0;
-                kept = (uint32_t)__popc(tmask_r[rk] & ((1u << bit) - 1u));
-            } else {
-                kept = band_meets(rec_y0(g), rec_y1(g), tile_y, band) ? RowSpan(g).kept_index(tile_x, tile_y) : 0u;
-            }
-            s_slot[lane] = toff[rk] + kept;
+    const int tile_x = tile % tiles_x, tile_y = tile / tiles_x;
+    for (int bend = maxlast + 1; bend > start; bend -= NT) {
+        const int bstart = max(start, bend - NT);
+        const int idx = bstart + (int)threadIdx.x;
+        if (idx < bend) {
+            const uint32_t rk = (uint32_t)(ikeys[idx] & rank_mask);
+            s_rank[threadIdx.x] = rk;
+            s_rec[threadIdx.x] = recs[rk];
         }
-        __syncwarp();
-        uint32_t rowm = 0, hitm = 0;   // warp-uniform: band reached / some pixel passed
-        for (int j = cnt - 1; j >= 0; j--) {
+        for (int i = threadIdx.x; i < NW * NT * 10; i += NT) (&s_part[0][0][0])[i] = 0.f;
+        __syncthreads();
+        const int jtop = min(bend - 1, wmax) - bstart;
+        for (int j = jtop; j >= 0; j--) {
             const ProjRec &g = s_rec[j];
             const int y0 = rec_y0(g), y1 = rec_y1(g);
-            if (y1 < wy0 || y0 > wy0 + kBandRows - 1) continue;   // = !band_meets: no partial
-            rowm |= 1u << j;
-            const int k = cstart + j;
+            if (y1 < wy0 || y0 > wy0 + 3) continue;   // warp-uniform row cull
+            const int k = bstart + j;
             const int x0 = rec_x0(g);
             // both rows at once; the same q <= 9 decisions as the forward
             // (q_within_cutoff: an fp32 q outside the error band decides alike)
@@ -264,58 +261,58 @@ composite_bwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
                 h1 = h1 && d.y >= 0.f;
             }
             if (!__any_sync(0xffffffffu, h0 || h1)) continue;
-            hitm |= 1u << j;
             float v[16];
             pp.step(g, dx, dy, pw, h0, h1, k, v);
-            const float2 sv = transpose_reduce10(v, lane);
-            if (!(lane & 3)) s_out[j][via] = sv.x;
-            if (!(lane & 15)) s_out[j][vib] = sv.y;
+            const float2 s = transpose_reduce10(v, lane);
+            if (!(lane & 3)) s_part[warp][j][via] = s.x;
+            if (!(lane & 15)) s_part[warp][j][vib] = s.y;
         }
-        __syncwarp();
-        if (lane < cnt && ((rowm >> lane) & 1u)) {   // lane j writes instance j's partial
-            float2 *dst = reinterpret_cast<float2 *>(gbuf + (int64_t)s_slot[lane] * kPartStride + band * 10);
-            if ((hitm >> lane) & 1u) {
-#pragma unroll
-                for (int q = 0; q < 5; q++) dst[q] = make_float2(s_out[lane][2 * q], s_out[lane][2 * q + 1]);
+        __syncthreads();
+        if (idx < bend) {   // warp-ordered sum -> the instance's emission slot
+            const ProjRec &g = s_rec[threadIdx.x];
+            const uint32_t rk = s_rank[threadIdx.x];
+            uint32_t kept;   // the tile's index among the splat's kept tiles
+            if (bbox_tiles(g) <= kEmitSmall) {
+                const int tx0 = rec_x0(g) / kTile, ty0r = rec_y0(g) / kTile;
+                const int bit = (tile_y - ty0r) * (rec_x1(g) / kTile - tx0 + 1) + tile_x - tx0;
+                kept = (uint32_t)__popc(tmask_r[rk] & ((1u << bit) - 1u));
             } else {
-#pragma unroll
-                for (int q = 0; q < 5; q++) dst[q] = make_float2(0.f, 0.f);
+                kept = RowSpan(g).kept_index(tile_x, tile_y);
             }
+            const uint32_t slot = toff[rk] + kept;
+            float acc[10];
+#pragma unroll
+            for (int k = 0; k < 10; k++) {
+                float a = 0.f;
+#pragma unroll
+                for (int w = 0; w < NW; w++) a += s_part[w][threadIdx.x][k];
+                acc[k] = a;
+            }
+            float4 *dst = reinterpret_cast<float4 *>(gbuf + (int64_t)slot * kG2dStride);
+            dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+            dst[2] = make_float4(acc[8], acc[9], 0.f, 0.f);
         }
-        __syncwarp();
+        __syncthreads();
     }
 }
 
-// One instance's band partials, added in band order: band b counts when the
-// splat's box rows meet it and the band revisited the instance (rank <=
-// its horizon) -- exactly the pairs composite_bwd wrote.
-__device__ __forceinline__ void add_instance(const float *gbuf, uint32_t slot, int64_t r, int y0, int y1, int ty,
-                                             int tile, const int32_t *band_hor, float (&acc)[10]) {
-#pragma unroll
-    for (int b = 0; b < kBands; b++) {
-        if (!band_meets(y0, y1, ty, b) || r > (int64_t)band_hor[tile * kBands + b]) continue;
-        const float2 *src = reinterpret_cast<const float2 *>(gbuf + (int64_t)slot * kPartStride + b * 10);
-#pragma unroll
-        for (int q = 0; q < 5; q++) {
-            const float2 t = src[q];
-            acc[2 * q] += t.x;
-            acc[2 * q + 1] += t.y;
-        }
-    }
-}
-
-// Sum of a small splat's visited instance partials, walking the kept-tile
-// mask in emission order: a culled tile only removes a zero term, so
-// ellipse culling stays bit-exact.
+// Sum of a small splat's visited instance slots (an instance was visited iff
+// its rank is <= its tile's horizon rank), walking the kept-tile mask in
+// emission order: a culled tile only removes a zero term, so ellipse culling
+// stays bit-exact.
 __device__ __forceinline__ void sum_slots(const ProjRec &g, uint32_t mask, int64_t r, uint32_t o,
-                                          const float *gbuf, const int32_t *band_hor, int tiles_x,
+                                          const float *gbuf, const int32_t *tile_hor, int tiles_x,
                                           float (&acc)[10]) {
     const int tx0 = rec_x0(g) / kTile, ty0 = rec_y0(g) / kTile, ntx = rec_x1(g) / kTile - tx0 + 1;
-    const int y0 = rec_y0(g), y1 = rec_y1(g);
     for (uint32_t m = mask; m; m &= m - 1, o++) {
         const int bit = __ffs(m) - 1;
-        const int ty = ty0 + bit / ntx;
-        add_instance(gbuf, o, r, y0, y1, ty, ty * tiles_x + tx0 + bit % ntx, band_hor, acc);
+        if (r > (int64_t)tile_hor[(ty0 + bit / ntx) * tiles_x + tx0 + bit % ntx]) continue;
+        const float4 *src = reinterpret_cast<const float4 *>(gbuf + (int64_t)o * kG2dStride);
+        const float4 a = src[0], b = src[1], cc = src[2];
+        acc[0] += a.x, acc[1] += a.y, acc[2] += a.z, acc[3] += a.w;
+        acc[4] += b.x, acc[5] += b.y, acc[6] += b.z, acc[7] += b.w;
+        acc[8] += cc.x, acc[9] += cc.y;
     }
 }
 
@@ -326,7 +323,7 @@ __global__ void __launch_bounds__(256)
 grad_gather_big(const ProjRec *__restrict__ recs, const uint32_t *__restrict__ toff,
                 const sm_render_counters *ctr,
                 const uint32_t *__restrict__ big, const float *__restrict__ gbuf,
-                const int32_t *__restrict__ band_hor, int tiles_x, float *__restrict__ g2d) {
+                const int32_t *__restrict__ tile_hor, int tiles_x, float *__restrict__ g2d) {
     __shared__ BigRowTable tab;
     __shared__ float s_part[kBigThreads / 32][10];
     const uint32_t nbig = ctr->overflow ? 0u : ctr->reserved[1];
@@ -335,9 +332,7 @@ grad_gather_big(const ProjRec *__restrict__ recs, const uint32_t *__restrict__ t
     const int vib = 8 + ((lane >> 4) & 1);
     for (uint32_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {   // a block per big splat
         const int64_t r = big[bi];
-        const ProjRec g = recs[r];
-        const RowSpan sp(g);
-        const int y0 = rec_y0(g), y1 = rec_y1(g);
+        const RowSpan sp(recs[r]);
         const uint32_t o = toff[r];
         float v[16];
 #pragma unroll
@@ -349,20 +344,22 @@ grad_gather_big(const ProjRec *__restrict__ recs, const uint32_t *__restrict__ t
             base = fill_row_table(sp, tyb, base, tab);
             const int nrows = min(kBigThreads, sp.ty1 - tyb + 1);
             for (int i = warp; i < nrows; i += kBigThreads / 32) {
-                const int c0 = tab.c0[i], c1 = tab.c1[i], ty = tyb + i, row = ty * tiles_x;
+                const int c0 = tab.c0[i], c1 = tab.c1[i], row = (tyb + i) * tiles_x;
                 const uint32_t src0 = o + tab.off[i] - (uint32_t)c0;
-                float acc[10];
-#pragma unroll
-                for (int k = 0; k < 10; k++) acc[k] = 0.f;
-                for (int c = c0 + (((lane - row - c0) % 32) + 32) % 32; c <= c1; c += 32)
-                    add_instance(gbuf, src0 + (uint32_t)c, r, y0, y1, ty, row + c, band_hor, acc);
-#pragma unroll
-                for (int k = 0; k < 10; k++) v[k] += acc[k];
+                for (int c = c0 + (((lane - row - c0) % 32) + 32) % 32; c <= c1; c += 32) {
+                    if (r > (int64_t)tile_hor[row + c]) continue;
+                    const float4 *src =
+                        reinterpret_cast<const float4 *>(gbuf + (int64_t)(src0 + (uint32_t)c) * kG2dStride);
+                    const float4 a = src[0], b = src[1], cc = src[2];
+                    v[0] += a.x, v[1] += a.y, v[2] += a.z, v[3] += a.w;
+                    v[4] += b.x, v[5] += b.y, v[6] += b.z, v[7] += b.w;
+                    v[8] += cc.x, v[9] += cc.y;
+                }
             }
         }
-        const float2 sv = transpose_reduce10(v, lane);   // fixed butterfly, then warps in order
-        if (!(lane & 3)) s_part[warp][via] = sv.x;
-        if (!(lane & 15)) s_part[warp][vib] = sv.y;
+        const float2 s = transpose_reduce10(v, lane);   // fixed butterfly, then warps in order
+        if (!(lane & 3)) s_part[warp][via] = s.x;
+        if (!(lane & 15)) s_part[warp][vib] = s.y;
         __syncthreads();
         if (threadIdx.x < 10) {
             float a = 0.f;
@@ -594,7 +591,7 @@ static void launch_composite_bwd(const RenderBufs &b, const RenderLayout &L, con
                                  cudaStream_t st) {
     const KeyT rank_mask = (KeyT)((1ull << L.rank_bits) - 1ull);
     const KeyT *ik = static_cast<const KeyT *>(L.tile_passes & 1 ? b.ikey1 : b.ikey0);
-    composite_bwd<KeyT><<<(unsigned)(L.n_tiles * kBands), 32, 0, st>>>(
+    composite_bwd<KeyT><<<(unsigned)L.n_tiles, kBwdThreads, 0, st>>>(
         b.ranges, ik, rank_mask, b.rec_sorted, b.p64, b.order0, dims.width, dims.height, L.tiles_x, d_rgb,
         d_depth, d_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, b.toff, b.tmask_r, b.gbuf, b.tile_hor,
         b.ctr, b.tile_order);

@@ -70,11 +70,10 @@ RenderLayout render_layout(const sm_render_dims &d) {
     L.o_g2d = take(G * (int64_t)sizeof(float) * kG2dStride);
     L.o_sort_hist = take(sort_scratch_bytes(G > I ? G : I));
     L.o_scan = take(scan_scratch_bytes(G));
-    L.o_gbuf = take(I * (int64_t)sizeof(float) * kPartStride);
-    L.o_tile_hor = take(L.n_tiles * kBands * 4);
+    L.o_gbuf = take(I * (int64_t)sizeof(float) * kG2dStride);
+    L.o_tile_hor = take(L.n_tiles * 4);
     L.o_tile_work = take(L.n_tiles * 4);
-    L.o_tile_order = take(L.n_tiles * kBands * 4);
-    L.o_band_work = take(L.n_tiles * kBands * 4);
+    L.o_tile_order = take(L.n_tiles * 4);
     L.total = off;
     return L;
 }
@@ -388,13 +387,12 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
               int height, int tiles_x, float *__restrict__ out_rgb, float *__restrict__ out_depth,
               float *__restrict__ out_alpha, float4 *__restrict__ st_cd, float *__restrict__ st_t,
               float *__restrict__ st_tlast, int32_t *__restrict__ st_last, uint32_t *__restrict__ tile_work,
-              uint32_t *__restrict__ band_work, const uint32_t *__restrict__ launch_order,
-              sm_render_counters *__restrict__ ctr) {
+              const uint32_t *__restrict__ launch_order) {
     constexpr int NT = kTilePx;
     __shared__ ProjRec s_rec[NT];
     __shared__ int4 s_box[NT];
     __shared__ uint32_t s_rank[NT];
-    __shared__ int s_bandlast[kBands];
+    __shared__ int s_maxlast;
     // longest-first when the caller keeps the previous render's order of this view
     const int tile = launch_order ? (int)launch_order[blockIdx.x] : (int)blockIdx.x;
     const int ty0 = (tile / tiles_x) * kTile;
@@ -439,24 +437,13 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
     }
     if (in)
         s.store((int64_t)py * width + px, out_rgb, out_depth, out_alpha, st_cd, st_t, st_tlast, st_last);
-    // each backward band revisits [start, its max last]: the work estimates
-    // for scheduling (per band: the backward's order; per tile: the next
-    // forward of this view).  Warp w covers rows 2w, 2w + 1 (band w / 2).
-    if (threadIdx.x < kBands) s_bandlast[threadIdx.x] = -1;
+    // the backward revisits [start, max last]: its work estimate for scheduling
+    if (threadIdx.x == 0) s_maxlast = -1;
     __syncthreads();
     const int wl = __reduce_max_sync(0xffffffffu, s.last);
-    if ((threadIdx.x & 31) == 0) atomicMax(&s_bandlast[threadIdx.x / 64], wl);
+    if ((threadIdx.x & 31) == 0) atomicMax(&s_maxlast, wl);
     __syncthreads();
-    if (threadIdx.x < kBands) {
-        const int bl = s_bandlast[threadIdx.x];
-        band_work[tile * kBands + threadIdx.x] = bl >= (int)start ? (uint32_t)(bl - (int)start + 1) : 0u;
-    }
-    if (threadIdx.x == 0) {
-        const int ml = max(max(s_bandlast[0], s_bandlast[1]), max(s_bandlast[2], s_bandlast[3]));
-        const uint32_t w = ml >= (int)start ? (uint32_t)(ml - (int)start + 1) : 0u;
-        tile_work[tile] = w;
-        if (w) atomicAdd(&ctr->reserved[3], w);   // instances composited (the tile horizons)
-    }
+    if (threadIdx.x == 0) tile_work[tile] = s_maxlast >= (int)start ? (uint32_t)(s_maxlast - (int)start + 1) : 0u;
 }
 
 // Longest-first launch order of the tiles for the backward: a counting sort
@@ -490,7 +477,7 @@ order_tiles(const uint32_t *__restrict__ work, int n_tiles, uint32_t *__restrict
     __syncthreads();
     for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) {
         const uint32_t o = atomicAdd(&base[kWorkBuckets - 1 - min(work[i] / div, (uint32_t)kWorkBuckets - 1)], 1u);
-        if (order) order[o] = (uint32_t)i;
+        order[o] = (uint32_t)i;
         if (keep) keep[o] = (uint32_t)i;
     }
 }
@@ -562,11 +549,8 @@ static void launch_composite_fwd(const RenderBufs &b, const RenderLayout &L, con
     const KeyT *ik = static_cast<const KeyT *>(L.tile_passes & 1 ? b.ikey1 : b.ikey0);
     composite_fwd<KeyT><<<(unsigned)L.n_tiles, kTilePx, 0, st>>>(
         b.ranges, ik, rank_mask, b.rec_sorted, b.p64, b.order0, dims.width, dims.height, L.tiles_x,
-        out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, b.tile_work, b.band_work,
-        view_order, b.ctr);
-    // the backward's band order; the next forward of this view gets the tile order
-    order_tiles<<<1, 1024, 0, st>>>(b.band_work, (int)(L.n_tiles * kBands), b.tile_order, nullptr);
-    if (view_order) order_tiles<<<1, 1024, 0, st>>>(b.tile_work, (int)L.n_tiles, nullptr, view_order);
+        out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, b.tile_work, view_order);
+    order_tiles<<<1, 1024, 0, st>>>(b.tile_work, (int)L.n_tiles, b.tile_order, view_order);
 }
 
 int render_forward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,
@@ -627,7 +611,7 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
     else
         launch_composite_fwd<uint32_t>(b, L, dims, out_rgb, out_depth, out_alpha, view_order, st);
     prof_end(ST_COMPOSITE_FWD, st);
-    count_launches(view_order ? 3 : 2);
+    count_launches(2);
     SM_CHECK_LAUNCH("render_forward");
     return SM_OK;
 }

@@ -415,19 +415,18 @@ class MappingEngine:
         _lib.check(rc, "adam_step")
 
     def _queue_readback(self) -> None:
-        """D2H copy of {loss[4], sm_render_counters[0:8]} into pinned memory (async)."""
+        """D2H copy of {loss[4], n_instances, overflow} into pinned memory (async)."""
         rb = self._readback
         rb[:4].copy_(self.loss.out, non_blocking=True)
-        rb[4:12].copy_(self.render.ws[:32].view(self.torch.float32), non_blocking=True)
+        rb[4:11].copy_(self.render.ws[:28].view(self.torch.float32), non_blocking=True)
 
     def _finish_readback(self) -> tuple[float, bool]:
         self.torch.cuda.current_stream(self.device).synchronize()
-        self.d2h_bytes += 48
+        self.d2h_bytes += 44
         v = self._readback.numpy()
-        ctr = v[4:12].view(np.uint32)   # sm_render_counters[0:8]
+        ctr = v[4:11].view(np.uint32)   # sm_render_counters[0:7]
         self.counter_instances += int(ctr[0])
-        self.counter_band_visits += int(ctr[6])   # (instance, band) pairs the backward revisited
-        self.counter_visited += int(ctr[7])       # instances the forward composited (tile horizons)
+        self.counter_visited += int(ctr[6])   # instances the backward revisited
         return float(v[0]), bool(ctr[1])
 
     counter_speculative = 0   # steps whose graph was launched before their host policy
@@ -438,9 +437,8 @@ class MappingEngine:
         self.counter_gaussians = 0
         self.counter_instances = 0
         self.counter_visited = 0
-        self.counter_band_visits = 0
 
-    counter_steps = counter_gaussians = counter_instances = counter_visited = counter_band_visits = 0
+    counter_steps = counter_gaussians = counter_instances = counter_visited = 0
     counter_replays = counter_eager = 0
     use_graphs = True
     capture_after = 2   # eager visits of a (keyframe, active set) before its graph is captured
