@@ -79,8 +79,9 @@ class ChunkStreamer:
         self.slab = slab
         self.device_pool_bytes = device_pool_bytes
         if device_pool_bytes is not None:
-            # 4 load staging slots + the synchronous staging buffer stay inside the bound
-            self.DEVICE_SLOTS = max(2, int(device_pool_bytes) // self.PINNED_SLOT_BYTES - 5)
+            # headroom for the 4 load staging slots + the synchronous staging
+            # buffer (<= 1.25 x the largest chunk each) and oversized packs
+            self.DEVICE_SLOTS = max(2, int(device_pool_bytes) // self.PINNED_SLOT_BYTES - 8)
             victim_bytes = min(victim_bytes, (self.DEVICE_SLOTS // 2) * self.PINNED_SLOT_BYTES)
         self.lib = _lib.load()
         self.copy_stream = torch.cuda.Stream(device=slab.device)   # H2D + validation of loads
@@ -202,10 +203,11 @@ class ChunkStreamer:
                 t0 = time.perf_counter()
                 self._freed.wait(timeout=left if not hard else 1.0)   # a write landing returns its buffers
                 self.stats["pool_wait_s"] += time.perf_counter() - t0
-        if not pinned and self.device_pool_bytes is not None and nbytes <= self.PINNED_SLOT_BYTES:
-            from .errors import HbmCapExceeded
-            raise HbmCapExceeded("the streamer's device pool is exhausted under the HBM cap")
         size = -(-(nbytes + 4096) // self._QUANTUM) * self._QUANTUM
+        if not pinned and self.device_pool_bytes is not None and self.device_bytes + size > self.device_pool_bytes:
+            from .errors import HbmCapExceeded
+            raise HbmCapExceeded(f"the streamer's device pool ({self.device_pool_bytes} B of the HBM cap) "
+                                 f"cannot hold another {size} B buffer")
         t0 = time.perf_counter()
         if pinned:
             buf = torch.empty(size, dtype=torch.uint8, pin_memory=True)
