@@ -204,10 +204,14 @@ class ChunkStreamer:
                 self._freed.wait(timeout=left if not hard else 1.0)   # a write landing returns its buffers
                 self.stats["pool_wait_s"] += time.perf_counter() - t0
         size = -(-(nbytes + 4096) // self._QUANTUM) * self._QUANTUM
-        if not pinned and self.device_pool_bytes is not None and self.device_bytes + size > self.device_pool_bytes:
-            from .errors import HbmCapExceeded
-            raise HbmCapExceeded(f"the streamer's device pool ({self.device_pool_bytes} B of the HBM cap) "
-                                 f"cannot hold another {size} B buffer")
+        if not pinned and self.device_pool_bytes is not None:
+            with self._lock:   # trade free (too small) pool buffers for one that fits the cap
+                while self.device_bytes + size > self.device_pool_bytes and pool:
+                    self.device_bytes -= pool.pop().numel()
+            if self.device_bytes + size > self.device_pool_bytes:
+                from .errors import HbmCapExceeded
+                raise HbmCapExceeded(f"the streamer's device pool ({self.device_pool_bytes} B of the HBM cap) "
+                                     f"cannot hold another {size} B buffer")
         t0 = time.perf_counter()
         if pinned:
             buf = torch.empty(size, dtype=torch.uint8, pin_memory=True)
