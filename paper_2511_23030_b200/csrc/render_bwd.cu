@@ -119,7 +119,6 @@ struct BwdPair {
 
     // d{u v ia ib ic op r g b z} of splat g (instance position k) summed over
     // the pair into v[0..9]; then one step back.
-    template <bool ACC = false>
     __device__ __forceinline__ void step(const ProjRec &g, float dx, float2 dy, float2 pw, bool h0,
                                          bool h1, int k, float (&v)[16]) {
         const float2 G = make_float2(h0 ? ex2_approx(pw.x) : 0.f, h1 ? ex2_approx(pw.y) : 0.f);
@@ -137,23 +136,20 @@ struct BwdPair {
         ga = fma2(sub2(f2s(g.z), Bz), gD, ga);
         ga = mul2(Tk, fma2(gA, P, ga));
         const float2 wt = mul2(Tk, alpha);
-        float u[10];
-        u[6] = hsum(mul2(wt, gCr));
-        u[7] = hsum(mul2(wt, gCg));
-        u[8] = hsum(mul2(wt, gCb));
-        u[9] = hsum(mul2(wt, gD));
-        u[5] = hsum(mul2(ga, G));
+        v[6] = hsum(mul2(wt, gCr));
+        v[7] = hsum(mul2(wt, gCg));
+        v[8] = hsum(mul2(wt, gCb));
+        v[9] = hsum(mul2(wt, gD));
+        v[5] = hsum(mul2(ga, G));
         // q = pw / kPowScale; conic grads are w.r.t. the unscaled conic
         const float2 gq = mul2(f2s(-0.5f), mul2(alpha, ga));
         const float2 gqdx = mul2(gq, f2s(dx));
-        u[2] = hsum(mul2(gqdx, f2s(dx)));
-        u[3] = hsum(mul2(mul2(gqdx, f2s(2.f)), dy));
-        u[4] = hsum(mul2(mul2(gq, dy), dy));
+        v[2] = hsum(mul2(gqdx, f2s(dx)));
+        v[3] = hsum(mul2(mul2(gqdx, f2s(2.f)), dy));
+        v[4] = hsum(mul2(mul2(gq, dy), dy));
         const float2 gqi = mul2(gq, f2s((float)(-2.0 / kPowScale)));
-        u[0] = hsum(mul2(gqi, fma2(f2s(g.ib), dy, f2s(g.ia * dx))));
-        u[1] = hsum(mul2(gqi, fma2(f2s(g.ic), dy, f2s(g.ib * dx))));
-#pragma unroll
-        for (int i = 0; i < 10; i++) v[i] = ACC ? v[i] + u[i] : u[i];
+        v[0] = hsum(mul2(gqi, fma2(f2s(g.ib), dy, f2s(g.ia * dx))));
+        v[1] = hsum(mul2(gqi, fma2(f2s(g.ic), dy, f2s(g.ib * dx))));
         Br = fma2(alpha, f2s(g.r), mul2(oma, Br));
         Bg = fma2(alpha, f2s(g.g), mul2(oma, Bg));
         Bb = fma2(alpha, f2s(g.b), mul2(oma, Bb));
@@ -293,158 +289,6 @@ composite_bwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
                 acc[k] = a;
             }
             float4 *dst = reinterpret_cast<float4 *>(gbuf + (int64_t)slot * kG2dStride);
-            dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-            dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
-            dst[2] = make_float4(acc[8], acc[9], 0.f, 0.f);
-        }
-        __syncthreads();
-    }
-}
-
-// The same backward with four pixels per thread: lane l of warp w owns
-// column l % 16, rows 8w + 4 (l / 16) .. + 3 as two pixel pairs (A: rows
-// 0-1, B: rows 2-3), so a 64-thread CTA covers the 16x16 tile.  Per
-// (warp, instance) the record decode, the hit tests' setup and the 10-value
-// warp reduction are paid once for 128 pixels instead of 64, and the two
-// pairs give two independent dependency chains per thread.  Batches of 128
-// instances (two staged per thread); same determinism as composite_bwd (warp
-// partials in shared memory, summed in warp order).
-constexpr int kBwd4Threads = kTilePx / 4;
-constexpr int kBwd4Batch = 128;
-#ifndef SM_BWD4_MINB
-#define SM_BWD4_MINB 8
-#endif
-
-template <typename KeyT>
-__global__ void __launch_bounds__(kBwd4Threads, SM_BWD4_MINB)
-composite_bwd4(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikeys,
-               KeyT rank_mask, const ProjRec *__restrict__ recs,
-               const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
-               int height, int tiles_x, const float *__restrict__ d_rgb,
-               const float *__restrict__ d_depth, const float *__restrict__ d_alpha,
-               const float4 *__restrict__ st_cd, const float *__restrict__ st_t,
-               const float *__restrict__ st_tlast, const int32_t *__restrict__ st_last,
-               const uint32_t *__restrict__ toff, const uint32_t *__restrict__ tmask_r,
-               float *__restrict__ gbuf, int32_t *__restrict__ tile_hor, sm_render_counters *ctr,
-               const uint32_t *__restrict__ tile_order) {
-    constexpr int NT = kBwd4Threads, NB = kBwd4Batch, NW = NT / 32;
-    __shared__ ProjRec s_rec[NB];
-    __shared__ uint32_t s_rank[NB];
-    __shared__ float s_part[NW][NB][10];
-    __shared__ int s_maxlast;
-    const int warp = threadIdx.x / 32;
-    const int tile = (int)tile_order[blockIdx.x];   // heaviest tiles first
-    const int lane = threadIdx.x & 31;
-    const int ty0 = (tile / tiles_x) * kTile;
-    const int wy0 = ty0 + 8 * warp;                          // the warp's first row
-    const int px = (tile % tiles_x) * kTile + (lane & (kTile - 1));
-    const int pa = wy0 + 4 * (lane / kTile), pb = pa + 2;    // first rows of pairs A and B
-    const int start = (int)ranges[2 * tile];
-    BwdPair qa, qb;
-    {
-        BwdPix a, b;
-        a.init(px < width && pa < height, (int64_t)pa * width + px, d_rgb, d_depth, d_alpha, st_cd, st_t, st_tlast,
-               st_last);
-        b.init(px < width && pa + 1 < height, (int64_t)(pa + 1) * width + px, d_rgb, d_depth, d_alpha, st_cd, st_t,
-               st_tlast, st_last);
-        qa.init(a, b);
-        a.init(px < width && pb < height, (int64_t)pb * width + px, d_rgb, d_depth, d_alpha, st_cd, st_t, st_tlast,
-               st_last);
-        b.init(px < width && pb + 1 < height, (int64_t)(pb + 1) * width + px, d_rgb, d_depth, d_alpha, st_cd, st_t,
-               st_tlast, st_last);
-        qb.init(a, b);
-    }
-    int wmax = max(max(qa.last0, qa.last1), max(qb.last0, qb.last1));
-    if (threadIdx.x == 0) s_maxlast = -1;
-    __syncthreads();
-    wmax = __reduce_max_sync(0xffffffffu, wmax);
-    if (lane == 0) atomicMax(&s_maxlast, wmax);
-    __syncthreads();
-    const int maxlast = s_maxlast;
-    if (threadIdx.x == 0) {   // rank of the tile's last visited instance (grad_gather's horizon)
-        tile_hor[tile] = maxlast >= start ? (int32_t)(uint32_t)(ikeys[maxlast] & rank_mask) : -1;
-        if (maxlast >= start) atomicAdd(&ctr->reserved[2], (uint32_t)(maxlast - start + 1));
-    }
-    const int via = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);   // 0..7
-    const int vib = 8 + ((lane >> 4) & 1);                                                // 8..9
-    const int tile_x = tile % tiles_x, tile_y = tile / tiles_x;
-    for (int bend = maxlast + 1; bend > start; bend -= NB) {
-        const int bstart = max(start, bend - NB);
-#pragma unroll
-        for (int h = 0; h < NB / NT; h++) {
-            const int t = threadIdx.x + h * NT;
-            if (bstart + t < bend) {
-                const uint32_t rk = (uint32_t)(ikeys[bstart + t] & rank_mask);
-                s_rank[t] = rk;
-                s_rec[t] = recs[rk];
-            }
-        }
-        for (int i = threadIdx.x; i < NW * NB * 10; i += NT) (&s_part[0][0][0])[i] = 0.f;
-        __syncthreads();
-        const int jtop = min(bend - 1, wmax) - bstart;
-        for (int j = jtop; j >= 0; j--) {
-            const ProjRec &g = s_rec[j];
-            const int y0 = rec_y0(g), y1 = rec_y1(g);
-            if (y1 < wy0 || y0 > wy0 + 7) continue;   // warp-uniform row cull
-            const int k = bstart + j;
-            const int x0 = rec_x0(g);
-            const float dx = (float)(px - x0) + g.ox;
-            const float2 dya = make_float2((float)(pa - y0) + g.oy, (float)(pa + 1 - y0) + g.oy);
-            const float2 dyb = make_float2((float)(pb - y0) + g.oy, (float)(pb + 1 - y0) + g.oy);
-            const float2 lin = f2s(2.f * g.ib * dx), con = f2s(g.ia * dx * dx);
-            const float2 pwa = fma2(dya, fma2(f2s(g.ic), dya, lin), con);
-            const float2 pwb = fma2(dyb, fma2(f2s(g.ic), dyb, lin), con);
-            const float2 da = sub2(pwa, f2s(kPowCut)), db = sub2(pwb, f2s(kPowCut));
-            const bool col = (unsigned)(px - x0) <= (unsigned)(rec_x1(g) - x0);
-            const unsigned span = (unsigned)(y1 - y0);
-            bool a0 = col && (unsigned)(pa - y0) <= span && k <= qa.last0;
-            bool a1 = col && (unsigned)(pa + 1 - y0) <= span && k <= qa.last1;
-            bool b0 = col && (unsigned)(pb - y0) <= span && k <= qb.last0;
-            bool b1 = col && (unsigned)(pb + 1 - y0) <= span && k <= qb.last1;
-            if ((a0 && fabsf(da.x) <= g.eps) || (a1 && fabsf(da.y) <= g.eps) || (b0 && fabsf(db.x) <= g.eps) ||
-                (b1 && fabsf(db.y) <= g.eps)) {   // rare: fp64 band
-                a0 = a0 && q_within_cutoff(pwa.x, g.eps, p64, order, s_rank[j], px, pa);
-                a1 = a1 && q_within_cutoff(pwa.y, g.eps, p64, order, s_rank[j], px, pa + 1);
-                b0 = b0 && q_within_cutoff(pwb.x, g.eps, p64, order, s_rank[j], px, pb);
-                b1 = b1 && q_within_cutoff(pwb.y, g.eps, p64, order, s_rank[j], px, pb + 1);
-            } else {
-                a0 = a0 && da.x >= 0.f;
-                a1 = a1 && da.y >= 0.f;
-                b0 = b0 && db.x >= 0.f;
-                b1 = b1 && db.y >= 0.f;
-            }
-            if (!__any_sync(0xffffffffu, a0 || a1 || b0 || b1)) continue;
-            float v[16];
-            qa.step(g, dx, dya, pwa, a0, a1, k, v);
-            qb.step<true>(g, dx, dyb, pwb, b0, b1, k, v);
-            const float2 sv = transpose_reduce10(v, lane);
-            if (!(lane & 3)) s_part[warp][j][via] = sv.x;
-            if (!(lane & 15)) s_part[warp][j][vib] = sv.y;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int h = 0; h < NB / NT; h++) {   // warp-ordered sums -> the instances' emission slots
-            const int t = threadIdx.x + h * NT;
-            if (bstart + t >= bend) continue;
-            const ProjRec &g = s_rec[t];
-            const uint32_t rk = s_rank[t];
-            uint32_t kept;   // the tile's index among the splat's kept tiles
-            if (bbox_tiles(g) <= kEmitSmall) {
-                const int tx0 = rec_x0(g) / kTile, ty0r = rec_y0(g) / kTile;
-                const int bit = (tile_y - ty0r) * (rec_x1(g) / kTile - tx0 + 1) + tile_x - tx0;
-                kept = (uint32_t)__popc(tmask_r[rk] & ((1u << bit) - 1u));
-            } else {
-                kept = RowSpan(g).kept_index(tile_x, tile_y);
-            }
-            float acc[10];
-#pragma unroll
-            for (int q = 0; q < 10; q++) {
-                float a = 0.f;
-#pragma unroll
-                for (int w = 0; w < NW; w++) a += s_part[w][t][q];
-                acc[q] = a;
-            }
-            float4 *dst = reinterpret_cast<float4 *>(gbuf + (int64_t)(toff[rk] + kept) * kG2dStride);
             dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
             dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
             dst[2] = make_float4(acc[8], acc[9], 0.f, 0.f);
@@ -747,19 +591,10 @@ static void launch_composite_bwd(const RenderBufs &b, const RenderLayout &L, con
                                  cudaStream_t st) {
     const KeyT rank_mask = (KeyT)((1ull << L.rank_bits) - 1ull);
     const KeyT *ik = static_cast<const KeyT *>(L.tile_passes & 1 ? b.ikey1 : b.ikey0);
-#ifndef SM_BWD_QUAD
-#define SM_BWD_QUAD 1   // 0: two pixels per thread (composite_bwd, A/B)
-#endif
-    if (SM_BWD_QUAD)
-        composite_bwd4<KeyT><<<(unsigned)L.n_tiles, kBwd4Threads, 0, st>>>(
-            b.ranges, ik, rank_mask, b.rec_sorted, b.p64, b.order0, dims.width, dims.height, L.tiles_x, d_rgb,
-            d_depth, d_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, b.toff, b.tmask_r, b.gbuf, b.tile_hor,
-            b.ctr, b.tile_order);
-    else
-        composite_bwd<KeyT><<<(unsigned)L.n_tiles, kBwdThreads, 0, st>>>(
-            b.ranges, ik, rank_mask, b.rec_sorted, b.p64, b.order0, dims.width, dims.height, L.tiles_x, d_rgb,
-            d_depth, d_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, b.toff, b.tmask_r, b.gbuf, b.tile_hor,
-            b.ctr, b.tile_order);
+    composite_bwd<KeyT><<<(unsigned)L.n_tiles, kBwdThreads, 0, st>>>(
+        b.ranges, ik, rank_mask, b.rec_sorted, b.p64, b.order0, dims.width, dims.height, L.tiles_x, d_rgb,
+        d_depth, d_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, b.toff, b.tmask_r, b.gbuf, b.tile_hor,
+        b.ctr, b.tile_order);
 }
 
 int render_backward(const float *params, const int32_t *slots, int64_t n, const sm_camera &cam,
