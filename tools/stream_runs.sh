@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round-2 out-of-core runs: C4-lite (thrashing budget), full C4, C5 stress.
-python tools/stream_bench.py --budget 1100000 > gpurun_out/r02_stream_c4lite.json 2> gpurun_out/c4lite.err
+python tools/stream_bench.py --budget 1100000 --modes resident,streamed > gpurun_out/r02_stream_c4lite.json 2> gpurun_out/c4lite.err
 python -c "
 import json;d=json.loads(open('gpurun_out/r02_stream_c4lite.json').read().strip().splitlines()[-1]); print('c4lite', {k: round(v['steps_per_s'],1) for k,v in d['runs'].items()}, d['overlap'])"
 python tools/stress_bench.py --out gpurun_out/r02_stress_c5.json > gpurun_out/c5.out 2> gpurun_out/c5.err
