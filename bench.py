@@ -111,7 +111,7 @@ STAGE_BYTES = {
     "adam": lambda n, i, p, v: n * (4 + 7 * 64),
     "grad_gather": lambda n, i, p, v: n * (4 + 4 + 64 + 48) + v * (48 + 4),
 }
-NCU_SUMMARY = Path(__file__).resolve().parent / "profiles" / "r01_ncu_full.json"
+NCU_SUMMARY = Path(__file__).resolve().parent / "profiles" / "r02_ncu_full.json"
 
 
 def _ncu_kernel(name: str):

@@ -69,7 +69,8 @@ class DeviceRecords:
 
 class ChunkStreamer:
     def __init__(self, slab, write_behind: bool = True, reader_threads: int = 4,
-                 writer_threads: int = 4, victim_bytes: int = 4 << 30, device_pool_bytes: int | None = None):
+                 writer_threads: int = 4, victim_bytes: int = 4 << 30, device_pool_bytes: int | None = None,
+                 pinned_pool_bytes: int | None = None):
         """device_pool_bytes: a hard bound on the streamer's HBM (pack buffers
         + victim cache + the load staging ring) for an HBM-capped store; the
         pool is then never grown on demand -- a pack waits for a write-behind
@@ -78,6 +79,8 @@ class ChunkStreamer:
         self.torch = torch
         self.slab = slab
         self.device_pool_bytes = device_pool_bytes
+        if pinned_pool_bytes is not None:   # host staging: pending write-behinds + prefetched reads
+            self.PINNED_SLOTS = max(16, int(pinned_pool_bytes) // self.PINNED_SLOT_BYTES)
         if device_pool_bytes is not None:
             # headroom for the 4 load staging slots + the synchronous staging
             # buffer (<= 1.25 x the largest chunk each) and oversized packs
