@@ -103,6 +103,7 @@ def main():
     ap.add_argument("--length", type=float, default=5000.0)
     ap.add_argument("--slices", type=int, default=20)
     ap.add_argument("--cap-gb", type=float, default=8.0)
+    ap.add_argument("--pinned-gb", type=float, default=8.0, help="host staging (write-behind + prefetch)")
     ap.add_argument("--budget", type=int, default=0, help="Gaussian budget (default: 85%% of the cap's rows)")
     ap.add_argument("--spacing", type=float, default=2.0)
     ap.add_argument("--keyframes", type=int, default=0, help="limit (default: the whole corridor)")
@@ -134,7 +135,8 @@ def main():
     root = Path(tempfile.mkdtemp(prefix="c5_"))
     t_build = time.perf_counter()
     store = ChunkStore(StoreConfig(disk_root=root, chunk_size_m=10.0, gaussian_budget=budget,
-                                   keyframe_budget=400, io_ns_per_byte=1.0, hbm_cap_bytes=cap_bytes))
+                                   keyframe_budget=400, io_ns_per_byte=1.0, hbm_cap_bytes=cap_bytes,
+                                   pinned_pool_bytes=int(args.pinned_gb * (1 << 30))))
     sl = Slices(args.n, args.length, args.slices, device)
     frames = [None] * n_kf
     eng_r = default_engine(device)
