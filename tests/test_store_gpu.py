@@ -149,8 +149,60 @@ def test_corrupt_chunk_detected_on_device(cuda, tmp_path):
     data = bytearray(p.read_bytes())
     data[32 + 40:32 + 44] = np.float32(-1.0).tobytes()   # opacity of record 0 -> -1
     p.write_bytes(bytes(data))
+    used = st.slab.used()
     with pytest.raises(CorruptChunk):
         st.ensure_resident([cid])
+    assert st.slab.used() == used   # the rows reserved for the corrupt chunk were released
+    assert cid not in st.resident_chunk_ids()
+
+
+def test_write_behind_failure_keeps_data_and_retries(cuda, tmp_path, monkeypatch):
+    """A write-behind that fails (ENOSPC) must not lose the chunk: the error
+    surfaces at the next paging call, a reload is served from the kept packed
+    bytes (not from the stale file), and the next flush writes the file."""
+    import builtins
+    import errno
+
+    import torch
+
+    from paper_2511_23030_b200 import streamer as S
+    from paper_2511_23030_b200.core import Gaussian
+    from paper_2511_23030_b200.errors import IoFailure
+    from paper_2511_23030_b200.store import ChunkStore, StoreConfig
+    st = ChunkStore(StoreConfig(disk_root=tmp_path, chunk_size_m=10.0, gaussian_budget=100, io_ns_per_byte=1.0))
+    st.insert_gaussians([Gaussian(position=[1.0 + 0.1 * i, 2.0, 3.0]) for i in range(5)])
+    st.insert_gaussians([Gaussian(position=[31.0, 2.0 + 0.1 * i, 3.0]) for i in range(4)])
+    st.flush()
+    a = min(st.resident_chunk_ids())
+    ch = st.chunk(a)
+    st.slab.params[ch.offset:ch.offset + ch.count, 0] += 0.5   # new content, chunk dirty
+    st.mark_chunk_mutated(a)
+    want = st.slab.params[ch.offset:ch.offset + ch.count].clone()
+    path = tmp_path / "chunks" / f"{a:016x}.dcg"
+    stale = path.read_bytes()
+    fail = {"n": 1}
+
+    def fake_open(p, *args, **kw):
+        if fail["n"] and str(p).startswith(str(path)):
+            fail["n"] -= 1
+            raise OSError(errno.ENOSPC, "No space left on device")
+        return builtins.open(p, *args, **kw)
+    monkeypatch.setattr(S, "open", fake_open, raising=False)
+    st.evict_lru(ch.count, protected=set(st.resident_chunk_ids()) - {a})
+    st.streamer._queue.join()   # the write-behind ran (and failed)
+    assert path.read_bytes() == stale
+    with pytest.raises(IoFailure):   # surfaces at the next paging operation
+        st.ensure_resident([a])
+    st.ensure_resident([a])          # served from the kept packed bytes
+    ch = st.chunk(a)
+    assert torch.equal(st.slab.params[ch.offset:ch.offset + ch.count], want)
+    st.evict_lru(ch.count, protected=set(st.resident_chunk_ids()) - {a})
+    st.flush()                       # the retried / newer write lands
+    assert path.read_bytes() != stale
+    st2 = ChunkStore(StoreConfig(disk_root=tmp_path, chunk_size_m=10.0, gaussian_budget=100, io_ns_per_byte=1.0))
+    st2.ensure_resident([a])
+    c2 = st2.chunk(a)
+    assert torch.equal(st2.slab.params[c2.offset:c2.offset + c2.count], want)
 
 
 def test_device_encode_positions_bit_exact(cuda, golden):
