@@ -379,29 +379,23 @@ struct FwdPix {
 #ifndef SM_FWD_MINB
 #define SM_FWD_MINB 1
 #endif
-// HALF: the heaviest tiles of the view (the first `first` entries of its
-// longest-first order) are split into two 128-thread CTAs of 8 rows each,
-// launched on a second branch of the stream next to the ordinary launch: the
-// longest tiles stop setting the kernel's tail (pixels are independent in the
-// forward, so a half tile needs nothing from the other half).
-template <typename KeyT, bool HALF = false>
-__global__ void __launch_bounds__(HALF ? kTilePx / 2 : kTilePx, SM_FWD_MINB)
+template <typename KeyT>
+__global__ void __launch_bounds__(kTilePx, SM_FWD_MINB)
 composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikeys,
               KeyT rank_mask, const ProjRec *__restrict__ recs,
               const Proj64 *__restrict__ p64, const uint32_t *__restrict__ order, int width,
               int height, int tiles_x, float *__restrict__ out_rgb, float *__restrict__ out_depth,
               float *__restrict__ out_alpha, float4 *__restrict__ st_cd, float *__restrict__ st_t,
               float *__restrict__ st_tlast, int32_t *__restrict__ st_last, uint32_t *__restrict__ tile_work,
-              const uint32_t *__restrict__ launch_order, int first = 0) {
-    constexpr int NT = HALF ? kTilePx / 2 : kTilePx;
+              const uint32_t *__restrict__ launch_order) {
+    constexpr int NT = kTilePx;
     __shared__ ProjRec s_rec[NT];
     __shared__ int4 s_box[NT];
     __shared__ uint32_t s_rank[NT];
     __shared__ int s_maxlast;
     // longest-first when the caller keeps the previous render's order of this view
-    const int slot = HALF ? (int)(blockIdx.x >> 1) : first + (int)blockIdx.x;
-    const int tile = launch_order ? (int)launch_order[slot] : slot;
-    const int ty0 = (tile / tiles_x) * kTile + (HALF ? (int)(blockIdx.x & 1) * (kTile / 2) : 0);
+    const int tile = launch_order ? (int)launch_order[blockIdx.x] : (int)blockIdx.x;
+    const int ty0 = (tile / tiles_x) * kTile;
     const int px = (tile % tiles_x) * kTile + (threadIdx.x & (kTile - 1));
     const int py = ty0 + threadIdx.x / kTile;
     const int wy0 = ty0 + 2 * (threadIdx.x / 32);   // warp's first row
@@ -449,13 +443,7 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
     const int wl = __reduce_max_sync(0xffffffffu, s.last);
     if ((threadIdx.x & 31) == 0) atomicMax(&s_maxlast, wl);
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const uint32_t w = s_maxlast >= (int)start ? (uint32_t)(s_maxlast - (int)start + 1) : 0u;
-        if (HALF)
-            atomicMax(&tile_work[tile], w);   // the two halves' horizon (zeroed before the launch)
-        else
-            tile_work[tile] = w;
-    }
+    if (threadIdx.x == 0) tile_work[tile] = s_maxlast >= (int)start ? (uint32_t)(s_maxlast - (int)start + 1) : 0u;
 }
 
 // Longest-first launch order of the tiles for the backward: a counting sort
@@ -559,22 +547,9 @@ static void launch_composite_fwd(const RenderBufs &b, const RenderLayout &L, con
                                  cudaStream_t st) {
     const KeyT rank_mask = (KeyT)((1ull << L.rank_bits) - 1ull);
     const KeyT *ik = static_cast<const KeyT *>(L.tile_passes & 1 ? b.ikey1 : b.ikey0);
-#ifndef SM_FWD_SPLIT
-#define SM_FWD_SPLIT 148   // heaviest tiles of an ordered view split in two half-tile CTAs (0: off)
-#endif
-    const int split = view_order ? (int)min64(SM_FWD_SPLIT, L.n_tiles / 2) : 0;
-    StreamFork &fk = stream_fork();
-    if (split) {
-        cudaMemsetAsync(b.tile_work, 0, L.n_tiles * 4, st);
-        fk.begin(st);
-        composite_fwd<KeyT, true><<<(unsigned)(2 * split), kTilePx / 2, 0, fk.side>>>(
-            b.ranges, ik, rank_mask, b.rec_sorted, b.p64, b.order0, dims.width, dims.height, L.tiles_x,
-            out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, b.tile_work, view_order);
-    }
-    composite_fwd<KeyT><<<(unsigned)(L.n_tiles - split), kTilePx, 0, st>>>(
+    composite_fwd<KeyT><<<(unsigned)L.n_tiles, kTilePx, 0, st>>>(
         b.ranges, ik, rank_mask, b.rec_sorted, b.p64, b.order0, dims.width, dims.height, L.tiles_x,
-        out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, b.tile_work, view_order, split);
-    if (split) fk.end(st);
+        out_rgb, out_depth, out_alpha, b.pix_cd, b.pix_t, b.pix_tlast, b.pix_last, b.tile_work, view_order);
     order_tiles<<<1, 1024, 0, st>>>(b.tile_work, (int)L.n_tiles, b.tile_order, view_order);
 }
 
@@ -636,7 +611,7 @@ int render_forward(const float *params, const int32_t *slots, int64_t n, const s
     else
         launch_composite_fwd<uint32_t>(b, L, dims, out_rgb, out_depth, out_alpha, view_order, st);
     prof_end(ST_COMPOSITE_FWD, st);
-    count_launches(2 + (view_order && SM_FWD_SPLIT ? 1 : 0));
+    count_launches(2);
     SM_CHECK_LAUNCH("render_forward");
     return SM_OK;
 }
