@@ -470,22 +470,30 @@ class MappingEngine:
         ext = store.coord_extent()
         if ext is None:
             return
-        try:
-            cands = candidate_set(self.index.position_of(self.latest_kf), self.index)
-        except EmptyCandidates:
-            cands = [self.latest_kf]
-        want: set[int] = set()
-        for c in cands:
-            kf = store._keyframes.get(c)
-            if kf is None:
-                continue
-            # only views the cache already knows (no cull on the step's host
-            # path); a new keyframe's view is computed once, in add_keyframe
-            vis = self.cache.peek(kf.pose, self.intr, store.generation, store.chunk_size)
-            if vis is not None:
-                want.update(vis)
-        if want:
-            store.prefetch(sorted(want))
+        key = (self.latest_kf, self.index.version, store.generation)
+        memo = getattr(self, "_ahead", None)
+        if memo is None or memo[0] != key or memo[2] >= 8:
+            # the union of the candidates' views (only views the cache already
+            # knows: no cull on the step's host path; a new keyframe's view is
+            # computed once, in add_keyframe); rebuilt when the candidate set or
+            # the chunk set changes, and every 8 steps for views cached since
+            try:
+                cands = candidate_set(self.index.position_of(self.latest_kf), self.index)
+            except EmptyCandidates:
+                cands = [self.latest_kf]
+            want: set[int] = set()
+            for c in cands:
+                kf = store._keyframes.get(c)
+                if kf is None:
+                    continue
+                vis = self.cache.peek(kf.pose, self.intr, store.generation, store.chunk_size)
+                if vis is not None:
+                    want.update(vis)
+            memo = self._ahead = [key, sorted(want), 0]
+        memo[2] += 1
+        want = memo[1]
+        if want and store.resident_count_of(want) < len(want):
+            store.prefetch(want)
 
     def _prefetch_view(self, pose: Pose) -> None:
         """A new keyframe's on-disk chunks start streaming in (one cull, no
