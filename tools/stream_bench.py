@@ -86,7 +86,10 @@ def run(mode: str, scene, poses, frames, args):
            "bytes_written": st.bytes_written - wb0, "active_gaussians_end": st.active_gaussians,
            "mean_visible": eng.counter_gaussians / max(eng.counter_steps, 1),
            "ensure_resident_s": blocked[0], "graph_replays": eng.counter_replays,
-           "eager_steps": eng.counter_eager}
+           "eager_steps": eng.counter_eager,
+           # the training itself must not depend on the paging: the (keyframe,
+           # loss) sequence of every mode is compared in main()
+           "trace": [(r.selected_kf, r.loss) for r in eng.rows]}
     if store.streamer is not None:
         out.update({k: v for k, v in store.streamer.stats.items()})
     store.flush()
@@ -146,6 +149,13 @@ def main():
             "runs": res}
     if "resident" in res and "streamed" in res:
         line["overlap"] = res["resident"]["seconds"] / res["streamed"]["seconds"]
+    traces = {m: r.pop("trace") for m, r in res.items()}
+    base = next(iter(traces.values()))
+    line["same_training"] = {m: t == base for m, t in traces.items()}
+    for m, t in traces.items():
+        if t != base:
+            k = next(i for i, (a, b) in enumerate(zip(t, base)) if a != b)
+            line.setdefault("first_divergence", {})[m] = [k, t[k], base[k]]
     if "resident" in res and "sync" in res:
         line["sync_vs_resident"] = res["resident"]["seconds"] / res["sync"]["seconds"]
     print(json.dumps(line))
