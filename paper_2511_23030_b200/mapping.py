@@ -145,18 +145,30 @@ class _ActiveSet:
             self._cache[key] = hit
             self.key, self.n = key, hit[1]
             return hit
-        torch = self.torch
+        total = sum(c for _, c in segments)
+        slots = self.torch.empty(max(total, 1), dtype=self.torch.int32, device=self.device)
+        return self._fill(slots, key, segments)
+
+    def rebuild(self, slots, segments: list[tuple[int, int]]):
+        """The same chunks (same row count) at new slab rows: re-expand into
+        the existing buffer, stream-ordered behind the passes that read it,
+        so the CUDA graphs captured over this buffer stay valid."""
+        for k in [k for k, v in self._cache.items() if v[0] is slots]:
+            del self._cache[k]
+        return self._fill(slots, tuple(segments), segments)
+
+    def _fill(self, slots, key, segments):
         counts = np.array([c for _, c in segments], dtype=np.int64)
         offs = np.array([o for o, _ in segments], dtype=np.int64)
         total = int(counts.sum())
-        slots = torch.empty(max(total, 1), dtype=torch.int32, device=self.device)
         if total:
             prefix = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
-            meta = torch.as_tensor(np.stack([offs, counts, prefix]), device=self.device)
+            meta = self.torch.as_tensor(np.stack([offs, counts, prefix]), device=self.device)
             rc = _lib.load().sm_expand_segments(_lib.ptr(meta[0]), _lib.ptr(meta[1]), _lib.ptr(meta[2]),
                                                 len(segments), total, _lib.ptr(slots),
                                                 _lib.stream_handle())
             _lib.check(rc, "expand_segments")
+        self._cache.pop(key, None)
         self._cache[key] = (slots, total)
         while len(self._cache) > self.CAPACITY:
             self._cache.pop(next(iter(self._cache)))
@@ -746,10 +758,17 @@ class MappingEngine:
         if ent is not None and ent[0] == store.layout_version:   # same chunks at the same rows
             slots, n = ent[1]
         else:
-            slots, n = self.active.build(store.segments(ids))
-            if len(self._layout_cache) >= 64:
-                self._layout_cache.clear()
+            segs = store.segments(ids)
+            if ent is not None and ent[1][1] == sum(c for _, c in segs):
+                # a chunk of this view was paged out and back in elsewhere:
+                # refill its slot buffer in place, its graphs keep replaying
+                slots, n = self.active.rebuild(ent[1][0], segs)
+            else:
+                slots, n = self.active.build(segs)
+            self._layout_cache.pop(ids_t, None)
             self._layout_cache[ids_t] = (store.layout_version, (slots, n))
+            while len(self._layout_cache) > 64:
+                self._layout_cache.pop(next(iter(self._layout_cache)))
         if spec is not None and (ids_t != spec[0] or slots.data_ptr() != spec[1].data_ptr() or n != spec[2]):
             raise RuntimeError("speculative launch diverged from the step's policy")
 

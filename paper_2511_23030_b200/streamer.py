@@ -15,10 +15,11 @@ Load:   the file is read straight into a pinned buffer (readinto; reader
         A chunk whose eviction write is still pending is unpacked straight
         from the device buffer it was packed into (no host round trip).
 Evict:  K9 sm_chunk_pack on the compute stream into a device buffer (so the
-        slab rows can be reused immediately, stream-ordered), the D2H copy
-        into pinned memory on the copy stream, and a writer thread that
-        waits on that copy's event and writes the file: eviction write-back
-        overlaps with rendering (write-behind).
+        slab rows can be reused immediately, stream-ordered); a writer
+        thread then takes a pinned buffer, copies the records down on its
+        own stream (after the pack's event) and writes the file: eviction
+        write-back overlaps with rendering (write-behind), and the backlog
+        of unwritten chunks waits in HBM, not in pinned memory.
 flush():  drains the writer queue (the store's durability point).
 """
 
@@ -88,7 +89,6 @@ class ChunkStreamer:
             victim_bytes = min(victim_bytes, (self.DEVICE_SLOTS // 2) * self.PINNED_SLOT_BYTES)
         self.lib = _lib.load()
         self.copy_stream = torch.cuda.Stream(device=slab.device)   # H2D + validation of loads
-        self.d2h_stream = torch.cuda.Stream(device=slab.device)    # write-behind D2H (own copy engine)
         self.device_bytes = 0   # every device buffer this streamer allocated (pool, staging)
         self._dev = torch.empty(0, dtype=torch.uint8, device=slab.device)
         self._pin = torch.empty(0, dtype=torch.uint8, pin_memory=True)
@@ -123,7 +123,10 @@ class ChunkStreamer:
         self.stats = {"prefetch_hits": 0, "pending_hits": 0, "victim_hits": 0, "async_writes": 0,
                       "superseded_writes": 0, "pool_wait_s": 0.0, "alloc_pinned": 0,
                       "alloc_device": 0, "alloc_s": 0.0, "read_s": 0.0, "stage_wait_s": 0.0,
-                      "validate_wait_s": 0.0, "read_file_s": 0.0, "unpack_s": 0.0, "write_async_s": 0.0}
+                      "validate_wait_s": 0.0, "read_file_s": 0.0, "unpack_s": 0.0, "write_async_s": 0.0,
+                      "disk_bytes_read": 0, "write_s": 0.0, "write_d2h_s": 0.0, "writer_pin_wait_s": 0.0, "prefetch_issued": 0, "prefetch_dropped": 0}
+        self._largest = {True: 2 * self.PINNED_SLOT_BYTES, False: 2 * self.PINNED_SLOT_BYTES}   # per pool kind
+        self._wlocal = threading.local()   # per writer thread: its D2H stream
 
     # ---------------------------------------------------------------- staging
     def _staging(self, nbytes: int):
@@ -151,10 +154,13 @@ class ChunkStreamer:
         self._arena_ready = True
         torch = self.torch
         t0 = time.perf_counter()
-        bufs = [torch.empty(self.PINNED_SLOT_BYTES, dtype=torch.uint8, pin_memory=True)
-                for _ in range(self.PINNED_SLOTS)]
-        devs = [torch.empty(self.PINNED_SLOT_BYTES, dtype=torch.uint8, device=self.slab.device)
-                for _ in range(self.DEVICE_SLOTS if self.write_behind else 0)]
+        # every 16th slot is twice the size: dense chunks (C4: the largest
+        # file is ~1.3 slots) never wait for, or allocate, a buffer
+        def size(i):
+            return self.PINNED_SLOT_BYTES * (2 if i % 16 == 15 else 1)
+        bufs = [torch.empty(size(i), dtype=torch.uint8, pin_memory=True) for i in range(self.PINNED_SLOTS)]
+        devs = [torch.empty(size(i), dtype=torch.uint8, device=self.slab.device)
+                for i in range(self.DEVICE_SLOTS if self.write_behind else 0)]
         self.device_bytes += sum(d.numel() for d in devs)
         with self._lock:
             self._free_pins.extend(bufs)
@@ -169,12 +175,13 @@ class ChunkStreamer:
         with self._lock:
             return len(self._free_pins)
 
-    def _take(self, pool: list, nbytes: int, pinned: bool):
+    def _take(self, pool: list, nbytes: int, pinned: bool, wait_stat: str = "pool_wait_s", steal: bool = True):
         """A pooled buffer of >= nbytes.  When the pool is empty: a device
         buffer is taken back from the oldest victim-cache entry, a pinned one
-        is waited for while write-behinds are in flight (they free one per
-        landed file, far sooner than page-locking a new buffer takes); only
-        then is a buffer allocated."""
+        from the oldest unclaimed prefetch (unless the caller is a prefetch
+        read itself), else it is waited for briefly while write-behinds are
+        in flight (each landed file frees one) -- under a hard HBM cap for as
+        long as it takes; only then is a buffer allocated."""
         torch = self.torch
         self._ensure_arena()
 
@@ -186,9 +193,24 @@ class ChunkStreamer:
             return best
 
         with self._lock:
-            deadline = time.perf_counter() + 2.0
+            # without a hard cap, wait for a landing write about as long as
+            # allocating would take (page-locking 32 MB: ~10-40 ms; a pooled
+            # cudaMalloc: well under that), then grow the pool
+            deadline = time.perf_counter() + (0.03 if pinned else 0.005)
             while True:
                 best = fit()
+                if best is None and pinned and steal:
+                    # speculative reads never block real I/O: take back the
+                    # buffer of the oldest finished, still unclaimed prefetch
+                    for path, fut in list(self._prefetched.items()):   # oldest first
+                        if not fut.done() or fut.exception() is not None:
+                            continue
+                        del self._prefetched[path]
+                        pool.append(fut.result().pin)
+                        self.stats["prefetch_dropped"] += 1
+                        best = fit()
+                        if best is not None:
+                            break
                 if best is None and not pinned:
                     for path in list(self._victims):   # oldest first
                         old = self._victims.pop(path)
@@ -203,9 +225,11 @@ class ChunkStreamer:
                 hard = not pinned and self.device_pool_bytes is not None
                 if not self._pending or (left <= 0 and not hard):
                     break
+                if nbytes > self._largest[pinned] and not hard:
+                    break   # no buffer in circulation fits: waiting cannot help
                 t0 = time.perf_counter()
                 self._freed.wait(timeout=left if not hard else 1.0)   # a write landing returns its buffers
-                self.stats["pool_wait_s"] += time.perf_counter() - t0
+                self.stats[wait_stat] += time.perf_counter() - t0
         size = -(-(nbytes + 4096) // self._QUANTUM) * self._QUANTUM
         if not pinned and self.device_pool_bytes is not None:
             with self._lock:   # trade free (too small) pool buffers for one that fits the cap
@@ -216,6 +240,8 @@ class ChunkStreamer:
                 raise HbmCapExceeded(f"the streamer's device pool ({self.device_pool_bytes} B of the HBM cap) "
                                      f"cannot hold another {size} B buffer")
         t0 = time.perf_counter()
+        with self._lock:
+            self._largest[pinned] = max(self._largest[pinned], size)
         if pinned:
             buf = torch.empty(size, dtype=torch.uint8, pin_memory=True)
         else:
@@ -227,14 +253,15 @@ class ChunkStreamer:
         return buf
 
     # ------------------------------------------------------------------- load
-    def _read_pinned(self, path: Path) -> PinnedFile:
+    def _read_pinned(self, path: Path, steal: bool = True) -> PinnedFile:
         size = path.stat().st_size
-        pin = self._take(self._free_pins, max(size, 1), pinned=True)
+        pin = self._take(self._free_pins, max(size, 1), pinned=True, steal=steal)
         t0 = time.perf_counter()
         with open(path, "rb", buffering=0) as f:
             got = f.readinto(memoryview(pin.numpy())[:size])
         with self._lock:
             self.stats["read_s"] += time.perf_counter() - t0
+            self.stats["disk_bytes_read"] += got
         if got != size:
             raise OSError(f"short read of {path}: {got} of {size} bytes")
         return PinnedFile(pin, size)
@@ -283,14 +310,15 @@ class ChunkStreamer:
         """Speculatively read chunk files into pinned memory (reader threads);
         never takes the last pinned buffers a load or eviction needs."""
         self._ensure_arena()
-        reserve = 8
+        reserve = max(8, self.PINNED_SLOTS // 4)   # loads and write-behinds come first
         with self._lock:
             spare = len(self._free_pins) - reserve
             for p in paths:
                 p = Path(p)
                 if p in self._prefetched or p in self._pending or spare <= 0:
                     continue
-                self._prefetched[p] = self._pool.submit(self._read_pinned, p)
+                self._prefetched[p] = self._pool.submit(self._read_pinned, p, False)
+                self.stats["prefetch_issued"] += 1
                 spare -= 1
 
     def drop_prefetch(self, path: Path) -> None:
@@ -400,21 +428,21 @@ class ChunkStreamer:
             self.stats["write_async_s"] += time.perf_counter() - t0
 
     def _write_async(self, path: Path, header: bytes, offset: int, n: int, stride: int) -> None:
-        """Write-behind eviction of slab rows [offset, offset+n) to `path`."""
+        """Write-behind eviction of slab rows [offset, offset+n) to `path`.
+
+        The compute stream packs the rows into a pooled device buffer; the
+        rest is a writer thread's: it takes a pinned buffer only when it
+        starts the write (D2H on its own stream, then the file), so the
+        write-behind backlog waits in HBM -- where a reload is served from --
+        and pinned memory is held by in-flight I/O only."""
         torch = self.torch
         nbytes = n * stride
         dev = self._take(self._free_devs, max(nbytes, 1), pinned=False)
-        pin = self._take(self._free_pins, max(nbytes, 1), pinned=True)
         if n:
             self._pack_to_device(offset, n, stride, dev)
-        cur = torch.cuda.current_stream(self.slab.device)
-        self.d2h_stream.wait_stream(cur)
         ev = torch.cuda.Event()
-        with torch.cuda.stream(self.d2h_stream):
-            if n:
-                pin[:nbytes].copy_(dev[:nbytes], non_blocking=True)
-            ev.record(self.d2h_stream)
-        pw = _PendingWrite(Path(path), header, pin, nbytes, ev, dev, stride)
+        ev.record(torch.cuda.current_stream(self.slab.device))
+        pw = _PendingWrite(Path(path), header, None, nbytes, ev, dev, stride)
         with self._lock:
             self._release_superseded(self._pending.get(pw.path))
             self._pending[pw.path] = pw
@@ -473,9 +501,9 @@ class ChunkStreamer:
                 self._writer_error = exc
                 failed = True
             if pw.event is not None:
-                # a superseded write skipped its wait: the D2H may still be
-                # reading `dev` / filling `pin`, so neither goes back to a pool
-                # before it completes
+                # a superseded write skipped its wait: the pack (or fill)
+                # kernel may still be writing `dev` / `pin`, so neither goes
+                # back to a pool before it completes
                 pw.event.synchronize()
             self._settle(pw, failed)
             pw.done.set()
@@ -487,8 +515,27 @@ class ChunkStreamer:
         if stale:
             self.stats["superseded_writes"] += 1
             return
-        if pw.event is not None:
-            pw.event.synchronize()   # the D2H copy of the packed records
+        if pw.dev is not None and pw.pin is None:   # chunk: D2H of the packed records now
+            t0 = time.perf_counter()
+            pin = self._take(self._free_pins, max(pw.nbytes, 1), pinned=True, wait_stat="writer_pin_wait_s")
+            t1 = time.perf_counter()
+            torch = self.torch
+            stream = getattr(self._wlocal, "stream", None)
+            if stream is None:
+                stream = self._wlocal.stream = torch.cuda.Stream(device=self.slab.device)
+            with torch.cuda.stream(stream):
+                stream.wait_event(pw.event)   # the pack kernel
+                if pw.nbytes:
+                    pin[:pw.nbytes].copy_(pw.dev[:pw.nbytes], non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(stream)
+            pw.pin = pin
+            done.synchronize()
+            with self._lock:
+                self.stats["write_d2h_s"] += time.perf_counter() - t1
+        elif pw.event is not None:
+            pw.event.synchronize()   # the kernel that filled the pinned buffer
+        t0 = time.perf_counter()
         tmp = pw.path.with_name(f"{pw.path.name}.{threading.get_ident()}.tmp")
         with open(tmp, "wb") as f:   # straight from pinned memory, no bytes copy
             if pw.make is not None:
@@ -500,6 +547,7 @@ class ChunkStreamer:
             current = self._pending.get(pw.path) is pw
             if current:
                 tmp.replace(pw.path)
+            self.stats["write_s"] += time.perf_counter() - t0
         if not current:
             tmp.unlink(missing_ok=True)
 

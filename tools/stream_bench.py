@@ -29,6 +29,7 @@ import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parent))
 
 
 def run(mode: str, scene, poses, frames, args):
@@ -111,6 +112,8 @@ def main():
     ap.add_argument("--writers", type=int, default=4, help="write-behind threads")
     ap.add_argument("--modes", default="resident,sync,streamed")
     ap.add_argument("--profile", action="store_true", help="cProfile each run (host hot spots to stderr)")
+    ap.add_argument("--repeat", type=int, default=1,
+                    help="run the modes this many times, interleaved; each mode reports its median run")
     args = ap.parse_args()
     import torch
 
@@ -130,25 +133,43 @@ def main():
     # warm-up (library init, kernels, allocator): a short resident run, discarded
     warm = argparse.Namespace(**{**vars(args), "steps": 2})
     run("resident", scene, poses[:5], frames[:5], warm)
-    for mode in args.modes.split(","):
+    runs: dict[str, list] = {}
+    for mode in [m for _ in range(args.repeat) for m in args.modes.split(",")]:
         if args.profile:
             import cProfile
             import io
             import pstats
             pr = cProfile.Profile()
             pr.enable()
-        res[mode] = run(mode, scene, poses, frames, args)
+        out = run(mode, scene, poses, frames, args)
+        runs.setdefault(mode, []).append(out)
         if args.profile:
             pr.disable()
             buf = io.StringIO()
             pstats.Stats(pr, stream=buf).sort_stats("tottime").print_stats(25)
             print(f"==== {mode}\n" + buf.getvalue(), file=sys.stderr)
-        print(json.dumps(res[mode]), file=sys.stderr, flush=True)
-    line = {"workload": f"C4-lite: {args.n} splats over {args.length:.0f} m (s = 10 m), 1241x376, "
+        print(json.dumps({k: v for k, v in out.items() if k != "trace"}), file=sys.stderr, flush=True)
+    for mode, rs in runs.items():
+        rs = sorted(rs, key=lambda r: r["seconds"])
+        res[mode] = rs[len(rs) // 2]
+        res[mode]["seconds_all"] = [r["seconds"] for r in rs]
+        if any(r["trace"] != rs[0]["trace"] for r in rs):
+            res[mode]["repeat_diverged"] = True
+    from stress_bench import disk_bandwidth
+    bw_root = Path(tempfile.mkdtemp(prefix="c4_bw_"))
+    disk = disk_bandwidth(bw_root)
+    shutil.rmtree(bw_root, ignore_errors=True)
+    name = "C4" if args.n >= 20_000_000 else "C4-lite"
+    line = {"disk": disk, "workload": f"{name}: {args.n} splats over {args.length:.0f} m (s = 10 m), 1241x376, "
                         f"budget {args.budget}, {args.keyframes} keyframes x {args.steps} steps",
             "runs": res}
     if "resident" in res and "streamed" in res:
         line["overlap"] = res["resident"]["seconds"] / res["streamed"]["seconds"]
+        # what the disk alone forces: every write-back has to reach it (reads
+        # of recently written chunks may come from the page cache: not counted)
+        floor = max(res["resident"]["seconds"], res["streamed"]["bytes_written"] / disk["write_gbs"] / 1e9)
+        line["disk_floor_seconds"] = floor
+        line["vs_disk_floor"] = floor / res["streamed"]["seconds"]
     traces = {m: r.pop("trace") for m, r in res.items()}
     base = next(iter(traces.values()))
     line["same_training"] = {m: t == base for m, t in traces.items()}
