@@ -290,7 +290,10 @@ class ChunkStreamer:
             vic = self._victims.get(path)
             if vic is not None:
                 self._victims.move_to_end(path)
-            fut = self._prefetched.pop(path, None) if pw is None and vic is None else None
+            fut = self._prefetched.pop(path, None)
+        if fut is not None and (pw is not None or vic is not None):   # served from HBM: the read was moot
+            fut.add_done_callback(lambda f: f.exception() is None and self.release(f.result()))
+            fut = None
         if pw is not None:
             self.stats["pending_hits"] += 1
             return DeviceRecords(pw.header, pw.dev, pw.nbytes, pw.stride)
@@ -308,15 +311,26 @@ class ChunkStreamer:
 
     def prefetch(self, paths) -> None:
         """Speculatively read chunk files into pinned memory (reader threads);
-        never takes the last pinned buffers a load or eviction needs."""
+        never takes the last pinned buffers a load or eviction needs.  The
+        prefetch tier is FIFO: when it is full, the oldest finished,
+        unclaimed reads make room for the newer speculation."""
         self._ensure_arena()
         reserve = max(8, self.PINNED_SLOTS // 4)   # loads and write-behinds come first
+        paths = [Path(p) for p in paths]
+        asked = set(paths)
         with self._lock:
             spare = len(self._free_pins) - reserve
             for p in paths:
-                p = Path(p)
-                if p in self._prefetched or p in self._pending or spare <= 0:
+                if p in self._prefetched or p in self._pending or p in self._victims:
                     continue
+                if spare <= 0:
+                    old = next((q for q, f in self._prefetched.items()
+                                if q not in asked and f.done() and f.exception() is None), None)
+                    if old is None:
+                        break
+                    self._free_pins.append(self._prefetched.pop(old).result().pin)
+                    self.stats["prefetch_dropped"] += 1
+                    spare += 1
                 self._prefetched[p] = self._pool.submit(self._read_pinned, p, False)
                 self.stats["prefetch_issued"] += 1
                 spare -= 1
