@@ -126,7 +126,8 @@ class ChunkStreamer:
                       "validate_wait_s": 0.0, "read_file_s": 0.0, "unpack_s": 0.0, "write_async_s": 0.0,
                       "disk_bytes_read": 0, "write_s": 0.0, "write_d2h_s": 0.0, "writer_pin_wait_s": 0.0, "prefetch_issued": 0, "prefetch_dropped": 0}
         self._largest = {True: 2 * self.PINNED_SLOT_BYTES, False: 2 * self.PINNED_SLOT_BYTES}   # per pool kind
-        self._wlocal = threading.local()   # per writer thread: its D2H stream
+        self._wlocal = threading.local()
+        self._rename_locks = [threading.Lock() for _ in range(64)]   # per writer thread: its D2H stream
 
     # ---------------------------------------------------------------- staging
     def _staging(self, nbytes: int):
@@ -557,10 +558,16 @@ class ChunkStreamer:
             else:
                 f.write(pw.header)
                 f.write(memoryview(pw.pin.numpy())[:pw.nbytes])
-        with self._lock:   # several writers: only the newest write of a path lands
-            current = self._pending.get(pw.path) is pw
+        # several writers: only the newest write of a path lands.  The rename
+        # (milliseconds on some filesystems) holds only the path's stripe
+        # lock, never the streamer lock the paging path needs: a newer write
+        # of the same path renames after this one, under the same stripe
+        with self._rename_locks[hash(pw.path) % len(self._rename_locks)]:
+            with self._lock:
+                current = self._pending.get(pw.path) is pw
             if current:
                 tmp.replace(pw.path)
+        with self._lock:
             self.stats["write_s"] += time.perf_counter() - t0
         if not current:
             tmp.unlink(missing_ok=True)

@@ -32,7 +32,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 sys.path.insert(0, str(Path(__file__).resolve().parent))
 
 
-def run(mode: str, scene, poses, frames, args):
+def run(mode: str, scene, poses, frames, args, prof=None):
     import torch
 
     from paper_2511_23030_b200.core import Keyframe
@@ -71,15 +71,52 @@ def run(mode: str, scene, poses, frames, args):
     kfs = [Keyframe(id=k, pose=pose, intrinsics=C4_INTR, rgb=rgb, depth=depth)
            for k, (pose, (rgb, depth)) in enumerate(zip(poses, frames))]
     torch.cuda.synchronize()
+    if prof is not None:   # the timed loop only
+        prof.enable()
+    import gc
+    gc_t = [0.0, 0, 0.0]   # total, collections, longest
+
+    def gc_cb(phase, info, _t=[0.0]):
+        if phase == "start":
+            _t[0] = time.perf_counter()
+        else:
+            d = time.perf_counter() - _t[0]
+            gc_t[0] += d
+            gc_t[1] += 1
+            gc_t[2] = max(gc_t[2], d)
+    gc.callbacks.append(gc_cb)
     t0 = time.perf_counter()
     steps = 0
+    step_t = []   # host wall time of every step (where streaming costs show up)
+    eager_at = []
+    add_t = 0.0
     for k, (pose, kf) in enumerate(zip(poses, kfs)):
+        ta = time.perf_counter()
         eng.add_keyframe(kf)   # the engine itself prefetches (new keyframe, next draw's candidates)
+        tb = time.perf_counter()
+        add_t += tb - ta
         for s in range(args.steps):
+            e0 = eng.counter_eager
             eng.optimization_step(k, s)
+            eager_at.append(eng.counter_eager - e0)
+            tc = time.perf_counter()
+            step_t.append(tc - tb)
+            tb = tc
             steps += 1
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    if prof is not None:
+        prof.disable()
+    gc.callbacks.remove(gc_cb)
+    import numpy as np
+    st_ = np.sort(np.asarray(step_t))
+    step_stats = {"add_keyframe_s": add_t, "step_ms_p50": 1e3 * float(np.median(st_)),
+                  "step_ms_p90": 1e3 * float(st_[int(0.9 * len(st_))]),
+                  "step_ms_p99": 1e3 * float(st_[int(0.99 * len(st_))]), "step_ms_max": 1e3 * float(st_[-1]),
+                  "slowest_5pct_s": float(st_[int(0.95 * len(st_)):].sum()),
+                  "slowest_steps": [(int(i), round(1e3 * step_t[i], 2), eager_at[i])
+                                    for i in np.argsort(step_t)[::-1][:6]],
+                  "gc_s": gc_t[0], "gc_collections": gc_t[1], "gc_longest_ms": 1e3 * gc_t[2]}
     st = store.stats
     out = {"mode": mode, "seconds": dt, "steps": steps, "steps_per_s": steps / dt,
            "chunk_loads": st.chunk_loads - loads0, "chunk_evictions": st.chunk_evictions - ev0,
@@ -87,7 +124,7 @@ def run(mode: str, scene, poses, frames, args):
            "bytes_written": st.bytes_written - wb0, "active_gaussians_end": st.active_gaussians,
            "mean_visible": eng.counter_gaussians / max(eng.counter_steps, 1),
            "ensure_resident_s": blocked[0], "graph_replays": eng.counter_replays,
-           "eager_steps": eng.counter_eager,
+           "eager_steps": eng.counter_eager, **step_stats,
            # the training itself must not depend on the paging: the (keyframe,
            # loss) sequence of every mode is compared in main()
            "trace": [(r.selected_kf, r.loss) for r in eng.rows]}
@@ -135,19 +172,19 @@ def main():
     run("resident", scene, poses[:5], frames[:5], warm)
     runs: dict[str, list] = {}
     for mode in [m for _ in range(args.repeat) for m in args.modes.split(",")]:
+        pr = None
         if args.profile:
             import cProfile
             import io
             import pstats
             pr = cProfile.Profile()
-            pr.enable()
-        out = run(mode, scene, poses, frames, args)
+        out = run(mode, scene, poses, frames, args, pr)
         runs.setdefault(mode, []).append(out)
         if args.profile:
-            pr.disable()
-            buf = io.StringIO()
-            pstats.Stats(pr, stream=buf).sort_stats("tottime").print_stats(25)
-            print(f"==== {mode}\n" + buf.getvalue(), file=sys.stderr)
+            for key in ("tottime", "cumulative"):
+                buf = io.StringIO()
+                pstats.Stats(pr, stream=buf).sort_stats(key).print_stats(30)
+                print(f"==== {mode} ({key})\n" + buf.getvalue(), file=sys.stderr)
         print(json.dumps({k: v for k, v in out.items() if k != "trace"}), file=sys.stderr, flush=True)
     for mode, rs in runs.items():
         rs = sorted(rs, key=lambda r: r["seconds"])
