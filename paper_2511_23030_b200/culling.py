@@ -225,7 +225,10 @@ class VisibilityCache:
 
     def query(self, pose: Pose, intr: CameraIntrinsics, extent: ChunkExtent,
               existing: Callable[[int], bool], generation: int, s: float,
-              candidates: Iterable[int] | None = None) -> tuple[set[int], bool]:
+              candidates: Iterable[int] | None = None,
+              compute: Callable[[], set[int] | None] | None = None) -> tuple[set[int], bool]:
+        """compute: on a miss, a caller-held visible set of this very pose and
+        chunk set (e.g. computed for a speculative read), else None."""
         # Most recent matching entry, as the reference scan (culling.py:213-229).
         # A vectorised distance prefilter (with a relative margin) limits the
         # exact per-entry test to plausible entries; the verdict is the exact one.
@@ -244,9 +247,11 @@ class VisibilityCache:
                 if self._match_fast(e, d, qa, pose, intr, generation, s):
                     self._entries.append(self._entries.pop(i))
                     return set(e.result), True
-        if callable(candidates):   # built only on a miss
-            candidates = candidates()
-        result = visible_chunks(pose, intr, extent, existing, self.cfg, s, candidates)
+        result = compute() if compute is not None else None
+        if result is None:
+            if callable(candidates):   # built only on a miss
+                candidates = candidates()
+            result = visible_chunks(pose, intr, extent, existing, self.cfg, s, candidates)
         self._entries.append(_CacheEntry(pose.translation.copy(), pose.rotation.copy(), intr, s,
                                          generation, frozenset(result),
                                          tuple(float(v) for v in pose.translation),

@@ -386,9 +386,14 @@ class MappingEngine:
         ext = self.store.coord_extent()
         if ext is None:
             return set(), False
+        memo = self._view_memo
+        key = (pose.translation.tobytes(), pose.rotation.tobytes(), self.store.generation)
         return self.cache.query(pose, self.intr, ChunkExtent(*ext), self.store.has_chunk,
                                 self.store.generation, self.store.chunk_size,
-                                candidates=self.store.known_chunk_ids)
+                                candidates=self.store.known_chunk_ids,
+                                compute=lambda: set(memo[1]) if memo is not None and memo[0] == key else None)
+
+    _view_memo = None   # (pose bytes, chunk-set generation) -> the visible set _prefetch_view culled
 
     # ------------------------------------------------------------ device
     # single-keyframe steps: Adam fused into the backward (sm_render_backward_adam).  Measured
@@ -516,6 +521,10 @@ class MappingEngine:
             return
         vis = visible_chunks(pose, self.intr, ChunkExtent(*ext), store.has_chunk, self.cull_cfg,
                              store.chunk_size, candidates=store.known_chunk_ids())
+        # the step that first draws this keyframe misses the visibility cache
+        # with exactly this pose and chunk set: it takes this set, not a second cull
+        self._view_memo = ((pose.translation.tobytes(), pose.rotation.tobytes(), store.generation),
+                           frozenset(vis))
         store.prefetch(sorted(vis))
 
     def _precompute_next_draw(self) -> None:

@@ -39,13 +39,17 @@ from .errors import CorruptChunk, IoFailure
 
 
 class _PendingWrite:
-    __slots__ = ("path", "header", "pin", "nbytes", "event", "done", "dev", "stride", "make", "cache")
+    __slots__ = ("path", "header", "pin", "nbytes", "event", "done", "dev", "stride", "make", "cache",
+                 "inline", "borrowers", "settled")
 
     def __init__(self, path, header, pin, nbytes, event, dev, stride, make=None, cache=True):
         self.path, self.header, self.pin, self.nbytes = path, header, pin, nbytes
         self.event, self.dev, self.stride = event, dev, stride
         self.make = make   # host-built file (keyframes): bytes produced on the writer thread
         self.cache = cache   # keep the device bytes in the victim cache once written (chunks)
+        self.inline = False   # pin holds the whole file (header + records), D2H issued at eviction
+        self.borrowers = 0   # reloads reading `pin` right now (it returns to the pool after them)
+        self.settled = False
         self.done = threading.Event()
 
 
@@ -58,6 +62,16 @@ class PinnedFile:
 
     def view(self) -> np.ndarray:
         return self.pin[:self.size].numpy()
+
+
+class BorrowedPinned(PinnedFile):
+    """A pending write-behind's pinned file bytes lent to a reload (capped
+    stores, whose device copy already went back to the pool)."""
+    __slots__ = ("pw",)
+
+    def __init__(self, pw):
+        super().__init__(pw.pin, len(pw.header) + pw.nbytes)
+        self.pw = pw
 
 
 class DeviceRecords:
@@ -124,10 +138,12 @@ class ChunkStreamer:
                       "superseded_writes": 0, "pool_wait_s": 0.0, "alloc_pinned": 0,
                       "alloc_device": 0, "alloc_s": 0.0, "read_s": 0.0, "stage_wait_s": 0.0,
                       "validate_wait_s": 0.0, "read_file_s": 0.0, "unpack_s": 0.0, "write_async_s": 0.0,
-                      "disk_bytes_read": 0, "write_s": 0.0, "write_d2h_s": 0.0, "writer_pin_wait_s": 0.0, "prefetch_issued": 0, "prefetch_dropped": 0}
+                      "disk_bytes_read": 0, "write_s": 0.0, "write_d2h_s": 0.0, "writer_pin_wait_s": 0.0, "prefetch_issued": 0, "prefetch_dropped": 0, "pending_pinned_hits": 0}
         self._largest = {True: 2 * self.PINNED_SLOT_BYTES, False: 2 * self.PINNED_SLOT_BYTES}   # per pool kind
         self._wlocal = threading.local()
-        self._rename_locks = [threading.Lock() for _ in range(64)]   # per writer thread: its D2H stream
+        self._rename_locks = [threading.Lock() for _ in range(64)]
+        self._early: list = []   # capped stores: write-behinds whose device copy is still held
+        self._d2h = torch.cuda.Stream(device=slab.device)   # capped stores: eviction D2H   # per writer thread: its D2H stream
 
     # ---------------------------------------------------------------- staging
     def _staging(self, nbytes: int):
@@ -212,6 +228,9 @@ class ChunkStreamer:
                         best = fit()
                         if best is not None:
                             break
+                if best is None and not pinned and self._early:
+                    self._reclaim_early()
+                    best = fit()
                 if best is None and not pinned:
                     for path in list(self._victims):   # oldest first
                         old = self._victims.pop(path)
@@ -229,7 +248,9 @@ class ChunkStreamer:
                 if nbytes > self._largest[pinned] and not hard:
                     break   # no buffer in circulation fits: waiting cannot help
                 t0 = time.perf_counter()
-                self._freed.wait(timeout=left if not hard else 1.0)   # a write landing returns its buffers
+                # a write landing returns its buffers (a completed eviction
+                # D2H does not notify: poll for those)
+                self._freed.wait(timeout=left if not hard else (0.0005 if self._early else 1.0))
                 self.stats[wait_stat] += time.perf_counter() - t0
         size = -(-(nbytes + 4096) // self._QUANTUM) * self._QUANTUM
         if not pinned and self.device_pool_bytes is not None:
@@ -269,7 +290,15 @@ class ChunkStreamer:
 
     def release(self, src) -> None:
         """Return a PinnedFile's buffer to the pool (after its H2D completed)."""
-        if isinstance(src, PinnedFile):
+        if isinstance(src, BorrowedPinned):
+            with self._lock:
+                pw = src.pw
+                pw.borrowers -= 1
+                if pw.borrowers == 0 and pw.settled and pw.pin is not None:
+                    self._free_pins.append(pw.pin)
+                    pw.pin = None
+                    self._freed.notify_all()
+        elif isinstance(src, PinnedFile):
             with self._lock:
                 self._free_pins.append(src.pin)
                 self._freed.notify_all()
@@ -297,7 +326,14 @@ class ChunkStreamer:
             fut = None
         if pw is not None:
             self.stats["pending_hits"] += 1
-            return DeviceRecords(pw.header, pw.dev, pw.nbytes, pw.stride)
+            with self._lock:
+                dev = pw.dev
+                if dev is None:   # capped store: the device copy is back in the pool,
+                    pw.borrowers += 1   # the pinned one (D2H completed) serves the reload
+            if dev is None:
+                self.stats["pending_pinned_hits"] += 1
+                return BorrowedPinned(pw)
+            return DeviceRecords(pw.header, dev, pw.nbytes, pw.stride)
         if vic is not None:
             self.stats["victim_hits"] += 1
             return vic
@@ -456,8 +492,25 @@ class ChunkStreamer:
         if n:
             self._pack_to_device(offset, n, stride, dev)
         ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream(self.slab.device))
-        pw = _PendingWrite(Path(path), header, None, nbytes, ev, dev, stride)
+        cur = torch.cuda.current_stream(self.slab.device)
+        if self.device_pool_bytes is None:
+            ev.record(cur)
+            pw = _PendingWrite(Path(path), header, None, nbytes, ev, dev, stride)
+        else:
+            # hard HBM cap: the device share is small, so the backlog waits in
+            # pinned memory -- copy down now; the device buffer returns to the
+            # pool as soon as that copy completed (_reclaim_early)
+            h = len(header)
+            pin = self._take(self._free_pins, h + max(nbytes, 1), pinned=True)
+            pin[:h].numpy()[:] = np.frombuffer(header, dtype=np.uint8)
+            self._d2h.wait_stream(cur)
+            with torch.cuda.stream(self._d2h):
+                if n:
+                    pin[h:h + nbytes].copy_(dev[:nbytes], non_blocking=True)
+                ev.record(self._d2h)
+            pw = _PendingWrite(Path(path), header, pin, nbytes, ev, dev, stride, cache=False)
+            pw.inline = True
+            self._early.append(pw)
         with self._lock:
             self._release_superseded(self._pending.get(pw.path))
             self._pending[pw.path] = pw
@@ -468,6 +521,21 @@ class ChunkStreamer:
         self.bytes_d2h += nbytes
         self.stats["async_writes"] += 1
         self._queue.put(pw)
+
+    def _reclaim_early(self) -> None:   # caller holds the lock
+        """Capped stores: device buffers of write-behinds whose D2H completed
+        go back to the pool (reloads of those chunks read the pinned copy)."""
+        if not self._early:
+            return
+        keep = []
+        for pw in self._early:
+            if pw.event.query():
+                if pw.dev is not None:
+                    self._free_devs.append(pw.dev)
+                    pw.dev = None
+            else:
+                keep.append(pw)
+        self._early = keep
 
     def write_file_async(self, path: Path, nbytes: int, fill) -> None:
         """Write-behind of a file assembled by a kernel: fill(pin) writes its
@@ -555,6 +623,8 @@ class ChunkStreamer:
         with open(tmp, "wb") as f:   # straight from pinned memory, no bytes copy
             if pw.make is not None:
                 f.write(pw.make())
+            elif pw.inline:
+                f.write(memoryview(pw.pin.numpy())[:len(pw.header) + pw.nbytes])
             else:
                 f.write(pw.header)
                 f.write(memoryview(pw.pin.numpy())[:pw.nbytes])
@@ -586,21 +656,24 @@ class ChunkStreamer:
             landed = current and not failed
             if current:
                 del self._pending[pw.path]
-            if pw.pin is not None:
+            pw.settled = True
+            if pw.pin is not None and pw.borrowers == 0:   # (else the last borrower returns it)
                 self._free_pins.append(pw.pin)
+                pw.pin = None
             self._freed.notify_all()   # (waiters run once this block releases the lock)
-            if pw.dev is None:
+            dev, pw.dev = pw.dev, None
+            if dev is None:
                 pass
             elif landed and pw.cache and self.victim_limit > 0:   # keep the packed bytes in HBM
                 self._drop_victim(pw.path)
-                self._victims[pw.path] = DeviceRecords(pw.header, pw.dev, pw.nbytes, pw.stride)
-                self._victim_bytes += pw.dev.numel()
+                self._victims[pw.path] = DeviceRecords(pw.header, dev, pw.nbytes, pw.stride)
+                self._victim_bytes += dev.numel()
                 while self._victim_bytes > self.victim_limit and self._victims:
                     _, old = self._victims.popitem(last=False)
                     self._victim_bytes -= old.dev.numel()
                     self._free_devs.append(old.dev)
             else:
-                self._free_devs.append(pw.dev)
+                self._free_devs.append(dev)
 
     def _drop_victim(self, path: Path) -> None:   # caller holds the lock
         old = self._victims.pop(path, None)
@@ -639,10 +712,13 @@ class ChunkStreamer:
         return to the pools (its D2H completed before it was attempted)."""
         if old is not None and old in self._failed:
             self._failed.remove(old)
-            if old.pin is not None:
+            old.settled = True
+            if old.pin is not None and old.borrowers == 0:
                 self._free_pins.append(old.pin)
+                old.pin = None
             if old.dev is not None:
                 self._free_devs.append(old.dev)
+                old.dev = None
 
     def drain(self) -> None:
         """Block until every pending write reached the disk (flush point).

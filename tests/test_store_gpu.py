@@ -432,6 +432,68 @@ def test_streamer_under_pool_pressure_matches_sync(cuda, tmp_path):
         assert (tmp_path / "sync" / "chunks" / name).read_bytes() == (tmp_path / "tight" / "chunks" / name).read_bytes()
 
 
+def test_capped_write_behind_backlog_in_pinned_memory(cuda, tmp_path):
+    """Under a hard HBM cap the eviction D2H is issued at eviction and the
+    device buffer goes back to the small pool once it completed; a chunk
+    reloaded while its write is still queued is served from the pinned copy.
+    With the writers held back (every write pending), the paging sequence
+    still matches synchronous I/O row for row and, once the writers run,
+    byte for byte on disk."""
+    import threading
+
+    import torch
+
+    from paper_2511_23030_b200.core import Gaussian, quat_normalize
+    from paper_2511_23030_b200.store import ChunkStore, StoreConfig
+    rng = np.random.default_rng(23)
+    gs = []
+    for cx in range(8):   # eight chunks of 300
+        for _ in range(300):
+            gs.append(Gaussian(position=[cx * 10.0 + rng.uniform(-4, 4), rng.uniform(-4, 4), rng.uniform(-4, 4)],
+                               rotation=quat_normalize(rng.normal(size=4)), scale=rng.uniform(0.01, 0.2, 3),
+                               opacity=float(rng.uniform(0, 1)), sh=rng.normal(size=48)))
+    sync = ChunkStore(StoreConfig(disk_root=tmp_path / "sync", chunk_size_m=10.0, gaussian_budget=900,
+                                  io_ns_per_byte=1.0, write_behind=False))
+    capped = ChunkStore(StoreConfig(disk_root=tmp_path / "capped", chunk_size_m=10.0, gaussian_budget=900,
+                                    io_ns_per_byte=1.0, hbm_cap_bytes=1 << 30))
+    gate = threading.Event()
+    orig = capped.streamer._write_one
+
+    def held(pw):
+        gate.wait()
+        return orig(pw)
+    capped.streamer._write_one = held
+    stores = (sync, capped)
+    try:
+        for st in stores:
+            st.insert_gaussians(gs)
+        ids = sorted(sync.known_chunk_ids())
+        order = np.random.default_rng(5).integers(0, len(ids), size=(30, 3))
+        for step, pick in enumerate(order):
+            want = sorted({ids[int(k)] for k in pick})
+            for st in stores:
+                st.ensure_resident(want)
+                for c in want:
+                    ch = st.chunk(c)
+                    st.slab.params[ch.offset:ch.offset + ch.count, 0] += 1e-3 * (step + 1)
+                st.mark_trained(want)
+            assert _stats(sync) == _stats(capped)
+            for c in want:
+                a, b = sync.chunk(c), capped.chunk(c)
+                assert torch.equal(sync.slab.params[a.offset:a.offset + a.count],
+                                   capped.slab.params[b.offset:b.offset + b.count])
+        stats = capped.streamer.stats
+        assert stats["pending_pinned_hits"] > 0, stats
+    finally:
+        gate.set()
+    for st in stores:
+        st.flush()
+    for c in ids:
+        name = f"{c:016x}.dcg"
+        assert (tmp_path / "sync" / "chunks" / name).read_bytes() == \
+               (tmp_path / "capped" / "chunks" / name).read_bytes()
+
+
 def test_write_through_views_match_reference_bytes(cuda, tmp_path):
     """chunk.gaussians / gather_visible are live views (store.py:361-379): the
     reference's refine_reset loop (loopclose.py:236-242), nudge-style in-place
