@@ -24,8 +24,17 @@ constexpr int kTilePx = kTile * kTile;     // 256 threads per tile CTA
 
 // 64-byte per-Gaussian screen-space record, produced by the projection
 // (renderloss.py:176-201) and consumed by compositing (renderloss.py:106-152).
-// dx for pixel px is (px - x0) + ox with ox = x0 - u computed in fp64, so
-// the fp32 offset keeps ~1e-7 relative precision whatever |u| is.
+// Compositing evaluates the quadratic form expanded around the box corner
+// (x0, y0): qa and (hax, hay) = the form and half its gradient there
+// (stage_anchor, when a tile stages the splat) and pw = qa + cx (hx + hax) +
+// cy (hy + hay), (cx, cy) = the pixel's integer offset from the corner,
+// (hx, hy) = C (x - u).  No fp32 term carries the centre offset: a splat next
+// to the near plane has its centre ~1e5 px off screen, and the direct form
+// dx (ia dx + 2 ib dy) + ic dy^2 with dx = (px - x0) + ox lost ~1e-3 of q to
+// cancellation there (a full-size C4 view's opacity gradients were 1.8e-3
+// off; ~3e-7 with the expansion).  ox = x0 - u (fp64-rounded) feeds the
+// binning's row spans, the backward's conic gradients (products, no
+// cancellation) and the anchors of ordinary splats.
 struct __align__(16) ProjRec {
     float ox, oy;          // x0 - u, y0 - v
     float ia, ib, ic;      // conic (c, -b, a)/det pre-scaled by kPowScale (log2 units)
@@ -38,6 +47,7 @@ struct __align__(16) ProjRec {
     float beta, G, K;      // ellipse row extent (RowSpan); K <= 0: whole bbox rows
 };
 static_assert(sizeof(ProjRec) == 64, "ProjRec must be 64 bytes");
+constexpr double kAnchorPx = 64.0;
 
 // fp64 side copy for decisions near the q = 9 cutoff (hard part 1)
 struct Proj64 {
@@ -139,6 +149,29 @@ __device__ __forceinline__ double quad_q64(const Proj64 &p, int px, int py) {
 constexpr double kPowScale = -0.72134752044448170368;   // -0.5 * log2(e)
 constexpr float kPowCut = (float)(9.0 * -0.72134752044448170368);
 
+// The corner expansion's {qa, hax, hay} (see ProjRec).  For a splat whose
+// corner lies within kAnchorPx of its centre, fp32 from (ox, oy) is as exact
+// as the direct form was; beyond that (huge splats, rare) fp64 from the
+// Proj64 side record with explicit roundings.  Both compositing kernels stage
+// identical values.
+__device__ __forceinline__ float4 anchor_of(const Proj64 &p, int x0, int y0) {
+    const double dax = __dsub_rn((double)x0, p.u), day = __dsub_rn((double)y0, p.v);
+    const double sia = __dmul_rn(kPowScale, p.ia), sib = __dmul_rn(kPowScale, p.ib);
+    const double sic = __dmul_rn(kPowScale, p.ic);
+    const double hax = __dadd_rn(__dmul_rn(sia, dax), __dmul_rn(sib, day));
+    const double hay = __dadd_rn(__dmul_rn(sib, dax), __dmul_rn(sic, day));
+    const double qa = __dadd_rn(__dmul_rn(dax, hax), __dmul_rn(day, hay));
+    return make_float4((float)qa, (float)hax, (float)hay, 0.f);
+}
+
+__device__ __forceinline__ float4 stage_anchor(const ProjRec &r, const Proj64 *p64, const uint32_t *order,
+                                              uint32_t rank) {
+    if (fabsf(r.ox) > (float)kAnchorPx || fabsf(r.oy) > (float)kAnchorPx)
+        return anchor_of(p64[order[rank]], rec_x0(r), rec_y0(r));
+    const float hax = fmaf(r.ia, r.ox, r.ib * r.oy), hay = fmaf(r.ib, r.ox, r.ic * r.oy);
+    return make_float4(fmaf(r.ox, hax, r.oy * hay), hax, hay, 0.f);
+}
+
 // Packed fp32x2 arithmetic (sm_100 FFMA2 / FMUL2 / FADD2): two pixels' math
 // per issue slot in the compositing kernels.
 __device__ __forceinline__ float2 f2s(float a) { return make_float2(a, a); }
@@ -173,9 +206,9 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 // The q <= 9 decision (renderloss.py:141) both compositing kernels take for
-// pixel (px, py) inside a splat's box: pw = dx (ia dx + 2 ib dy) + ic dy^2 in
-// fp32 (dx = (px - x0) + ox, dy = (py - y0) + oy); when |pw - kPowCut| lies
-// within the splat's error band eps the exact fp64 quad_q64 decides.  The
+// pixel (px, py) inside a splat's box: pw from the corner expansion in fp32
+// (see ProjRec); when |pw - kPowCut| lies within the splat's error band eps
+// the exact fp64 quad_q64 decides.  The
 // forward and the backward evaluate pw in different (fp32 / packed fp32x2)
 // orders; outside the band both equal the exact verdict, inside it both use
 // quad_q64, so they always agree.

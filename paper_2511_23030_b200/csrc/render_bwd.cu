@@ -119,8 +119,8 @@ struct BwdPair {
 
     // d{u v ia ib ic op r g b z} of splat g (instance position k) summed over
     // the pair into v[0..9]; then one step back.
-    __device__ __forceinline__ void step(const ProjRec &g, float dx, float2 dy, float2 pw, bool h0,
-                                         bool h1, int k, float (&v)[16]) {
+    __device__ __forceinline__ void step(const ProjRec &g, float dx, float2 dy, float2 pw, float2 hx,
+                                         float2 hy, bool h0, bool h1, int k, float (&v)[16]) {
         const float2 G = make_float2(h0 ? ex2_approx(pw.x) : 0.f, h1 ? ex2_approx(pw.y) : 0.f);
         const float2 alpha = mul2(G, f2s(g.op));
         const float2 oma = sub2(f2s(1.f), alpha);
@@ -148,8 +148,8 @@ struct BwdPair {
         v[3] = hsum(mul2(mul2(gqdx, f2s(2.f)), dy));
         v[4] = hsum(mul2(mul2(gq, dy), dy));
         const float2 gqi = mul2(gq, f2s((float)(-2.0 / kPowScale)));
-        v[0] = hsum(mul2(gqi, fma2(f2s(g.ib), dy, f2s(g.ia * dx))));
-        v[1] = hsum(mul2(gqi, fma2(f2s(g.ic), dy, f2s(g.ib * dx))));
+        v[0] = hsum(mul2(gqi, hx));   // C (x - u), from the corner expansion
+        v[1] = hsum(mul2(gqi, hy));
         Br = fma2(alpha, f2s(g.r), mul2(oma, Br));
         Bg = fma2(alpha, f2s(g.g), mul2(oma, Bg));
         Bb = fma2(alpha, f2s(g.b), mul2(oma, Bb));
@@ -193,6 +193,7 @@ composite_bwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
     constexpr int NW = NT / 32;
     __shared__ ProjRec s_rec[NT];
     __shared__ uint32_t s_rank[NT];
+    __shared__ float4 s_anch[NT];   // {qa, hax, hay, -}: the corner expansion (stage_anchor)
     __shared__ float s_part[NW][NT][10];
     __shared__ int s_maxlast;
     const int warp = threadIdx.x / 32;
@@ -233,7 +234,9 @@ composite_bwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
         if (idx < bend) {
             const uint32_t rk = (uint32_t)(ikeys[idx] & rank_mask);
             s_rank[threadIdx.x] = rk;
-            s_rec[threadIdx.x] = recs[rk];
+            const ProjRec r = recs[rk];
+            s_rec[threadIdx.x] = r;
+            s_anch[threadIdx.x] = stage_anchor(r, p64, order, rk);
         }
         for (int i = threadIdx.x; i < NW * NT * 10; i += NT) (&s_part[0][0][0])[i] = 0.f;
         __syncthreads();
@@ -246,23 +249,30 @@ composite_bwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
             const int x0 = rec_x0(g);
             // both rows at once; the same q <= 9 decisions as the forward
             // (q_within_cutoff: an fp32 q outside the error band decides alike)
-            const float dx = (float)(px - x0) + g.ox;
-            const float2 dy = make_float2((float)(py - y0) + g.oy, (float)(py + 1 - y0) + g.oy);
-            const float2 pw = fma2(dy, fma2(f2s(g.ic), dy, f2s(2.f * g.ib * dx)), f2s(g.ia * dx * dx));
+            // pw from the corner expansion, both rows at once; hx, hy = C (x - u)
+            const float cx = (float)(px - x0);
+            const float2 cy = make_float2((float)(py - y0), (float)(py + 1 - y0));
+            const float dx = cx + g.ox;   // offsets from the centre: the conic gradients' factors
+            const float2 dy = add2(cy, f2s(g.oy));
+            const float4 an = s_anch[j];
+            const float2 hx = fma2(f2s(g.ib), cy, f2s(fmaf(g.ia, cx, an.y)));
+            const float2 hy = fma2(f2s(g.ic), cy, f2s(fmaf(g.ib, cx, an.z)));
+            const float2 pw = fma2(f2s(cx), add2(hx, f2s(an.y)), fma2(cy, add2(hy, f2s(an.z)), f2s(an.x)));
+            const float eps = g.eps;
             const float2 d = sub2(pw, f2s(kPowCut));
             const bool col = (unsigned)(px - x0) <= (unsigned)(rec_x1(g) - x0);
             bool h0 = col && (unsigned)(py - y0) <= (unsigned)(y1 - y0) && k <= pp.last0;
             bool h1 = col && (unsigned)(py + 1 - y0) <= (unsigned)(y1 - y0) && k <= pp.last1;
-            if ((h0 && fabsf(d.x) <= g.eps) || (h1 && fabsf(d.y) <= g.eps)) {   // rare: fp64 band
-                h0 = h0 && q_within_cutoff(pw.x, g.eps, p64, order, s_rank[j], px, py);
-                h1 = h1 && q_within_cutoff(pw.y, g.eps, p64, order, s_rank[j], px, py + 1);
+            if ((h0 && fabsf(d.x) <= eps) || (h1 && fabsf(d.y) <= eps)) {   // rare: fp64 band
+                h0 = h0 && q_within_cutoff(pw.x, eps, p64, order, s_rank[j], px, py);
+                h1 = h1 && q_within_cutoff(pw.y, eps, p64, order, s_rank[j], px, py + 1);
             } else {
                 h0 = h0 && d.x >= 0.f;
                 h1 = h1 && d.y >= 0.f;
             }
             if (!__any_sync(0xffffffffu, h0 || h1)) continue;
             float v[16];
-            pp.step(g, dx, dy, pw, h0, h1, k, v);
+            pp.step(g, dx, dy, pw, hx, hy, h0, h1, k, v);
             const float2 s = transpose_reduce10(v, lane);
             if (!(lane & 3)) s_part[warp][j][via] = s.x;
             if (!(lane & 15)) s_part[warp][j][vib] = s.y;

@@ -147,15 +147,27 @@ __device__ __forceinline__ uint32_t project_one(
     fx1 = fmax(fmin(fx1, (double)(cam.width - 1)), -1.0);
     fy1 = fmax(fmin(fy1, (double)(cam.height - 1)), -1.0);
     const int x0 = (int)fx0, x1 = (int)fx1, y0 = (int)fy0, y1 = (int)fy1;
-    r.ox = (float)DS((double)x0, g.u);
-    r.oy = (float)DS((double)y0, g.v);
-    r.ia = (float)DM(kPowScale, ia);
-    r.ib = (float)DM(kPowScale, ib);
-    r.ic = (float)DM(kPowScale, ic);
-    // fp32 error bound of the quadratic form near q = 9 scales with the
-    // anisotropy K = ac/det (sum of |terms| <= 36 K); generous margin.
-    const double K = DD(DM(a, c), det);
-    r.eps = (float)DM(DM(1e-4, DA(1.0, K)), -kPowScale);
+    const double dax = DS((double)x0, g.u), day = DS((double)y0, g.v);
+    const double sia = DM(kPowScale, ia), sib = DM(kPowScale, ib), sic = DM(kPowScale, ic);
+    r.ox = (float)dax;
+    r.oy = (float)day;
+    r.ia = (float)sia;
+    r.ib = (float)sib;
+    r.ic = (float)sic;
+    {
+        // fp32 error band of the corner expansion (stage_anchor +
+        // compositing): a few roundings of partial sums bounded by S, the sum
+        // of |terms| at the far box corner (<= ~10 ulp of S), plus the
+        // direct form's anisotropy bound 36 K for the fp32 anchors of
+        // ordinary splats; both with a wide margin
+        const double hax = DA(DM(sia, dax), DM(sib, day)), hay = DA(DM(sib, dax), DM(sic, day));
+        const double qa = DA(DM(dax, hax), DM(day, hay));
+        const double wx = fmax((double)(x1 - x0), 0.0), wy = fmax((double)(y1 - y0), 0.0);
+        const double S = fabs(qa) + 2.0 * (fabs(hax) * wx + fabs(hay) * wy) + fabs(sia) * wx * wx +
+                         2.0 * fabs(sib) * wx * wy + fabs(sic) * wy * wy;
+        const double K = DD(DM(a, c), det);
+        r.eps = (float)fmax(1e-5 * S + 1e-6, DM(DM(1e-4, DA(1.0, K)), -kPowScale));
+    }
     r.x0y0 = (int32_t)(((uint32_t)y0 << 16) | ((uint32_t)x0 & 0xffffu));
     r.x1y1 = (int32_t)(((uint32_t)(y1 & 0xffff) << 16) | ((uint32_t)x1 & 0xffffu));
     r.beta = (float)DD(b, c);
@@ -391,6 +403,7 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
     constexpr int NT = kTilePx;
     __shared__ ProjRec s_rec[NT];
     __shared__ int4 s_box[NT];
+    __shared__ float4 s_anch[NT];   // the corner expansion (stage_anchor), gradient doubled
     __shared__ uint32_t s_rank[NT];
     __shared__ int s_maxlast;
     // longest-first when the caller keeps the previous render's order of this view
@@ -412,6 +425,8 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
             const ProjRec r = recs[rk];
             s_rec[threadIdx.x] = r;
             s_box[threadIdx.x] = make_int4(rec_x0(r), rec_x1(r) - rec_x0(r), rec_y0(r), rec_y1(r) - rec_y0(r));
+            const float4 an = stage_anchor(r, p64, order, rk);   // {qa, 2 hax, 2 hay, 2 ib}
+            s_anch[threadIdx.x] = make_float4(an.x, 2.f * an.y, 2.f * an.z, 2.f * r.ib);
         }
         __syncthreads();
         const int cnt = (int)min((uint32_t)NT, end - base);
@@ -421,9 +436,10 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
                 if (bx.z + bx.w < wy0 || bx.z > wy0 + 1) continue;   // warp-uniform row cull
                 if ((unsigned)(px - bx.x) > (unsigned)bx.y || (unsigned)(py - bx.z) > (unsigned)bx.w) continue;
                 const ProjRec &g = s_rec[j];
-                const float dx = (float)(px - bx.x) + g.ox;
-                const float dy = (float)(py - bx.z) + g.oy;
-                const float pw = dx * (g.ia * dx + 2.f * g.ib * dy) + g.ic * dy * dy;
+                // pw = qa + cx (2 hax + ia cx + 2 ib cy) + cy (2 hay + ic cy)
+                const float cx = (float)(px - bx.x), cy = (float)(py - bx.z);
+                const float4 an = s_anch[j];
+                const float pw = fmaf(cx, fmaf(g.ia, cx, fmaf(an.w, cy, an.y)), fmaf(cy, fmaf(g.ic, cy, an.z), an.x));
                 if (q_within_cutoff(pw, g.eps, p64, order, s_rank[j], px, py)) {
                     s.add(g, pw, (int32_t)(base + j));
                     if (s.done) {

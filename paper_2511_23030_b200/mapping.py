@@ -129,6 +129,7 @@ class _ActiveSet:
     segment layout so revisited keyframes reuse their list (and CUDA graph)."""
 
     CAPACITY = 64
+    rebuilds = 0   # slot buffers refilled in place after paging
 
     def __init__(self, device):
         import torch
@@ -155,6 +156,7 @@ class _ActiveSet:
         so the CUDA graphs captured over this buffer stay valid."""
         for k in [k for k, v in self._cache.items() if v[0] is slots]:
             del self._cache[k]
+        self.rebuilds += 1
         return self._fill(slots, tuple(segments), segments)
 
     def _fill(self, slots, key, segments):

@@ -113,6 +113,38 @@ def test_paging_steps_are_deterministic(cuda, tmp_path):
     assert rows[0] == rows[1]
 
 
+def test_paging_keeps_graphs_and_training(cuda, tmp_path):
+    """Paging never changes the training, and a view whose chunks come back at
+    other slab rows keeps its CUDA graph (its slot buffer is refilled in
+    place).  (1) Under a paging budget: same keyframe draws and bit-identical
+    losses as the all-resident run and as an eager run.  (2) Graph-captured
+    views, then every chunk evicted and reloaded in reverse order (new rows):
+    the next steps replay the captured graphs after an in-place refill and
+    still equal the eager run."""
+    runs = {}
+    for name, budget, graphs in (("resident", 100_000, True), ("paged", 12_000, True),
+                                 ("paged_eager", 12_000, False)):
+        eng = _c1_engine(tmp_path / name, budget=budget, use_graphs=graphs)
+        runs[name] = [(r.selected_kf, r.loss) for r in (eng.optimization_step(f, s)
+                                                        for f in range(4) for s in range(10))]
+        if name == "paged":
+            assert eng.store.stats.chunk_evictions > 0 and eng.counter_replays > 0
+    assert runs["paged"] == runs["resident"] == runs["paged_eager"]
+    a = _c1_engine(tmp_path / "ga", budget=100_000, use_graphs=True)
+    b = _c1_engine(tmp_path / "gb", budget=100_000, use_graphs=False)
+    for s in range(12):
+        assert a.optimization_step(0, s).loss == b.optimization_step(0, s).loss
+    for eng in (a, b):
+        st = eng.store
+        st.evict_lru(st.stats.active_gaussians, protected=set())
+        st.ensure_resident(sorted(st.known_chunk_ids())[::-1])
+    replays = a.counter_replays
+    for s in range(12, 24):
+        ra, rb = a.optimization_step(0, s), b.optimization_step(0, s)
+        assert (ra.selected_kf, ra.loss) == (rb.selected_kf, rb.loss)
+    assert a.active.rebuilds > 0 and a.counter_replays > replays
+
+
 def test_render_through_store_matches_oracle(cuda, tmp_path):
     """The active set rendered from the slab equals the oracle render of the
     same splats gathered in sorted-chunk-id order (sim.py:236-253)."""
