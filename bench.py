@@ -380,9 +380,15 @@ def main():
     _lib.profile_collect()
     # (C3: single-keyframe steps -- the same per-keyframe kernels; the K-keyframe
     # step's per-stage events are not all recorded inside its graphs)
+    if c3:
+        eng.reset_counters()
     pms, _ = timed(4, fn=(lambda f, s: eng.optimization_step(f, s)) if c3 else None)
     prof = _lib.profile_collect()
     lib.sm_profile_enable(0)
+    if c3:   # the per-keyframe work of the profiled (single-keyframe) steps
+        n_vis = eng.counter_gaussians / max(eng.counter_steps, 1)
+        n_inst = eng.counter_instances / max(eng.counter_steps, 1)
+        n_visit = eng.counter_visited / max(eng.counter_steps, 1)
     # ------------------------------------------------------------ roofline of the dominant kernel
     peaks = _peaks()
     px = eng.intr.width * eng.intr.height
