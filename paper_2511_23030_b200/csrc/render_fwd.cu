@@ -354,13 +354,14 @@ struct FwdPix {
     int32_t last;
     bool done;
 
-    __device__ __forceinline__ void add(const ProjRec &g, float pw, int32_t k) {
-        const float alpha = g.op * ex2_approx(pw);
+    // c = {r, g, b, z} of the splat
+    __device__ __forceinline__ void add(float op, const float4 &c, float pw, int32_t k) {
+        const float alpha = op * ex2_approx(pw);
         const float w = T * alpha;
-        cr += w * g.r;
-        cg += w * g.g;
-        cb += w * g.b;
-        cd += w * g.z;
+        cr += w * c.x;
+        cg += w * c.y;
+        cb += w * c.z;
+        cd += w * c.w;
         tlast = T;
         last = k;
         T = T * (1.f - alpha);
@@ -401,9 +402,11 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
               float *__restrict__ st_tlast, int32_t *__restrict__ st_last, uint32_t *__restrict__ tile_work,
               const uint32_t *__restrict__ launch_order) {
     constexpr int NT = kTilePx;
-    __shared__ ProjRec s_rec[NT];
-    __shared__ int4 s_box[NT];
-    __shared__ float4 s_anch[NT];   // the corner expansion (stage_anchor), gradient doubled
+    // per staged instance, exactly what the pixel loop reads (64 B):
+    __shared__ int4 s_box[NT];      // x0, x1 - x0, y0, y1 - y0
+    __shared__ float4 s_anch[NT];   // qa, 2 hax, 2 hay, 2 ib (stage_anchor, gradient doubled)
+    __shared__ float4 s_cof[NT];    // ia, ic, op, eps
+    __shared__ float4 s_col[NT];    // r, g, b, z
     __shared__ uint32_t s_rank[NT];
     __shared__ int s_maxlast;
     // longest-first when the caller keeps the previous render's order of this view
@@ -423,10 +426,11 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
             const uint32_t rk = (uint32_t)(ikeys[idx] & rank_mask);
             s_rank[threadIdx.x] = rk;
             const ProjRec r = recs[rk];
-            s_rec[threadIdx.x] = r;
             s_box[threadIdx.x] = make_int4(rec_x0(r), rec_x1(r) - rec_x0(r), rec_y0(r), rec_y1(r) - rec_y0(r));
-            const float4 an = stage_anchor(r, p64, order, rk);   // {qa, 2 hax, 2 hay, 2 ib}
+            const float4 an = stage_anchor(r, p64, order, rk);   // {qa, hax, hay, -}
             s_anch[threadIdx.x] = make_float4(an.x, 2.f * an.y, 2.f * an.z, 2.f * r.ib);
+            s_cof[threadIdx.x] = make_float4(r.ia, r.ic, r.op, r.eps);
+            s_col[threadIdx.x] = make_float4(r.r, r.g, r.b, r.z);
         }
         __syncthreads();
         const int cnt = (int)min((uint32_t)NT, end - base);
@@ -435,13 +439,12 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
                 const int4 bx = s_box[j];   // x0, x1 - x0, y0, y1 - y0 (decoded once at staging)
                 if (bx.z + bx.w < wy0 || bx.z > wy0 + 1) continue;   // warp-uniform row cull
                 if ((unsigned)(px - bx.x) > (unsigned)bx.y || (unsigned)(py - bx.z) > (unsigned)bx.w) continue;
-                const ProjRec &g = s_rec[j];
                 // pw = qa + cx (2 hax + ia cx + 2 ib cy) + cy (2 hay + ic cy)
                 const float cx = (float)(px - bx.x), cy = (float)(py - bx.z);
-                const float4 an = s_anch[j];
-                const float pw = fmaf(cx, fmaf(g.ia, cx, fmaf(an.w, cy, an.y)), fmaf(cy, fmaf(g.ic, cy, an.z), an.x));
-                if (q_within_cutoff(pw, g.eps, p64, order, s_rank[j], px, py)) {
-                    s.add(g, pw, (int32_t)(base + j));
+                const float4 an = s_anch[j], cf = s_cof[j];
+                const float pw = fmaf(cx, fmaf(cf.x, cx, fmaf(an.w, cy, an.y)), fmaf(cy, fmaf(cf.y, cy, an.z), an.x));
+                if (q_within_cutoff(pw, cf.w, p64, order, s_rank[j], px, py)) {
+                    s.add(cf.z, s_col[j], pw, (int32_t)(base + j));
                     if (s.done) {
                         all_done = true;
                         break;
