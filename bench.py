@@ -152,6 +152,14 @@ def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("SM_BENCH_ONE_GPU"):
+        # plumbing check of the N-rank path on a one-GPU box: every rank on
+        # cuda:0, exchanging through gloo (host copies), so no rank's kernels
+        # wait on another's; never a measurement (the line says so)
+        local = 0
+        if world > 1 and not dist.is_initialized():
+            dist.init_process_group("gloo")
+        return world, rank, local
     if world > 1 and not dist.is_initialized():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
@@ -437,6 +445,8 @@ def main():
         "stages_mode": "single-keyframe steps" if c3 else "the timed steps",
         "c3_g1": c3_g1,
     }
+    if os.environ.get("SM_BENCH_ONE_GPU"):
+        line["plumbing_check"] = "all ranks on one GPU over gloo: not a measurement"
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
