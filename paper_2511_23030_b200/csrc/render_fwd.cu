@@ -407,6 +407,7 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
     __shared__ float4 s_anch[NT];   // qa, 2 hax, 2 hay, 2 ib (stage_anchor, gradient doubled)
     __shared__ float4 s_cof[NT];    // ia, ic, op, eps
     __shared__ float4 s_col[NT];    // r, g, b, z
+    __shared__ uint32_t s_wm[NT];   // bit w: the box reaches warp w's two rows
     __shared__ uint32_t s_rank[NT];
     __shared__ int s_maxlast;
     // longest-first when the caller keeps the previous render's order of this view
@@ -431,13 +432,21 @@ composite_fwd(const uint32_t *__restrict__ ranges, const KeyT *__restrict__ ikey
             s_anch[threadIdx.x] = make_float4(an.x, 2.f * an.y, 2.f * an.z, 2.f * r.ib);
             s_cof[threadIdx.x] = make_float4(r.ia, r.ic, r.op, r.eps);
             s_col[threadIdx.x] = make_float4(r.r, r.g, r.b, r.z);
+            const int lo = max(rec_y0(r) - ty0, 0) >> 1, hi = min(rec_y1(r) - ty0, kTile - 1) >> 1;
+            s_wm[threadIdx.x] = hi >= lo ? ((2u << hi) - 1u) & ~((1u << lo) - 1u) : 0u;
         }
         __syncthreads();
         const int cnt = (int)min((uint32_t)NT, end - base);
-        if (!all_done) {
-            for (int j = 0; j < cnt; j++) {
+        // the warp walks only the staged splats whose box reaches its two rows,
+        // in order: a ballot per 32 of them over the staging-time row masks
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int c = 0; c < cnt; c += 32) {
+            if (__all_sync(0xffffffffu, all_done)) break;
+            uint32_t m = __ballot_sync(0xffffffffu, c + lane < cnt && ((s_wm[c + lane] >> warp) & 1u));
+            if (all_done) continue;
+            for (; m; m &= m - 1) {
+                const int j = c + __ffs(m) - 1;
                 const int4 bx = s_box[j];   // x0, x1 - x0, y0, y1 - y0 (decoded once at staging)
-                if (bx.z + bx.w < wy0 || bx.z > wy0 + 1) continue;   // warp-uniform row cull
                 if ((unsigned)(px - bx.x) > (unsigned)bx.y || (unsigned)(py - bx.z) > (unsigned)bx.w) continue;
                 // pw = qa + cx (2 hax + ia cx + 2 ib cy) + cy (2 hay + ic cy)
                 const float cx = (float)(px - bx.x), cy = (float)(py - bx.z);
