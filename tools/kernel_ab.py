@@ -62,8 +62,19 @@ def main():
     prof = _lib.profile_collect()
     lib.sm_profile_enable(0)
     stages = {k: round(v[0] / passes, 5) for k, v in prof.items() if v[1]}
+    # outputs of one pass per view (images, depth, alpha, gradients): equal
+    # hashes across builds = bit-identical results
+    import hashlib
+    h = hashlib.sha1()
+    for kf, slots, n in views:
+        eng.store.slab.grads.zero_()
+        eng._device_pass(kf, slots, n, backward=True, adam=False)
+        torch.cuda.synchronize()
+        for t in (eng.rgb, eng.depth, eng.alpha, eng.store.slab.grads):
+            h.update(t.cpu().numpy().tobytes())
     print(json.dumps({"variant": __import__("os").environ.get("SM_LIB_VARIANT", "main"),
                       "pass_ms": round(total, 5), "passes": passes, "stages_ms": stages,
+                      "outputs_sha1": h.hexdigest()[:16],
                       "visible": [n for _, _, n in views]}))
 
 
