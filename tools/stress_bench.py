@@ -190,6 +190,7 @@ def main():
                 blocked[0] += time.perf_counter() - t
         st.ensure_resident = timed
         st.streamer.warm()
+        sstats0 = dict(st.streamer.stats)   # (the build phase's paging is not the run's)
         s0 = st.stats
         base = (s0.chunk_loads, s0.chunk_evictions, s0.chunk_writes, s0.bytes_read, s0.bytes_written,
                 s0.keyframe_writes, s0.keyframe_loads)
@@ -205,9 +206,12 @@ def main():
             prof.enable()
         t0 = time.perf_counter()
         steps = 0
+        add_s = 0.0
         for kf_i in range(k):
             pose = poses[kf_i]
+            ta = time.perf_counter()
             eng.add_keyframe(kfs[kf_i])   # the engine prefetches itself (look-ahead); no harness prefetch
+            add_s += time.perf_counter() - ta
             for s in range(args.steps):
                 eng.optimization_step(kf_i, s)
                 steps += 1
@@ -227,13 +231,14 @@ def main():
         res[mode] = {"keyframes": k, "steps": steps, "seconds": dt, "steps_per_s": steps / dt,
                      "chunk_loads": d[0], "chunk_evictions": d[1], "chunk_writes": d[2],
                      "bytes_read": d[3], "bytes_written": d[4], "keyframe_writes": d[5],
-                     "keyframe_loads": d[6], "ensure_resident_s": blocked[0],
+                     "keyframe_loads": d[6], "ensure_resident_s": blocked[0], "add_keyframe_s": add_s,
                      "mean_visible": eng.counter_gaussians / max(eng.counter_steps, 1),
                      "slab_bytes": st.slab.hbm_bytes(), "slab_compactions": st.slab.compactions,
                      "hbm_bytes_store": st.slab.hbm_bytes() + st.streamer.device_bytes,
                      "graph_replays": eng.counter_replays, "eager_steps": eng.counter_eager}
         if st.streamer is not None:
-            res[mode].update({f"streamer_{a}": b for a, b in st.streamer.stats.items()})
+            res[mode].update({f"streamer_{a}": (b - sstats0.get(a, 0) if a != "arena_s" else b)
+                              for a, b in st.streamer.stats.items()})
         print(json.dumps({mode: res[mode]}), file=sys.stderr, flush=True)
         st.flush()
         st.streamer.drain()
