@@ -516,36 +516,18 @@ class MappingEngine:
 
     def _prefetch_view(self, pose: Pose) -> None:
         """A new keyframe's on-disk chunks start streaming in (one cull, no
-        visibility-cache insertion: no policy effect).  The cull runs on a
-        helper thread and its own CUDA stream, off the step's host path; the
-        chunk set it culls is snapshotted here."""
+        visibility-cache insertion: no policy effect)."""
         store = self.store
         ext = store.coord_extent()
         if not self.prefetch_lookahead or ext is None or not store.has_disk_chunks():
             return
-        prev, self._view_job = self._view_job, None
-        if prev is not None:
-            prev.result()   # a failed cull surfaces here
-        if self._view_pool is None:
-            from concurrent.futures import ThreadPoolExecutor
-            self._view_pool = ThreadPoolExecutor(max_workers=1)
-            self._view_stream = self.torch.cuda.Stream(device=self.device)
-        key = (pose.translation.tobytes(), pose.rotation.tobytes(), store.generation)
-        extent, cands, size = ChunkExtent(*ext), list(store.known_chunk_ids()), store.chunk_size
-
-        def cull():
-            with self.torch.cuda.device(self.device), self.torch.cuda.stream(self._view_stream):
-                vis = visible_chunks(pose, self.intr, extent, store.has_chunk, self.cull_cfg, size,
-                                     candidates=cands)
-            # the step that first draws this keyframe misses the visibility
-            # cache with exactly this pose and chunk set: it takes this set,
-            # not a second cull (if it is ready by then)
-            self._view_memo = (key, frozenset(vis))
-            store.prefetch(sorted(vis))
-        self._view_job = self._view_pool.submit(cull)
-
-    _view_pool = None
-    _view_job = None
+        vis = visible_chunks(pose, self.intr, ChunkExtent(*ext), store.has_chunk, self.cull_cfg,
+                             store.chunk_size, candidates=store.known_chunk_ids())
+        # the step that first draws this keyframe misses the visibility cache
+        # with exactly this pose and chunk set: it takes this set, not a second cull
+        self._view_memo = ((pose.translation.tobytes(), pose.rotation.tobytes(), store.generation),
+                           frozenset(vis))
+        store.prefetch(sorted(vis))
 
     def _precompute_next_draw(self) -> None:
         """The next single-GPU step's uniform draw depends only on its derived
