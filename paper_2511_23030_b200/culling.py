@@ -113,10 +113,25 @@ def cull_ids(ids: np.ndarray, pose: Pose, intr: CameraIntrinsics, max_distance: 
     ids = np.asarray(ids, dtype=np.uint64)
     if ids.size == 0:
         return ids
+    coords = torch.as_tensor(decode_ids(ids).astype(np.int32), device="cuda")
+    return cull_table(ids, coords, pose, intr, max_distance, s, frustum)
+
+
+def cull_table(ids: np.ndarray, coords, pose: Pose, intr: CameraIntrinsics, max_distance: float,
+               s: float, frustum: Frustum | None = None) -> np.ndarray:
+    """K1 over a chunk table already on the device (`coords` = the ids'
+    int32 chunk coordinates, e.g. ChunkStore.chunk_table's, kept per chunk-set
+    generation); returns the visible subset of `ids` (sorted)."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    if ids.size == 0:
+        return ids
     lib = _lib.load()
     fr = frustum or extract_frustum(pose, intr)
-    coords = torch.as_tensor(decode_ids(ids).astype(np.int32), device="cuda")
-    out = torch.empty(ids.size, dtype=torch.uint8, device="cuda")
+    out = torch.empty(ids.size, dtype=torch.uint8, device=coords.device)
     planes = np.ascontiguousarray(fr.planes, dtype=np.float64)
     cam = np.ascontiguousarray(pose.translation, dtype=np.float64)
     dp = ctypes.POINTER(ctypes.c_double)

@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _lib
 from .core import CameraIntrinsics, Keyframe, Pose
-from .culling import ChunkExtent, CullConfig, VisibilityCache, visible_chunks
+from .culling import ChunkExtent, CullConfig, VisibilityCache, cull_table
 from .errors import DeviceFailure, EmptyCandidates
 from .renderloss import LossEngine, LossWeights, RenderEngine, camera_for
 from .select import (KeyframeIndex, SelectConfig, candidate_set, draw_uniform, overlap, record_loss,
@@ -392,8 +392,16 @@ class MappingEngine:
         key = (pose.translation.tobytes(), pose.rotation.tobytes(), self.store.generation)
         return self.cache.query(pose, self.intr, ChunkExtent(*ext), self.store.has_chunk,
                                 self.store.generation, self.store.chunk_size,
-                                candidates=self.store.known_chunk_ids,
-                                compute=lambda: set(memo[1]) if memo is not None and memo[0] == key else None)
+                                compute=lambda: set(memo[1]) if memo is not None and memo[0] == key
+                                else self._cull_view(pose))
+
+    def _cull_view(self, pose: Pose) -> set[int]:
+        """visible_chunks over the store's cached device chunk table (the
+        brute-force candidates of culling.py:134-182, without rebuilding and
+        uploading them for every cull)."""
+        ids, coords = self.store.chunk_table()
+        return {int(i) for i in cull_table(ids, coords, pose, self.intr, self.cull_cfg.max_distance_m,
+                                           self.store.chunk_size)}
 
     _view_memo = None   # (pose bytes, chunk-set generation) -> the visible set _prefetch_view culled
 
@@ -521,8 +529,7 @@ class MappingEngine:
         ext = store.coord_extent()
         if not self.prefetch_lookahead or ext is None or not store.has_disk_chunks():
             return
-        vis = visible_chunks(pose, self.intr, ChunkExtent(*ext), store.has_chunk, self.cull_cfg,
-                             store.chunk_size, candidates=store.known_chunk_ids())
+        vis = self._cull_view(pose)
         # the step that first draws this keyframe misses the visibility cache
         # with exactly this pose and chunk set: it takes this set, not a second cull
         self._view_memo = ((pose.translation.tobytes(), pose.rotation.tobytes(), store.generation),

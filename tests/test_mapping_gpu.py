@@ -145,6 +145,23 @@ def test_paging_keeps_graphs_and_training(cuda, tmp_path):
     assert a.active.rebuilds > 0 and a.counter_replays > replays
 
 
+def test_cached_chunk_table_cull_equals_visible_chunks(cuda, tmp_path):
+    """The engine culls over the store's cached device chunk table; across
+    paging (chunks created, evicted, reloaded) it returns exactly
+    visible_chunks' brute-force answer over the known chunks."""
+    from paper_2511_23030_b200.culling import ChunkExtent, visible_chunks
+    eng = _c1_engine(tmp_path, budget=12_000)
+    st = eng.store
+    for f in range(3):
+        for s in range(4):
+            eng.optimization_step(f, s)
+        for kid in sorted(st.resident_keyframe_ids()):
+            pose = st.keyframe_get(kid).pose
+            want = visible_chunks(pose, eng.intr, ChunkExtent(*st.coord_extent()), st.has_chunk, eng.cull_cfg,
+                                  st.chunk_size, candidates=st.known_chunk_ids())
+            assert eng._cull_view(pose) == want
+
+
 def test_render_through_store_matches_oracle(cuda, tmp_path):
     """The active set rendered from the slab equals the oracle render of the
     same splats gathered in sorted-chunk-id order (sim.py:236-253)."""
