@@ -315,8 +315,15 @@ class ChunkStreamer:
         """PinnedFile of `path` from the prefetch tier or the disk, or a
         DeviceRecords if its eviction write is still pending."""
         path = Path(path)
-        with self._lock:
+        with self._lock:   # one critical section: a write cannot settle in between
             pw = self._pending.get(path)
+            pending = None
+            if pw is not None:
+                if pw.dev is not None:
+                    pending = DeviceRecords(pw.header, pw.dev, pw.nbytes, pw.stride)
+                elif pw.pin is not None:   # capped store: the device copy is back in the
+                    pw.borrowers += 1      # pool, the pinned one (D2H done) serves the reload
+                    pending = BorrowedPinned(pw)
             vic = self._victims.get(path)
             if vic is not None:
                 self._victims.move_to_end(path)
@@ -324,16 +331,14 @@ class ChunkStreamer:
         if fut is not None and (pw is not None or vic is not None):   # served from HBM: the read was moot
             fut.add_done_callback(lambda f: f.exception() is None and self.release(f.result()))
             fut = None
-        if pw is not None:
+        if pending is not None:
             self.stats["pending_hits"] += 1
-            with self._lock:
-                dev = pw.dev
-                if dev is None:   # capped store: the device copy is back in the pool,
-                    pw.borrowers += 1   # the pinned one (D2H completed) serves the reload
-            if dev is None:
+            if isinstance(pending, BorrowedPinned):
                 self.stats["pending_pinned_hits"] += 1
-                return BorrowedPinned(pw)
-            return DeviceRecords(pw.header, dev, pw.nbytes, pw.stride)
+            return pending
+        if pw is not None:   # a host-built file still being written: let it land
+            pw.done.wait()
+            self.check()
         if vic is not None:
             self.stats["victim_hits"] += 1
             return vic
