@@ -202,7 +202,10 @@ __device__ __forceinline__ uint32_t project_one(
 // K2 over the visible set; also zeroes the pass's device counters and tile
 // ranges and counts the depth keys' digits for the sort (saves two memsets
 // and the sort's histogram pass).
-__global__ void __launch_bounds__(256)
+#ifndef SM_PROJ_MINB
+#define SM_PROJ_MINB 4   // <= 64 registers: 4 x 256 threads per SM, measured best of 1 and 4-6
+#endif
+__global__ void __launch_bounds__(256, SM_PROJ_MINB)
 project_fwd(const float4 *__restrict__ params, const int32_t *__restrict__ slots, int64_t n,
             CamDev cam, int cull, ProjRec *__restrict__ rec, Proj64 *__restrict__ p64,
             uint32_t *__restrict__ dkey, unsigned long long *__restrict__ zbits,
