@@ -432,6 +432,62 @@ def test_streamer_under_pool_pressure_matches_sync(cuda, tmp_path):
         assert (tmp_path / "sync" / "chunks" / name).read_bytes() == (tmp_path / "tight" / "chunks" / name).read_bytes()
 
 
+def test_streamer_prefetch_tier_and_oversize_buffers(cuda, tmp_path):
+    """The speculative tier under pressure: prefetches of chunks that are
+    never loaded are dropped oldest-first (FIFO) or taken back by real I/O,
+    chunks bigger than a pool slot get a buffer without waiting, and the
+    paging sequence still matches synchronous I/O row for row and, after
+    flush, byte for byte."""
+    import torch
+
+    from paper_2511_23030_b200.core import Gaussian, quat_normalize
+    from paper_2511_23030_b200.store import ChunkStore, StoreConfig
+    rng = np.random.default_rng(31)
+    gs = []
+    for cx in range(12):   # twelve chunks, every third ten times denser
+        for _ in range(3000 if cx % 3 == 0 else 300):
+            gs.append(Gaussian(position=[cx * 10.0 + rng.uniform(-4, 4), rng.uniform(-4, 4), rng.uniform(-4, 4)],
+                               rotation=quat_normalize(rng.normal(size=4)), scale=rng.uniform(0.01, 0.2, 3),
+                               opacity=float(rng.uniform(0, 1)), sh=rng.normal(size=48)))
+    stores = []
+    for name, wb in (("sync", False), ("spec", True)):
+        st = ChunkStore(StoreConfig(disk_root=tmp_path / name, chunk_size_m=10.0, gaussian_budget=4000,
+                                    io_ns_per_byte=1.0, write_behind=wb))
+        if wb:   # small slots: the dense chunks (~0.9 MB) exceed two of them
+            sm = st.streamer
+            sm.PINNED_SLOT_BYTES = 256 << 10
+            sm.PINNED_SLOTS = 12
+            sm.DEVICE_SLOTS = 6
+            sm._largest = {True: 2 * sm.PINNED_SLOT_BYTES, False: 2 * sm.PINNED_SLOT_BYTES}
+        st.insert_gaussians(gs)
+        stores.append(st)
+    ids = sorted(stores[0].known_chunk_ids())
+    order = np.random.default_rng(4).integers(0, len(ids), size=(40, 4))
+    for step, pick in enumerate(order):
+        want = sorted({ids[int(k)] for k in pick[:2]})
+        stores[1].prefetch([ids[int(k)] for k in pick[2:]])   # speculation, often never used
+        for st in stores:
+            st.ensure_resident(want)
+            for c in want:
+                ch = st.chunk(c)
+                st.slab.params[ch.offset:ch.offset + ch.count, 0] += 1e-3 * (step + 1)
+            st.mark_trained(want)
+        assert _stats(stores[0]) == _stats(stores[1])
+        for c in want:
+            a, b = stores[0].chunk(c), stores[1].chunk(c)
+            assert torch.equal(stores[0].slab.params[a.offset:a.offset + a.count],
+                               stores[1].slab.params[b.offset:b.offset + b.count])
+    stats = stores[1].streamer.stats
+    assert stats["prefetch_issued"] > 0 and stats["prefetch_dropped"] > 0, stats
+    assert stats["alloc_pinned"] + stats["alloc_device"] > 0, stats   # oversize chunks: no waiting
+    assert stats["pool_wait_s"] < 1.0, stats
+    for st in stores:
+        st.flush()
+    for c in ids:
+        name = f"{c:016x}.dcg"
+        assert (tmp_path / "sync" / "chunks" / name).read_bytes() == (tmp_path / "spec" / "chunks" / name).read_bytes()
+
+
 def test_capped_write_behind_backlog_in_pinned_memory(cuda, tmp_path):
     """Under a hard HBM cap the eviction D2H is issued at eviction and the
     device buffer goes back to the small pool once it completed; a chunk
