@@ -19,7 +19,14 @@ Evict:  K9 sm_chunk_pack on the compute stream into a device buffer (so the
         thread then takes a pinned buffer, copies the records down on its
         own stream (after the pack's event) and writes the file: eviction
         write-back overlaps with rendering (write-behind), and the backlog
-        of unwritten chunks waits in HBM, not in pinned memory.
+        of unwritten chunks waits in HBM, not in pinned memory.  Under a
+        hard HBM cap (small device share) the copy down is issued at
+        eviction instead and the device buffer returns to the pool once it
+        completed; the backlog then waits in pinned memory, and a reload of
+        a chunk still queued is served from that pinned copy.
+Prefetch: speculative reads on reader threads into a FIFO tier of pinned
+        buffers that never blocks real I/O (loads and write-behinds take
+        back the oldest unclaimed read when the pool is empty).
 flush():  drains the writer queue (the store's durability point).
 """
 
