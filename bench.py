@@ -340,7 +340,9 @@ def main():
     # ------------------------------------------------------------ timed (device-resident)
     eng.reset_counters()
     launches0 = lib.sm_launch_count()
+    te0 = eng.counter_eager
     ms, clk = timed(1, clocks_gpu=local)
+    timed_eager = eng.counter_eager - te0
     launches = lib.sm_launch_count() - launches0
     kf_seq = [r.selected_kf for r in eng.rows[-args.steps * (kps if c3 else 1):]]
     ms_step = ms / args.steps
@@ -373,10 +375,16 @@ def main():
     eng.warm_graphs()
     eng.reset_counters()
     h2d0, d2h0 = eng.h2d_bytes, eng.d2h_bytes
+    e0, r0 = eng.counter_eager, eng.counter_replays
     ems, _ = timed(3)
     e2e = {"value": units / (ems / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": int((eng.h2d_bytes - h2d0) / args.steps),
-           "d2h_bytes_per_step": int((eng.d2h_bytes - d2h0) / args.steps)}
+           "d2h_bytes_per_step": int((eng.d2h_bytes - d2h0) / args.steps),
+           # the pass's own work (it trains later steps of the same run)
+           "visible_gaussians_per_step": eng.counter_gaussians / max(eng.counter_steps, 1),
+           "revisited_instances_per_step": eng.counter_visited / max(eng.counter_steps, 1),
+           "eager_steps": eng.counter_eager - e0, "graph_replays": eng.counter_replays - r0,
+           "kf_sequence_distinct": len(set(r.selected_kf for r in eng.rows[-units:]))}
     eng.upload_keyframes_each_step = False
     # ------------------------------------------------------------ per-kernel timing pass
     # Same steps again with CUDA-event pairs around every stage (external event
@@ -437,7 +445,7 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(args),
         "measured": {"visible_gaussians_per_step": n_vis, "tile_instances_per_step": n_inst,
-                     "revisited_instances_per_step": n_visit},
+                     "revisited_instances_per_step": n_visit, "eager_steps": timed_eager},
         "kf_sequence": kf_seq,
         "gaussians_per_s": gauss_s,
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clk, "roofline": roof,
